@@ -1,0 +1,173 @@
+/*
+ * rmpc_b200.h — C ABI of the B200-native batched real-time-iteration MPC solver.
+ *
+ * This is the drop-in boundary for the reference's batched solve entry point
+ *   rmpc::BatchRunner(int n_envs, const ModelParams&, const MpcSettings&, int workers)
+ *   std::vector<MpcSolution> BatchRunner::solve(states, cmds, gaits, prev, order)
+ *   (/root/reference/proj/include/rmpc/batch.hpp:24-46, proj/src/batch.cpp:26-79)
+ * and its single-agent twin MpcController::rti_step (proj/include/rmpc/mpc.hpp:137-153).
+ *
+ * Plain C: POD structs, pointers and sizes; no C++ or torch types in any signature.
+ * Inputs are FP64 (the reference's own types); the solve computes in FP32 on sm_100a and
+ * returns FP32 solution records.  Per-agent failures never abort the batch: they are
+ * reported in rmpc_solution.status, as the reference reports MpcStatus::kFailed
+ * (proj/src/mpc.cpp:333-336, batch.hpp:29-31).
+ */
+#ifndef RMPC_B200_H_
+#define RMPC_B200_H_
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMPC_NQ 9            /* generalized coordinates, robot.hpp:14 */
+#define RMPC_NJ 6            /* actuated joints, robot.hpp:15 */
+#define RMPC_NC 4            /* contact points (R toe, R heel, L toe, L heel), robot.hpp:16 */
+#define RMPC_NF 8            /* contact force components, robot.hpp:17 */
+#define RMPC_NV 26           /* decision variables per node (dq, dqd, dF), mpc.hpp:14 */
+#define RMPC_MAX_HORIZON 32  /* one warp lane per horizon node during linearization */
+#define RMPC_NUM_STAGES 7    /* MpcStage, mpc.hpp:79-88 */
+
+/* ---- return codes of the API calls (structural errors of the reference map here) ---- */
+#define RMPC_OK 0
+#define RMPC_ERR_STRUCTURAL 1   /* StructuralError: sizes, horizon < 2, length mismatch */
+#define RMPC_ERR_INVALID_ARG 2  /* NULL handle / pointer */
+#define RMPC_ERR_CUDA 3         /* CUDA runtime failure (no device, launch failure) */
+#define RMPC_ERR_NO_KERNEL 4    /* kernel image for this device missing (not sm_100a) */
+
+/* ---- per-agent status codes (MpcStatus + the exception class that caused kFailed) ---- */
+#define RMPC_STATUS_OK 0
+#define RMPC_STATUS_NONFINITE_INPUT 1  /* StructuralError "build_qp: non-finite linearization point" */
+#define RMPC_STATUS_DIVERGED 2         /* DivergenceError "admm: non-finite iterate at iteration k" */
+#define RMPC_STATUS_SINGULAR 3         /* SingularityError: non-positive pivot in the factorization */
+
+/* ModelParams (robot.hpp:24-50).  Defaults from rmpc_model_default(). */
+typedef struct rmpc_model {
+  double torso_mass, torso_len, torso_inertia;
+  double thigh_mass, thigh_len, thigh_inertia;
+  double shank_mass, shank_len, shank_inertia;
+  double foot_mass, foot_half_len, foot_inertia;
+  double ankle_drop;
+  double joint_lo[RMPC_NJ], joint_hi[RMPC_NJ];
+  double qd_limit[RMPC_NJ], tau_limit[RMPC_NJ];
+  double kp[RMPC_NJ], kd[RMPC_NJ];
+  double mu;        /* model friction (unused by the MPC: it uses settings.mu, mpc.cpp:188) */
+  double gravity;
+  double nominal_stagger, nominal_drop;
+} rmpc_model;
+
+/* MpcSettings (mpc.hpp:16-57) + AdmmSettings::ruiz_iters (qp.hpp:34). */
+typedef struct rmpc_settings {
+  int32_t horizon;                       /* T, 2 <= T <= RMPC_MAX_HORIZON */
+  double dt_schedule[RMPC_MAX_HORIZON];  /* first `horizon` entries used */
+  double w_q[RMPC_NQ], w_qd[RMPC_NQ], w_f[RMPC_NF];
+  double gait_period, phase_switch, phase_offsets[RMPC_NC];
+  double z_swing, v_to, v_td;
+  int32_t n_qp;                          /* fixed ADMM iteration count, no early exit */
+  double mu, sigma, rho, over_relax;
+  int32_t warm_start;                    /* 0: cold nominal guess (default) */
+  int32_t ruiz_iters;                    /* 10 (AdmmSettings default); 0 disables */
+} rmpc_settings;
+
+/* RobotState (robot.hpp:52-55). */
+typedef struct rmpc_state {
+  double q[RMPC_NQ];
+  double qd[RMPC_NQ];
+} rmpc_state;
+
+/* MpcCommand (mpc.hpp:59-63). */
+typedef struct rmpc_command {
+  double height, vx, wpitch;
+} rmpc_command;
+
+/* GaitState (gait.hpp:16-29). */
+typedef struct rmpc_gait {
+  double phase, period, phase_switch;
+  double offsets[RMPC_NC];
+} rmpc_gait;
+
+/* MpcSolution (mpc.hpp:100-116), node-0 quantities; z_star is a separate optional array
+ * laid out [agent][node][26] = (q 9, qd 9, F 8) per node. */
+typedef struct rmpc_solution {
+  float tau_ff[RMPC_NJ];
+  float q_set[RMPC_NJ];
+  float qd_set[RMPC_NJ];
+  float f0[RMPC_NF];          /* z_star.F row 0 */
+  float base_residual[3];
+  float v_mpc;                /* QP objective at the solution step */
+  float prim_res, dual_res;
+  float delta_inf_norm;       /* ||dz||_inf of the accepted step */
+  int32_t status;             /* RMPC_STATUS_* */
+  int32_t fail_iter;          /* DivergenceError::iteration, -1 otherwise */
+} rmpc_solution;
+
+/* TimingReport (batch.hpp:12-18), measured on the device.  stage_ms splits the fused
+ * kernel's time by the reference's 7 stages when stage profiling is enabled, else 0. */
+typedef struct rmpc_timing {
+  int32_t batch_size;
+  int32_t devices;
+  double total_ms;     /* wall time of the whole call (host clock) */
+  double h2d_ms;       /* host->device copies (max over devices, CUDA events) */
+  double kernel_ms;    /* solve kernel (max over devices, CUDA events) */
+  double d2h_ms;       /* device->host copies (max over devices, CUDA events) */
+  double stage_ms[RMPC_NUM_STAGES];
+} rmpc_timing;
+
+typedef struct rmpc_handle rmpc_handle;
+
+void rmpc_model_default(rmpc_model* model);
+/* Defaults of MpcSettings with `horizon` nodes of dt = 0.05 (config.cpp:149-151). */
+void rmpc_settings_default(rmpc_settings* settings, int32_t horizon);
+
+/* BatchRunner ctor.  Agents are split into contiguous ranges over `devices`
+ * (n_devices >= 1; NULL devices = {0}).  Returns RMPC_ERR_STRUCTURAL for n_agents < 1,
+ * horizon < 2 or > RMPC_MAX_HORIZON (batch.cpp:19, mpc.cpp:243-245). */
+int32_t rmpc_create(const rmpc_model* model, const rmpc_settings* settings, int32_t n_agents,
+                    const int32_t* devices, int32_t n_devices, rmpc_handle** out);
+void rmpc_destroy(rmpc_handle* handle);
+
+/* BatchRunner::solve with HOST arrays of length n_agents (rmpc_state/command/gait, and
+ * optionally prev/prev_z_star for warm start).  Blocks until every device finished (the
+ * tick barrier).  Host buffers may be pageable; they are staged through pinned memory.
+ * z_star_out may be NULL. */
+int32_t rmpc_solve(rmpc_handle* handle, const rmpc_state* states, const rmpc_command* cmds,
+                   const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z_star,
+                   rmpc_solution* out, float* z_star_out);
+
+/* Same solve with DEVICE arrays already resident on the handle's single device; enqueued on
+ * `stream` (a cudaStream_t, NULL = the handle's stream) without host synchronisation. */
+int32_t rmpc_solve_device(rmpc_handle* handle, const rmpc_state* d_states,
+                          const rmpc_command* d_cmds, const rmpc_gait* d_gaits,
+                          const rmpc_solution* d_prev, const float* d_prev_z_star,
+                          rmpc_solution* d_out, float* d_z_star_out, void* stream);
+
+int32_t rmpc_size(const rmpc_handle* handle);        /* BatchRunner::size() */
+int32_t rmpc_workers(const rmpc_handle* handle);     /* BatchRunner::workers(): devices */
+int32_t rmpc_horizon(const rmpc_handle* handle);
+int32_t rmpc_last_timing(const rmpc_handle* handle, rmpc_timing* out);  /* last_timing() */
+const char* rmpc_last_error(const rmpc_handle* handle);  /* NULL handle: creation error */
+const char* rmpc_status_message(int32_t status);
+const char* rmpc_stage_name(int32_t stage);              /* mpc_stage_name, mpc.cpp:22-26 */
+
+/* Nominal standing pose of the model (robot.cpp:245-306), FP64 host computation. */
+void rmpc_nominal_pose(const rmpc_model* model, double q_out[RMPC_NQ]);
+
+/* PD + feed-forward torque from a solution (mpc_torque -> pd_torque, mpc.cpp:340-344,
+ * robot.cpp:235-241); returns RMPC_ERR_STRUCTURAL for a failed solution. */
+int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol,
+                        const rmpc_state* state, double tau_out[RMPC_NJ]);
+
+/* Stage-profiling switch: when on, the kernel samples the SM clock at the reference's stage
+ * boundaries and rmpc_last_timing() reports the per-stage split of kernel_ms. */
+int32_t rmpc_set_stage_profiling(rmpc_handle* handle, int32_t enabled);
+
+/* Build provenance: "sm_100a" and the kernel variant compiled in. */
+const char* rmpc_build_info(void);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* RMPC_B200_H_ */

@@ -166,6 +166,12 @@ int32_t rmpc_set_stage_profiling(rmpc_handle* handle, int32_t enabled);
 /* Build provenance: "sm_100a" and the kernel variant compiled in. */
 const char* rmpc_build_info(void);
 
+/* Dynamic shared memory one agent (one warp) needs at `horizon` nodes. */
+int32_t rmpc_smem_bytes(int32_t horizon);
+/* sizeof of the ABI structs (0 model, 1 settings, 2 state, 3 command, 4 gait, 5 solution,
+ * 6 timing) for binding-side layout checks. */
+int32_t rmpc_sizeof(int32_t which);
+
 #ifdef __cplusplus
 }  /* extern "C" */
 #endif

@@ -1,0 +1,107 @@
+// rmpc_device.cuh — launch parameters and shared-memory layout of the fused RTI-MPC kernel.
+//
+// One warp solves one agent (MpcController::rti_step, /root/reference/proj/src/mpc.cpp:248-338)
+// end to end.  The ADMM linear system of the reference (quasi-definite KKT, qp.cpp:11-34, solved
+// by sparse LDL^T, ldl.cpp:123-192) is replaced by its mathematically identical reduced form
+//     (P^ + sigma I + rho A^T A) x~ = sigma x - q^ + A^T (rho z - y),   z~ = A^ x~,
+// which is block tridiagonal over horizon nodes (26 x 26 blocks) and is solved by block
+// elimination with explicit Schur-complement inverses S_i^-1 kept in shared memory.
+// See DESIGN.md for the derivation and the HBM / shared-memory budget.
+#pragma once
+
+#include <stdint.h>
+
+#include "../../include/rmpc_b200.h"
+
+namespace rmpc_dev {
+
+constexpr int NV = 26, NQ = 9, NF = 8, NC = 4, NJ = 6;
+constexpr int MAXT = RMPC_MAX_HORIZON;
+constexpr int SROW = 26;      // S^-1 row stride in floats (LDS.64 rows, conflict-free)
+constexpr int NSLOT = 40;     // constraint-row slots owned by each node
+constexpr int NINIT = 18;     // initial-state rows (node 0 only)
+
+// Row slots of node i (padded universal pattern; unused slots are zero rows with lo=hi=0,
+// an exact ADMM no-op):
+//   [0, 9)   integration rows of interval i      (mpc.cpp:138-148), exist for i < T-1
+//   [9, 12)  base-dynamics rows of interval i     (mpc.cpp:150-175), exist for i < T-1
+//   [12, 28) contact c = (s-12)/4, t = (s-12)%4   (mpc.cpp:181-218)
+//              t0,t1: friction pair (stance) or zero-force rows (swing)
+//              t2,t3: contact-velocity rows (stance, i >= 1) / t2 swing height (i >= 1)
+//   [28, 34) joint position boxes, [34, 40) joint velocity boxes (mpc.cpp:220-232), i >= 1
+// Initial-state rows (mpc.cpp:126-136) are 18 extra slots after all nodes.
+
+// Per-node coefficient block (floats).  Unscaled A values during setup/Ruiz, scaled A^ after.
+constexpr int C_INT = 0;      // [9][4]: a1 (on q_{i+1,k}), a2 (on q_{i,k}), a3 (on qd_{i+1,k}), 0
+constexpr int C_DYNV = 36;    // [3][28]: dynamics row b on node-i vars (q part = 0)
+constexpr int C_DYNU = 120;   // [3][12]: dynamics row b on qd_{i+1,k}
+constexpr int C_FORCE = 156;  // [4][4]: contact c rows t0 (Fx,Fz), t1 (Fx,Fz)
+constexpr int C_JQ = 172;     // [4][9]: row t2 on q_k   (swing height)
+constexpr int C_JV0 = 208;    // [4][9]: row t2 on qd_k  (stance velocity, x axis)
+constexpr int C_JV1 = 244;    // [4][9]: row t3 on qd_k  (stance velocity, z axis)
+constexpr int C_BOX = 280;    // [12]: joint q boxes (6) then qd boxes (6)
+constexpr int C_SIZE = 292;
+
+// Per-node vectors, V_STRIDE floats each.
+constexpr int V_X = 0;    // ADMM x (scaled space)
+constexpr int V_QH = 1;   // q^ = e * q
+constexpr int V_E = 2;    // Ruiz column scale e
+constexpr int V_S = 3;    // forward-sweep s_i, then x~_i
+constexpr int V_PD = 4;   // P^ diagonal
+constexpr int V_NUM = 5;
+constexpr int V_STRIDE = 28;
+
+struct KParams {
+  int32_t NT, n_qp, ruiz_iters, warm_start;
+  int32_t n_agents, profile;
+  double dt[MAXT];
+  double wq[NQ], wqd[NQ], wf[NF];
+  double z_swing, v_to, v_td;
+  double mu, sigma, rho, alpha;
+  double m_link[7], I_link[7];
+  double torso_len, thigh_len, shank_len, foot_half, ankle_drop, gravity;
+  double jlo[NJ], jhi[NJ], qdlim[NJ];
+  double nominal[NQ];
+  double weight;  // total mass * gravity
+  const rmpc_state* states;
+  const rmpc_command* cmds;
+  const rmpc_gait* gaits;
+  const rmpc_solution* prev;
+  const float* prev_z;
+  rmpc_solution* out;
+  float* z_out;
+  unsigned long long* prof;  // [RMPC_NUM_STAGES] cycle accumulators (profile only)
+};
+
+// Shared-memory footprint of one warp (one agent) in floats, every region 16-byte aligned.
+struct Layout {
+  int sinv, coef, vec, row, dsc, icoef, tbuf, bc, g, flags, total;
+};
+
+__host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
+
+__host__ __device__ inline Layout make_layout(int NT) {
+  Layout L;
+  int o = 0;
+  L.sinv = o;  o += align4(NT * NV * SROW);
+  L.coef = o;  o += align4(NT * C_SIZE);
+  L.vec = o;   o += align4(NT * V_NUM * V_STRIDE);
+  L.row = o;   o += 4 * (NT * NSLOT + NINIT);       // float4 {lo, hi, z, y}
+  L.dsc = o;   o += align4(NT * NSLOT + NINIT);     // Ruiz row scale d
+  L.icoef = o; o += align4(NINIT);
+  L.tbuf = o;  o += 2 * 64;                         // t = rho z - y, double-buffered by node
+  L.bc = o;    o += 64;                             // broadcast buffers (2 x 32)
+  L.g = o;     o += 256;                            // [0, 96) scratch, [96, 252) G (12 x 13)
+  L.flags = o; o += align4(NT);
+  L.total = o;
+  return L;
+}
+
+inline int smem_bytes(int NT) { return make_layout(NT).total * 4; }
+
+}  // namespace rmpc_dev
+
+// Launch the fused kernel for params.n_agents agents on `stream` (implemented in
+// rmpc_kernel.cu).  Returns a cudaError_t value.
+int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream);
+int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory

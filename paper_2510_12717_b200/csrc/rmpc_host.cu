@@ -1,0 +1,502 @@
+// rmpc_host.cu — host runtime behind the C ABI (include/rmpc_b200.h).
+//
+// BatchRunner (/root/reference/proj/src/batch.cpp:17-79) becomes a handle owning, per device,
+// a contiguous agent shard, a stream, device buffers and pinned staging buffers.  A solve
+// enqueues H2D copies, the fused kernel and D2H copies on every shard's stream (one host
+// thread per device when several are used) and blocks until all shards finished: the tick
+// barrier of SPEC.md's batch_runtime.  There is no collective: agents are independent.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <chrono>
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <mutex>
+#include <string>
+#include <thread>
+#include <vector>
+
+#include "rmpc_device.cuh"
+
+namespace {
+
+thread_local std::string g_create_error;
+
+struct Shard {
+  int device = 0;
+  int begin = 0, count = 0;
+  cudaStream_t stream = nullptr;
+  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  rmpc_state* d_states = nullptr;
+  rmpc_command* d_cmds = nullptr;
+  rmpc_gait* d_gaits = nullptr;
+  rmpc_solution* d_prev = nullptr;
+  float* d_prev_z = nullptr;
+  rmpc_solution* d_out = nullptr;
+  float* d_z = nullptr;
+  unsigned long long* d_prof = nullptr;
+  // pinned staging for pageable caller buffers
+  char* h_stage_in = nullptr;
+  char* h_stage_out = nullptr;
+  size_t stage_in_bytes = 0, stage_out_bytes = 0;
+  double h2d_ms = 0, kernel_ms = 0, d2h_ms = 0;
+  unsigned long long prof[RMPC_NUM_STAGES] = {0};
+  int err = 0;
+  std::string msg;
+};
+
+}  // namespace
+
+struct rmpc_handle {
+  rmpc_model model;
+  rmpc_settings settings;
+  int n = 0;
+  int NT = 0;
+  double nominal[RMPC_NQ];
+  std::vector<Shard> shards;
+  rmpc_timing timing;
+  std::string err;
+  int profile = 0;
+};
+
+namespace {
+
+// ---------------------------------------------------------------- host model helpers (FP64)
+struct P2 {
+  double x, z;
+};
+
+// Standing pose (robot.cpp:245-306): per-leg 2-link IK for a flat foot with the ankles at
+// +-stagger around a shift that is iterated until the CoM is over the contact centroid.
+void nominal_pose_host(const rmpc_model& p, double q[RMPC_NQ]) {
+  auto leg = [&](double x_off, double out[3]) {
+    const double l1 = p.thigh_len, l2 = p.shank_len;
+    const double r = std::hypot(x_off, p.nominal_drop);
+    const double ck = std::min(1.0, std::max(-1.0, (r * r - l1 * l1 - l2 * l2) / (2.0 * l1 * l2)));
+    const double knee = std::acos(ck);
+    const double thigh = std::atan2(x_off, p.nominal_drop) - std::atan2(l2 * std::sin(knee), l1 + l2 * std::cos(knee));
+    out[0] = thigh;
+    out[1] = knee;
+    out[2] = -(thigh + knee);
+  };
+  const double m[7] = {p.torso_mass, p.thigh_mass, p.shank_mass, p.foot_mass,
+                       p.thigh_mass, p.shank_mass, p.foot_mass};
+  double shift = 0.0;
+  for (int it = 0; it < 60; ++it) {
+    double L[3], R[3];
+    leg(shift + p.nominal_stagger, L);
+    leg(shift - p.nominal_stagger, R);
+    q[0] = 0.0;
+    q[1] = p.ankle_drop + p.nominal_drop + 0.5 * p.torso_len;
+    q[2] = 0.0;
+    for (int k = 0; k < 3; ++k) { q[3 + k] = L[k]; q[6 + k] = R[k]; }
+    // CoM x of the 7 links at zero velocity
+    const P2 hip{0.0, q[1] - 0.5 * p.torso_len};
+    double cx = m[0] * 0.0, tot = m[0];
+    for (int lg = 0; lg < 2; ++lg) {
+      const double* a = lg == 0 ? L : R;
+      const double a1 = a[0], a2 = a1 + a[1], a3 = a2 + a[2];
+      auto pt = [](P2 f, double ang, double x, double z) {
+        return P2{f.x + std::cos(ang) * x - std::sin(ang) * z, f.z + std::sin(ang) * x + std::cos(ang) * z};
+      };
+      const P2 knee = pt(hip, a1, 0.0, -p.thigh_len);
+      const P2 ankle = pt(knee, a2, 0.0, -p.shank_len);
+      cx += m[1] * pt(hip, a1, 0.0, -0.5 * p.thigh_len).x;
+      cx += m[2] * pt(knee, a2, 0.0, -0.5 * p.shank_len).x;
+      cx += m[3] * pt(ankle, a3, 0.0, -p.ankle_drop).x;
+      tot += m[1] + m[2] + m[3];
+    }
+    cx /= tot;
+    if (std::abs(cx - shift) < 1e-14) break;
+    shift = cx;
+  }
+}
+
+rmpc_dev::KParams make_params(const rmpc_handle& h) {
+  rmpc_dev::KParams P;
+  std::memset(&P, 0, sizeof(P));
+  const rmpc_settings& s = h.settings;
+  const rmpc_model& m = h.model;
+  P.NT = s.horizon;
+  P.n_qp = s.n_qp;
+  P.ruiz_iters = s.ruiz_iters;
+  P.warm_start = s.warm_start;
+  for (int i = 0; i < RMPC_MAX_HORIZON; ++i) P.dt[i] = s.dt_schedule[i];
+  for (int k = 0; k < RMPC_NQ; ++k) { P.wq[k] = s.w_q[k]; P.wqd[k] = s.w_qd[k]; P.nominal[k] = h.nominal[k]; }
+  for (int k = 0; k < RMPC_NF; ++k) P.wf[k] = s.w_f[k];
+  P.z_swing = s.z_swing; P.v_to = s.v_to; P.v_td = s.v_td;
+  P.mu = s.mu; P.sigma = s.sigma; P.rho = s.rho; P.alpha = s.over_relax;
+  const double ml[7] = {m.torso_mass, m.thigh_mass, m.shank_mass, m.foot_mass, m.thigh_mass, m.shank_mass, m.foot_mass};
+  const double il[7] = {m.torso_inertia, m.thigh_inertia, m.shank_inertia, m.foot_inertia,
+                        m.thigh_inertia, m.shank_inertia, m.foot_inertia};
+  for (int l = 0; l < 7; ++l) { P.m_link[l] = ml[l]; P.I_link[l] = il[l]; }
+  P.torso_len = m.torso_len; P.thigh_len = m.thigh_len; P.shank_len = m.shank_len;
+  P.foot_half = m.foot_half_len; P.ankle_drop = m.ankle_drop; P.gravity = m.gravity;
+  for (int j = 0; j < RMPC_NJ; ++j) { P.jlo[j] = m.joint_lo[j]; P.jhi[j] = m.joint_hi[j]; P.qdlim[j] = m.qd_limit[j]; }
+  double tm = 0.0;
+  for (double v : ml) tm += v;
+  P.weight = tm * m.gravity;
+  P.profile = h.profile;
+  return P;
+}
+
+#define CK(expr)                                                   \
+  do {                                                             \
+    cudaError_t e_ = (expr);                                       \
+    if (e_ != cudaSuccess) {                                       \
+      sh.err = RMPC_ERR_CUDA;                                      \
+      sh.msg = std::string(#expr) + ": " + cudaGetErrorString(e_); \
+      return;                                                      \
+    }                                                              \
+  } while (0)
+
+bool is_pinned(const void* p) {
+  if (!p) return true;
+  cudaPointerAttributes a;
+  if (cudaPointerGetAttributes(&a, p) != cudaSuccess) {
+    cudaGetLastError();
+    return false;
+  }
+  return a.type == cudaMemoryTypeHost;
+}
+
+void alloc_shard(rmpc_handle& h, Shard& sh) {
+  CK(cudaSetDevice(sh.device));
+  CK(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+  for (auto& e : sh.ev) CK(cudaEventCreate(&e));
+  const size_t n = std::max(sh.count, 1);
+  const size_t zn = n * h.NT * RMPC_NV;
+  CK(cudaMalloc(&sh.d_states, n * sizeof(rmpc_state)));
+  CK(cudaMalloc(&sh.d_cmds, n * sizeof(rmpc_command)));
+  CK(cudaMalloc(&sh.d_gaits, n * sizeof(rmpc_gait)));
+  CK(cudaMalloc(&sh.d_prev, n * sizeof(rmpc_solution)));
+  CK(cudaMalloc(&sh.d_prev_z, zn * sizeof(float)));
+  CK(cudaMalloc(&sh.d_out, n * sizeof(rmpc_solution)));
+  CK(cudaMalloc(&sh.d_z, zn * sizeof(float)));
+  CK(cudaMalloc(&sh.d_prof, RMPC_NUM_STAGES * sizeof(unsigned long long)));
+  sh.stage_in_bytes = n * (sizeof(rmpc_state) + sizeof(rmpc_command) + sizeof(rmpc_gait) + sizeof(rmpc_solution)) +
+                      zn * sizeof(float) + 8 * 256;  // 256-byte aligned sub-buffers
+  sh.stage_out_bytes = n * sizeof(rmpc_solution) + zn * sizeof(float) + 2 * 256;
+  CK(cudaMallocHost(&sh.h_stage_in, sh.stage_in_bytes));
+  CK(cudaMallocHost(&sh.h_stage_out, sh.stage_out_bytes));
+  const int rc = rmpc_kernel_setup(rmpc_dev::MAXT);
+  if (rc != 0) {
+    sh.err = RMPC_ERR_CUDA;
+    sh.msg = std::string("cudaFuncSetAttribute: ") + cudaGetErrorString((cudaError_t)rc);
+  }
+}
+
+void free_shard(Shard& sh) {
+  cudaSetDevice(sh.device);
+  if (sh.stream) cudaStreamSynchronize(sh.stream);
+  cudaFree(sh.d_states); cudaFree(sh.d_cmds); cudaFree(sh.d_gaits); cudaFree(sh.d_prev);
+  cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof);
+  cudaFreeHost(sh.h_stage_in); cudaFreeHost(sh.h_stage_out);
+  for (auto& e : sh.ev) if (e) cudaEventDestroy(e);
+  if (sh.stream) cudaStreamDestroy(sh.stream);
+}
+
+// H2D (staging pageable buffers through pinned memory), kernel, D2H, synchronize.
+void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
+               const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z,
+               rmpc_solution* out, float* z_out) {
+  sh.err = 0;
+  if (sh.count == 0) return;
+  CK(cudaSetDevice(sh.device));
+  const size_t n = sh.count, b = sh.begin;
+  const size_t zrow = (size_t)h.NT * RMPC_NV;
+  const bool use_prev = h.settings.warm_start && prev && prev_z;
+  struct In {
+    const void* src;
+    void* dst;
+    size_t bytes;
+  };
+  std::vector<In> ins = {{states + b, sh.d_states, n * sizeof(rmpc_state)},
+                         {cmds + b, sh.d_cmds, n * sizeof(rmpc_command)},
+                         {gaits + b, sh.d_gaits, n * sizeof(rmpc_gait)}};
+  if (use_prev) {
+    ins.push_back({prev + b, sh.d_prev, n * sizeof(rmpc_solution)});
+    ins.push_back({prev_z + b * zrow, sh.d_prev_z, n * zrow * sizeof(float)});
+  }
+  CK(cudaEventRecord(sh.ev[0], sh.stream));
+  size_t off = 0;
+  for (const In& c : ins) {
+    const void* src = c.src;
+    if (!is_pinned(c.src)) {
+      std::memcpy(sh.h_stage_in + off, c.src, c.bytes);
+      src = sh.h_stage_in + off;
+      off += (c.bytes + 255) & ~size_t(255);
+    }
+    CK(cudaMemcpyAsync(c.dst, src, c.bytes, cudaMemcpyHostToDevice, sh.stream));
+  }
+  CK(cudaEventRecord(sh.ev[1], sh.stream));
+  rmpc_dev::KParams P = make_params(h);
+  P.n_agents = sh.count;
+  P.states = sh.d_states;
+  P.cmds = sh.d_cmds;
+  P.gaits = sh.d_gaits;
+  P.prev = use_prev ? sh.d_prev : nullptr;
+  P.prev_z = use_prev ? sh.d_prev_z : nullptr;
+  P.out = sh.d_out;
+  P.z_out = z_out ? sh.d_z : nullptr;
+  P.prof = sh.d_prof;
+  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, RMPC_NUM_STAGES * sizeof(unsigned long long), sh.stream));
+  const int rc = rmpc_launch_rti(P, sh.stream);
+  if (rc != 0) {
+    sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+    sh.msg = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    return;
+  }
+  CK(cudaEventRecord(sh.ev[2], sh.stream));
+  const bool out_pinned = is_pinned(out), z_pinned = is_pinned(z_out);
+  rmpc_solution* out_dst = out_pinned ? out + b : reinterpret_cast<rmpc_solution*>(sh.h_stage_out);
+  CK(cudaMemcpyAsync(out_dst, sh.d_out, n * sizeof(rmpc_solution), cudaMemcpyDeviceToHost, sh.stream));
+  float* z_dst = nullptr;
+  if (z_out) {
+    z_dst = z_pinned ? z_out + b * zrow
+                     : reinterpret_cast<float*>(sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255)));
+    CK(cudaMemcpyAsync(z_dst, sh.d_z, n * zrow * sizeof(float), cudaMemcpyDeviceToHost, sh.stream));
+  }
+  if (h.profile)
+    CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, sh.stream));
+  CK(cudaEventRecord(sh.ev[3], sh.stream));
+  CK(cudaStreamSynchronize(sh.stream));
+  if (!out_pinned) std::memcpy(out + b, out_dst, n * sizeof(rmpc_solution));
+  if (z_out && !z_pinned) std::memcpy(z_out + b * zrow, z_dst, n * zrow * sizeof(float));
+  float t01 = 0, t12 = 0, t23 = 0;
+  cudaEventElapsedTime(&t01, sh.ev[0], sh.ev[1]);
+  cudaEventElapsedTime(&t12, sh.ev[1], sh.ev[2]);
+  cudaEventElapsedTime(&t23, sh.ev[2], sh.ev[3]);
+  sh.h2d_ms = t01;
+  sh.kernel_ms = t12;
+  sh.d2h_ms = t23;
+}
+
+void fill_timing(rmpc_handle& h, double total_ms) {
+  rmpc_timing& t = h.timing;
+  std::memset(&t, 0, sizeof(t));
+  t.batch_size = h.n;
+  t.devices = (int)h.shards.size();
+  t.total_ms = total_ms;
+  unsigned long long prof[RMPC_NUM_STAGES] = {0};
+  for (const Shard& sh : h.shards) {
+    t.h2d_ms = std::max(t.h2d_ms, sh.h2d_ms);
+    t.kernel_ms = std::max(t.kernel_ms, sh.kernel_ms);
+    t.d2h_ms = std::max(t.d2h_ms, sh.d2h_ms);
+    for (int s = 0; s < RMPC_NUM_STAGES; ++s) prof[s] += sh.prof[s];
+  }
+  if (h.profile) {
+    double tot = 0;
+    for (int s = 0; s < RMPC_NUM_STAGES; ++s) tot += (double)prof[s];
+    if (tot > 0)
+      for (int s = 0; s < RMPC_NUM_STAGES; ++s) t.stage_ms[s] = t.kernel_ms * (double)prof[s] / tot;
+  }
+}
+
+}  // namespace
+
+extern "C" {
+
+void rmpc_model_default(rmpc_model* p) {
+  std::memset(p, 0, sizeof(*p));
+  p->torso_mass = 10.0; p->torso_len = 0.4; p->torso_inertia = 10.0 * 0.4 * 0.4 / 12.0;
+  p->thigh_mass = 2.5; p->thigh_len = 0.4; p->thigh_inertia = 2.5 * 0.4 * 0.4 / 12.0;
+  p->shank_mass = 1.5; p->shank_len = 0.4; p->shank_inertia = 1.5 * 0.4 * 0.4 / 12.0;
+  p->foot_mass = 0.5; p->foot_half_len = 0.09; p->foot_inertia = 0.5 * 0.18 * 0.18 / 12.0;
+  p->ankle_drop = 0.05;
+  const double lo[6] = {-1.5, 0.05, -1.2, -1.5, 0.05, -1.2}, hi[6] = {1.5, 2.4, 1.2, 1.5, 2.4, 1.2};
+  const double tl[6] = {60.0, 60.0, 30.0, 60.0, 60.0, 30.0};
+  for (int j = 0; j < 6; ++j) {
+    p->joint_lo[j] = lo[j]; p->joint_hi[j] = hi[j]; p->qd_limit[j] = 20.0;
+    p->tau_limit[j] = tl[j]; p->kp[j] = 30.0; p->kd[j] = 1.0;
+  }
+  p->mu = 0.8; p->gravity = 9.81; p->nominal_stagger = 0.15; p->nominal_drop = 0.75;
+}
+
+void rmpc_settings_default(rmpc_settings* s, int32_t horizon) {
+  std::memset(s, 0, sizeof(*s));
+  s->horizon = horizon;
+  for (int i = 0; i < RMPC_MAX_HORIZON; ++i) s->dt_schedule[i] = i < horizon ? 0.05 : 0.0;
+  const double wq[9] = {0.0, 500.0, 300.0, 5.0, 5.0, 5.0, 5.0, 5.0, 5.0};
+  const double wqd[9] = {100.0, 100.0, 50.0, 0.1, 0.1, 0.1, 0.1, 0.1, 0.1};
+  for (int k = 0; k < 9; ++k) { s->w_q[k] = wq[k]; s->w_qd[k] = wqd[k]; }
+  for (int k = 0; k < 8; ++k) s->w_f[k] = 1e-3;
+  s->gait_period = 0.8; s->phase_switch = 0.5;
+  s->phase_offsets[0] = 0.5; s->phase_offsets[1] = 0.5; s->phase_offsets[2] = 0.0; s->phase_offsets[3] = 0.0;
+  s->z_swing = 0.075; s->v_to = 0.2; s->v_td = -0.3;
+  s->n_qp = 25; s->mu = 0.6; s->sigma = 1e-6; s->rho = 0.1; s->over_relax = 1.6;
+  s->warm_start = 0; s->ruiz_iters = 10;
+}
+
+void rmpc_nominal_pose(const rmpc_model* model, double q_out[RMPC_NQ]) { nominal_pose_host(*model, q_out); }
+
+int32_t rmpc_create(const rmpc_model* model, const rmpc_settings* settings, int32_t n_agents,
+                    const int32_t* devices, int32_t n_devices, rmpc_handle** out) {
+  if (!out || !model || !settings) { g_create_error = "rmpc_create: NULL argument"; return RMPC_ERR_INVALID_ARG; }
+  *out = nullptr;
+  if (n_agents < 1) { g_create_error = "BatchRunner: n_envs must be >= 1"; return RMPC_ERR_STRUCTURAL; }
+  if (settings->horizon < 2) { g_create_error = "MpcController: horizon must be >= 2"; return RMPC_ERR_STRUCTURAL; }
+  if (settings->horizon > RMPC_MAX_HORIZON) { g_create_error = "MpcController: horizon > RMPC_MAX_HORIZON"; return RMPC_ERR_STRUCTURAL; }
+  if (settings->n_qp < 1) { g_create_error = "AdmmSolver: n_iters must be >= 1"; return RMPC_ERR_STRUCTURAL; }
+  for (int i = 0; i < settings->horizon; ++i)
+    if (!(settings->dt_schedule[i] > 0.0)) { g_create_error = "MpcController: dt_schedule entries must be > 0"; return RMPC_ERR_STRUCTURAL; }
+  int ndev = 0;
+  if (cudaGetDeviceCount(&ndev) != cudaSuccess || ndev == 0) {
+    cudaGetLastError();
+    g_create_error = "rmpc_create: no CUDA device";
+    return RMPC_ERR_CUDA;
+  }
+  std::vector<int> devs;
+  if (devices && n_devices > 0) devs.assign(devices, devices + n_devices);
+  else devs.push_back(0);
+  for (int d : devs)
+    if (d < 0 || d >= ndev) { g_create_error = "rmpc_create: device index out of range"; return RMPC_ERR_INVALID_ARG; }
+  rmpc_handle* h = new rmpc_handle();
+  h->model = *model;
+  h->settings = *settings;
+  h->n = n_agents;
+  h->NT = settings->horizon;
+  nominal_pose_host(*model, h->nominal);
+  std::memset(&h->timing, 0, sizeof(h->timing));
+  const int G = (int)devs.size();
+  h->shards.resize(G);
+  for (int g = 0; g < G; ++g) {  // contiguous ranges [g n / G, (g+1) n / G)
+    Shard& sh = h->shards[g];
+    sh.device = devs[g];
+    sh.begin = (int)((long long)g * n_agents / G);
+    sh.count = (int)((long long)(g + 1) * n_agents / G) - sh.begin;
+    alloc_shard(*h, sh);
+    if (sh.err) {
+      g_create_error = sh.msg;
+      for (int k = 0; k <= g; ++k) free_shard(h->shards[k]);
+      delete h;
+      return RMPC_ERR_CUDA;
+    }
+  }
+  *out = h;
+  return RMPC_OK;
+}
+
+void rmpc_destroy(rmpc_handle* h) {
+  if (!h) return;
+  for (Shard& sh : h->shards) free_shard(sh);
+  delete h;
+}
+
+int32_t rmpc_solve(rmpc_handle* h, const rmpc_state* states, const rmpc_command* cmds, const rmpc_gait* gaits,
+                   const rmpc_solution* prev, const float* prev_z_star, rmpc_solution* out, float* z_star_out) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (!states || !cmds || !gaits || !out) {
+    h->err = "BatchRunner::solve: input lengths != n_envs (NULL array)";
+    return RMPC_ERR_STRUCTURAL;
+  }
+  const auto t0 = std::chrono::steady_clock::now();
+  if (h->shards.size() == 1) {
+    run_shard(*h, h->shards[0], states, cmds, gaits, prev, prev_z_star, out, z_star_out);
+  } else {
+    std::vector<std::thread> pool;
+    for (Shard& sh : h->shards)
+      pool.emplace_back([&, ptr = &sh]() { run_shard(*h, *ptr, states, cmds, gaits, prev, prev_z_star, out, z_star_out); });
+    for (auto& t : pool) t.join();
+  }
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  for (const Shard& sh : h->shards)
+    if (sh.err) { h->err = sh.msg; return sh.err; }
+  fill_timing(*h, ms);
+  return RMPC_OK;
+}
+
+int32_t rmpc_solve_device(rmpc_handle* h, const rmpc_state* d_states, const rmpc_command* d_cmds,
+                          const rmpc_gait* d_gaits, const rmpc_solution* d_prev, const float* d_prev_z_star,
+                          rmpc_solution* d_out, float* d_z_star_out, void* stream) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (h->shards.size() != 1) { h->err = "rmpc_solve_device: single-device handles only"; return RMPC_ERR_INVALID_ARG; }
+  if (!d_states || !d_cmds || !d_gaits || !d_out) { h->err = "rmpc_solve_device: NULL array"; return RMPC_ERR_STRUCTURAL; }
+  Shard& sh = h->shards[0];
+  cudaSetDevice(sh.device);
+  rmpc_dev::KParams P = make_params(*h);
+  P.n_agents = h->n;
+  P.states = d_states;
+  P.cmds = d_cmds;
+  P.gaits = d_gaits;
+  const bool use_prev = h->settings.warm_start && d_prev && d_prev_z_star;
+  P.prev = use_prev ? d_prev : nullptr;
+  P.prev_z = use_prev ? d_prev_z_star : nullptr;
+  P.out = d_out;
+  P.z_out = d_z_star_out;
+  P.prof = sh.d_prof;
+  P.profile = 0;
+  const int rc = rmpc_launch_rti(P, stream ? stream : (void*)sh.stream);
+  if (rc != 0) {
+    h->err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+  }
+  return RMPC_OK;
+}
+
+int32_t rmpc_size(const rmpc_handle* h) { return h ? h->n : 0; }
+int32_t rmpc_workers(const rmpc_handle* h) { return h ? (int32_t)h->shards.size() : 0; }
+int32_t rmpc_horizon(const rmpc_handle* h) { return h ? h->NT : 0; }
+
+int32_t rmpc_last_timing(const rmpc_handle* h, rmpc_timing* out) {
+  if (!h || !out) return RMPC_ERR_INVALID_ARG;
+  *out = h->timing;
+  return RMPC_OK;
+}
+
+const char* rmpc_last_error(const rmpc_handle* h) { return h ? h->err.c_str() : g_create_error.c_str(); }
+
+const char* rmpc_status_message(int32_t status) {
+  switch (status) {
+    case RMPC_STATUS_OK: return "ok";
+    case RMPC_STATUS_NONFINITE_INPUT: return "build_qp: non-finite linearization point";
+    case RMPC_STATUS_DIVERGED: return "admm: non-finite iterate";
+    case RMPC_STATUS_SINGULAR: return "factorization: non-positive pivot";
+    default: return "unknown status";
+  }
+}
+
+const char* rmpc_stage_name(int32_t stage) {
+  static const char* names[RMPC_NUM_STAGES] = {"init_guess", "param", "kkt_build", "ruiz",
+                                               "factorize", "admm_iters", "rnea"};
+  return (stage >= 0 && stage < RMPC_NUM_STAGES) ? names[stage] : "unknown";
+}
+
+int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol, const rmpc_state* state,
+                        double tau_out[RMPC_NJ]) {
+  if (!model || !sol || !state || !tau_out) return RMPC_ERR_INVALID_ARG;
+  if (sol->status != RMPC_STATUS_OK) return RMPC_ERR_STRUCTURAL;  // mpc.cpp:341-342
+  for (int j = 0; j < RMPC_NJ; ++j) {  // robot.cpp:235-241
+    const double t = model->kp[j] * ((double)sol->q_set[j] - state->q[3 + j]) +
+                     model->kd[j] * ((double)sol->qd_set[j] - state->qd[3 + j]) + (double)sol->tau_ff[j];
+    tau_out[j] = std::min(std::max(t, -model->tau_limit[j]), model->tau_limit[j]);
+  }
+  return RMPC_OK;
+}
+
+int32_t rmpc_set_stage_profiling(rmpc_handle* h, int32_t enabled) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  h->profile = enabled ? 1 : 0;
+  return RMPC_OK;
+}
+
+const char* rmpc_build_info(void) {
+  return "rmpc_b200 sm_100a fused warp-per-agent RTI kernel (reduced SPD block-tridiagonal ADMM, FP32 + FP64 linearization)";
+}
+
+int32_t rmpc_smem_bytes(int32_t horizon) { return rmpc_dev::smem_bytes(horizon); }
+int32_t rmpc_sizeof(int32_t which) {
+  switch (which) {
+    case 0: return (int32_t)sizeof(rmpc_model);
+    case 1: return (int32_t)sizeof(rmpc_settings);
+    case 2: return (int32_t)sizeof(rmpc_state);
+    case 3: return (int32_t)sizeof(rmpc_command);
+    case 4: return (int32_t)sizeof(rmpc_gait);
+    case 5: return (int32_t)sizeof(rmpc_solution);
+    case 6: return (int32_t)sizeof(rmpc_timing);
+    default: return -1;
+  }
+}
+
+}  // extern "C"

@@ -1,0 +1,209 @@
+"""ctypes binding of lib/librmpc_b200.so and the BatchRunner mirror.
+
+BatchRunner keeps the reference's method names and argument order
+(/root/reference/proj/include/rmpc/batch.hpp:24-46):
+    BatchRunner(n_envs, model, settings, workers=0)   # workers -> number of GPUs
+    solve(states, cmds, gaits, prev=None, order=None) -> solutions
+    size(), workers(), last_timing()
+Batches are numpy arrays whose rows are the C structs (abi.py); solutions come back as a
+numpy structured array with SOLUTION_DTYPE (rmpc_solution).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+from .abi import (NV, RMPC_ERR_STRUCTURAL, SOLUTION_DTYPE, STAGE_NAMES, Model, Settings, Timing,
+                  default_model, default_settings)
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "lib", "librmpc_b200.so")
+_lib = None
+
+_VP = C.c_void_p
+_I = C.c_int32
+
+EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_destroy",
+           "rmpc_solve", "rmpc_solve_device", "rmpc_size", "rmpc_workers", "rmpc_horizon",
+           "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
+           "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
+           "rmpc_smem_bytes", "rmpc_sizeof")
+
+
+class RmpcError(RuntimeError):
+    def __init__(self, code: int, message: str):
+        super().__init__(f"rmpc error {code}: {message}")
+        self.code = code
+
+
+def load_library(path: str | None = None, build_if_missing: bool = True):
+    """Load (and if needed build) the sm_100a library; raises if it cannot be loaded."""
+    path = path or LIB_PATH
+    if not os.path.exists(path):
+        if not build_if_missing:
+            raise OSError(f"{path} missing: run paper_2510_12717_b200/build.py")
+        from .build import build
+        build()
+    L = C.CDLL(path)
+    L.rmpc_create.argtypes = [_VP, _VP, _I, C.POINTER(_I), _I, C.POINTER(_VP)]
+    L.rmpc_create.restype = _I
+    L.rmpc_destroy.argtypes = [_VP]
+    L.rmpc_destroy.restype = None
+    L.rmpc_solve.argtypes = [_VP] * 8
+    L.rmpc_solve.restype = _I
+    L.rmpc_solve_device.argtypes = [_VP] * 9
+    L.rmpc_solve_device.restype = _I
+    for f in ("rmpc_size", "rmpc_workers", "rmpc_horizon"):
+        getattr(L, f).argtypes = [_VP]
+        getattr(L, f).restype = _I
+    L.rmpc_last_timing.argtypes = [_VP, _VP]
+    L.rmpc_last_timing.restype = _I
+    L.rmpc_last_error.argtypes = [_VP]
+    L.rmpc_last_error.restype = C.c_char_p
+    L.rmpc_status_message.argtypes = [_I]
+    L.rmpc_status_message.restype = C.c_char_p
+    L.rmpc_stage_name.argtypes = [_I]
+    L.rmpc_stage_name.restype = C.c_char_p
+    L.rmpc_nominal_pose.argtypes = [_VP, _VP]
+    L.rmpc_mpc_torque.argtypes = [_VP, _VP, _VP, _VP]
+    L.rmpc_mpc_torque.restype = _I
+    L.rmpc_set_stage_profiling.argtypes = [_VP, _I]
+    L.rmpc_set_stage_profiling.restype = _I
+    L.rmpc_build_info.restype = C.c_char_p
+    L.rmpc_smem_bytes.argtypes = [_I]
+    L.rmpc_smem_bytes.restype = _I
+    L.rmpc_sizeof.argtypes = [_I]
+    L.rmpc_sizeof.restype = _I
+    return L
+
+
+def library():
+    global _lib
+    if _lib is None:
+        _lib = load_library()
+    return _lib
+
+
+def _arr(a, cols, dtype=np.float64):
+    a = np.ascontiguousarray(a, dtype=dtype)
+    if a.ndim == 1:
+        a = a.reshape(1, -1)
+    if a.shape[1] != cols:
+        raise ValueError(f"expected rows of {cols} values, got shape {a.shape}")
+    return a
+
+
+def nominal_pose(model: Model | None = None) -> np.ndarray:
+    q = np.zeros(9)
+    library().rmpc_nominal_pose(C.byref(model or default_model()), q.ctypes.data)
+    return q
+
+
+class BatchRunner:
+    """rmpc::BatchRunner on B200: n_envs independent RTI-MPC instances per solve."""
+
+    def __init__(self, n_envs: int, model: Model | None = None, settings: Settings | None = None,
+                 workers: int = 0, devices=None):
+        self._lib = library()
+        self.model = model if model is not None else default_model()
+        self.settings = settings if settings is not None else default_settings()
+        if devices is None:
+            devices = list(range(workers)) if workers > 0 else [0]
+        devs = (_I * len(devices))(*devices)
+        h = _VP()
+        rc = self._lib.rmpc_create(C.byref(self.model), C.byref(self.settings), int(n_envs), devs,
+                                   len(devices), C.byref(h))
+        if rc != 0:
+            raise RmpcError(rc, self._lib.rmpc_last_error(None).decode())
+        self._h = h
+        self._n = int(n_envs)
+        self.horizon = int(self.settings.horizon)
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.rmpc_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def size(self) -> int:
+        return self._lib.rmpc_size(self._h)
+
+    def workers(self) -> int:
+        return self._lib.rmpc_workers(self._h)
+
+    def _err(self, rc):
+        raise RmpcError(rc, self._lib.rmpc_last_error(self._h).decode())
+
+    def solve(self, states, cmds, gaits, prev=None, order=None, *, want_z: bool = False,
+              out: np.ndarray | None = None, z_out: np.ndarray | None = None):
+        """BatchRunner::solve.  states (n,18), cmds (n,3), gaits (n,7) float64; prev =
+        (solutions, z_star) of the previous tick (read only when settings.warm_start).  `order`
+        is accepted for API parity: results never depend on processing order.  Returns
+        (solutions, z_star or None)."""
+        del order
+        states, cmds, gaits = _arr(states, 18), _arr(cmds, 3), _arr(gaits, 7)
+        n = self._n
+        if states.shape[0] != n or cmds.shape[0] != n or gaits.shape[0] != n:
+            raise RmpcError(RMPC_ERR_STRUCTURAL, "BatchRunner::solve: input lengths != n_envs")
+        if out is None:
+            out = np.zeros(n, dtype=SOLUTION_DTYPE)
+        if want_z and z_out is None:
+            z_out = np.zeros((n, self.horizon, NV), dtype=np.float32)
+        pv = pz = None
+        if prev is not None:
+            psol, pzs = prev
+            if len(psol) != n:
+                raise RmpcError(RMPC_ERR_STRUCTURAL, "BatchRunner::solve: prev length != n_envs")
+            pv = np.ascontiguousarray(psol, dtype=SOLUTION_DTYPE)
+            pz = np.ascontiguousarray(pzs, dtype=np.float32)
+        rc = self._lib.rmpc_solve(self._h, states.ctypes.data, cmds.ctypes.data, gaits.ctypes.data,
+                                  pv.ctypes.data if pv is not None else None,
+                                  pz.ctypes.data if pz is not None else None, out.ctypes.data,
+                                  z_out.ctypes.data if z_out is not None else None)
+        if rc != 0:
+            self._err(rc)
+        return out, z_out
+
+    def solve_device(self, states, cmds, gaits, out, z_out=None, prev=None, prev_z=None,
+                     stream=None):
+        """Device-resident solve: arguments are CUDA tensors (or raw device pointers) on this
+        runner's device; enqueued on `stream` (torch.cuda.Stream / cudaStream_t int), no sync."""
+        def p(t):
+            if t is None:
+                return None
+            return t if isinstance(t, int) else t.data_ptr()
+        s = None
+        if stream is not None:
+            s = stream if isinstance(stream, int) else stream.cuda_stream
+        rc = self._lib.rmpc_solve_device(self._h, p(states), p(cmds), p(gaits), p(prev), p(prev_z),
+                                         p(out), p(z_out), s)
+        if rc != 0:
+            self._err(rc)
+
+    def set_stage_profiling(self, enabled: bool = True):
+        self._lib.rmpc_set_stage_profiling(self._h, int(enabled))
+
+    def last_timing(self) -> dict:
+        t = Timing()
+        self._lib.rmpc_last_timing(self._h, C.byref(t))
+        return dict(batch_size=t.batch_size, devices=t.devices, total_ms=t.total_ms,
+                    h2d_ms=t.h2d_ms, kernel_ms=t.kernel_ms, d2h_ms=t.d2h_ms,
+                    stage_ms=dict(zip(STAGE_NAMES, list(t.stage_ms))))
+
+    def mpc_torque(self, solution, state) -> np.ndarray:
+        """mpc_torque (mpc.cpp:340-344): PD + feed-forward, clamped; raises on a failed solve."""
+        sol = np.ascontiguousarray(np.asarray(solution, dtype=SOLUTION_DTYPE).reshape(1))
+        st = _arr(state, 18)
+        tau = np.zeros(6)
+        rc = self._lib.rmpc_mpc_torque(C.byref(self.model), sol.ctypes.data, st.ctypes.data,
+                                       tau.ctypes.data)
+        if rc != 0:
+            raise RmpcError(rc, "mpc_torque: solution status is failed")
+        return tau

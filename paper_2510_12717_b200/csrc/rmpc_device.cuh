@@ -17,9 +17,11 @@ namespace rmpc_dev {
 
 constexpr int NV = 26, NQ = 9, NF = 8, NC = 4, NJ = 6;
 constexpr int MAXT = RMPC_MAX_HORIZON;
-constexpr int SROW = 26;      // S^-1 row stride in floats (LDS.64 rows, conflict-free)
-constexpr int NSLOT = 40;     // constraint-row slots owned by each node
-constexpr int NINIT = 18;     // initial-state rows (node 0 only)
+constexpr int SROW = 26;      // row stride of the S^-1 block (LDS.64 rows, conflict-free)
+constexpr int SROWS = 29;     // 26 rows of S_i^-1, then W_b = S_i^-1 v_b (b = 0..2)
+constexpr int NSLOT = 40;     // constraint-row slots per node block
+constexpr int NINIT = 18;     // initial-state rows
+constexpr int INIT0 = 12;     // initial-state rows live in block -1, slots [12, 30)
 
 // Row slots of node i (padded universal pattern; unused slots are zero rows with lo=hi=0,
 // an exact ADMM no-op):
@@ -27,28 +29,30 @@ constexpr int NINIT = 18;     // initial-state rows (node 0 only)
 //   [9, 12)  base-dynamics rows of interval i     (mpc.cpp:150-175), exist for i < T-1
 //   [12, 28) contact c = (s-12)/4, t = (s-12)%4   (mpc.cpp:181-218)
 //              t0,t1: friction pair (stance) or zero-force rows (swing)
-//              t2,t3: contact-velocity rows (stance, i >= 1) / t2 swing height (i >= 1)
+//              t2: stance x-velocity on qd / swing height on q (i >= 1); t3: stance z-velocity
 //   [28, 34) joint position boxes, [34, 40) joint velocity boxes (mpc.cpp:220-232), i >= 1
-// Initial-state rows (mpc.cpp:126-136) are 18 extra slots after all nodes.
+// Block -1 (before node 0) is all-zero except the 18 initial-state rows (mpc.cpp:126-136) at
+// slots [12, 30); node 0 sees it as its "previous node", so every node has the same pattern.
 
 // Per-node coefficient block (floats).  Unscaled A values during setup/Ruiz, scaled A^ after.
 constexpr int C_INT = 0;      // [9][4]: a1 (on q_{i+1,k}), a2 (on q_{i,k}), a3 (on qd_{i+1,k}), 0
-constexpr int C_DYNV = 36;    // [3][28]: dynamics row b on node-i vars (q part = 0)
-constexpr int C_DYNU = 120;   // [3][12]: dynamics row b on qd_{i+1,k}
-constexpr int C_FORCE = 156;  // [4][4]: contact c rows t0 (Fx,Fz), t1 (Fx,Fz)
-constexpr int C_JQ = 172;     // [4][9]: row t2 on q_k   (swing height)
-constexpr int C_JV0 = 208;    // [4][9]: row t2 on qd_k  (stance velocity, x axis)
-constexpr int C_JV1 = 244;    // [4][9]: row t3 on qd_k  (stance velocity, z axis)
-constexpr int C_BOX = 280;    // [12]: joint q boxes (6) then qd boxes (6)
-constexpr int C_SIZE = 292;
+constexpr int C_DYNV = 36;    // [3][20]: dynamics row b on node-i vars 9..25 (index j - 9)
+constexpr int C_DYNU = 96;    // [3][12]: dynamics row b on qd_{i+1,k}
+constexpr int C_FORCE = 132;  // [4][4]: contact c rows t0 (Fx,Fz), t1 (Fx,Fz)
+constexpr int C_JA = 148;     // [4][9]: row t2: on qd_k (stance) or q_k (swing height)
+constexpr int C_JB = 184;     // [4][9]: row t3 on qd_k (stance; zero for swing)
+constexpr int C_BOX = 220;    // [12]: joint q boxes (6) then qd boxes (6)
+constexpr int C_INIT = 232;   // [18]: initial-state rows (node 0 only, rows in block -1)
+constexpr int C_G = 250;      // [9]: G_bb' = v_b^T S_i^-1 v_b' (dynamics rows)
+constexpr int C_SIZE = 260;
+constexpr int C_ZERO = C_INT + 3;  // an entry that is always 0
 
-// Per-node vectors, V_STRIDE floats each.
+// Per-node vectors, V_STRIDE floats each; [26, 28) are spare (gamma of the forward sweep).
 constexpr int V_X = 0;    // ADMM x (scaled space)
 constexpr int V_QH = 1;   // q^ = e * q
 constexpr int V_E = 2;    // Ruiz column scale e
-constexpr int V_S = 3;    // forward-sweep s_i, then x~_i
-constexpr int V_PD = 4;   // P^ diagonal
-constexpr int V_NUM = 5;
+constexpr int V_S = 3;    // r_i -> s_i -> x~_i -> next r_i
+constexpr int V_NUM = 4;
 constexpr int V_STRIDE = 28;
 
 struct KParams {
@@ -75,7 +79,7 @@ struct KParams {
 
 // Shared-memory footprint of one warp (one agent) in floats, every region 16-byte aligned.
 struct Layout {
-  int sinv, coef, vec, row, dsc, icoef, tbuf, bc, g, flags, total;
+  int sinv, coef, vec, row, dsc, bc, flags, total;
 };
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
@@ -83,15 +87,12 @@ __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 __host__ __device__ inline Layout make_layout(int NT) {
   Layout L;
   int o = 0;
-  L.sinv = o;  o += align4(NT * NV * SROW);
-  L.coef = o;  o += align4(NT * C_SIZE);
-  L.vec = o;   o += align4(NT * V_NUM * V_STRIDE);
-  L.row = o;   o += 4 * (NT * NSLOT + NINIT);       // float4 {lo, hi, z, y}
-  L.dsc = o;   o += align4(NT * NSLOT + NINIT);     // Ruiz row scale d
-  L.icoef = o; o += align4(NINIT);
-  L.tbuf = o;  o += 2 * 64;                         // t = rho z - y, double-buffered by node
+  L.sinv = o;  o += align4(NT * SROWS * SROW);
+  L.coef = o;  o += (NT + 1) * C_SIZE;              // block -1 first
+  L.vec = o;   o += NT * V_NUM * V_STRIDE;
+  L.row = o;   o += 4 * (NT + 1) * NSLOT;           // float4 {lo, hi, z, t = rho z - y}
+  L.dsc = o;   o += (NT + 1) * NSLOT;               // Ruiz row scale d
   L.bc = o;    o += 64;                             // broadcast buffers (2 x 32)
-  L.g = o;     o += 256;                            // [0, 96) scratch, [96, 252) G (12 x 13)
   L.flags = o; o += align4(NT);
   L.total = o;
   return L;

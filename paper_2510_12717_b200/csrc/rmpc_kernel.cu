@@ -3,19 +3,24 @@
 // One warp runs MpcController::rti_step (/root/reference/proj/src/mpc.cpp:248-338) for one
 // agent: gait schedule and cold/warm guess (f_init, gait.cpp:37-99), FP64 linearization of
 // the floating-base dynamics and contacts (robot.cpp:29-195), QP rows (build_qp,
-// mpc.cpp:64-238), 10 Ruiz passes (ruiz.cpp:7-36 via qp.cpp:64-95), factorization, exactly
-// n_qp ADMM iterations (qp.cpp:156-190), unscaled residuals/objective (qp.cpp:192-200), the
-// full step z* = guess + dz and inverse dynamics at node 0 (mpc.cpp:305-330, robot.cpp:211-233).
+// mpc.cpp:64-238), Ruiz passes (ruiz.cpp:7-36 via qp.cpp:64-95), factorization, exactly n_qp
+// ADMM iterations (qp.cpp:156-190), unscaled residuals/objective (qp.cpp:192-200), the full
+// step z* = guess + dz and inverse dynamics at node 0 (mpc.cpp:305-330, robot.cpp:211-233).
 //
-// Linear algebra: instead of the reference's quasi-definite KKT + sparse LDL^T (qp.cpp:11-34,
+// Linear algebra.  Instead of the reference's quasi-definite KKT + sparse LDL^T (qp.cpp:11-34,
 // ldl.cpp:123-192) each iteration solves the reduced SPD system
-//     H x~ = sigma x - q^ + A^T (rho z - y),  H = P^ + sigma I + rho A^T A,  z~ = A^ x~,
+//     H x~ = r,  r = sigma x - q^ + A^T (rho z - y),  H = P^ + sigma I + rho A^T A,  z~ = A^ x~,
 // identical in exact arithmetic (nu = rho (A^ x~ - z) + y eliminates the dual block).  H is
-// block tridiagonal over horizon nodes; it is eliminated node by node with explicit
-// Schur-complement inverses S_i^-1 (26 x 26, shared memory), the off-diagonal blocks
-// C_i = rho A_int/dyn^(i+1)^T A_int/dyn^(i) being applied in their rank-12 factored form.
+// block tridiagonal over horizon nodes; its off-diagonal blocks C_i = rho U_i V_i^T have rank
+// 12 (the 9 integration + 3 dynamics rows of interval i).  Block elimination keeps
+//     S_0 = H_00,  S_{i+1} = H_{i+1,i+1} - rho^2 U_i (V_i^T S_i^-1 V_i) U_i^T
+// with S_i^-1 and W_i = S_i^-1 V_i(dyn) in shared memory, so each iteration is
+//     forward:  u_i = r_i - rho U_{i-1} gamma_{i-1},  s_i = S_i^-1 u_i,  gamma_i = V_i^T s_i
+//     backward: x~_i = s_i - rho [S_i^-1 | W_i] xi_i,   xi_i = diag(a2, 1) U_i^T x~_{i+1}
+// where gamma comes out of the same 29-row matvec as s (rows 26..28 = W^T) and the backward
+// step is a 12-column update: no warp reductions on either recurrence.
 //
-// Precision: gait, guess, linearization, constraint right-hand sides, the objective sum and
+// Precision: gait, guess, linearization, constraint right-hand sides, the objective and the
 // inverse dynamics in FP64; Ruiz, H, S^-1 and the ADMM iterations in FP32.
 #include <cuda_runtime.h>
 #include <math.h>
@@ -30,24 +35,20 @@ namespace rmpc_dev {
 // ------------------------------------------------------------------------- helpers
 struct Sm {
   float* sinv;
-  float* coef;
+  float* coef;  // block -1 at coef, node i at coef + (i + 1) * C_SIZE
   float* vec;
-  float4* row;
+  float4* row;  // block -1 at row, node i at row + (i + 1) * NSLOT
   float* dsc;
-  float* icoef;
-  float* tbuf;
   float* bc;
-  float* g;
   uint32_t* flags;
   int NT;
+  __device__ __forceinline__ float* C(int i) const { return coef + (i + 1) * C_SIZE; }
+  __device__ __forceinline__ float4* R(int i) const { return row + (i + 1) * NSLOT; }
+  __device__ __forceinline__ float* D(int i) const { return dsc + (i + 1) * NSLOT; }
   __device__ __forceinline__ float* V(int i, int which) const {
     return vec + (i * V_NUM + which) * V_STRIDE;
   }
-  __device__ __forceinline__ float* C(int i) const { return coef + i * C_SIZE; }
-  __device__ __forceinline__ float* Sinv(int i) const { return sinv + i * NV * SROW; }
-  __device__ __forceinline__ int ridx(int i, int s) const {
-    return s < NSLOT ? i * NSLOT + s : NT * NSLOT + (s - NSLOT);
-  }
+  __device__ __forceinline__ float* Sinv(int i) const { return sinv + i * SROWS * SROW; }
 };
 
 __device__ __forceinline__ float wsum(float v) {
@@ -81,41 +82,158 @@ struct OpMax {  // max_j |A_rj| v_j  (v = positive Ruiz scales)
 // joints (right foot coords 6..8 for contacts 0,1; left foot 3..5 for contacts 2,3).
 __device__ __forceinline__ int chain_col(int c, int s) { return s < 3 ? s : (c < 2 ? 6 : 3) + s - 3; }
 
-// ------------------------------------------------------------------------- A^ views
-// Row view: for the 40 (+18 at node 0) row slots of node i, out_r = Op_j(A_rj, v_j) with v
-// the per-node vector `which` of nodes i and i+1.  Lane l returns slot l in o0, slot 32+l
-// (l < 8) in o1, init slot l (node 0, l < 18) in o2.
+__device__ __forceinline__ double wcost(const KParams& P, int j) {
+  return j < 9 ? P.wq[j] : (j < 18 ? P.wqd[j - 9] : P.wf[j - 18]);
+}
+
+// Ruiz-scaled P diagonal of node i, var j: w_j dt_i e_j^2 (mpc.cpp:81-103).
+__device__ __forceinline__ float phat(const KParams& P, const Sm& sm, int i, int j) {
+  const float e = sm.V(i, V_E)[j];
+  return (float)(wcost(P, j) * P.dt[i]) * e * e;
+}
+
+// ------------------------------------------------------------------------- column view
+// Every variable j of node i is touched by at most 17 constraint rows, from its own block
+// and from block i-1 (integration/dynamics rows of interval i-1; the initial-state rows in
+// block -1 for node 0).  Lane j keeps the 17 (coefficient offset, row offset) pairs of the
+// universal pattern in registers; absent rows point at a zero coefficient, so the same
+// instruction stream serves every node.  Terms 2..5 are contact row t2 (JA), which acts on
+// q for a swing contact and on qd for a stance contact: a per-node 0/1 multiplier selects.
+struct Terms {
+  int co[17];
+  int to[17];
+  int kind;  // 0 q, 1 qd, 2 F, 3 idle
+};
+
+__device__ __forceinline__ void build_terms(int lane, Terms& T) {
+#pragma unroll
+  for (int k = 0; k < 17; ++k) { T.co[k] = C_ZERO; T.to[k] = 0; }
+  const int CS = C_SIZE;
+  if (lane < 9) {
+    const int k = lane;
+    T.kind = 0;
+    T.co[0] = C_INT + 4 * k + 1;        T.to[0] = k;
+    T.co[1] = -CS + C_INT + 4 * k;      T.to[1] = -NSLOT + k;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) { T.co[2 + c] = C_JA + 9 * c + k; T.to[2 + c] = 14 + 4 * c; }
+    if (k >= 3) { T.co[6] = C_BOX + k - 3; T.to[6] = 28 + k - 3; }
+    T.co[7] = C_INIT + k;               T.to[7] = -NSLOT + INIT0 + k;
+  } else if (lane < 18) {
+    const int k = lane - 9;
+    T.kind = 1;
+    T.co[0] = -CS + C_INT + 4 * k + 2;  T.to[0] = -NSLOT + k;
+    T.co[1] = -CS + C_DYNU + k;         T.to[1] = -NSLOT + 9;
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      T.co[2 + c] = C_JA + 9 * c + k; T.to[2 + c] = 14 + 4 * c;
+      T.co[6 + c] = C_JB + 9 * c + k; T.to[6 + c] = 15 + 4 * c;
+    }
+    T.co[10] = -CS + C_DYNU + 12 + k;   T.to[10] = -NSLOT + 10;
+    T.co[11] = -CS + C_DYNU + 24 + k;   T.to[11] = -NSLOT + 11;
+#pragma unroll
+    for (int b = 0; b < 3; ++b) { T.co[12 + b] = C_DYNV + 20 * b + k; T.to[12 + b] = 9 + b; }
+    if (k >= 3) { T.co[15] = C_BOX + 6 + k - 3; T.to[15] = 34 + k - 3; }
+    T.co[16] = C_INIT + 9 + k;          T.to[16] = -NSLOT + INIT0 + 9 + k;
+  } else if (lane < NV) {
+    const int c = (lane - 18) >> 1, a = (lane - 18) & 1, idx = lane - 9;
+    T.kind = 2;
+    T.co[0] = C_DYNV + idx;             T.to[0] = 9;
+    T.co[1] = C_DYNV + 20 + idx;        T.to[1] = 10;
+    T.co[6] = C_DYNV + 40 + idx;        T.to[6] = 11;
+    T.co[7] = C_FORCE + 4 * c + a;      T.to[7] = 12 + 4 * c;
+    T.co[8] = C_FORCE + 4 * c + 2 + a;  T.to[8] = 13 + 4 * c;
+  } else {
+    T.kind = 3;
+  }
+}
+
+// Multipliers of terms 2..5 at a node with stance bits `bits`.
+__device__ __forceinline__ void ja_masks(const Terms& T, uint32_t bits, float m[4]) {
+#pragma unroll
+  for (int c = 0; c < 4; ++c) {
+    const bool st = (bits >> c) & 1u;
+    m[c] = T.kind == 0 ? (st ? 0.f : 1.f) : (T.kind == 1 ? (st ? 1.f : 0.f) : 1.f);
+  }
+}
+
+// Byte offsets of the 17 terms: coefficients relative to C(i), row values relative to R(i)
+// (+12 = t, +8 = {z, t}) or to D(i).
+struct TermBytes {
+  int cb[17];
+  int tb[17];
+};
+enum { TV_T = 0, TV_Y = 1, TV_D = 2 };
+template <int MODE>
+__device__ __forceinline__ void term_bytes(const Terms& T, TermBytes& B) {
+#pragma unroll
+  for (int k = 0; k < 17; ++k) {
+    B.cb[k] = T.co[k] * 4;
+    B.tb[k] = MODE == TV_D ? T.to[k] * 4 : T.to[k] * 16 + (MODE == TV_T ? 12 : 8);
+  }
+}
+
+// acc_j = Op_r (A_rj, t_r) over the rows touching var j of node i; t_r is rows[r].t (TV_T),
+// y_r = rho z_r - t_r (TV_Y) or the Ruiz row scale d_r (TV_D).
+template <class Op, int MODE>
+__device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, const TermBytes& B,
+                                          float rho = 0.f) {
+  const char* cb = reinterpret_cast<const char*>(sm.C(i));
+  const char* tb = MODE == TV_D ? reinterpret_cast<const char*>(sm.D(i))
+                                : reinterpret_cast<const char*>(sm.R(i));
+  float m[4];
+  ja_masks(T, sm.flags[i], m);
+  float acc0 = Op::id(), acc1 = Op::id();
+#pragma unroll
+  for (int k = 0; k < 17; ++k) {
+    float c = *reinterpret_cast<const float*>(cb + B.cb[k]);
+    if (k >= 2 && k <= 5) c *= m[k - 2];
+    float v;
+    if (MODE == TV_Y) {
+      const float2 zt = *reinterpret_cast<const float2*>(tb + B.tb[k]);
+      v = fmaf(rho, zt.x, -zt.y);
+    } else {
+      v = *reinterpret_cast<const float*>(tb + B.tb[k]);
+    }
+    if (k & 1) acc1 = Op::comb(acc1, c, v);
+    else acc0 = Op::comb(acc0, c, v);
+  }
+  return Op::red(acc0, acc1);
+}
+
+// ------------------------------------------------------------------------- full row view
+// out_r = Op_j(A_rj, v_j) for the 40 slots of node i (lane l: slot l in o0, slot 32+l in
+// o1) and, at node 0, the 18 initial-state rows (lane l < 18 in o2).  Used by Ruiz and the
+// residuals; the ADMM loop gets the integration/dynamics rows from the recurrences instead.
 template <class Op>
 __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int which, float& o0,
                                          float& o1, float& o2) {
   const float* cf = sm.C(i);
   const float* vi = sm.V(i, which);
   const float* vn = (i + 1 < sm.NT) ? sm.V(i + 1, which) : vi;  // coefficients are 0 then
+  const uint32_t bits = sm.flags[i];
   o0 = Op::id();
   o1 = Op::id();
   o2 = Op::id();
-  if (lane < 9) {  // integration rows: a1 q_{i+1,k} + a2 q_{i,k} + a3 qd_{i+1,k}
+  if (lane < 9) {
     const float4 a = *reinterpret_cast<const float4*>(cf + C_INT + 4 * lane);
     o0 = Op::comb(o0, a.x, vn[lane]);
     o0 = Op::comb(o0, a.y, vi[lane]);
     o0 = Op::comb(o0, a.z, vn[NQ + lane]);
-  } else if (lane >= 12 && lane < 28) {  // contact force rows t0, t1
+  } else if (lane >= 12 && lane < 28) {
     const int c = (lane - 12) >> 2, t = (lane - 12) & 3;
     if (t < 2) {
       o0 = Op::comb(o0, cf[C_FORCE + 4 * c + 2 * t], vi[18 + 2 * c]);
       o0 = Op::comb(o0, cf[C_FORCE + 4 * c + 2 * t + 1], vi[19 + 2 * c]);
     }
-  } else if (lane >= 28) {  // joint position boxes 0..3
-    const int m = lane - 28;
-    o0 = Op::comb(o0, cf[C_BOX + m], vi[3 + m]);
+  } else if (lane >= 28) {
+    o0 = Op::comb(o0, cf[C_BOX + lane - 28], vi[3 + lane - 28]);
   }
-  if (lane < 8) {  // boxes 4..11
+  if (lane < 8) {
     const int m = 4 + lane;
-    const int var = m < 6 ? 3 + m : NQ + 3 + (m - 6);
-    o1 = Op::comb(o1, cf[C_BOX + m], vi[var]);
+    o1 = Op::comb(o1, cf[C_BOX + m], vi[m < 6 ? 3 + m : NQ + 3 + (m - 6)]);
   }
-  if (i == 0 && lane < NINIT) o2 = Op::comb(o2, sm.icoef[lane], vi[lane]);
-  {  // base-dynamics rows: lane = one of the 26 support entries (qd_{i+1}: 9, node-i 9..25)
+  if (i == 0 && lane < NINIT) o2 = Op::comb(o2, cf[C_INIT + lane], vi[lane]);
+  {  // dynamics rows: lane = support entry (qd_{i+1}: 0..8, node-i vars 9..25)
     float p0 = Op::id(), p1 = Op::id(), p2 = Op::id();
     if (lane < 9) {
       const float v = vn[NQ + lane];
@@ -124,9 +242,9 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
       p2 = Op::comb(p2, cf[C_DYNU + 24 + lane], v);
     } else if (lane < NV) {
       const float v = vi[lane];
-      p0 = Op::comb(p0, cf[C_DYNV + lane], v);
-      p1 = Op::comb(p1, cf[C_DYNV + 28 + lane], v);
-      p2 = Op::comb(p2, cf[C_DYNV + 56 + lane], v);
+      p0 = Op::comb(p0, cf[C_DYNV + lane - 9], v);
+      p1 = Op::comb(p1, cf[C_DYNV + 20 + lane - 9], v);
+      p2 = Op::comb(p2, cf[C_DYNV + 40 + lane - 9], v);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -138,16 +256,15 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
     else if (lane == 10) o0 = p1;
     else if (lane == 11) o0 = p2;
   }
-  {  // contact Jacobian rows (t2: height on q / velocity-x on qd, t3: velocity-z on qd):
-     // 8-lane group per contact, one lane per non-zero column
+  {  // contact Jacobian rows t2, t3: 8-lane group per contact
     const int c = lane >> 3, s = lane & 7;
     float pa = Op::id(), pb = Op::id();
     if (s < 6) {
       const int col = chain_col(c, s);
-      const float vq = vi[col], vd = vi[NQ + col];
-      pa = Op::comb(pa, cf[C_JQ + 9 * c + col], vq);
-      pa = Op::comb(pa, cf[C_JV0 + 9 * c + col], vd);
-      pb = Op::comb(pb, cf[C_JV1 + 9 * c + col], vd);
+      const float vd = vi[NQ + col];
+      const float vt = ((bits >> c) & 1u) ? vd : vi[col];
+      pa = Op::comb(pa, cf[C_JA + 9 * c + col], vt);
+      pb = Op::comb(pb, cf[C_JB + 9 * c + col], vd);
     }
 #pragma unroll
     for (int o = 4; o > 0; o >>= 1) {
@@ -163,93 +280,6 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
       else if (t == 3) o0 = gb;
     }
   }
-}
-
-// Column view: for var j = lane (< 26) of node i, Op_r(A_rj, t_r) over every row touching
-// node i: its own slots (tc[0..40), init slots tc[40..58) at node 0) and the integration /
-// dynamics slots of node i-1 (tp[0..12)).
-template <class Op>
-__device__ __forceinline__ float col_view(const Sm& sm, int i, int lane, const float* tc,
-                                          const float* tp) {
-  const float* cf = sm.C(i);
-  float acc = Op::id();
-  if (lane < 9) {  // q_k
-    const int k = lane;
-    acc = Op::comb(acc, cf[C_INT + 4 * k + 1], tc[k]);
-    if (i > 0) acc = Op::comb(acc, sm.C(i - 1)[C_INT + 4 * k], tp[k]);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) acc = Op::comb(acc, cf[C_JQ + 9 * c + k], tc[14 + 4 * c]);
-    if (k >= 3) acc = Op::comb(acc, cf[C_BOX + k - 3], tc[28 + k - 3]);
-    if (i == 0) acc = Op::comb(acc, sm.icoef[k], tc[NSLOT + k]);
-  } else if (lane < 18) {  // qd_k
-    const int k = lane - 9;
-    if (i > 0) {
-      const float* cp = sm.C(i - 1);
-      acc = Op::comb(acc, cp[C_INT + 4 * k + 2], tp[k]);
-#pragma unroll
-      for (int b = 0; b < 3; ++b) acc = Op::comb(acc, cp[C_DYNU + 12 * b + k], tp[9 + b]);
-    }
-#pragma unroll
-    for (int b = 0; b < 3; ++b) acc = Op::comb(acc, cf[C_DYNV + 28 * b + lane], tc[9 + b]);
-#pragma unroll
-    for (int c = 0; c < NC; ++c) {
-      acc = Op::comb(acc, cf[C_JV0 + 9 * c + k], tc[14 + 4 * c]);
-      acc = Op::comb(acc, cf[C_JV1 + 9 * c + k], tc[15 + 4 * c]);
-    }
-    if (k >= 3) acc = Op::comb(acc, cf[C_BOX + 6 + k - 3], tc[34 + k - 3]);
-    if (i == 0) acc = Op::comb(acc, sm.icoef[NQ + k], tc[NSLOT + NQ + k]);
-  } else if (lane < NV) {  // F_{2c+a}
-    const int c = (lane - 18) >> 1, a = (lane - 18) & 1;
-#pragma unroll
-    for (int b = 0; b < 3; ++b) acc = Op::comb(acc, cf[C_DYNV + 28 * b + lane], tc[9 + b]);
-    acc = Op::comb(acc, cf[C_FORCE + 4 * c + a], tc[12 + 4 * c]);
-    acc = Op::comb(acc, cf[C_FORCE + 4 * c + 2 + a], tc[13 + 4 * c]);
-  }
-  return acc;
-}
-
-// Fill tc (node i's slot values) from the row data with f(row{lo,hi,z,y}, d).
-template <class F>
-__device__ __forceinline__ void fill_t(const Sm& sm, int i, int lane, float* tc, F f) {
-  __syncwarp();
-  int r = sm.ridx(i, lane);
-  tc[lane] = f(sm.row[r], sm.dsc[r]);
-  if (lane < 8) {
-    r = sm.ridx(i, 32 + lane);
-    tc[32 + lane] = f(sm.row[r], sm.dsc[r]);
-  }
-  if (i == 0 && lane < NINIT) {
-    r = sm.ridx(0, NSLOT + lane);
-    tc[NSLOT + lane] = f(sm.row[r], sm.dsc[r]);
-  }
-  __syncwarp();
-}
-
-// out_j = sum_l S_i^-1[j][l] u_l for j = lane < 26 (u published through bcbuf).
-__device__ __forceinline__ float sinv_mv(const Sm& sm, int i, int lane, float* bcbuf, float u) {
-  bcbuf[lane] = lane < NV ? u : 0.f;
-  __syncwarp();
-  const int j = lane < NV ? lane : NV - 1;
-  const float2* rw = reinterpret_cast<const float2*>(sm.Sinv(i) + j * SROW);
-  const float4* b4 = reinterpret_cast<const float4*>(bcbuf);
-  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
-#pragma unroll
-  for (int q = 0; q < 6; ++q) {
-    const float4 bb = b4[q];
-    const float2 r0 = rw[2 * q], r1 = rw[2 * q + 1];
-    a0 = fmaf(r0.x, bb.x, a0);
-    a1 = fmaf(r0.y, bb.y, a1);
-    a2 = fmaf(r1.x, bb.z, a2);
-    a3 = fmaf(r1.y, bb.w, a3);
-  }
-  {
-    const float2 bb = reinterpret_cast<const float2*>(bcbuf)[12];
-    const float2 r = rw[12];
-    a0 = fmaf(r.x, bb.x, a0);
-    a1 = fmaf(r.y, bb.y, a1);
-  }
-  __syncwarp();
-  return (a0 + a1) + (a2 + a3);
 }
 
 // ------------------------------------------------------------------------- FP64 kinematics
@@ -438,8 +468,8 @@ __device__ __forceinline__ double bezier_height(double t_sw, double zs, double v
          5.0 * s * t * t * t * t * p4;
 }
 
-// Stance bits (bit c) of node i and, for swing contacts, progress (gait.cpp:37-63): node i
-// uses the cumulative dt of nodes < i, summed in the reference's order.
+// Stance bits (bit c) of node i and swing progress (gait.cpp:37-63): node i uses the
+// cumulative dt of nodes < i, summed in the reference's order.
 __device__ __forceinline__ uint32_t node_schedule(const KParams& P, const rmpc_gait& g, int i,
                                                   double swing_t[4]) {
   double shift = 0.0;
@@ -487,19 +517,39 @@ __device__ __forceinline__ void node_guess(const KParams& P, int i, bool warm, c
   }
 }
 
+// Guess component j (< 26) of node i and its tracking target (mpc.cpp:28-62, 266-276).
+__device__ __forceinline__ void guess_and_target(const KParams& P, int i, int j, bool warm,
+                                                 const float* pz, const rmpc_state& st,
+                                                 const rmpc_command& cmd, uint32_t bits,
+                                                 double& g, double& des) {
+  const int na = __popc(bits);
+  if (j < 9) {
+    des = j == 0 ? 0.0 : (j == 1 ? cmd.height : (j == 2 ? 0.0 : P.nominal[j]));
+    g = j == 0 ? st.q[0] : P.nominal[j];
+  } else if (j < 18) {
+    des = j == 9 ? cmd.vx : (j == 11 ? cmd.wpitch : 0.0);
+    g = 0.0;
+  } else {
+    const int c = (j - 18) >> 1;
+    const bool fz = (j - 18) & 1;
+    des = fz && ((bits >> c) & 1u) && na > 0 ? P.weight / na : 0.0;
+    g = des;
+  }
+  if (warm) g = (double)pz[min(i + 1, P.NT - 1) * NV + j];
+}
+
 __device__ __forceinline__ float to_f(double v) { return (float)v; }
 __device__ __forceinline__ float bound_f(double v) {  // kInf sentinel -> +-inf in FP32
   return v <= -1e29 ? -INFINITY : (v >= 1e29 ? INFINITY : (float)v);
 }
-
-__device__ __forceinline__ void set_row(const Sm& sm, int r, double lo, double hi) {
-  sm.row[r] = make_float4(bound_f(lo), bound_f(hi), 0.f, 0.f);
+__device__ __forceinline__ void set_row(float4* r, double lo, double hi) {
+  *r = make_float4(bound_f(lo), bound_f(hi), 0.f, 0.f);
 }
 
 // ------------------------------------------------------------------------- stage: setup
 // Lane i < NT builds node i of the QP (build_qp, mpc.cpp:64-238) in FP64 and stores the
-// unscaled coefficients, bounds, P diagonal and q in shared memory.  Returns false if the
-// linearization point is non-finite (StructuralError, mpc.cpp:70-72).
+// unscaled coefficients, bounds and q in shared memory.  Returns false if the linearization
+// point is non-finite (StructuralError, mpc.cpp:70-72).
 __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc_state& st,
                             const rmpc_command& cmd, const rmpc_gait& gait, bool warm,
                             const float* pz) {
@@ -519,6 +569,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
     for (int k = 0; k < 8; ++k) ok = ok && isfinite(gF[k]);
     sm.flags[i] = bits;
     float* cf = sm.C(i);
+    float4* rw = sm.R(i);
     const double dt = P.dt[i];
 
     Frames F;
@@ -527,44 +578,25 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
 #pragma unroll
     for (int c = 0; c < 4; ++c) contact_jac(F, c, Jx[c], Jz[c]);
 
-    // cost (mpc.cpp:81-103): P = diag(w dt), q = w dt (guess - desired)
-    {
-      const int na = __popc(bits);
-      float* pd = sm.V(i, V_PD);
+    {  // q = w dt (guess - desired)  (mpc.cpp:81-103)
       float* qh = sm.V(i, V_QH);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        double qdes = P.nominal[k];
-        if (k == 0) qdes = 0.0;
-        if (k == 1) qdes = cmd.height;
-        if (k == 2) qdes = 0.0;
-        const double qddes = k == 0 ? cmd.vx : (k == 2 ? cmd.wpitch : 0.0);
-        const double wq = P.wq[k] * dt, wqd = P.wqd[k] * dt;
-        pd[k] = to_f(wq);
-        pd[NQ + k] = to_f(wqd);
-        qh[k] = to_f(wq * (gq[k] - qdes));
-        qh[NQ + k] = to_f(wqd * (gqd[k] - qddes));
-      }
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const double fdes = ((k & 1) && ((bits >> (k >> 1)) & 1u) && na > 0) ? P.weight / na : 0.0;
-        const double wf = P.wf[k] * dt;
-        pd[18 + k] = to_f(wf);
-        qh[18 + k] = to_f(wf * (gF[k] - fdes));
+#pragma unroll 1
+      for (int j = 0; j < NV; ++j) {
+        double g, des;
+        guess_and_target(P, i, j, warm, pz, st, cmd, bits, g, des);
+        qh[j] = to_f(wcost(P, j) * dt * (g - des));
       }
     }
     if (i + 1 < NT) {
-      // integration rows (mpc.cpp:138-148)
 #pragma unroll
-      for (int k = 0; k < 9; ++k) {
+      for (int k = 0; k < 9; ++k) {  // integration (mpc.cpp:138-148)
         cf[C_INT + 4 * k + 0] = 1.f;
         cf[C_INT + 4 * k + 1] = -1.f;
         cf[C_INT + 4 * k + 2] = to_f(-dt);
         const double r = -(nq[k] - gq[k] - dt * nqd[k]);
-        set_row(sm, sm.ridx(i, k), r, r);
+        set_row(rw + k, r, r);
       }
-      // base dynamics with qdd eliminated (mpc.cpp:150-175)
-      double Mb[3][9], hb[3];
+      double Mb[3][9], hb[3];  // base dynamics with qdd eliminated (mpc.cpp:150-175)
       base_dynamics(P, gqd, F, Mb, hb);
       const double dt_inv = 1.0 / dt;
 #pragma unroll
@@ -580,51 +612,50 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
         for (int k = 0; k < 9; ++k) {
           const double mv = Mb[b][k] * dt_inv;
           cf[C_DYNU + 12 * b + k] = to_f(mv);
-          cf[C_DYNV + 28 * b + NQ + k] = to_f(-mv);
+          cf[C_DYNV + 20 * b + k] = to_f(-mv);
         }
 #pragma unroll
         for (int c = 0; c < 4; ++c) {
-          cf[C_DYNV + 28 * b + 18 + 2 * c] = to_f(-Jx[c][b]);
-          cf[C_DYNV + 28 * b + 19 + 2 * c] = to_f(-Jz[c][b]);
+          cf[C_DYNV + 20 * b + 9 + 2 * c] = to_f(-Jx[c][b]);
+          cf[C_DYNV + 20 * b + 10 + 2 * c] = to_f(-Jz[c][b]);
         }
-        set_row(sm, sm.ridx(i, 9 + b), -resid, -resid);
+        set_row(rw + 9 + b, -resid, -resid);
       }
     }
-    // contact rows (mpc.cpp:181-218)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 4; ++c) {  // contacts (mpc.cpp:181-218)
       const double fx = gF[2 * c], fz = gF[2 * c + 1];
-      const int s0 = 12 + 4 * c;
+      float4* r0 = rw + 12 + 4 * c;
       if ((bits >> c) & 1u) {
         cf[C_FORCE + 4 * c + 0] = 1.f;
         cf[C_FORCE + 4 * c + 1] = to_f(-P.mu);
         cf[C_FORCE + 4 * c + 2] = -1.f;
         cf[C_FORCE + 4 * c + 3] = to_f(-P.mu);
-        set_row(sm, sm.ridx(i, s0), -1e30, -(fx - P.mu * fz));
-        set_row(sm, sm.ridx(i, s0 + 1), -1e30, -(-fx - P.mu * fz));
+        set_row(r0, -1e30, -(fx - P.mu * fz));
+        set_row(r0 + 1, -1e30, -(-fx - P.mu * fz));
         if (i > 0) {
-          double r0 = 0.0, r1 = 0.0;
+          double v0 = 0.0, v1 = 0.0;
 #pragma unroll
           for (int k = 0; k < 9; ++k) {
-            r0 += Jx[c][k] * gqd[k];
-            r1 += Jz[c][k] * gqd[k];
-            cf[C_JV0 + 9 * c + k] = to_f(Jx[c][k]);
-            cf[C_JV1 + 9 * c + k] = to_f(Jz[c][k]);
+            v0 += Jx[c][k] * gqd[k];
+            v1 += Jz[c][k] * gqd[k];
+            cf[C_JA + 9 * c + k] = to_f(Jx[c][k]);
+            cf[C_JB + 9 * c + k] = to_f(Jz[c][k]);
           }
-          set_row(sm, sm.ridx(i, s0 + 2), -r0, -r0);
-          set_row(sm, sm.ridx(i, s0 + 3), -r1, -r1);
+          set_row(r0 + 2, -v0, -v0);
+          set_row(r0 + 3, -v1, -v1);
         }
       } else {
         cf[C_FORCE + 4 * c + 0] = 1.f;
         cf[C_FORCE + 4 * c + 3] = 1.f;
-        set_row(sm, sm.ridx(i, s0), -fx, -fx);
-        set_row(sm, sm.ridx(i, s0 + 1), -fz, -fz);
+        set_row(r0, -fx, -fx);
+        set_row(r0 + 1, -fz, -fz);
         if (i > 0) {
           const double h = bezier_height(swt[c], P.z_swing, P.v_to, P.v_td);
           const double r = h - F.con[c].pz;
 #pragma unroll
-          for (int k = 0; k < 9; ++k) cf[C_JQ + 9 * c + k] = to_f(Jz[c][k]);
-          set_row(sm, sm.ridx(i, s0 + 2), r, r);
+          for (int k = 0; k < 9; ++k) cf[C_JA + 9 * c + k] = to_f(Jz[c][k]);
+          set_row(r0 + 2, r, r);
         }
       }
     }
@@ -632,18 +663,19 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
 #pragma unroll
       for (int m = 0; m < 6; ++m) {
         cf[C_BOX + m] = 1.f;
-        set_row(sm, sm.ridx(i, 28 + m), P.jlo[m] - gq[3 + m], P.jhi[m] - gq[3 + m]);
+        set_row(rw + 28 + m, P.jlo[m] - gq[3 + m], P.jhi[m] - gq[3 + m]);
         cf[C_BOX + 6 + m] = 1.f;
-        set_row(sm, sm.ridx(i, 34 + m), -P.qdlim[m] - gqd[3 + m], P.qdlim[m] - gqd[3 + m]);
+        set_row(rw + 34 + m, -P.qdlim[m] - gqd[3 + m], P.qdlim[m] - gqd[3 + m]);
       }
-    } else {  // initial state (mpc.cpp:126-136)
+    } else {  // initial state (mpc.cpp:126-136), rows in block -1
+      float4* ri = sm.R(-1) + INIT0;
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
-        sm.icoef[k] = 1.f;
-        sm.icoef[NQ + k] = 1.f;
+        cf[C_INIT + k] = 1.f;
+        cf[C_INIT + 9 + k] = 1.f;
         const double rq = st.q[k] - gq[k], rqd = st.qd[k] - gqd[k];
-        set_row(sm, sm.ridx(0, NSLOT + k), rq, rq);
-        set_row(sm, sm.ridx(0, NSLOT + NQ + k), rqd, rqd);
+        set_row(ri + k, rq, rq);
+        set_row(ri + 9 + k, rqd, rqd);
       }
     }
   }
@@ -652,101 +684,108 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
 
 // ------------------------------------------------------------------------- stage: Ruiz
 // AdmmSolver::equilibrate (qp.cpp:64-95) + ruiz_equilibrate (ruiz.cpp:7-36) on
-// [[P, A^T], [A, 0]]: per pass delta = 1/sqrt(inf-norm) of every row/column of the current
-// scaled matrix (1 for empty ones), d *= delta (rows), e *= delta (columns).
-__device__ void ruiz(const KParams& P, const Sm& sm, int lane) {
+// [[P, A^T], [A, 0]]: each pass takes delta = 1/sqrt(inf-norm) of every row/column of the
+// current scaled matrix (1 for empty ones), then d *= delta (rows), e *= delta (columns).
+// Row deltas are parked in row.z, column deltas in V_S until the pass is applied.
+__device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
+  Terms T;
+  build_terms(lane, T);
+  TermBytes B;
+  term_bytes<TV_D>(T, B);
 #pragma unroll 1
   for (int pass = 0; pass < P.ruiz_iters; ++pass) {
 #pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
+    for (int i = warp; i < NT; i += 2) {  // nodes are independent within a pass
       float o0, o1, o2;
       row_view<OpMax>(sm, i, lane, V_E, o0, o1, o2);
-      auto stash = [&](int s, float o) {  // delta of row slot s into row.z (z is 0 here)
-        const int r = sm.ridx(i, s);
-        const float nrm = sm.dsc[r] * o;
-        sm.row[r].z = nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f;
+      const float* d = sm.D(i);
+      const float cv = col_view<OpMax, TV_D>(sm, i, T, B);
+      float4* rw = sm.R(i);
+      auto stash = [](float4* r, const float* dp, float o) {
+        const float nrm = *dp * o;
+        r->z = nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f;
       };
-      float* tc = sm.tbuf + (i & 1) * 64;
-      const float* tp = sm.tbuf + ((i + 1) & 1) * 64;
-      // row deltas must not be visible before every column norm of this pass is formed:
-      // column norms use d (dsc), deltas live in row.z until the apply step.
-      fill_t(sm, i, lane, tc, [](float4, float d) { return d; });
-      const float cv = col_view<OpMax>(sm, i, lane, tc, tp);
-      stash(lane, o0);
-      if (lane < 8) stash(32 + lane, o1);
-      if (i == 0 && lane < NINIT) stash(NSLOT + lane, o2);
+      stash(rw + lane, d + lane, o0);
+      if (lane < 8) stash(rw + 32 + lane, d + 32 + lane, o1);
+      if (i == 0 && lane < NINIT) stash(sm.R(-1) + INIT0 + lane, sm.D(-1) + INIT0 + lane, o2);
       if (lane < NV) {
         const float e = sm.V(i, V_E)[lane];
-        const float nrm = e * fmaxf(fabsf(sm.V(i, V_PD)[lane]) * e, cv);
+        const float pd = (float)wcost(P, lane) * (float)P.dt[i];
+        const float nrm = e * fmaxf(fabsf(pd) * e, cv);
         sm.V(i, V_S)[lane] = nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f;
       }
     }
-    __syncwarp();
-    const int nrow = NT * NSLOT + NINIT;
-    for (int r = lane; r < nrow; r += 32) {
-      sm.dsc[r] *= sm.row[r].z;
-      sm.row[r].z = 0.f;
-    }
-    for (int i = 0; i < NT; ++i)
+    __syncthreads();  // every norm of this pass uses the scales of the previous pass
+#pragma unroll 1
+    for (int i = warp; i < NT; i += 2) {
+      float4* rw = sm.R(i);
+      float* d = sm.D(i);
+      d[lane] *= rw[lane].z;
+      rw[lane].z = 0.f;
+      if (lane < 8) {
+        d[32 + lane] *= rw[32 + lane].z;
+        rw[32 + lane].z = 0.f;
+      }
+      if (i == 0 && lane < NINIT) {
+        sm.D(-1)[INIT0 + lane] *= sm.R(-1)[INIT0 + lane].z;
+        sm.R(-1)[INIT0 + lane].z = 0.f;
+      }
       if (lane < NV) sm.V(i, V_E)[lane] *= sm.V(i, V_S)[lane];
-    __syncwarp();
+    }
+    __syncthreads();
   }
 }
 
-// Scale coefficients, bounds and cost in place: A^ = D A E, P^ = E P E, q^ = E q,
-// lo^ = D lo, hi^ = D hi (qp.cpp:86-94).
-__device__ void apply_scaling(const KParams& P, const Sm& sm, int lane) {
+// A^ = D A E, q^ = E q, lo^ = D lo, hi^ = D hi in place (qp.cpp:86-94); P^ = E P E is
+// recomputed where needed (phat).
+__device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
-  for (int i = 0; i < NT; ++i) {
+  for (int i = warp; i < NT; i += 2) {
     float* cf = sm.C(i);
     const float* ei = sm.V(i, V_E);
     const float* en = i + 1 < NT ? sm.V(i + 1, V_E) : ei;
-    auto d = [&](int s) { return sm.dsc[sm.ridx(i, s)]; };
+    const float* d = sm.D(i);
+    const uint32_t bits = sm.flags[i];
     if (lane < 9) {
-      const float dr = d(lane);
+      const float dr = d[lane];
       cf[C_INT + 4 * lane + 0] *= dr * en[lane];
       cf[C_INT + 4 * lane + 1] *= dr * ei[lane];
       cf[C_INT + 4 * lane + 2] *= dr * en[NQ + lane];
 #pragma unroll
-      for (int b = 0; b < 3; ++b) cf[C_DYNU + 12 * b + lane] *= d(9 + b) * en[NQ + lane];
+      for (int b = 0; b < 3; ++b) cf[C_DYNU + 12 * b + lane] *= d[9 + b] * en[NQ + lane];
     } else if (lane < NV) {
 #pragma unroll
-      for (int b = 0; b < 3; ++b) cf[C_DYNV + 28 * b + lane] *= d(9 + b) * ei[lane];
+      for (int b = 0; b < 3; ++b) cf[C_DYNV + 20 * b + lane - 9] *= d[9 + b] * ei[lane];
     }
     if (lane < 16) {
       const int c = lane >> 2, t = (lane >> 1) & 1, a = lane & 1;
-      cf[C_FORCE + lane] *= d(12 + 4 * c + t) * ei[18 + 2 * c + a];
+      cf[C_FORCE + lane] *= d[12 + 4 * c + t] * ei[18 + 2 * c + a];
     }
     for (int idx = lane; idx < 36; idx += 32) {
       const int c = idx / 9, k = idx % 9;
-      cf[C_JQ + idx] *= d(14 + 4 * c) * ei[k];
-      cf[C_JV0 + idx] *= d(14 + 4 * c) * ei[NQ + k];
-      cf[C_JV1 + idx] *= d(15 + 4 * c) * ei[NQ + k];
+      const bool st = (bits >> c) & 1u;
+      cf[C_JA + idx] *= d[14 + 4 * c] * ei[st ? NQ + k : k];
+      cf[C_JB + idx] *= d[15 + 4 * c] * ei[NQ + k];
     }
-    if (lane < 12) cf[C_BOX + lane] *= d(28 + lane) * ei[lane < 6 ? 3 + lane : NQ + 3 + (lane - 6)];
-    if (i == 0 && lane < NINIT) sm.icoef[lane] *= d(NSLOT + lane) * ei[lane];
-    if (lane < NV) {
-      const float e = ei[lane];
-      sm.V(i, V_PD)[lane] *= e * e;
-      sm.V(i, V_QH)[lane] *= e;
-    }
+    if (lane < 12) cf[C_BOX + lane] *= d[28 + lane] * ei[lane < 6 ? 3 + lane : NQ + 3 + (lane - 6)];
+    if (i == 0 && lane < NINIT) cf[C_INIT + lane] *= sm.D(-1)[INIT0 + lane] * ei[lane];
+    if (lane < NV) sm.V(i, V_QH)[lane] *= ei[lane];
   }
-  const int nrow = NT * NSLOT + NINIT;
-  for (int r = lane; r < nrow; r += 32) {
+  for (int r = lane + 32 * warp; r < (NT + 1) * NSLOT; r += 64) {
     float4 rd = sm.row[r];
     const float dr = sm.dsc[r];
     rd.x *= dr;
     rd.y *= dr;
     sm.row[r] = rd;
   }
-  __syncwarp();
+  __syncthreads();
 }
 
 // ------------------------------------------------------------------------- stage: factor
-// Block elimination of H: S_0 = H_00, S_{i+1} = H_{i+1,i+1} - C_i S_i^-1 C_i^T, S_i^-1
-// stored.  Lane j holds row j of the 26 x 26 blocks in registers.  Returns false on a
-// non-positive pivot (SingularityError analogue, ldl.cpp:155-160).
+// Block elimination of H.  Lane j holds row j of the 26 x 26 blocks in registers; S_i^-1 is
+// formed by Gauss-Jordan (SPD, no pivoting) and stored with W_b = S_i^-1 v_b appended as
+// rows 26..28.  Returns false on a non-positive pivot (SingularityError, ldl.cpp:155-160).
 __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
   const int NT = P.NT;
   const float rho = (float)P.rho, sigma = (float)P.sigma;
@@ -758,35 +797,26 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
 #pragma unroll 1
   for (int i = 0; i < NT; ++i) {
     const float* cf = sm.C(i);
-    const float* cp = i > 0 ? sm.C(i - 1) : cf;
+    const float* cp = sm.C(i - 1);  // block -1 is zero for i == 0
     const uint32_t bits = sm.flags[i];
     float S[NV];
-    // (a) diagonal and the single paired off-diagonal entry per row
-    {
+    {  // (a) diagonal and the single paired off-diagonal entry of row j
       float dg = 0.f, pt = 0.f;
       int pidx = -1;
-      if (j < NV) dg = sm.V(i, V_PD)[j] + sigma;
+      if (j < NV) dg = phat(P, sm, i, j) + sigma;
       if (j < 9) {
-        const float a2 = cf[C_INT + 4 * j + 1];
-        dg += rho * a2 * a2;
-        if (i > 0) {
-          const float a1 = cp[C_INT + 4 * j], a3 = cp[C_INT + 4 * j + 2];
-          dg += rho * a1 * a1;
-          pt = rho * a1 * a3;
-          pidx = NQ + j;
-        }
-        if (j >= 3) { const float b = cf[C_BOX + j - 3]; dg += rho * b * b; }
-        if (i == 0) { const float b = sm.icoef[j]; dg += rho * b * b; }
+        const float a2 = cf[C_INT + 4 * j + 1], a1 = cp[C_INT + 4 * j], a3 = cp[C_INT + 4 * j + 2];
+        const float bx = j >= 3 ? cf[C_BOX + j - 3] : 0.f, bi = cf[C_INIT + j];
+        dg += rho * (a2 * a2 + a1 * a1 + bx * bx + bi * bi);
+        pt = rho * a1 * a3;
+        pidx = NQ + j;
       } else if (j < 18) {
         const int k = j - 9;
-        if (i > 0) {
-          const float a1 = cp[C_INT + 4 * k], a3 = cp[C_INT + 4 * k + 2];
-          dg += rho * a3 * a3;
-          pt = rho * a1 * a3;
-          pidx = k;
-        }
-        if (k >= 3) { const float b = cf[C_BOX + 6 + k - 3]; dg += rho * b * b; }
-        if (i == 0) { const float b = sm.icoef[NQ + k]; dg += rho * b * b; }
+        const float a1 = cp[C_INT + 4 * k], a3 = cp[C_INT + 4 * k + 2];
+        const float bx = k >= 3 ? cf[C_BOX + 6 + k - 3] : 0.f, bi = cf[C_INIT + j];
+        dg += rho * (a3 * a3 + bx * bx + bi * bi);
+        pt = rho * a1 * a3;
+        pidx = k;
       } else if (j < NV) {
         const int c = (j - 18) >> 1, a = (j - 18) & 1;
         const float f0 = cf[C_FORCE + 4 * c + a], g0 = cf[C_FORCE + 4 * c + 1 - a];
@@ -798,52 +828,45 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
 #pragma unroll
       for (int l = 0; l < NV; ++l) S[l] = (l == j ? dg : 0.f) + (l == pidx ? pt : 0.f);
     }
-    // (b) dense rank-1 terms: dynamics rows of intervals i and i-1, contact Jacobian rows
+    // (b) dense rank-1 terms: dynamics rows of intervals i (qd_i, F_i) and i-1 (qd_i),
+    //     contact Jacobian rows (qd for stance, q for swing)
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
-      const float* vb = cf + C_DYNV + 28 * b;
-      const float s = j < NV ? rho * vb[j] : 0.f;
+      const float* vb = cf + C_DYNV + 20 * b;
+      const float s = (j >= 9 && j < NV) ? rho * vb[j - 9] : 0.f;
       const float4* v4 = reinterpret_cast<const float4*>(vb);
 #pragma unroll
-      for (int q = 0; q < 7; ++q) {
+      for (int q = 0; q < 5; ++q) {
         const float4 w = v4[q];
-        S[4 * q] = fmaf(s, w.x, S[4 * q]);
-        S[4 * q + 1] = fmaf(s, w.y, S[4 * q + 1]);
-        if (4 * q + 2 < NV) S[4 * q + 2] = fmaf(s, w.z, S[4 * q + 2]);
-        if (4 * q + 3 < NV) S[4 * q + 3] = fmaf(s, w.w, S[4 * q + 3]);
+        if (9 + 4 * q < NV) S[9 + 4 * q] = fmaf(s, w.x, S[9 + 4 * q]);
+        if (10 + 4 * q < NV) S[10 + 4 * q] = fmaf(s, w.y, S[10 + 4 * q]);
+        if (11 + 4 * q < NV) S[11 + 4 * q] = fmaf(s, w.z, S[11 + 4 * q]);
+        if (12 + 4 * q < NV) S[12 + 4 * q] = fmaf(s, w.w, S[12 + 4 * q]);
       }
+      const float* ub = cp + C_DYNU + 12 * b;
+      const float s2 = (j >= 9 && j < 18) ? rho * ub[j - 9] : 0.f;
+#pragma unroll
+      for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s2, ub[m], S[NQ + m]);
     }
-    if (i > 0) {
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const float* ub = cp + C_DYNU + 12 * b;
-        const float s = (j >= 9 && j < 18) ? rho * ub[j - 9] : 0.f;
+    for (int c = 0; c < 4; ++c) {
+      const float* ja = cf + C_JA + 9 * c;
+      if ((bits >> c) & 1u) {  // stance: velocity rows on qd
+        const float* jb = cf + C_JB + 9 * c;
+        const bool mine = j >= 9 && j < 18;
+        const float s0 = mine ? rho * ja[j - 9] : 0.f, s1 = mine ? rho * jb[j - 9] : 0.f;
 #pragma unroll
-        for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s, ub[m], S[NQ + m]);
-      }
-    }
-    if (i > 0) {
+        for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s0, ja[m], fmaf(s1, jb[m], S[NQ + m]));
+      } else {  // swing: height row on q
+        const float s = j < 9 ? rho * ja[j] : 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        if ((bits >> c) & 1u) {  // stance: velocity rows on qd
-          const float* j0 = cf + C_JV0 + 9 * c;
-          const float* j1 = cf + C_JV1 + 9 * c;
-          const bool mine = j >= 9 && j < 18;
-          const float s0 = mine ? rho * j0[j - 9] : 0.f, s1 = mine ? rho * j1[j - 9] : 0.f;
-#pragma unroll
-          for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s0, j0[m], fmaf(s1, j1[m], S[NQ + m]));
-        } else {  // swing: height row on q
-          const float* jq = cf + C_JQ + 9 * c;
-          const float s = j < 9 ? rho * jq[j] : 0.f;
-#pragma unroll
-          for (int m = 0; m < 9; ++m) S[m] = fmaf(s, jq[m], S[m]);
-        }
+        for (int m = 0; m < 9; ++m) S[m] = fmaf(s, ja[m], S[m]);
       }
     }
     // (c) Schur update from the previous node
 #pragma unroll
     for (int l = 0; l < 18; ++l) S[l] -= Yp[l];
-    // (d) Gauss-Jordan inversion in place (SPD, no pivoting), rows exchanged through smem
+    // (d) Gauss-Jordan inversion in place, rows exchanged through smem
 #pragma unroll
     for (int k = 0; k < NV; ++k) {
       float* buf = sm.bc + 32 * (k & 1);
@@ -877,32 +900,26 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
       for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], keep * S[l]);
       S[k] = me ? pinv : -f * pinv;
     }
-    // (e) store S_i^-1
-    if (j < NV) {
-      float2* dst = reinterpret_cast<float2*>(sm.Sinv(i) + j * SROW);
+    float* Sd = sm.Sinv(i);
+    if (j < NV) {  // (e) store S_i^-1
+      float2* dst = reinterpret_cast<float2*>(Sd + j * SROW);
 #pragma unroll
       for (int q = 0; q < 13; ++q) dst[q] = make_float2(S[2 * q], S[2 * q + 1]);
     }
-    // (f) Schur update for node i+1 in factored form: Y = rho^2 U G U^T,
-    //     G = V^T S^-1 V (12 x 12), V/U = node-i / node-(i+1) parts of the 9 integration and
-    //     3 dynamics rows of interval i.
     if (i + 1 < NT) {
+      // (f) W_b = S^-1 v_b (rows 26..28), G = V^T S^-1 V and the Schur update for node i+1:
+      //     Y = rho^2 U G U^T with V/U the node-i / node-(i+1) parts of interval i's rows.
       float W[3];
 #pragma unroll
-      for (int b = 0; b < 3; ++b) {  // W_b = S^-1 v_b (lane j: component j)
-        const float4* v4 = reinterpret_cast<const float4*>(cf + C_DYNV + 28 * b);
+      for (int b = 0; b < 3; ++b) {
+        const float* vb = cf + C_DYNV + 20 * b;
         float acc = 0.f;
 #pragma unroll
-        for (int q = 0; q < 7; ++q) {
-          const float4 w = v4[q];
-          acc = fmaf(S[4 * q], w.x, acc);
-          acc = fmaf(S[4 * q + 1], w.y, acc);
-          if (4 * q + 2 < NV) acc = fmaf(S[4 * q + 2], w.z, acc);
-          if (4 * q + 3 < NV) acc = fmaf(S[4 * q + 3], w.w, acc);
-        }
+        for (int l = 9; l < NV; ++l) acc = fmaf(S[l], vb[l - 9], acc);
         W[b] = j < NV ? acc : 0.f;
+        if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
       }
-      float* G = sm.g + 96;  // 12 x 13 (odd stride)
+      float* G = sm.Sinv(i + 1);  // node i+1's block is free until it is factorized: 12 x 13
       if (j < 9) {
         const float a2 = cf[C_INT + 4 * j + 1];
 #pragma unroll
@@ -916,7 +933,7 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
       float gdd[3][3];
 #pragma unroll
       for (int b = 0; b < 3; ++b) {
-        const float vb = j < NV ? cf[C_DYNV + 28 * b + j] : 0.f;
+        const float vb = (j >= 9 && j < NV) ? cf[C_DYNV + 20 * b + j - 9] : 0.f;
 #pragma unroll
         for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(vb * W[b2]);
       }
@@ -924,7 +941,11 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
 #pragma unroll
         for (int b = 0; b < 3; ++b)
 #pragma unroll
-          for (int b2 = 0; b2 < 3; ++b2) G[(9 + b) * 13 + 9 + b2] = 0.5f * (gdd[b][b2] + gdd[b2][b]);
+          for (int b2 = 0; b2 < 3; ++b2) {
+            const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
+            G[(9 + b) * 13 + 9 + b2] = gv;
+            sm.C(i)[C_G + 3 * b + b2] = gv;
+          }
       }
       __syncwarp();
       float Z[12];
@@ -951,104 +972,251 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
         Yp[NQ + k] = r2 * (Z[k] * cf[C_INT + 4 * k + 2] + Z[9] * cf[C_DYNU + k] +
                            Z[10] * cf[C_DYNU + 12 + k] + Z[11] * cf[C_DYNU + 24 + k]);
       __syncwarp();
+    } else if (j < NV) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) Sd[(NV + b) * SROW + j] = 0.f;
     }
   }
+  __syncwarp();
   return __all_sync(FULL, good);
 }
 
 // ------------------------------------------------------------------------- stage: ADMM
+// One constraint-row update (qp.cpp:163-170) on the stored {lo, hi, z, t = rho z - y}.
+__device__ __forceinline__ bool row_update(float4* r, float zt, float alpha, float oma, float rho,
+                                           float rho_inv) {
+  float4 rd = *r;
+  const float y = fmaf(rho, rd.z, -rd.w);
+  const float w = alpha * zt + oma * rd.z;
+  const float zn = fminf(fmaxf(w + rho_inv * y, rd.x), rd.y);
+  const float yn = y + rho * (w - zn);
+  rd.z = zn;
+  rd.w = fmaf(rho, zn, -yn);
+  *r = rd;
+  return isfinite(zt);
+}
+
+// [S_i^-1 ; W_i^T] u for lanes 0..28 (u published through buf).
+__device__ __forceinline__ float ext_mv(const float* Sd, int lane, float* buf, float u) {
+  buf[lane] = lane < NV ? u : 0.f;
+  __syncwarp();
+  const int j = lane < SROWS ? lane : SROWS - 1;
+  const float2* rw = reinterpret_cast<const float2*>(Sd + j * SROW);
+  const float4* b4 = reinterpret_cast<const float4*>(buf);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float4 bb = b4[q];
+    const float2 r0 = rw[2 * q], r1 = rw[2 * q + 1];
+    a0 = fmaf(r0.x, bb.x, a0);
+    a1 = fmaf(r0.y, bb.y, a1);
+    a2 = fmaf(r1.x, bb.z, a2);
+    a3 = fmaf(r1.y, bb.w, a3);
+  }
+  {
+    const float2 bb = reinterpret_cast<const float2*>(buf)[12];
+    const float2 r = rw[12];
+    a0 = fmaf(r.x, bb.x, a0);
+    a1 = fmaf(r.y, bb.y, a1);
+  }
+  return (a0 + a1) + (a2 + a3);
+}
+
+struct AdmmConst {
+  float rho, sigma, alpha, oma, rho_inv;
+};
+
+// Rows of node i that act on node-i variables only (contact forces, contact Jacobian rows,
+// joint boxes; the initial-state rows at node 0): z~ from x~_i, then the row update.  Lanes
+// 8c..8c+5 reduce rows t2/t3 of contact c, 8c+2..4 also own boxes, 8c+6/8c+7 rows t0/t1.
+__device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const float* xs,
+                                          const AdmmConst& K) {
+  const int c = lane >> 3, s = lane & 7;
+  const float* cf = sm.C(i);
+  const uint32_t bits = sm.flags[i];
+  float pa = 0.f, pb = 0.f;
+  if (s < 6) {
+    const int col = chain_col(c, s);
+    const float vd = xs[NQ + col];
+    const float vt = ((bits >> c) & 1u) ? vd : xs[col];
+    pa = cf[C_JA + 9 * c + col] * vt;
+    pb = cf[C_JB + 9 * c + col] * vd;
+  }
+#pragma unroll
+  for (int o = 4; o > 0; o >>= 1) {
+    pa += __shfl_xor_sync(FULL, pa, o);
+    pb += __shfl_xor_sync(FULL, pb, o);
+  }
+  float zt = 0.f;
+  int slot = -1;
+  if (s == 0) {
+    zt = pa;
+    slot = 14 + 4 * c;
+  } else if (s == 1) {
+    zt = pb;
+    slot = 15 + 4 * c;
+  } else if (s >= 6) {
+    const int t = s - 6;
+    zt = cf[C_FORCE + 4 * c + 2 * t] * xs[18 + 2 * c] + cf[C_FORCE + 4 * c + 2 * t + 1] * xs[19 + 2 * c];
+    slot = 12 + 4 * c + t;
+  } else if (s <= 4) {  // s == 5 has no row
+    const int m = 3 * c + (s - 2);
+    zt = cf[C_BOX + m] * xs[m < 6 ? 3 + m : NQ + 3 + (m - 6)];
+    slot = 28 + m;
+  }
+  bool bad = false;
+  if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv);
+  if (i == 0 && lane < NINIT) {
+    const float z0 = cf[C_INIT + lane] * xs[lane];
+    bad = !row_update(sm.R(-1) + INIT0 + lane, z0, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+  }
+  return bad;
+}
+
 // AdmmSolver::run (qp.cpp:156-190): exactly n_qp iterations from x = y = z = 0.  Returns the
-// first iteration with a non-finite iterate, or -1.
-__device__ int admm(const KParams& P, const Sm& sm, int lane) {
+// first iteration with a non-finite iterate, or -1 (CTA-uniform).
+//
+// Two warps per agent, in lock step (one __syncthreads per node step):
+//   warp 0 (solver) runs the recurrences
+//     forward  i = 0..T-1: u_i = r_i - rho U_{i-1} gamma_{i-1}; [s_i; gamma_i] = [S_i^-1; W_i^T] u_i
+//     backward i = T-1..0: x~_i = s_i - rho [S_i^-1 | W_i] xi_i, and updates the integration /
+//                          dynamics rows of interval i whose z~ falls out of the recurrence;
+//   warp 1 (helper) does the node-local work one node ahead of / behind it
+//     forward : r_{i+1} = sigma x_{i+1} - q^_{i+1} + (A^T(rho z - y))_{i+1} (column view)
+//     backward: node i+1's own rows (contacts, boxes, initial state) and x_{i+1} from x~_{i+1}.
+__device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
-  const float rho = (float)P.rho, sigma = (float)P.sigma, alpha = (float)P.alpha;
-  const float rho_inv = (float)(1.0 / P.rho);
-  const float oma = 1.f - alpha;
+  const AdmmConst K{(float)P.rho, (float)P.sigma, (float)P.alpha, 1.f - (float)P.alpha,
+                    (float)(1.0 / P.rho)};
+  const float rho = K.rho;
+  Terms T;
+  build_terms(lane, T);
+  TermBytes B;
+  term_bytes<TV_T>(T, B);
+  float* ubuf = sm.bc;      // forward broadcast of u_i
+  float* xib = sm.bc + 32;  // backward broadcast of xi_i
+  // helper: r_i -> V_S(i)
+  auto put_r = [&](int i, bool first) {
+    const float cv = first ? 0.f : col_view<OpSum, TV_T>(sm, i, T, B);
+    if (lane < NV) sm.V(i, V_S)[lane] = K.sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv;
+  };
+  // helper: node i's own rows and x_i
+  auto finish_node = [&](int i) {
+    float* xs = sm.V(i, V_S);
+    bool b = node_rows(sm, lane, i, xs, K);
+    if (lane < NV) {
+      float* x = sm.V(i, V_X);
+      x[lane] = K.alpha * xs[lane] + K.oma * x[lane];
+    }
+    return b;
+  };
 #pragma unroll 1
   for (int it = 0; it < P.n_qp; ++it) {
-    // forward sweep: r_i = sigma x - q^ + A^T(rho z - y); u_i = r_i - C_{i-1} s_{i-1};
-    // s_i = S_i^-1 u_i
-    float g_int = 0.f, gd0 = 0.f, gd1 = 0.f, gd2 = 0.f;
+    const bool first = it == 0;  // x = y = z = 0: r = -q^
+    bool bad = false;
+    // ---- forward
+    if (warp == 1) put_r(0, first);
+    __syncthreads();
+    float gint = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
 #pragma unroll 1
     for (int i = 0; i < NT; ++i) {
-      float* tc = sm.tbuf + (i & 1) * 64;
-      const float* tp = sm.tbuf + ((i + 1) & 1) * 64;
-      fill_t(sm, i, lane, tc, [rho](float4 r, float) { return rho * r.z - r.w; });
-      const float cv = col_view<OpSum>(sm, i, lane, tc, tp);
-      float r = 0.f;
-      if (lane < NV) r = sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv;
-      if (i > 0) {
-        const float* cp = sm.C(i - 1);
-        const float gk = __shfl_sync(FULL, g_int, lane >= 9 && lane < 18 ? lane - 9 : 0);
-        if (lane < 9) {
-          r -= rho * cp[C_INT + 4 * lane] * g_int;
-        } else if (lane < 18) {
-          const int k = lane - 9;
-          r -= rho * (cp[C_INT + 4 * k + 2] * gk + cp[C_DYNU + k] * gd0 +
-                      cp[C_DYNU + 12 + k] * gd1 + cp[C_DYNU + 24 + k] * gd2);
+      if (warp == 0) {
+        float* vs = sm.V(i, V_S);
+        float u = lane < NV ? vs[lane] : 0.f;
+        if (i > 0) {
+          const float* cp = sm.C(i - 1);
+          const float gk = __shfl_sync(FULL, gint, lane >= 9 && lane < 18 ? lane - 9 : 0);
+          if (lane < 9) {
+            u -= rho * cp[C_INT + 4 * lane] * gint;
+          } else if (lane < 18) {
+            const int k = lane - 9;
+            u -= rho * (cp[C_INT + 4 * k + 2] * gk + cp[C_DYNU + k] * g0 + cp[C_DYNU + 12 + k] * g1 +
+                        cp[C_DYNU + 24 + k] * g2);
+          }
         }
+        const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
+        if (lane < NV + 2) vs[lane] = s;          // s_i, gamma_0,1 -> V_S[26,27]
+        if (lane == NV + 2) sm.V(i, V_X)[NV] = s;  // gamma_2 -> V_X[26]
+        gint = lane < 9 ? sm.C(i)[C_INT + 4 * lane + 1] * s : 0.f;
+        g0 = __shfl_sync(FULL, s, 26);
+        g1 = __shfl_sync(FULL, s, 27);
+        g2 = __shfl_sync(FULL, s, 28);
+      } else if (i + 1 < NT) {
+        put_r(i + 1, first);
       }
-      const float s = sinv_mv(sm, i, lane, sm.bc, r);
-      if (lane < NV) sm.V(i, V_S)[lane] = s;
-      if (i + 1 < NT) {
-        const float* cf = sm.C(i);
-        g_int = lane < 9 ? cf[C_INT + 4 * lane + 1] * s : 0.f;
-        const bool dv = lane >= 9 && lane < NV;
-        gd0 = wsum(dv ? cf[C_DYNV + lane] * s : 0.f);
-        gd1 = wsum(dv ? cf[C_DYNV + 28 + lane] * s : 0.f);
-        gd2 = wsum(dv ? cf[C_DYNV + 56 + lane] * s : 0.f);
-      }
+      __syncthreads();
     }
-    // backward sweep: x~_i = s_i - S_i^-1 C_i^T x~_{i+1}; then the row updates of node i
-    // (z~ = A^ x~, relaxation, projection, dual step) and the x relaxation.
-    bool bad = false;
+    // ---- backward
 #pragma unroll 1
     for (int i = NT - 1; i >= 0; --i) {
-      __syncwarp();
-      float xt = lane < NV ? sm.V(i, V_S)[lane] : 0.f;
-      if (i + 1 < NT) {
+      if (warp == 0) {
         const float* cf = sm.C(i);
-        const float* xn = sm.V(i + 1, V_S);
-        float dint = 0.f;
-        if (lane < 9) dint = cf[C_INT + 4 * lane] * xn[lane] + cf[C_INT + 4 * lane + 2] * xn[NQ + lane];
-        const float xq = lane < 9 ? xn[NQ + lane] : 0.f;
-        const float e0 = wsum(lane < 9 ? cf[C_DYNU + lane] * xq : 0.f);
-        const float e1 = wsum(lane < 9 ? cf[C_DYNU + 12 + lane] * xq : 0.f);
-        const float e2 = wsum(lane < 9 ? cf[C_DYNU + 24 + lane] * xq : 0.f);
-        float w = 0.f;
-        if (lane < 9) {
-          w = rho * cf[C_INT + 4 * lane + 1] * dint;
-        } else if (lane < NV) {
-          w = rho * (cf[C_DYNV + lane] * e0 + cf[C_DYNV + 28 + lane] * e1 + cf[C_DYNV + 56 + lane] * e2);
+        float* vs = sm.V(i, V_S);
+        float xt = lane < NV ? vs[lane] : 0.f;
+        if (i + 1 < NT) {
+          const float* xn = sm.V(i + 1, V_S);
+          float dl = 0.f, xi = 0.f;
+          if (lane < 9) {
+            dl = cf[C_INT + 4 * lane] * xn[lane] + cf[C_INT + 4 * lane + 2] * xn[NQ + lane];
+            xi = cf[C_INT + 4 * lane + 1] * dl;
+          } else if (lane < 12) {
+            const float* ub = cf + C_DYNU + 12 * (lane - 9);
+            float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
+            a0 = fmaf(ub[3], xn[NQ + 3], a0);
+            a1 = fmaf(ub[4], xn[NQ + 4], a1);
+            a2 = fmaf(ub[5], xn[NQ + 5], a2);
+            a0 = fmaf(ub[6], xn[NQ + 6], a0);
+            a1 = fmaf(ub[7], xn[NQ + 7], a1);
+            a2 = fmaf(ub[8], xn[NQ + 8], a2);
+            xi = a0 + a1 + a2;
+          }
+          xib[lane] = xi;
+          __syncwarp();
+          const float* Sd = sm.Sinv(i);
+          const int j = lane < SROWS ? lane : SROWS - 1;
+          const float* rw = Sd + j * SROW;  // lanes < 26: row j (= column j); 26..28: W_b
+          float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 9; k += 2) {
+            acc0 = fmaf(rw[k], xib[k], acc0);
+            if (k + 1 < 9) acc1 = fmaf(rw[k + 1], xib[k + 1], acc1);
+          }
+          if (lane < NV) {
+#pragma unroll
+            for (int b = 0; b < 3; ++b) acc1 = fmaf(Sd[(NV + b) * SROW + j], xib[9 + b], acc1);
+          } else {
+            const int b = j - NV;
+#pragma unroll
+            for (int b2 = 0; b2 < 3; ++b2) acc1 = fmaf(cf[C_G + 3 * b + b2], xib[9 + b2], acc1);
+          }
+          const float acc = acc0 + acc1;
+          float zt = 0.f;
+          int slot = -1;
+          if (lane < NV) {
+            xt -= rho * acc;
+            vs[lane] = xt;
+            if (lane < 9) {  // z~ of integration row k: a2 x~_i[q_k] + (a1, a3) . x~_{i+1}
+              zt = fmaf(cf[C_INT + 4 * lane + 1], xt, dl);
+              slot = lane;
+            }
+          } else if (lane < SROWS) {  // z~ of dynamics row b: v_b.x~_i + u_b.x~_{i+1}
+            const int b = lane - NV;
+            const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
+            zt = gam - rho * acc + xib[9 + b];
+            slot = 9 + b;
+          }
+          if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+          __syncwarp();
         }
-        xt -= sinv_mv(sm, i, lane, sm.bc, w);
-        if (lane < NV) sm.V(i, V_S)[lane] = xt;
-        __syncwarp();
+        bad = bad || !isfinite(xt);
+      } else if (i + 1 < NT) {
+        bad = finish_node(i + 1) || bad;
       }
-      bad = bad || !isfinite(xt);
-      float o0, o1, o2;
-      row_view<OpSum>(sm, i, lane, V_S, o0, o1, o2);
-      auto upd = [&](int s, float zt) {
-        const int ri = sm.ridx(i, s);
-        float4 rd = sm.row[ri];
-        const float w = alpha * zt + oma * rd.z;
-        const float zn = fminf(fmaxf(w + rho_inv * rd.w, rd.x), rd.y);
-        rd.w = rd.w + rho * (w - zn);
-        rd.z = zn;
-        sm.row[ri] = rd;
-        bad = bad || !isfinite(zt);
-      };
-      upd(lane, o0);
-      if (lane < 8) upd(32 + lane, o1);
-      if (i == 0 && lane < NINIT) upd(NSLOT + lane, o2);
-      if (lane < NV) {
-        float* x = sm.V(i, V_X);
-        x[lane] = alpha * xt + oma * x[lane];
-      }
+      __syncthreads();
     }
-    if (__any_sync(FULL, bad)) return it;
+    if (warp == 1) bad = finish_node(0) || bad;
+    if (__syncthreads_or(bad)) return it;
   }
-  __syncwarp();
   return -1;
 }
 
@@ -1061,11 +1229,12 @@ __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage,
   }
 }
 
-__global__ void __launch_bounds__(32) rti_kernel(const KParams P) {
+__global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
   extern __shared__ __align__(16) float smem[];
   const int agent = blockIdx.x;
   if (agent >= P.n_agents) return;
-  const int lane = threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int warp = threadIdx.x >> 5;
   const int NT = P.NT;
   const Layout L = make_layout(NT);
   Sm sm;
@@ -1074,28 +1243,23 @@ __global__ void __launch_bounds__(32) rti_kernel(const KParams P) {
   sm.vec = smem + L.vec;
   sm.row = reinterpret_cast<float4*>(smem + L.row);
   sm.dsc = smem + L.dsc;
-  sm.icoef = smem + L.icoef;
-  sm.tbuf = smem + L.tbuf;
   sm.bc = smem + L.bc;
-  sm.g = smem + L.g;
   sm.flags = reinterpret_cast<uint32_t*>(smem + L.flags);
   sm.NT = NT;
   long long t0 = P.profile ? clock64() : 0;
 
-  // zero-initialise coefficients, rows, vectors; d = e = 1
-  for (int k = lane; k < NT * C_SIZE; k += 32) sm.coef[k] = 0.f;
-  const int nrow = NT * NSLOT + NINIT;
-  for (int r = lane; r < nrow; r += 32) {
+  // zero coefficients (incl. block -1), rows, vectors; d = e = 1
+  const int tid = threadIdx.x;
+  for (int k = tid; k < (NT + 1) * C_SIZE; k += 64) sm.coef[k] = 0.f;
+  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
     sm.row[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     sm.dsc[r] = 1.f;
   }
-  for (int k = lane; k < NT * V_NUM * V_STRIDE; k += 32) sm.vec[k] = 0.f;
-  for (int i = 0; i < NT; ++i)
+  for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;
+  __syncthreads();
+  for (int i = warp; i < NT; i += 2)
     if (lane < NV) sm.V(i, V_E)[lane] = 1.f;
-  if (lane < 20) sm.icoef[lane] = 0.f;
-  for (int k = lane; k < 256; k += 32) sm.g[k] = 0.f;
-  if (lane < 32) { sm.tbuf[lane] = 0.f; sm.tbuf[32 + lane] = 0.f; sm.tbuf[64 + lane] = 0.f; sm.tbuf[96 + lane] = 0.f; }
-  __syncwarp();
+  sm.bc[tid] = 0.f;
 
   const rmpc_state st = P.states[agent];
   const rmpc_command cmd = P.cmds[agent];
@@ -1114,55 +1278,70 @@ __global__ void __launch_bounds__(32) rti_kernel(const KParams P) {
   bool st_ok = true;
 #pragma unroll
   for (int k = 0; k < 9; ++k) st_ok = st_ok && isfinite(st.q[k]) && isfinite(st.qd[k]);
-  prof_mark(P, lane, 0, t0);
+  prof_mark(P, threadIdx.x, 0, t0);
+  __syncthreads();
 
-  bool ok = setup_nodes(P, sm, lane, st, cmd, gait, warm, pz) && st_ok;
-  __syncwarp();
-  prof_mark(P, lane, 2, t0);
+  int ok = 1;
+  if (warp == 0) ok = setup_nodes(P, sm, lane, st, cmd, gait, warm, pz) && st_ok;
+  ok = __syncthreads_and(ok);
+  prof_mark(P, threadIdx.x, 2, t0);
   if (!ok) {
     out.status = RMPC_STATUS_NONFINITE_INPUT;
   } else {
-    if (P.ruiz_iters > 0) ruiz(P, sm, lane);
-    apply_scaling(P, sm, lane);
-    prof_mark(P, lane, 3, t0);
-    if (!factorize(P, sm, lane)) {
+    if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
+    apply_scaling(P, sm, lane, warp);
+    prof_mark(P, threadIdx.x, 3, t0);
+    int good = 1;
+    if (warp == 0) good = factorize(P, sm, lane);
+    good = __syncthreads_and(good);
+    if (!good) {
       out.status = RMPC_STATUS_SINGULAR;
     } else {
-      prof_mark(P, lane, 4, t0);
-      const int bad_it = admm(P, sm, lane);
-      prof_mark(P, lane, 5, t0);
+      prof_mark(P, threadIdx.x, 4, t0);
+      const int bad_it = admm(P, sm, lane, warp);
+      prof_mark(P, threadIdx.x, 5, t0);
       if (bad_it >= 0) {
         out.status = RMPC_STATUS_DIVERGED;
         out.fail_iter = bad_it;
       }
     }
   }
+  if (warp != 0) return;  // residuals, z* and inverse dynamics on the solver warp
 
   if (out.status == RMPC_STATUS_OK) {
-    // residuals and objective on the unscaled problem (qp.cpp:192-200), z*, ||dz||_inf
+    // unscaled residuals (qp.cpp:192-200): prim = |A^x - z| / d, dual = |P^x + q^ + A^T y| / e
+    Terms T;
+    build_terms(lane, T);
+    TermBytes B;
+    term_bytes<TV_Y>(T, B);
     float prim = 0.f, dual = 0.f, dinf = 0.f;
     double obj = 0.0;
+    const float rho = (float)P.rho;
 #pragma unroll 1
     for (int i = 0; i < NT; ++i) {
       float o0, o1, o2;
       row_view<OpSum>(sm, i, lane, V_X, o0, o1, o2);
-      auto pr = [&](int s, float ax) {
-        const int r = sm.ridx(i, s);
-        prim = fmaxf(prim, fabsf(ax - sm.row[r].z) / sm.dsc[r]);
-      };
-      pr(lane, o0);
-      if (lane < 8) pr(32 + lane, o1);
-      if (i == 0 && lane < NINIT) pr(NSLOT + lane, o2);
-      float* tc = sm.tbuf + (i & 1) * 64;
-      const float* tp = sm.tbuf + ((i + 1) & 1) * 64;
-      fill_t(sm, i, lane, tc, [](float4 r, float) { return r.w; });
-      const float aty = col_view<OpSum>(sm, i, lane, tc, tp);
+      const float4* rw = sm.R(i);
+      const float* d = sm.D(i);
+      prim = fmaxf(prim, fabsf(o0 - rw[lane].z) / d[lane]);
+      if (lane < 8) prim = fmaxf(prim, fabsf(o1 - rw[32 + lane].z) / d[32 + lane]);
+      if (i == 0 && lane < NINIT)
+        prim = fmaxf(prim, fabsf(o2 - sm.R(-1)[INIT0 + lane].z) / sm.D(-1)[INIT0 + lane]);
+      const float aty = col_view<OpSum, TV_Y>(sm, i, T, B, rho);
+      const uint32_t bits = sm.flags[i];
       if (lane < NV) {
         const float x = sm.V(i, V_X)[lane], e = sm.V(i, V_E)[lane];
-        const float pd = sm.V(i, V_PD)[lane], qh = sm.V(i, V_QH)[lane];
-        dual = fmaxf(dual, fabsf(pd * x + qh + aty) / e);
-        obj += 0.5 * (double)pd * (double)x * (double)x + (double)qh * (double)x;
+        dual = fmaxf(dual, fabsf(phat(P, sm, i, lane) * x + sm.V(i, V_QH)[lane] + aty) / e);
+        // objective on the unscaled problem in FP64: 1/2 w dt dz^2 + w dt (g - des) dz
+        double g, des;
+        guess_and_target(P, i, lane, warm, pz, st, cmd, bits, g, des);
+        const double w = wcost(P, lane) * P.dt[i];
+        const double dz = (double)e * (double)x;
+        obj += 0.5 * w * dz * dz + w * (g - des) * dz;
         dinf = fmaxf(dinf, fabsf(e * x));
+        const double zv = g + dz;  // z* = guess + dz (mpc.cpp:308-314)
+        if (P.z_out) P.z_out[((size_t)agent * NT + i) * NV + lane] = (float)zv;
+        if (i < 2) reinterpret_cast<double*>(sm.sinv)[i * 32 + lane] = zv;  // S^-1 is dead
       }
     }
     prim = wmax(prim);
@@ -1173,31 +1352,8 @@ __global__ void __launch_bounds__(32) rti_kernel(const KParams P) {
     out.dual_res = dual;
     out.delta_inf_norm = dinf;
     out.v_mpc = (float)obj;
-
-    // z* = guess + dz (mpc.cpp:308-314), double guess + float step
-    const bool want_z = P.z_out != nullptr;
-#pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
-      const uint32_t bits = sm.flags[i];
-      double g = 0.0;
-      if (lane < NV) {
-        if (warm) {
-          g = (double)pz[min(i + 1, NT - 1) * NV + lane];
-        } else if (lane < 9) {
-          g = lane == 0 ? st.q[0] : P.nominal[lane];
-        } else if (lane >= 18) {
-          const int c = (lane - 18) >> 1;
-          const int na = __popc(bits);
-          g = ((lane - 18) & 1) && ((bits >> c) & 1u) && na > 0 ? P.weight / na : 0.0;
-        }
-        const double zv = g + (double)sm.V(i, V_E)[lane] * (double)sm.V(i, V_X)[lane];
-        if (want_z) P.z_out[((size_t)agent * NT + i) * NV + lane] = (float)zv;
-        if (i < 2) reinterpret_cast<double*>(sm.sinv)[i * 32 + lane] = zv;  // S^-1 is dead now
-      }
-    }
     __syncwarp();
-    // inverse dynamics at node 0 (mpc.cpp:320-330), FP64 on lane 0
-    if (lane == 0) {
+    if (lane == 0) {  // inverse dynamics at node 0 (mpc.cpp:320-330), FP64
       const double* z0 = reinterpret_cast<const double*>(sm.sinv);
       const double* z1 = z0 + 32;
       double q[9], qd[9], qdd[9], F[8], gen[9];
@@ -1234,6 +1390,6 @@ int rmpc_kernel_setup(int NT) {
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   if (params.n_agents <= 0) return 0;
   const int bytes = rmpc_dev::smem_bytes(params.NT);
-  rmpc_dev::rti_kernel<<<params.n_agents, 32, bytes, (cudaStream_t)stream>>>(params);
+  rmpc_dev::rti_kernel<<<params.n_agents, 64, bytes, (cudaStream_t)stream>>>(params);
   return (int)cudaGetLastError();
 }

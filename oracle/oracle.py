@@ -22,7 +22,7 @@ ORACLE_SOLUTION_DTYPE = np.dtype([
     ("tau_ff", np.float64, (6,)), ("q_set", np.float64, (6,)), ("qd_set", np.float64, (6,)),
     ("f0", np.float64, (8,)), ("base_residual", np.float64, (3,)),
     ("v_mpc", np.float64), ("prim_res", np.float64), ("dual_res", np.float64),
-    ("delta_inf_norm", np.float64),
+    ("delta_inf_norm", np.float64), ("v_quad", np.float64), ("v_lin", np.float64),
     ("status", np.int32), ("fail_iter", np.int32), ("n_vars", np.int32), ("n_cons", np.int32),
     ("ldl_nnz", np.int32), ("pad", np.int32),
 ])
@@ -96,6 +96,13 @@ def flops(model: Model, settings: Settings, state, cmd, gait):
     lib().oracle_flops(C.byref(model), C.byref(settings), ptr(st), ptr(_f64(cmd, (3,))),
                        ptr(_f64(gait, (7,))), ptr(by), ptr(ops))
     return by, dict(zip(("add", "mul", "div", "sqrt", "trig", "cmp"), ops))
+
+
+def rng_uniform(seed: int, stream: int, n: int) -> np.ndarray:
+    """n uniform() draws of rmpc::Rng(seed, stream) (rng.hpp), C++ restatement."""
+    out = np.zeros(n)
+    lib().oracle_rng_uniform(C.c_uint64(seed), C.c_uint64(stream), C.c_int32(n), ptr(out))
+    return out
 
 
 def nominal_pose(model: Model) -> np.ndarray:

@@ -15,6 +15,7 @@ extern "C" {
 typedef struct oracle_solution {
   double tau_ff[6], q_set[6], qd_set[6], f0[8], base_residual[3];
   double v_mpc, prim_res, dual_res, delta_inf_norm;
+  double v_quad, v_lin;  // the two terms of V = 1/2 x^T P x + q^T x (cancellation scale)
   int32_t status, fail_iter, n_vars, n_cons, ldl_nnz, pad;
 } oracle_solution;
 
@@ -28,6 +29,7 @@ static void fill(const Solution& s, oracle_solution* o) {
   for (int k = 0; k < 8; ++k) o->f0[k] = s.f0[k];
   for (int b = 0; b < 3; ++b) o->base_residual[b] = s.base_res[b];
   o->v_mpc = s.v_mpc; o->prim_res = s.prim_res; o->dual_res = s.dual_res; o->delta_inf_norm = s.delta_inf;
+  o->v_quad = s.v_quad; o->v_lin = s.v_lin;
   o->status = s.status; o->fail_iter = s.fail_iter;
   o->n_vars = s.n; o->n_cons = s.m; o->ldl_nnz = s.ldl_nnz; o->pad = 0;
 }
@@ -108,6 +110,41 @@ int32_t oracle_flops(const rmpc_model* model, const rmpc_settings* st, const rmp
     ops[3] = (double)tot.sqrt; ops[4] = (double)tot.trig; ops[5] = (double)tot.cmp;
   }
   return s.status;
+}
+
+// xoshiro256++ with splitmix64 seeding, restated from rng.hpp:15-75 (stream constructor
+// Rng(seed, stream)).  out[n] = uniform() draws of one stream.
+namespace {
+struct Rng {
+  uint64_t s[4];
+  static uint64_t splitmix(uint64_t x) {
+    x += 0x9e3779b97f4a7c15ULL;
+    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+    return x ^ (x >> 31);
+  }
+  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+  Rng(uint64_t seed, uint64_t stream) {
+    uint64_t x = seed ^ splitmix(stream + 0x9e3779b97f4a7c15ULL);
+    for (auto& w : s) {
+      x += 0x9e3779b97f4a7c15ULL;
+      w = splitmix(x);
+    }
+  }
+  uint64_t next() {
+    const uint64_t r = rotl(s[0] + s[3], 23) + s[0];
+    const uint64_t t = s[1] << 17;
+    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t;
+    s[3] = rotl(s[3], 45);
+    return r;
+  }
+  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
+};
+}  // namespace
+
+void oracle_rng_uniform(uint64_t seed, uint64_t stream, int32_t n, double* out) {
+  Rng r(seed, stream);
+  for (int i = 0; i < n; ++i) out[i] = r.uniform();
 }
 
 // ---------------------------------------------------------------- model-level functions

@@ -735,7 +735,7 @@ struct AdmmSettings {  // qp.hpp:29-36
 template <class T>
 struct QpResult {
   std::vector<T> x, y, z;
-  T prim = T(0.0), dual = T(0.0), obj = T(0.0);
+  T prim = T(0.0), dual = T(0.0), obj = T(0.0), obj_quad = T(0.0), obj_lin = T(0.0);
   int iters_run = 0;
   int ldl_nnz = 0;
 };
@@ -876,6 +876,14 @@ QpResult<T> admm_solve(const Qp<T>& qp, const AdmmSettings& st, const std::vecto
   res.iters_run = it;
   residuals(res.prim, res.dual);
   res.obj = qp_value(qp, res.x);
+  {
+    std::vector<T> px;
+    symv_upper(qp.P, res.x, px);
+    T a = T(0.0), b = T(0.0);
+    for (int i = 0; i < n; ++i) { a += res.x[i] * px[i]; b += qp.q[i] * res.x[i]; }
+    res.obj_quad = T(0.5) * a;
+    res.obj_lin = b;
+  }
   res.ldl_nnz = ldl.Lp[ldl.n];
   lap(kAdmm);
   return res;
@@ -1112,6 +1120,7 @@ struct Solution {
   std::vector<double> z_star;  // T x 26 (q | qd | F per node)
   double tau_ff[kNj] = {0}, q_set[kNj] = {0}, qd_set[kNj] = {0}, f0[kNf] = {0};
   double v_mpc = 0, prim_res = 0, dual_res = 0, delta_inf = 0, base_res[3] = {0};
+  double v_quad = 0, v_lin = 0;
   double stage_s[kNumStages] = {0};
   int m = 0, n = 0, ldl_nnz = 0;
 };

@@ -103,6 +103,8 @@ Solution rti_step(const rmpc_model& model, const rmpc_settings& st, const double
     }
     sol.delta_inf = (double)dinf;
     sol.v_mpc = (double)r.obj;
+    sol.v_quad = (double)r.obj_quad;
+    sol.v_lin = (double)r.obj_lin;
     sol.prim_res = (double)r.prim;
     sol.dual_res = (double)r.dual;
     T qdd[kNq];

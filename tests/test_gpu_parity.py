@@ -1,0 +1,183 @@
+"""Parity of the sm_100a solver (through the C ABI) with the FP64 CPU oracle on identical
+synthetic inputs, plus the batch-runtime contracts of batch.hpp:20-46.  Needs a B200."""
+import numpy as np
+import pytest
+
+import paper_2510_12717_b200 as R
+from paper_2510_12717_b200.abi import (SOLUTION_DTYPE, STATUS_DIVERGED, STATUS_NONFINITE_INPUT,
+                                       STATUS_OK, default_model, default_settings)
+from parity import TOL, compare, summary
+
+pytestmark = pytest.mark.gpu
+
+
+def run_both(oracle, kind, T, n, seed=1, workers=16):
+    m, s = default_model(), default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, kind, seed=seed, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    sol, z = br.solve(st, cm, ga, want_z=True)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=workers)
+    return sol, z, ref, zr, (m, s, st, cm, ga, br)
+
+
+@pytest.mark.parametrize("kind,T,n", [("standing", 10, 1), ("standing", 12, 8), ("random", 10, 4096),
+                                      ("random", 5, 2048), ("random", 20, 1024),
+                                      ("mixed", 10, 2048), ("random", 12, 512)])
+def test_parity_with_oracle(oracle, kind, T, n):
+    sol, z, ref, zr, _ = run_both(oracle, kind, T, n)
+    c = compare(sol, ref, z, zr)
+    print(kind, T, n, summary(c))
+    assert c["status_equal"] and c["n_ok"] == n
+    assert c["tau"].max() <= TOL
+    assert c["f0"].max() <= TOL
+    assert c["v"].max() <= TOL
+    assert c["q_set"].max() <= 1e-4
+    assert c["z"].max() <= 1e-3
+
+
+def test_standing_equilibrium_on_gpu(oracle):
+    """test_mpc.cpp:235-259 on the device: dz ~ 0 and F_z = mg/4 at the equilibrium."""
+    m, s = default_model(), default_settings(12)
+    st, cm, ga = R.synthetic_batch(1, "standing", model=m, settings=s)
+    sol, z = R.BatchRunner(1, m, s).solve(st, cm, ga, want_z=True)
+    assert sol["status"][0] == STATUS_OK and sol["delta_inf_norm"][0] <= 1e-3
+    np.testing.assert_allclose(sol["f0"][0, 1::2], m.total_mass() * m.gravity / 4, rtol=1e-3)
+
+
+def test_nonfinite_inputs_fail_like_oracle(oracle):
+    """NaN state -> StructuralError (mpc.cpp:70-72); NaN command -> DivergenceError at
+    iteration 0 (qp.cpp:159-161); the other agents are untouched (batch.hpp:29-31)."""
+    m, s = default_model(), default_settings(10)
+    st, cm, ga = R.synthetic_batch(6, "random", seed=4, model=m, settings=s)
+    st[1, 3] = np.nan
+    st[2, 9] = np.inf
+    cm[4, 1] = np.nan
+    sol, _ = R.BatchRunner(6, m, s).solve(st, cm, ga)
+    ref, _, _, _ = oracle.solve_batch(m, s, st, cm, ga)
+    assert list(ref["status"]) == [STATUS_OK, STATUS_NONFINITE_INPUT, STATUS_NONFINITE_INPUT,
+                                   STATUS_OK, STATUS_DIVERGED, STATUS_OK]
+    assert list(sol["status"]) == list(ref["status"])
+    assert sol["fail_iter"][4] == ref["fail_iter"][4] == 0
+    good = [0, 3, 5]
+    c = compare(sol[good], ref[good])
+    assert c["tau"].max() <= TOL
+    assert np.all(sol["tau_ff"][[1, 2, 4]] == 0)
+
+
+def test_warm_start_chain(oracle):
+    """Warm start from the previous z* (mpc.cpp:258-265) over three ticks; the oracle gets the
+    same previous z* (the FP32 values), so each tick is compared on identical inputs."""
+    m = default_model()
+    s = default_settings(10)
+    s.warm_start = 1
+    n = 512
+    st, cm, ga = R.synthetic_batch(n, "random", seed=8, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    prev = None
+    for tick in range(3):
+        sol, z = br.solve(st, cm, ga, prev=prev, want_z=True)
+        pz = prev[1].astype(np.float64) if prev is not None else None
+        pok = prev[0]["status"] if prev is not None else None
+        ref, _, _, _ = oracle.solve_batch(m, s, st, cm, ga, prev_z=pz, prev_ok=pok, workers=16)
+        c = compare(sol, ref)
+        print("tick", tick, summary(c))
+        assert c["status_equal"] and c["tau"].max() <= TOL and c["f0"].max() <= TOL
+        assert c["v"].max() <= TOL
+        prev = (sol, z)
+        ga[:, 0] = (ga[:, 0] + 0.01 / ga[:, 1]) % 1.0
+
+
+def test_batch_equals_serial_and_order_free():
+    """batch.hpp:20-23, SPEC acceptance #8: element i is bit-identical to a serial solve and
+    does not depend on processing order or sharding."""
+    m, s = default_model(), default_settings(10)
+    n = 64
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=5, model=m, settings=s)
+    sol, z = R.BatchRunner(n, m, s).solve(st, cm, ga, want_z=True)
+    one = R.BatchRunner(1, m, s)
+    for i in (0, 17, 63):
+        si, zi = one.solve(st[i:i + 1], cm[i:i + 1], ga[i:i + 1], want_z=True)
+        assert si.tobytes() == sol[i:i + 1].tobytes() and zi.tobytes() == z[i:i + 1].tobytes()
+    perm = np.random.default_rng(0).permutation(n)
+    sp, _ = R.BatchRunner(n, m, s).solve(st[perm], cm[perm], ga[perm], order=list(range(n)))
+    assert sp.tobytes() == sol[perm].tobytes()
+    sh, zh = R.BatchRunner(n, m, s, devices=[0, 0, 0]).solve(st, cm, ga, want_z=True)
+    assert sh.tobytes() == sol.tobytes() and zh.tobytes() == z.tobytes()
+
+
+def test_device_path_matches_host_path():
+    import torch
+    m, s = default_model(), default_settings(10)
+    n = 1000
+    st, cm, ga = R.synthetic_batch(n, "random", seed=6, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    sol, z = br.solve(st, cm, ga, want_z=True)
+    dev = torch.device("cuda:0")
+    stream = torch.cuda.Stream()
+    with torch.cuda.stream(stream):
+        t = [torch.from_numpy(a).to(dev) for a in (st, cm, ga)]
+        out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        zd = torch.zeros(n * 10 * 26, dtype=torch.float32, device=dev)
+        br.solve_device(*t, out, z_out=zd, stream=stream)
+    stream.synchronize()
+    got = np.frombuffer(out.cpu().numpy().tobytes(), dtype=SOLUTION_DTYPE)
+    assert got.tobytes() == sol.tobytes()
+    assert zd.cpu().numpy().tobytes() == z.reshape(-1).tobytes()
+
+
+def test_full_size_properties_and_sampled_parity(oracle):
+    """16,384 agents (BASELINE config C3): every solve OK and finite; a 256-agent sample of the
+    same batch matches the oracle (a checksum of the full batch is also stable run to run)."""
+    m, s = default_model(), default_settings(10)
+    n = 16384
+    st, cm, ga = R.synthetic_batch(n, "random", seed=0, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    sol, z = br.solve(st, cm, ga, want_z=True)
+    assert np.all(sol["status"] == STATUS_OK)
+    for k in ("tau_ff", "f0", "v_mpc", "prim_res", "dual_res"):
+        assert np.all(np.isfinite(sol[k]))
+    sol2, _ = br.solve(st, cm, ga)
+    assert sol2.tobytes() == sol.tobytes()
+    idx = np.random.default_rng(1).choice(n, 256, replace=False)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st[idx], cm[idx], ga[idx], workers=16)
+    c = compare(sol[idx], ref, z[idx], zr)
+    print(summary(c))
+    assert c["tau"].max() <= TOL and c["f0"].max() <= TOL and c["v"].max() <= TOL
+
+
+def test_solution_record_consistency():
+    """q_set / qd_set / F*[0] are node 0 of z* (mpc.cpp:320-329)."""
+    m, s = default_model(), default_settings(10)
+    st, cm, ga = R.synthetic_batch(128, "random", seed=9, model=m, settings=s)
+    sol, z = R.BatchRunner(128, m, s).solve(st, cm, ga, want_z=True)
+    np.testing.assert_allclose(sol["q_set"], z[:, 0, 3:9], atol=1e-6)
+    np.testing.assert_allclose(sol["qd_set"], z[:, 0, 12:18], atol=1e-6)
+    np.testing.assert_allclose(sol["f0"], z[:, 0, 18:26], atol=1e-4)
+
+
+def test_timing_report_and_stage_profile():
+    m, s = default_model(), default_settings(10)
+    n = 2048
+    st, cm, ga = R.synthetic_batch(n, "random", seed=2, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    br.solve(st, cm, ga)
+    t = br.last_timing()
+    assert t["batch_size"] == n and t["devices"] == 1
+    assert t["kernel_ms"] > 0 and t["total_ms"] >= t["kernel_ms"]
+    br.set_stage_profiling(True)
+    br.solve(st, cm, ga)
+    t = br.last_timing()
+    assert abs(sum(t["stage_ms"].values()) - t["kernel_ms"]) <= 1e-6 * t["kernel_ms"] + 1e-9
+    assert t["stage_ms"]["admm_iters"] > 0 and t["stage_ms"]["ruiz"] > 0
+
+
+def test_mpc_torque_from_gpu_solution(oracle):
+    m, s = default_model(), default_settings(10)
+    st, cm, ga = R.synthetic_batch(4, "random", seed=3, model=m, settings=s)
+    br = R.BatchRunner(4, m, s)
+    sol, _ = br.solve(st, cm, ga)
+    for i in range(4):
+        tau = br.mpc_torque(sol[i], st[i])
+        ref = oracle.pd_torque(m, sol["q_set"][i].astype(np.float64), sol["qd_set"][i].astype(np.float64),
+                               st[i, :9], st[i, 9:], sol["tau_ff"][i].astype(np.float64))
+        np.testing.assert_allclose(tau, ref, atol=1e-12)

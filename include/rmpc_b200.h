@@ -166,7 +166,10 @@ int32_t rmpc_set_stage_profiling(rmpc_handle* handle, int32_t enabled);
 /* Build provenance: "sm_100a" and the kernel variant compiled in. */
 const char* rmpc_build_info(void);
 
-/* Dynamic shared memory one agent (one warp) needs at `horizon` nodes. */
+/* Measured FP32 FMA throughput of `device` (TFLOP/s): the CUDA-core roofline denominator. */
+int32_t rmpc_fma_peak(int32_t device, double* tflops);
+
+/* Dynamic shared memory one agent (one CTA) needs at `horizon` nodes. */
 int32_t rmpc_smem_bytes(int32_t horizon);
 /* sizeof of the ABI structs (0 model, 1 settings, 2 state, 3 command, 4 gait, 5 solution,
  * 6 timing) for binding-side layout checks. */

@@ -296,6 +296,22 @@ void fill_timing(rmpc_handle& h, double total_ms) {
 
 }  // namespace
 
+// FP32 FMA throughput probe: 8 independent FMA chains per thread, enough resident warps to
+// saturate every SM.  The roofline denominator of bench.py ("of measured").
+__global__ void fma_peak_kernel(float* out, int iters, float a, float b) {
+  float x0 = threadIdx.x * 1e-7f, x1 = x0 + 1e-7f, x2 = x0 + 2e-7f, x3 = x0 + 3e-7f;
+  float x4 = x0 + 4e-7f, x5 = x0 + 5e-7f, x6 = x0 + 6e-7f, x7 = x0 + 7e-7f;
+  for (int i = 0; i < iters; ++i) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
+      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+    }
+  }
+  const float r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (r == 1.2345f) out[0] = r;  // keep the chains alive
+}
+
 extern "C" {
 
 void rmpc_model_default(rmpc_model* p) {
@@ -483,6 +499,37 @@ int32_t rmpc_set_stage_profiling(rmpc_handle* h, int32_t enabled) {
 
 const char* rmpc_build_info(void) {
   return "rmpc_b200 sm_100a fused warp-per-agent RTI kernel (reduced SPD block-tridiagonal ADMM, FP32 + FP64 linearization)";
+}
+
+int32_t rmpc_fma_peak(int32_t device, double* tflops) {
+  if (!tflops) return RMPC_ERR_INVALID_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return RMPC_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  float* d = nullptr;
+  cudaMalloc(&d, sizeof(float));
+  const int threads = 256, blocks = sms * 8, iters = 4096;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fma_peak_kernel<<<blocks, threads>>>(d, 64, 0.999f, 1e-6f);  // warm-up
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    fma_peak_kernel<<<blocks, threads>>>(d, iters, 0.999f, 1e-6f);
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const cudaError_t e = cudaGetLastError();
+  *tflops = best;
+  return e == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
 }
 
 int32_t rmpc_smem_bytes(int32_t horizon) { return rmpc_dev::smem_bytes(horizon); }

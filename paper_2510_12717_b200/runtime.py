@@ -29,7 +29,7 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_solve", "rmpc_solve_device", "rmpc_size", "rmpc_workers", "rmpc_horizon",
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
-           "rmpc_smem_bytes", "rmpc_sizeof")
+           "rmpc_smem_bytes", "rmpc_sizeof", "rmpc_fma_peak")
 
 
 class RmpcError(RuntimeError):
@@ -76,7 +76,18 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_smem_bytes.restype = _I
     L.rmpc_sizeof.argtypes = [_I]
     L.rmpc_sizeof.restype = _I
+    L.rmpc_fma_peak.argtypes = [_I, _VP]
+    L.rmpc_fma_peak.restype = _I
     return L
+
+
+def fma_peak_tflops(device: int = 0) -> float:
+    """Measured FP32 FMA peak of `device` (TFLOP/s), the roofline denominator."""
+    v = C.c_double(0.0)
+    rc = library().rmpc_fma_peak(device, C.byref(v))
+    if rc != 0:
+        raise RmpcError(rc, "rmpc_fma_peak failed")
+    return v.value
 
 
 def library():
@@ -182,6 +193,8 @@ class BatchRunner:
         s = None
         if stream is not None:
             s = stream if isinstance(stream, int) else stream.cuda_stream
+            if s == 0:
+                s = 1  # cudaStreamLegacy: NULL would select the runner's own stream
         rc = self._lib.rmpc_solve_device(self._h, p(states), p(cmds), p(gaits), p(prev), p(prev_z),
                                          p(out), p(z_out), s)
         if rc != 0:

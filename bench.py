@@ -228,7 +228,8 @@ def main():
     m, s = R.default_model(), R.default_settings(T)
     # this rank's contiguous agent range [rank n, (rank+1) n) of the global batch
     st_all, cm_all, ga_all = R.synthetic_batch(n * world, args.kind, seed=0, model=m, settings=s)
-    lo, hi = rank * n, (rank + 1) * n
+    from paper_2510_12717_b200.sharding import shard_range
+    lo, hi = shard_range(rank, world, n * world)
     st, cm, ga = st_all[lo:hi].copy(), cm_all[lo:hi].copy(), ga_all[lo:hi].copy()
     br = R.BatchRunner(n, m, s, devices=[local])
     stream = torch.cuda.Stream(device=dev)

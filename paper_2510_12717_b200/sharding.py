@@ -1,0 +1,21 @@
+"""Agent sharding across ranks / devices: agents are independent, so each
+rank owns a contiguous agent range and there is no collective on the solve path.  The only
+cross-rank traffic is the benchmark's barrier and max-over-ranks timing reduction."""
+from __future__ import annotations
+
+
+def shard_range(rank: int, world: int, n_total: int) -> tuple[int, int]:
+    """Contiguous range [lo, hi) of rank `rank`: floor(r n / W) .. floor((r+1) n / W), the same
+    split rmpc_create uses across devices (rmpc_host.cu)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad rank/world")
+    return rank * n_total // world, (rank + 1) * n_total // world
+
+
+def max_over_ranks(values, dist=None, device=None):
+    """Element-wise max of a list of floats over all ranks (the timing rule of bench.py)."""
+    import torch
+    t = torch.tensor(list(values), dtype=torch.float64, device=device)
+    if dist is not None and dist.is_initialized() and dist.get_world_size() > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return t.cpu().tolist()

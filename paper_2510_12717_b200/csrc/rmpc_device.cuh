@@ -47,6 +47,10 @@ constexpr int C_G = 250;      // [9]: G_bb' = v_b^T S_i^-1 v_b' (dynamics rows)
 constexpr int C_SIZE = 260;
 constexpr int C_ZERO = C_INT + 3;  // an entry that is always 0
 
+// Split of the horizon for the two-sided (twisted) elimination: warp 0 owns nodes [0, m)
+// eliminated top-down plus the middle node m, warp 1 owns (m, T) eliminated bottom-up.
+__host__ __device__ inline int mid_node(int NT) { return NT >= 2 ? (NT - 2) / 2 : 0; }
+
 // Per-node vectors, V_STRIDE floats each; [26, 28) are spare (gamma of the forward sweep).
 constexpr int V_X = 0;    // ADMM x (scaled space)
 constexpr int V_QH = 1;   // q^ = e * q
@@ -92,7 +96,7 @@ __host__ __device__ inline Layout make_layout(int NT) {
   L.vec = o;   o += NT * V_NUM * V_STRIDE;
   L.row = o;   o += 4 * (NT + 1) * NSLOT;           // float4 {lo, hi, z, t = rho z - y}
   L.dsc = o;   o += (NT + 1) * NSLOT;               // Ruiz row scale d
-  L.bc = o;    o += 64;                             // broadcast buffers (2 x 32)
+  L.bc = o;    o += 128;                            // per warp: 2 x 32 broadcast buffers
   L.flags = o; o += align4(NT);
   L.total = o;
   return L;

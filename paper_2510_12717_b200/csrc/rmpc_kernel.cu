@@ -783,202 +783,342 @@ __device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp
 }
 
 // ------------------------------------------------------------------------- stage: factor
-// Block elimination of H.  Lane j holds row j of the 26 x 26 blocks in registers; S_i^-1 is
-// formed by Gauss-Jordan (SPD, no pivoting) and stored with W_b = S_i^-1 v_b appended as
-// rows 26..28.  Returns false on a non-positive pivot (SingularityError, ldl.cpp:155-160).
-__device__ bool factorize(const KParams& P, const Sm& sm, int lane) {
-  const int NT = P.NT;
+// Two-sided block elimination of the block-tridiagonal H (26 x 26 blocks):
+//   top    (warp 0, i = 0..m-1):   S_i = D_i - rho^2 U_{i-1} G_{i-1} U_{i-1}^T,  G = V^T S^-1 V
+//   bottom (warp 1, i = T-1..m+1): T_i = D_i - rho^2 V_i G'_i V_i^T,            G' = U^T T^-1 U
+//   middle (warp 0, i = m):        M   = D_m - (top update) - (bottom update)
+// with U/V the node-(i+1)/node-i parts of the 12 rows of interval i.  Lane j holds row j of a
+// block in registers; inverses by Gauss-Jordan (SPD, no pivoting).  Stored per node (29 x 26):
+// rows 0..25 the inverse, rows 26..28 W_b = S_i^-1 v_b (top) or W'_b = T_i^-1 u_b (bottom).
+// G_dd / G'_dd (3 x 3 dynamics part) go to C(i)[C_G] of the coupling interval.
+
+// D_i = P^_i + sigma I + rho sum (rows touching node i) a a^T, row j of it into S.
+__device__ __forceinline__ void assemble_diag(const KParams& P, const Sm& sm, int i, int j, float S[NV]) {
   const float rho = (float)P.rho, sigma = (float)P.sigma;
-  const int j = lane;
-  float Yp[18];
+  const float* cf = sm.C(i);
+  const float* cp = sm.C(i - 1);  // block -1 is zero for i == 0
+  const uint32_t bits = sm.flags[i];
+  float dg = 0.f, pt = 0.f;
+  int pidx = -1;
+  if (j < NV) dg = phat(P, sm, i, j) + sigma;
+  if (j < 9) {
+    const float a2 = cf[C_INT + 4 * j + 1], a1 = cp[C_INT + 4 * j], a3 = cp[C_INT + 4 * j + 2];
+    const float bx = j >= 3 ? cf[C_BOX + j - 3] : 0.f, bi = cf[C_INIT + j];
+    dg += rho * (a2 * a2 + a1 * a1 + bx * bx + bi * bi);
+    pt = rho * a1 * a3;
+    pidx = NQ + j;
+  } else if (j < 18) {
+    const int k = j - 9;
+    const float a1 = cp[C_INT + 4 * k], a3 = cp[C_INT + 4 * k + 2];
+    const float bx = k >= 3 ? cf[C_BOX + 6 + k - 3] : 0.f, bi = cf[C_INIT + j];
+    dg += rho * (a3 * a3 + bx * bx + bi * bi);
+    pt = rho * a1 * a3;
+    pidx = k;
+  } else if (j < NV) {
+    const int c = (j - 18) >> 1, a = (j - 18) & 1;
+    const float f0 = cf[C_FORCE + 4 * c + a], g0 = cf[C_FORCE + 4 * c + 1 - a];
+    const float f1 = cf[C_FORCE + 4 * c + 2 + a], g1 = cf[C_FORCE + 4 * c + 3 - a];
+    dg += rho * (f0 * f0 + f1 * f1);
+    pt = rho * (f0 * g0 + f1 * g1);
+    pidx = 18 + 2 * c + (1 - a);
+  }
 #pragma unroll
-  for (int l = 0; l < 18; ++l) Yp[l] = 0.f;
-  bool good = true;
-#pragma unroll 1
-  for (int i = 0; i < NT; ++i) {
-    const float* cf = sm.C(i);
-    const float* cp = sm.C(i - 1);  // block -1 is zero for i == 0
-    const uint32_t bits = sm.flags[i];
-    float S[NV];
-    {  // (a) diagonal and the single paired off-diagonal entry of row j
-      float dg = 0.f, pt = 0.f;
-      int pidx = -1;
-      if (j < NV) dg = phat(P, sm, i, j) + sigma;
-      if (j < 9) {
-        const float a2 = cf[C_INT + 4 * j + 1], a1 = cp[C_INT + 4 * j], a3 = cp[C_INT + 4 * j + 2];
-        const float bx = j >= 3 ? cf[C_BOX + j - 3] : 0.f, bi = cf[C_INIT + j];
-        dg += rho * (a2 * a2 + a1 * a1 + bx * bx + bi * bi);
-        pt = rho * a1 * a3;
-        pidx = NQ + j;
-      } else if (j < 18) {
-        const int k = j - 9;
-        const float a1 = cp[C_INT + 4 * k], a3 = cp[C_INT + 4 * k + 2];
-        const float bx = k >= 3 ? cf[C_BOX + 6 + k - 3] : 0.f, bi = cf[C_INIT + j];
-        dg += rho * (a3 * a3 + bx * bx + bi * bi);
-        pt = rho * a1 * a3;
-        pidx = k;
-      } else if (j < NV) {
-        const int c = (j - 18) >> 1, a = (j - 18) & 1;
-        const float f0 = cf[C_FORCE + 4 * c + a], g0 = cf[C_FORCE + 4 * c + 1 - a];
-        const float f1 = cf[C_FORCE + 4 * c + 2 + a], g1 = cf[C_FORCE + 4 * c + 3 - a];
-        dg += rho * (f0 * f0 + f1 * f1);
-        pt = rho * (f0 * g0 + f1 * g1);
-        pidx = 18 + 2 * c + (1 - a);
-      }
+  for (int l = 0; l < NV; ++l) S[l] = (l == j ? dg : 0.f) + (l == pidx ? pt : 0.f);
 #pragma unroll
-      for (int l = 0; l < NV; ++l) S[l] = (l == j ? dg : 0.f) + (l == pidx ? pt : 0.f);
+  for (int b = 0; b < 3; ++b) {  // dynamics rows of interval i (qd_i, F_i) and i-1 (qd_i)
+    const float* vb = cf + C_DYNV + 20 * b;
+    const float s = (j >= 9 && j < NV) ? rho * vb[j - 9] : 0.f;
+    const float4* v4 = reinterpret_cast<const float4*>(vb);
+#pragma unroll
+    for (int q = 0; q < 5; ++q) {
+      const float4 w = v4[q];
+      if (9 + 4 * q < NV) S[9 + 4 * q] = fmaf(s, w.x, S[9 + 4 * q]);
+      if (10 + 4 * q < NV) S[10 + 4 * q] = fmaf(s, w.y, S[10 + 4 * q]);
+      if (11 + 4 * q < NV) S[11 + 4 * q] = fmaf(s, w.z, S[11 + 4 * q]);
+      if (12 + 4 * q < NV) S[12 + 4 * q] = fmaf(s, w.w, S[12 + 4 * q]);
     }
-    // (b) dense rank-1 terms: dynamics rows of intervals i (qd_i, F_i) and i-1 (qd_i),
-    //     contact Jacobian rows (qd for stance, q for swing)
+    const float* ub = cp + C_DYNU + 12 * b;
+    const float s2 = (j >= 9 && j < 18) ? rho * ub[j - 9] : 0.f;
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
-      const float* vb = cf + C_DYNV + 20 * b;
-      const float s = (j >= 9 && j < NV) ? rho * vb[j - 9] : 0.f;
-      const float4* v4 = reinterpret_cast<const float4*>(vb);
+    for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s2, ub[m], S[NQ + m]);
+  }
 #pragma unroll
-      for (int q = 0; q < 5; ++q) {
-        const float4 w = v4[q];
-        if (9 + 4 * q < NV) S[9 + 4 * q] = fmaf(s, w.x, S[9 + 4 * q]);
-        if (10 + 4 * q < NV) S[10 + 4 * q] = fmaf(s, w.y, S[10 + 4 * q]);
-        if (11 + 4 * q < NV) S[11 + 4 * q] = fmaf(s, w.z, S[11 + 4 * q]);
-        if (12 + 4 * q < NV) S[12 + 4 * q] = fmaf(s, w.w, S[12 + 4 * q]);
-      }
-      const float* ub = cp + C_DYNU + 12 * b;
-      const float s2 = (j >= 9 && j < 18) ? rho * ub[j - 9] : 0.f;
+  for (int c = 0; c < 4; ++c) {  // contact rows t2/t3: velocity on qd (stance), height on q
+    const float* ja = cf + C_JA + 9 * c;
+    if ((bits >> c) & 1u) {
+      const float* jb = cf + C_JB + 9 * c;
+      const bool mine = j >= 9 && j < 18;
+      const float s0 = mine ? rho * ja[j - 9] : 0.f, s1 = mine ? rho * jb[j - 9] : 0.f;
 #pragma unroll
-      for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s2, ub[m], S[NQ + m]);
-    }
+      for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s0, ja[m], fmaf(s1, jb[m], S[NQ + m]));
+    } else {
+      const float s = j < 9 ? rho * ja[j] : 0.f;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      const float* ja = cf + C_JA + 9 * c;
-      if ((bits >> c) & 1u) {  // stance: velocity rows on qd
-        const float* jb = cf + C_JB + 9 * c;
-        const bool mine = j >= 9 && j < 18;
-        const float s0 = mine ? rho * ja[j - 9] : 0.f, s1 = mine ? rho * jb[j - 9] : 0.f;
-#pragma unroll
-        for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s0, ja[m], fmaf(s1, jb[m], S[NQ + m]));
-      } else {  // swing: height row on q
-        const float s = j < 9 ? rho * ja[j] : 0.f;
-#pragma unroll
-        for (int m = 0; m < 9; ++m) S[m] = fmaf(s, ja[m], S[m]);
-      }
-    }
-    // (c) Schur update from the previous node
-#pragma unroll
-    for (int l = 0; l < 18; ++l) S[l] -= Yp[l];
-    // (d) Gauss-Jordan inversion in place, rows exchanged through smem
-#pragma unroll
-    for (int k = 0; k < NV; ++k) {
-      float* buf = sm.bc + 32 * (k & 1);
-      if (j == k) {
-        float4* b4 = reinterpret_cast<float4*>(buf);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) b4[q] = make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
-        reinterpret_cast<float2*>(buf)[12] = make_float2(S[24], S[25]);
-      }
-      __syncwarp();
-      float R[NV];
-      {
-        const float4* b4 = reinterpret_cast<const float4*>(buf);
-#pragma unroll
-        for (int q = 0; q < 6; ++q) {
-          const float4 w = b4[q];
-          R[4 * q] = w.x; R[4 * q + 1] = w.y; R[4 * q + 2] = w.z; R[4 * q + 3] = w.w;
-        }
-        const float2 w = reinterpret_cast<const float2*>(buf)[12];
-        R[24] = w.x;
-        R[25] = w.y;
-      }
-      const float p = R[k];
-      good = good && (p > 0.f);
-      const float pinv = 1.f / p;
-      const float f = S[k];
-      const bool me = (j == k);
-      const float keep = me ? 0.f : 1.f;
-      const float alpha = me ? pinv : -f * pinv;
-#pragma unroll
-      for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], keep * S[l]);
-      S[k] = me ? pinv : -f * pinv;
-    }
-    float* Sd = sm.Sinv(i);
-    if (j < NV) {  // (e) store S_i^-1
-      float2* dst = reinterpret_cast<float2*>(Sd + j * SROW);
-#pragma unroll
-      for (int q = 0; q < 13; ++q) dst[q] = make_float2(S[2 * q], S[2 * q + 1]);
-    }
-    if (i + 1 < NT) {
-      // (f) W_b = S^-1 v_b (rows 26..28), G = V^T S^-1 V and the Schur update for node i+1:
-      //     Y = rho^2 U G U^T with V/U the node-i / node-(i+1) parts of interval i's rows.
-      float W[3];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const float* vb = cf + C_DYNV + 20 * b;
-        float acc = 0.f;
-#pragma unroll
-        for (int l = 9; l < NV; ++l) acc = fmaf(S[l], vb[l - 9], acc);
-        W[b] = j < NV ? acc : 0.f;
-        if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
-      }
-      float* G = sm.Sinv(i + 1);  // node i+1's block is free until it is factorized: 12 x 13
-      if (j < 9) {
-        const float a2 = cf[C_INT + 4 * j + 1];
-#pragma unroll
-        for (int k = 0; k < 9; ++k) G[j * 13 + k] = a2 * S[k] * cf[C_INT + 4 * k + 1];
-#pragma unroll
-        for (int b = 0; b < 3; ++b) {
-          G[j * 13 + 9 + b] = a2 * W[b];
-          G[(9 + b) * 13 + j] = a2 * W[b];
-        }
-      }
-      float gdd[3][3];
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        const float vb = (j >= 9 && j < NV) ? cf[C_DYNV + 20 * b + j - 9] : 0.f;
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(vb * W[b2]);
-      }
-      if (j == 0) {
-#pragma unroll
-        for (int b = 0; b < 3; ++b)
-#pragma unroll
-          for (int b2 = 0; b2 < 3; ++b2) {
-            const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
-            G[(9 + b) * 13 + 9 + b2] = gv;
-            sm.C(i)[C_G + 3 * b + b2] = gv;
-          }
-      }
-      __syncwarp();
-      float Z[12];
-      if (j < 9) {
-        const float a1 = cf[C_INT + 4 * j];
-#pragma unroll
-        for (int s = 0; s < 12; ++s) Z[s] = a1 * G[j * 13 + s];
-      } else if (j < 18) {
-        const int k = j - 9;
-        const float a3 = cf[C_INT + 4 * k + 2];
-        const float u0 = cf[C_DYNU + k], u1 = cf[C_DYNU + 12 + k], u2 = cf[C_DYNU + 24 + k];
-#pragma unroll
-        for (int s = 0; s < 12; ++s)
-          Z[s] = a3 * G[k * 13 + s] + u0 * G[9 * 13 + s] + u1 * G[10 * 13 + s] + u2 * G[11 * 13 + s];
-      } else {
-#pragma unroll
-        for (int s = 0; s < 12; ++s) Z[s] = 0.f;
-      }
-      const float r2 = rho * rho;
-#pragma unroll
-      for (int m = 0; m < 9; ++m) Yp[m] = r2 * Z[m] * cf[C_INT + 4 * m];
-#pragma unroll
-      for (int k = 0; k < 9; ++k)
-        Yp[NQ + k] = r2 * (Z[k] * cf[C_INT + 4 * k + 2] + Z[9] * cf[C_DYNU + k] +
-                           Z[10] * cf[C_DYNU + 12 + k] + Z[11] * cf[C_DYNU + 24 + k]);
-      __syncwarp();
-    } else if (j < NV) {
-#pragma unroll
-      for (int b = 0; b < 3; ++b) Sd[(NV + b) * SROW + j] = 0.f;
+      for (int m = 0; m < 9; ++m) S[m] = fmaf(s, ja[m], S[m]);
     }
   }
+}
+
+// In-place Gauss-Jordan inverse of the SPD block held row-wise by the warp (lane j: row j);
+// pivot rows are exchanged through `bc` (2 x 32 floats).  Returns false on a pivot <= 0.
+__device__ __forceinline__ bool gauss_jordan(int j, float S[NV], float* bc) {
+  bool good = true;
+#pragma unroll
+  for (int k = 0; k < NV; ++k) {
+    float* buf = bc + 32 * (k & 1);
+    if (j == k) {
+      float4* b4 = reinterpret_cast<float4*>(buf);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) b4[q] = make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
+      reinterpret_cast<float2*>(buf)[12] = make_float2(S[24], S[25]);
+    }
+    __syncwarp();
+    float R[NV];
+    {
+      const float4* b4 = reinterpret_cast<const float4*>(buf);
+#pragma unroll
+      for (int q = 0; q < 6; ++q) {
+        const float4 w = b4[q];
+        R[4 * q] = w.x; R[4 * q + 1] = w.y; R[4 * q + 2] = w.z; R[4 * q + 3] = w.w;
+      }
+      const float2 w = reinterpret_cast<const float2*>(buf)[12];
+      R[24] = w.x;
+      R[25] = w.y;
+    }
+    const float p = R[k];
+    good = good && (p > 0.f);
+    const float pinv = 1.f / p;
+    const float f = S[k];
+    const bool me = (j == k);
+    const float keep = me ? 0.f : 1.f;
+    const float alpha = me ? pinv : -f * pinv;
+#pragma unroll
+    for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], keep * S[l]);
+    S[k] = me ? pinv : -f * pinv;
+  }
+  return good;
+}
+
+__device__ __forceinline__ void store_inverse(float* Sd, int j, const float S[NV]) {
+  if (j < NV) {
+    float2* dst = reinterpret_cast<float2*>(Sd + j * SROW);
+#pragma unroll
+    for (int q = 0; q < 13; ++q) dst[q] = make_float2(S[2 * q], S[2 * q + 1]);
+  }
+}
+
+// Top Schur step after S_i^-1 (rows in S): W_b = S^-1 v_b -> rows 26..28, G_dd -> C(i)[C_G],
+// and the update Yp (rows j < 18, cols < 18) of node i+1: rho^2 U_i G_i U_i^T.
+__device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i, int j, const float S[NV],
+                                          float Yp[18]) {
+  const float rho = (float)P.rho;
+  const float* cf = sm.C(i);
+  float* Sd = sm.Sinv(i);
+  float W[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float* vb = cf + C_DYNV + 20 * b;
+    float acc = 0.f;
+#pragma unroll
+    for (int l = 9; l < NV; ++l) acc = fmaf(S[l], vb[l - 9], acc);
+    W[b] = j < NV ? acc : 0.f;
+    if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
+  }
+  float* G = sm.Sinv(i + 1);  // node i+1's block is free until it is factorized: 12 x 13
+  if (j < 9) {
+    const float a2 = cf[C_INT + 4 * j + 1];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) G[j * 13 + k] = a2 * S[k] * cf[C_INT + 4 * k + 1];
+#pragma unroll
+    for (int b = 0; b < 3; ++b) {
+      G[j * 13 + 9 + b] = a2 * W[b];
+      G[(9 + b) * 13 + j] = a2 * W[b];
+    }
+  }
+  float gdd[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float vb = (j >= 9 && j < NV) ? cf[C_DYNV + 20 * b + j - 9] : 0.f;
+#pragma unroll
+    for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(vb * W[b2]);
+  }
+  if (j == 0) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int b2 = 0; b2 < 3; ++b2) {
+        const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
+        G[(9 + b) * 13 + 9 + b2] = gv;
+        sm.C(i)[C_G + 3 * b + b2] = gv;
+      }
+  }
   __syncwarp();
-  return __all_sync(FULL, good);
+  float Z[12];
+  if (j < 9) {
+    const float a1 = cf[C_INT + 4 * j];
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = a1 * G[j * 13 + s];
+  } else if (j < 18) {
+    const int k = j - 9;
+    const float a3 = cf[C_INT + 4 * k + 2];
+    const float u0 = cf[C_DYNU + k], u1 = cf[C_DYNU + 12 + k], u2 = cf[C_DYNU + 24 + k];
+#pragma unroll
+    for (int s = 0; s < 12; ++s)
+      Z[s] = a3 * G[k * 13 + s] + u0 * G[9 * 13 + s] + u1 * G[10 * 13 + s] + u2 * G[11 * 13 + s];
+  } else {
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = 0.f;
+  }
+  const float r2 = rho * rho;
+#pragma unroll
+  for (int m = 0; m < 9; ++m) Yp[m] = r2 * Z[m] * cf[C_INT + 4 * m];
+#pragma unroll
+  for (int k = 0; k < 9; ++k)
+    Yp[NQ + k] = r2 * (Z[k] * cf[C_INT + 4 * k + 2] + Z[9] * cf[C_DYNU + k] + Z[10] * cf[C_DYNU + 12 + k] +
+                       Z[11] * cf[C_DYNU + 24 + k]);
+  __syncwarp();
+}
+
+// Bottom Schur step after T_i^-1 (rows in S), interval i-1 couples nodes i-1 and i:
+// W'_b = T^-1 u_b -> rows 26..28, G'_dd -> C(i-1)[C_G], and the full update Yb of node i-1:
+// rho^2 V_{i-1} G'_{i-1} V_{i-1}^T with G' = U^T T^-1 U (12 x 12).
+__device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int i, int j, const float S[NV],
+                                             float Yb[NV]) {
+  const float rho = (float)P.rho;
+  const float* cp = sm.C(i - 1);
+  float* Sd = sm.Sinv(i);
+  float W[3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {  // W'_b[j] = sum_k T^-1[j][9+k] u_b[k]
+    const float* ub = cp + C_DYNU + 12 * b;
+    float acc = 0.f;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) acc = fmaf(S[NQ + k], ub[k], acc);
+    W[b] = j < NV ? acc : 0.f;
+    if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
+  }
+  // int-int / int-dyn parts: lane k (row k) and lane 9+k (row 9+k) of T^-1
+  float Pk[9];
+#pragma unroll
+  for (int l = 0; l < 9; ++l) Pk[l] = cp[C_INT + 4 * l] * S[l] + cp[C_INT + 4 * l + 2] * S[NQ + l];
+  // node i-1's block is free until it is factorized (offset 200: at the middle node the top
+  // warp may be using [0, 156) of the same block concurrently): 12 x 13
+  float* G = sm.Sinv(i - 1) + 200;
+  const float a1 = j < 9 ? cp[C_INT + 4 * j] : 0.f, a3 = j < 9 ? cp[C_INT + 4 * j + 2] : 0.f;
+#pragma unroll
+  for (int l = 0; l < 9; ++l) {
+    const float q = __shfl_down_sync(FULL, Pk[l], 9);
+    if (j < 9) G[j * 13 + l] = a1 * Pk[l] + a3 * q;
+  }
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float w9 = __shfl_down_sync(FULL, W[b], 9);
+    if (j < 9) {
+      const float g = a1 * W[b] + a3 * w9;
+      G[j * 13 + 9 + b] = g;
+      G[(9 + b) * 13 + j] = g;
+    }
+  }
+  float gdd[3][3];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) {
+    const float ub = (j >= 9 && j < 18) ? cp[C_DYNU + 12 * b + j - 9] : 0.f;
+#pragma unroll
+    for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(ub * W[b2]);
+  }
+  if (j == 0) {
+#pragma unroll
+    for (int b = 0; b < 3; ++b)
+#pragma unroll
+      for (int b2 = 0; b2 < 3; ++b2) {
+        const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
+        G[(9 + b) * 13 + 9 + b2] = gv;
+        sm.C(i - 1)[C_G + 3 * b + b2] = gv;
+      }
+  }
+  __syncwarp();
+  float Z[12];  // Z[j][s] = sum_r V[j][r] G'[r][s]
+  if (j < 9) {
+    const float a2 = cp[C_INT + 4 * j + 1];
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = a2 * G[j * 13 + s];
+  } else if (j < NV) {
+    const float v0 = cp[C_DYNV + j - 9], v1 = cp[C_DYNV + 20 + j - 9], v2 = cp[C_DYNV + 40 + j - 9];
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = v0 * G[9 * 13 + s] + v1 * G[10 * 13 + s] + v2 * G[11 * 13 + s];
+  } else {
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = 0.f;
+  }
+  const float r2 = rho * rho;
+#pragma unroll
+  for (int l = 0; l < 9; ++l) Yb[l] = r2 * Z[l] * cp[C_INT + 4 * l + 1];
+#pragma unroll
+  for (int l = 9; l < NV; ++l)
+    Yb[l] = r2 * (Z[9] * cp[C_DYNV + l - 9] + Z[10] * cp[C_DYNV + 20 + l - 9] + Z[11] * cp[C_DYNV + 40 + l - 9]);
+  __syncwarp();
+}
+
+// Returns false (CTA-uniform) on a non-positive pivot (SingularityError, ldl.cpp:155-160).
+__device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
+  const int NT = P.NT;
+  const int m = mid_node(NT);
+  const int j = lane;
+  float* bc = sm.bc + 64 * warp;
+  bool good = true;
+  float Yp[18];  // warp 0: top update of the next node (rows j < 18, cols < 18)
+  float Yb[NV];  // warp 1: bottom update of the previous node (full row)
+#pragma unroll
+  for (int l = 0; l < 18; ++l) Yp[l] = 0.f;
+#pragma unroll
+  for (int l = 0; l < NV; ++l) Yb[l] = 0.f;
+  if (warp == 0) {
+#pragma unroll 1
+    for (int i = 0; i < m; ++i) {
+      float S[NV];
+      assemble_diag(P, sm, i, j, S);
+#pragma unroll
+      for (int l = 0; l < 18; ++l) S[l] -= Yp[l];
+      good = gauss_jordan(j, S, bc) && good;
+      store_inverse(sm.Sinv(i), j, S);
+      top_schur(P, sm, i, j, S, Yp);
+    }
+  } else {
+#pragma unroll 1
+    for (int i = NT - 1; i > m; --i) {
+      float S[NV];
+      assemble_diag(P, sm, i, j, S);
+#pragma unroll
+      for (int l = 0; l < NV; ++l) S[l] -= Yb[l];
+      good = gauss_jordan(j, S, bc) && good;
+      store_inverse(sm.Sinv(i), j, S);
+      bottom_schur(P, sm, i, j, S, Yb);
+    }
+  }
+  __syncthreads();  // both halves are done with their scratch in the middle block
+  if (warp == 1 && j < NV) {  // hand the bottom update of the middle node over
+    float* dst = sm.Sinv(m) + j * SROW;
+#pragma unroll
+    for (int l = 0; l < NV; ++l) dst[l] = Yb[l];
+  }
+  __syncthreads();
+  if (warp == 0) {
+    float S[NV];
+    assemble_diag(P, sm, m, j, S);
+    if (j < NV) {
+      const float* yb = sm.Sinv(m) + j * SROW;
+#pragma unroll
+      for (int l = 0; l < NV; ++l) S[l] -= yb[l] + (l < 18 ? Yp[l] : 0.f);
+    }
+    __syncwarp();
+    good = gauss_jordan(j, S, bc) && good;
+    store_inverse(sm.Sinv(m), j, S);
+    if (j < NV) {
+#pragma unroll
+      for (int b = 0; b < 3; ++b) sm.Sinv(m)[(NV + b) * SROW + j] = 0.f;
+    }
+  }
+  return __syncthreads_and(good);
 }
 
 // ------------------------------------------------------------------------- stage: ADMM
@@ -1076,16 +1216,20 @@ __device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const f
 // AdmmSolver::run (qp.cpp:156-190): exactly n_qp iterations from x = y = z = 0.  Returns the
 // first iteration with a non-finite iterate, or -1 (CTA-uniform).
 //
-// Two warps per agent, in lock step (one __syncthreads per node step):
-//   warp 0 (solver) runs the recurrences
-//     forward  i = 0..T-1: u_i = r_i - rho U_{i-1} gamma_{i-1}; [s_i; gamma_i] = [S_i^-1; W_i^T] u_i
-//     backward i = T-1..0: x~_i = s_i - rho [S_i^-1 | W_i] xi_i, and updates the integration /
-//                          dynamics rows of interval i whose z~ falls out of the recurrence;
-//   warp 1 (helper) does the node-local work one node ahead of / behind it
-//     forward : r_{i+1} = sigma x_{i+1} - q^_{i+1} + (A^T(rho z - y))_{i+1} (column view)
-//     backward: node i+1's own rows (contacts, boxes, initial state) and x_{i+1} from x~_{i+1}.
+// Two-sided solve of H x~ = r (factorize): warp 0 owns nodes [0, m) and the middle node m,
+// warp 1 owns (m, T); each warp also does the node-local work of its nodes (r_i from the
+// column view, the rows acting on node i alone, x_i), so the warps meet only at the middle:
+//   top forward     i = 0..m-1:   u_i = r_i - rho U_{i-1} g_{i-1};  [s_i; g_i^dyn] = [S_i^-1; W_i^T] u_i
+//   bottom forward  i = T-1..m+1: u_i = r_i - rho V_i g'_{i+1};     [s_i; g_i'^dyn] = [T_i^-1; W_i'^T] u_i
+//   middle:         x_m = M^-1 (r_m - rho U_{m-1} g_{m-1} - rho V_m g'_{m+1})
+//   top backward    i = m-1..0:   x_i = s_i - rho [S_i^-1(:, q) | W_i] xi_i,  xi = diag(a2,1) U_i^T x_{i+1}
+//   bottom backward i = m+1..T-1: x_i = s_i - rho [T_i^-1(:, q), T_i^-1(:, qd) | W'_i] xi'_i,
+//                                  xi' = (a1, a3) (x) V_{i-1}^T x_{i-1}
+// with g = V^T s, g' = U^T s'.  z~ of the integration/dynamics rows comes out of the
+// backward steps; no warp reduction sits on either recurrence.
 __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
+  const int m = mid_node(NT);
   const AdmmConst K{(float)P.rho, (float)P.sigma, (float)P.alpha, 1.f - (float)P.alpha,
                     (float)(1.0 / P.rho)};
   const float rho = K.rho;
@@ -1093,17 +1237,21 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   build_terms(lane, T);
   TermBytes B;
   term_bytes<TV_T>(T, B);
-  float* ubuf = sm.bc;      // forward broadcast of u_i
-  float* xib = sm.bc + 32;  // backward broadcast of xi_i
-  // helper: r_i -> V_S(i)
-  auto put_r = [&](int i, bool first) {
+  float* ubuf = sm.bc + 64 * warp;  // broadcast of u_i (this warp)
+  float* xib = ubuf + 32;           // broadcast of xi_i (this warp)
+  float* gb = sm.bc + 64 + 32;      // warp 1's xi buffer doubles as the g'_{m+1} hand-over
+  auto r_of = [&](int i, bool first) {  // (sigma x - q^ + A^T(rho z - y)) restricted to node i
     const float cv = first ? 0.f : col_view<OpSum, TV_T>(sm, i, T, B);
-    if (lane < NV) sm.V(i, V_S)[lane] = K.sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv;
+    return lane < NV ? K.sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv : 0.f;
   };
-  // helper: node i's own rows and x_i
-  auto finish_node = [&](int i) {
+  auto store_s = [&](int i, float s) {  // s_i, and g^dyn in the spare slots of node i
+    float* vs = sm.V(i, V_S);
+    if (lane < NV + 2) vs[lane] = s;
+    if (lane == NV + 2) sm.V(i, V_X)[NV] = s;
+  };
+  auto finish_node = [&](int i) {  // node i's own rows and the x relaxation, from x~_i
     float* xs = sm.V(i, V_S);
-    bool b = node_rows(sm, lane, i, xs, K);
+    const bool b = node_rows(sm, lane, i, xs, K);
     if (lane < NV) {
       float* x = sm.V(i, V_X);
       x[lane] = K.alpha * xs[lane] + K.oma * x[lane];
@@ -1114,15 +1262,12 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   for (int it = 0; it < P.n_qp; ++it) {
     const bool first = it == 0;  // x = y = z = 0: r = -q^
     bool bad = false;
-    // ---- forward
-    if (warp == 1) put_r(0, first);
-    __syncthreads();
-    float gint = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;
+    // ---------------------------------------------------------------- forward
+    float gint = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;  // g of the last eliminated node
+    if (warp == 0) {
 #pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
-      if (warp == 0) {
-        float* vs = sm.V(i, V_S);
-        float u = lane < NV ? vs[lane] : 0.f;
+      for (int i = 0; i < m; ++i) {
+        float u = r_of(i, first);
         if (i > 0) {
           const float* cp = sm.C(i - 1);
           const float gk = __shfl_sync(FULL, gint, lane >= 9 && lane < 18 ? lane - 9 : 0);
@@ -1135,86 +1280,195 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
           }
         }
         const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
-        if (lane < NV + 2) vs[lane] = s;          // s_i, gamma_0,1 -> V_S[26,27]
-        if (lane == NV + 2) sm.V(i, V_X)[NV] = s;  // gamma_2 -> V_X[26]
+        store_s(i, s);
         gint = lane < 9 ? sm.C(i)[C_INT + 4 * lane + 1] * s : 0.f;
         g0 = __shfl_sync(FULL, s, 26);
         g1 = __shfl_sync(FULL, s, 27);
         g2 = __shfl_sync(FULL, s, 28);
-      } else if (i + 1 < NT) {
-        put_r(i + 1, first);
+        __syncwarp();
       }
-      __syncthreads();
-    }
-    // ---- backward
+    } else {
 #pragma unroll 1
-    for (int i = NT - 1; i >= 0; --i) {
-      if (warp == 0) {
+      for (int i = NT - 1; i > m; --i) {
+        float u = r_of(i, first);
+        if (i < NT - 1) {  // - rho V_i g'_{i+1}
+          const float* cf = sm.C(i);
+          if (lane < 9) {
+            u -= rho * cf[C_INT + 4 * lane + 1] * gint;
+          } else if (lane < NV) {
+            u -= rho * (cf[C_DYNV + lane - 9] * g0 + cf[C_DYNV + 20 + lane - 9] * g1 +
+                        cf[C_DYNV + 40 + lane - 9] * g2);
+          }
+        }
+        const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
+        store_s(i, s);
+        const float* cp = sm.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
+        const float sq = __shfl_down_sync(FULL, s, 9);
+        gint = lane < 9 ? cp[C_INT + 4 * lane] * s + cp[C_INT + 4 * lane + 2] * sq : 0.f;
+        g0 = __shfl_sync(FULL, s, 26);
+        g1 = __shfl_sync(FULL, s, 27);
+        g2 = __shfl_sync(FULL, s, 28);
+        __syncwarp();
+      }
+      gb[lane] = lane < 9 ? gint : (lane == 9 ? g0 : (lane == 10 ? g1 : (lane == 11 ? g2 : 0.f)));
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- middle
+    if (warp == 0) {
+      float u = r_of(m, first);
+      if (m > 0) {
+        const float* cp = sm.C(m - 1);
+        const float gk = __shfl_sync(FULL, gint, lane >= 9 && lane < 18 ? lane - 9 : 0);
+        if (lane < 9) {
+          u -= rho * cp[C_INT + 4 * lane] * gint;
+        } else if (lane < 18) {
+          const int k = lane - 9;
+          u -= rho * (cp[C_INT + 4 * k + 2] * gk + cp[C_DYNU + k] * g0 + cp[C_DYNU + 12 + k] * g1 +
+                      cp[C_DYNU + 24 + k] * g2);
+        }
+      }
+      if (m + 1 < NT) {
+        const float* cf = sm.C(m);
+        if (lane < 9) {
+          u -= rho * cf[C_INT + 4 * lane + 1] * gb[lane];
+        } else if (lane < NV) {
+          u -= rho * (cf[C_DYNV + lane - 9] * gb[9] + cf[C_DYNV + 20 + lane - 9] * gb[10] +
+                      cf[C_DYNV + 40 + lane - 9] * gb[11]);
+        }
+      }
+      const float x = ext_mv(sm.Sinv(m), lane, ubuf, u);
+      if (lane < NV) sm.V(m, V_S)[lane] = x;
+      bad = bad || !isfinite(x);
+    }
+    __syncthreads();
+    // ---------------------------------------------------------------- backward
+    if (warp == 0) {
+      bad = finish_node(m) || bad;
+#pragma unroll 1
+      for (int i = m - 1; i >= 0; --i) {
         const float* cf = sm.C(i);
         float* vs = sm.V(i, V_S);
-        float xt = lane < NV ? vs[lane] : 0.f;
-        if (i + 1 < NT) {
-          const float* xn = sm.V(i + 1, V_S);
-          float dl = 0.f, xi = 0.f;
-          if (lane < 9) {
-            dl = cf[C_INT + 4 * lane] * xn[lane] + cf[C_INT + 4 * lane + 2] * xn[NQ + lane];
-            xi = cf[C_INT + 4 * lane + 1] * dl;
-          } else if (lane < 12) {
-            const float* ub = cf + C_DYNU + 12 * (lane - 9);
-            float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
-            a0 = fmaf(ub[3], xn[NQ + 3], a0);
-            a1 = fmaf(ub[4], xn[NQ + 4], a1);
-            a2 = fmaf(ub[5], xn[NQ + 5], a2);
-            a0 = fmaf(ub[6], xn[NQ + 6], a0);
-            a1 = fmaf(ub[7], xn[NQ + 7], a1);
-            a2 = fmaf(ub[8], xn[NQ + 8], a2);
-            xi = a0 + a1 + a2;
-          }
-          xib[lane] = xi;
-          __syncwarp();
-          const float* Sd = sm.Sinv(i);
-          const int j = lane < SROWS ? lane : SROWS - 1;
-          const float* rw = Sd + j * SROW;  // lanes < 26: row j (= column j); 26..28: W_b
-          float acc0 = 0.f, acc1 = 0.f;
-#pragma unroll
-          for (int k = 0; k < 9; k += 2) {
-            acc0 = fmaf(rw[k], xib[k], acc0);
-            if (k + 1 < 9) acc1 = fmaf(rw[k + 1], xib[k + 1], acc1);
-          }
-          if (lane < NV) {
-#pragma unroll
-            for (int b = 0; b < 3; ++b) acc1 = fmaf(Sd[(NV + b) * SROW + j], xib[9 + b], acc1);
-          } else {
-            const int b = j - NV;
-#pragma unroll
-            for (int b2 = 0; b2 < 3; ++b2) acc1 = fmaf(cf[C_G + 3 * b + b2], xib[9 + b2], acc1);
-          }
-          const float acc = acc0 + acc1;
-          float zt = 0.f;
-          int slot = -1;
-          if (lane < NV) {
-            xt -= rho * acc;
-            vs[lane] = xt;
-            if (lane < 9) {  // z~ of integration row k: a2 x~_i[q_k] + (a1, a3) . x~_{i+1}
-              zt = fmaf(cf[C_INT + 4 * lane + 1], xt, dl);
-              slot = lane;
-            }
-          } else if (lane < SROWS) {  // z~ of dynamics row b: v_b.x~_i + u_b.x~_{i+1}
-            const int b = lane - NV;
-            const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
-            zt = gam - rho * acc + xib[9 + b];
-            slot = 9 + b;
-          }
-          if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
-          __syncwarp();
+        const float* xn = sm.V(i + 1, V_S);
+        float dl = 0.f, xi = 0.f;
+        if (lane < 9) {
+          dl = cf[C_INT + 4 * lane] * xn[lane] + cf[C_INT + 4 * lane + 2] * xn[NQ + lane];
+          xi = cf[C_INT + 4 * lane + 1] * dl;
+        } else if (lane < 12) {
+          const float* ub = cf + C_DYNU + 12 * (lane - 9);
+          float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
+          a0 = fmaf(ub[3], xn[NQ + 3], a0);
+          a1 = fmaf(ub[4], xn[NQ + 4], a1);
+          a2 = fmaf(ub[5], xn[NQ + 5], a2);
+          a0 = fmaf(ub[6], xn[NQ + 6], a0);
+          a1 = fmaf(ub[7], xn[NQ + 7], a1);
+          a2 = fmaf(ub[8], xn[NQ + 8], a2);
+          xi = a0 + a1 + a2;
         }
-        bad = bad || !isfinite(xt);
-      } else if (i + 1 < NT) {
-        bad = finish_node(i + 1) || bad;
+        xib[lane] = xi;
+        __syncwarp();
+        const float* Sd = sm.Sinv(i);
+        const int j = lane < SROWS ? lane : SROWS - 1;
+        const float* rw = Sd + j * SROW;  // lanes < 26: row j (= column j); 26..28: W_b
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; k += 2) {
+          acc0 = fmaf(rw[k], xib[k], acc0);
+          if (k + 1 < 9) acc1 = fmaf(rw[k + 1], xib[k + 1], acc1);
+        }
+        if (lane < NV) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc1 = fmaf(Sd[(NV + b) * SROW + j], xib[9 + b], acc1);
+        } else {
+          const int b = j - NV;
+#pragma unroll
+          for (int b2 = 0; b2 < 3; ++b2) acc1 = fmaf(cf[C_G + 3 * b + b2], xib[9 + b2], acc1);
+        }
+        const float acc = acc0 + acc1;
+        float zt = 0.f, xt = 0.f;
+        int slot = -1;
+        if (lane < NV) {
+          xt = vs[lane] - rho * acc;
+          vs[lane] = xt;
+          bad = bad || !isfinite(xt);
+          if (lane < 9) {  // z~ of integration row k: a2 x~_i[q_k] + (a1, a3) . x~_{i+1}
+            zt = fmaf(cf[C_INT + 4 * lane + 1], xt, dl);
+            slot = lane;
+          }
+        } else if (lane < SROWS) {  // z~ of dynamics row b: v_b.x~_i + u_b.x~_{i+1}
+          const int b = lane - NV;
+          const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
+          zt = gam - rho * acc + xib[9 + b];
+          slot = 9 + b;
+        }
+        if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        __syncwarp();
+        bad = finish_node(i) || bad;
       }
-      __syncthreads();
+    } else {
+#pragma unroll 1
+      for (int i = m + 1; i < NT; ++i) {
+        const float* cp = sm.C(i - 1);  // interval i-1 couples nodes i-1 and i
+        const float* xp = sm.V(i - 1, V_S);
+        float* vs = sm.V(i, V_S);
+        float xiv = 0.f;  // xi'_k = a2_k x_{i-1}[q_k];  xi'_b = v_b . x_{i-1}
+        if (lane < 9) {
+          xiv = cp[C_INT + 4 * lane + 1] * xp[lane];
+          xib[lane] = cp[C_INT + 4 * lane] * xiv;
+          xib[9 + lane] = cp[C_INT + 4 * lane + 2] * xiv;
+        } else if (lane < 12) {
+          const float* vb = cp + C_DYNV + 20 * (lane - 9);
+          float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 17; k += 3) {
+            a0 = fmaf(vb[k], xp[9 + k], a0);
+            if (k + 1 < 17) a1 = fmaf(vb[k + 1], xp[10 + k], a1);
+            if (k + 2 < 17) a2 = fmaf(vb[k + 2], xp[11 + k], a2);
+          }
+          xiv = a0 + a1 + a2;
+          xib[18 + lane - 9] = xiv;
+        }
+        __syncwarp();
+        const float* Sd = sm.Sinv(i);
+        const int j = lane < SROWS ? lane : SROWS - 1;
+        const float* rw = Sd + j * SROW;  // lanes < 26: row j of T^-1; 26..28: W'_b
+        float acc0 = 0.f, acc1 = 0.f;
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          acc0 = fmaf(rw[k], xib[k], acc0);
+          acc1 = fmaf(rw[NQ + k], xib[9 + k], acc1);
+        }
+        if (lane < NV) {
+#pragma unroll
+          for (int b = 0; b < 3; ++b) acc0 = fmaf(Sd[(NV + b) * SROW + j], xib[18 + b], acc0);
+        } else {
+          const int b = j - NV;
+#pragma unroll
+          for (int b2 = 0; b2 < 3; ++b2) acc0 = fmaf(cp[C_G + 3 * b + b2], xib[18 + b2], acc0);
+        }
+        const float acc = acc0 + acc1;
+        float xt = 0.f;
+        if (lane < NV) {
+          xt = vs[lane] - rho * acc;
+          vs[lane] = xt;
+          bad = bad || !isfinite(xt);
+        }
+        const float xq = __shfl_down_sync(FULL, xt, 9);  // lane k: x_i[qd_k]
+        float zt = 0.f;
+        int slot = -1;
+        if (lane < 9) {  // z~ of integration row k of interval i-1
+          zt = xiv + cp[C_INT + 4 * lane] * xt + cp[C_INT + 4 * lane + 2] * xq;
+          slot = lane;
+        } else if (lane >= NV && lane < SROWS) {  // z~ of dynamics row b: v_b.x_{i-1} + u_b.x_i
+          const int b = lane - NV;
+          const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
+          zt = xib[18 + b] + gam - rho * acc;
+          slot = 9 + b;
+        }
+        if (slot >= 0) bad = !row_update(sm.R(i - 1) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        __syncwarp();
+        bad = finish_node(i) || bad;
+      }
     }
-    if (warp == 1) bad = finish_node(0) || bad;
     if (__syncthreads_or(bad)) return it;
   }
   return -1;
@@ -1291,9 +1545,7 @@ __global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
     if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
     apply_scaling(P, sm, lane, warp);
     prof_mark(P, threadIdx.x, 3, t0);
-    int good = 1;
-    if (warp == 0) good = factorize(P, sm, lane);
-    good = __syncthreads_and(good);
+    const int good = factorize(P, sm, lane, warp);
     if (!good) {
       out.status = RMPC_STATUS_SINGULAR;
     } else {

@@ -1060,71 +1060,71 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
 }
 
 // Returns false (CTA-uniform) on a non-positive pivot (SingularityError, ldl.cpp:155-160).
+// Both warps run the same loop (one Gauss-Jordan / assembly instance in the code): step t
+// factorizes node t (warp 0, top) or node T-1-t (warp 1, bottom); warp 0's last step is the
+// middle node, whose bottom update warp 1 hands over through the middle block.
 __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
   const int m = mid_node(NT);
+  const int nbot = NT - 1 - m;
+  const int steps = (m > nbot ? m : nbot) + 1;
   const int j = lane;
   float* bc = sm.bc + 64 * warp;
   bool good = true;
-  float Yp[18];  // warp 0: top update of the next node (rows j < 18, cols < 18)
-  float Yb[NV];  // warp 1: bottom update of the previous node (full row)
+  float Y[NV];  // update of the next node to eliminate (top: rows/cols < 18 non-zero)
 #pragma unroll
-  for (int l = 0; l < 18; ++l) Yp[l] = 0.f;
-#pragma unroll
-  for (int l = 0; l < NV; ++l) Yb[l] = 0.f;
-  if (warp == 0) {
+  for (int l = 0; l < NV; ++l) Y[l] = 0.f;
 #pragma unroll 1
-    for (int i = 0; i < m; ++i) {
-      float S[NV];
-      assemble_diag(P, sm, i, j, S);
+  for (int t = 0; t < steps; ++t) {
+    const bool middle = t == steps - 1;
+    if (middle) {
+      __syncthreads();  // both halves are done with their scratch in the middle block
+      if (warp == 1 && j < NV) {
+        float* dst = sm.Sinv(m) + j * SROW;
 #pragma unroll
-      for (int l = 0; l < 18; ++l) S[l] -= Yp[l];
-      good = gauss_jordan(j, S, bc) && good;
-      store_inverse(sm.Sinv(i), j, S);
-      top_schur(P, sm, i, j, S, Yp);
+        for (int l = 0; l < NV; ++l) dst[l] = Y[l];
+      }
+      __syncthreads();
+      if (warp == 1) break;
     }
-  } else {
-#pragma unroll 1
-    for (int i = NT - 1; i > m; --i) {
-      float S[NV];
-      assemble_diag(P, sm, i, j, S);
-#pragma unroll
-      for (int l = 0; l < NV; ++l) S[l] -= Yb[l];
-      good = gauss_jordan(j, S, bc) && good;
-      store_inverse(sm.Sinv(i), j, S);
-      bottom_schur(P, sm, i, j, S, Yb);
-    }
-  }
-  __syncthreads();  // both halves are done with their scratch in the middle block
-  if (warp == 1 && j < NV) {  // hand the bottom update of the middle node over
-    float* dst = sm.Sinv(m) + j * SROW;
-#pragma unroll
-    for (int l = 0; l < NV; ++l) dst[l] = Yb[l];
-  }
-  __syncthreads();
-  if (warp == 0) {
+    const int i = warp == 0 ? (middle ? m : t) : NT - 1 - t;
+    const bool active = middle || (warp == 0 ? t < m : t < nbot);
+    if (!active) continue;  // the shorter half waits at the middle
     float S[NV];
-    assemble_diag(P, sm, m, j, S);
-    if (j < NV) {
+    assemble_diag(P, sm, i, j, S);
+    if (middle && j < NV) {
       const float* yb = sm.Sinv(m) + j * SROW;
 #pragma unroll
-      for (int l = 0; l < NV; ++l) S[l] -= yb[l] + (l < 18 ? Yp[l] : 0.f);
+      for (int l = 0; l < NV; ++l) S[l] -= yb[l];
     }
+#pragma unroll
+    for (int l = 0; l < NV; ++l) S[l] -= Y[l];
     __syncwarp();
     good = gauss_jordan(j, S, bc) && good;
-    store_inverse(sm.Sinv(m), j, S);
-    if (j < NV) {
+    store_inverse(sm.Sinv(i), j, S);
+    if (middle) {
+      if (j < NV) {
 #pragma unroll
-      for (int b = 0; b < 3; ++b) sm.Sinv(m)[(NV + b) * SROW + j] = 0.f;
+        for (int b = 0; b < 3; ++b) sm.Sinv(m)[(NV + b) * SROW + j] = 0.f;
+      }
+    } else if (warp == 0) {
+      float Yp[18];
+      top_schur(P, sm, i, j, S, Yp);
+#pragma unroll
+      for (int l = 0; l < NV; ++l) Y[l] = l < 18 ? Yp[l] : 0.f;
+    } else {
+      bottom_schur(P, sm, i, j, S, Y);
     }
   }
   return __syncthreads_and(good);
 }
 
 // ------------------------------------------------------------------------- stage: ADMM
-// One constraint-row update (qp.cpp:163-170) on the stored {lo, hi, z, t = rho z - y}.
-__device__ __forceinline__ bool row_update(float4* r, float zt, float alpha, float oma, float rho,
-                                           float rho_inv) {
+// One constraint-row update (qp.cpp:163-170) on the stored {lo, hi, z, t = rho z - y}; the
+// store is predicated on `active` (r must point at a valid row either way).  Returns false
+// on a non-finite z~ of an active row.
+__device__ __forceinline__ bool row_update(float4* r, bool active, float zt, float alpha, float oma,
+                                           float rho, float rho_inv) {
   float4 rd = *r;
   const float y = fmaf(rho, rd.z, -rd.w);
   const float w = alpha * zt + oma * rd.z;
@@ -1132,8 +1132,8 @@ __device__ __forceinline__ bool row_update(float4* r, float zt, float alpha, flo
   const float yn = y + rho * (w - zn);
   rd.z = zn;
   rd.w = fmaf(rho, zn, -yn);
-  *r = rd;
-  return isfinite(zt);
+  if (active) *r = rd;
+  return !active || isfinite(zt);
 }
 
 // [S_i^-1 ; W_i^T] u for lanes 0..28 (u published through buf).
@@ -1168,49 +1168,38 @@ struct AdmmConst {
 
 // Rows of node i that act on node-i variables only (contact forces, contact Jacobian rows,
 // joint boxes; the initial-state rows at node 0): z~ from x~_i, then the row update.  Lanes
-// 8c..8c+5 reduce rows t2/t3 of contact c, 8c+2..4 also own boxes, 8c+6/8c+7 rows t0/t1.
+// 8c..8c+5 reduce rows t2/t3 of contact c; lane 8c takes t2, 8c+1 t3, 8c+2..4 boxes 3c..3c+2,
+// 8c+6/8c+7 the force rows t0/t1 (8c+5 has no row).  Branch-free: every lane evaluates every
+// candidate from clamped addresses and keeps its own.
 __device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const float* xs,
                                           const AdmmConst& K) {
   const int c = lane >> 3, s = lane & 7;
   const float* cf = sm.C(i);
-  const uint32_t bits = sm.flags[i];
-  float pa = 0.f, pb = 0.f;
-  if (s < 6) {
-    const int col = chain_col(c, s);
-    const float vd = xs[NQ + col];
-    const float vt = ((bits >> c) & 1u) ? vd : xs[col];
-    pa = cf[C_JA + 9 * c + col] * vt;
-    pb = cf[C_JB + 9 * c + col] * vd;
-  }
+  const bool st = (sm.flags[i] >> c) & 1u;
+  const int col = chain_col(c, s < 6 ? s : 0);
+  const float vd = xs[NQ + col];
+  const float vt = st ? vd : xs[col];
+  const float on = s < 6 ? 1.f : 0.f;
+  float pa = on * cf[C_JA + 9 * c + col] * vt;
+  float pb = on * cf[C_JB + 9 * c + col] * vd;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) {
     pa += __shfl_xor_sync(FULL, pa, o);
     pb += __shfl_xor_sync(FULL, pb, o);
   }
-  float zt = 0.f;
-  int slot = -1;
-  if (s == 0) {
-    zt = pa;
-    slot = 14 + 4 * c;
-  } else if (s == 1) {
-    zt = pb;
-    slot = 15 + 4 * c;
-  } else if (s >= 6) {
-    const int t = s - 6;
-    zt = cf[C_FORCE + 4 * c + 2 * t] * xs[18 + 2 * c] + cf[C_FORCE + 4 * c + 2 * t + 1] * xs[19 + 2 * c];
-    slot = 12 + 4 * c + t;
-  } else if (s <= 4) {  // s == 5 has no row
-    const int m = 3 * c + (s - 2);
-    zt = cf[C_BOX + m] * xs[m < 6 ? 3 + m : NQ + 3 + (m - 6)];
-    slot = 28 + m;
+  const int t = s & 1;  // force row t0 / t1 for s = 6 / 7
+  const float zf = cf[C_FORCE + 4 * c + 2 * t] * xs[18 + 2 * c] + cf[C_FORCE + 4 * c + 2 * t + 1] * xs[19 + 2 * c];
+  const int mb = 3 * c + (s >= 2 && s <= 4 ? s - 2 : 0);  // box index
+  const float zb = cf[C_BOX + mb] * xs[mb < 6 ? 3 + mb : NQ + 3 + (mb - 6)];
+  const float zt = s == 0 ? pa : (s == 1 ? pb : (s >= 6 ? zf : zb));
+  const int slot = s == 0 ? 14 + 4 * c : (s == 1 ? 15 + 4 * c : (s >= 6 ? 12 + 4 * c + t : 28 + mb));
+  bool ok = row_update(sm.R(i) + slot, s != 5, zt, K.alpha, K.oma, K.rho, K.rho_inv);
+  if (i == 0) {
+    const int l = lane < NINIT ? lane : 0;
+    ok = row_update(sm.R(-1) + INIT0 + l, lane < NINIT, cf[C_INIT + l] * xs[l], K.alpha, K.oma, K.rho,
+                    K.rho_inv) && ok;
   }
-  bool bad = false;
-  if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv);
-  if (i == 0 && lane < NINIT) {
-    const float z0 = cf[C_INIT + lane] * xs[lane];
-    bad = !row_update(sm.R(-1) + INIT0 + lane, z0, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
-  }
-  return bad;
+  return !ok;
 }
 
 // AdmmSolver::run (qp.cpp:156-190): exactly n_qp iterations from x = y = z = 0.  Returns the
@@ -1240,23 +1229,45 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   float* ubuf = sm.bc + 64 * warp;  // broadcast of u_i (this warp)
   float* xib = ubuf + 32;           // broadcast of xi_i (this warp)
   float* gb = sm.bc + 64 + 32;      // warp 1's xi buffer doubles as the g'_{m+1} hand-over
+  // lane roles, all branch-free below: q_k lanes 0..8, qd_k lanes 9..17, F lanes 18..25,
+  // W / dynamics lanes 26..28
+  const bool is_q = lane < 9, is_qd = lane >= 9 && lane < 18, is_var = lane < NV;
+  const bool is_dv = lane >= 9 && lane < NV, is_w = lane >= NV && lane < SROWS;
+  const int kq = is_q ? lane : (is_qd ? lane - 9 : 0);    // k of q_k / qd_k
+  const int jv = is_dv ? lane - 9 : 0;                     // index into v_b (node vars 9..25)
+  const int bw = is_w ? lane - NV : (lane >= 9 && lane < 12 ? lane - 9 : 0);
+  const int jr = lane < SROWS ? lane : SROWS - 1;          // row of the 29-row block
+  const float f_q = is_q ? 1.f : 0.f, f_qd = is_qd ? 1.f : 0.f, f_dv = is_dv ? 1.f : 0.f;
   auto r_of = [&](int i, bool first) {  // (sigma x - q^ + A^T(rho z - y)) restricted to node i
     const float cv = first ? 0.f : col_view<OpSum, TV_T>(sm, i, T, B);
-    return lane < NV ? K.sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv : 0.f;
+    return is_var ? K.sigma * sm.V(i, V_X)[lane] - sm.V(i, V_QH)[lane] + cv : 0.f;
   };
   auto store_s = [&](int i, float s) {  // s_i, and g^dyn in the spare slots of node i
     float* vs = sm.V(i, V_S);
     if (lane < NV + 2) vs[lane] = s;
     if (lane == NV + 2) sm.V(i, V_X)[NV] = s;
   };
+  auto gamma_of = [&](int i) { return bw < 2 ? sm.V(i, V_S)[NV + bw] : sm.V(i, V_X)[NV]; };
   auto finish_node = [&](int i) {  // node i's own rows and the x relaxation, from x~_i
     float* xs = sm.V(i, V_S);
     const bool b = node_rows(sm, lane, i, xs, K);
-    if (lane < NV) {
+    if (is_var) {
       float* x = sm.V(i, V_X);
       x[lane] = K.alpha * xs[lane] + K.oma * x[lane];
     }
     return b;
+  };
+  // - rho U g : top correction of node i from node i-1 (coefficients of interval i-1)
+  auto top_corr = [&](const float* cp, float gint, float g0, float g1, float g2) {
+    const float gk = __shfl_sync(FULL, gint, kq);
+    const float ci = cp[C_INT + 4 * kq + (is_q ? 0 : 2)];
+    return rho * ((f_q + f_qd) * ci * gk +
+                  f_qd * (cp[C_DYNU + kq] * g0 + cp[C_DYNU + 12 + kq] * g1 + cp[C_DYNU + 24 + kq] * g2));
+  };
+  // - rho V g' : bottom correction of node i from node i+1 (coefficients of interval i)
+  auto bot_corr = [&](const float* cf, float gint, float g0, float g1, float g2) {
+    return rho * (f_q * cf[C_INT + 4 * kq + 1] * gint +
+                  f_dv * (cf[C_DYNV + jv] * g0 + cf[C_DYNV + 20 + jv] * g1 + cf[C_DYNV + 40 + jv] * g2));
   };
 #pragma unroll 1
   for (int it = 0; it < P.n_qp; ++it) {
@@ -1267,21 +1278,10 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     if (warp == 0) {
 #pragma unroll 1
       for (int i = 0; i < m; ++i) {
-        float u = r_of(i, first);
-        if (i > 0) {
-          const float* cp = sm.C(i - 1);
-          const float gk = __shfl_sync(FULL, gint, lane >= 9 && lane < 18 ? lane - 9 : 0);
-          if (lane < 9) {
-            u -= rho * cp[C_INT + 4 * lane] * gint;
-          } else if (lane < 18) {
-            const int k = lane - 9;
-            u -= rho * (cp[C_INT + 4 * k + 2] * gk + cp[C_DYNU + k] * g0 + cp[C_DYNU + 12 + k] * g1 +
-                        cp[C_DYNU + 24 + k] * g2);
-          }
-        }
+        const float u = r_of(i, first) - top_corr(sm.C(i - 1), gint, g0, g1, g2);
         const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
         store_s(i, s);
-        gint = lane < 9 ? sm.C(i)[C_INT + 4 * lane + 1] * s : 0.f;
+        gint = f_q * sm.C(i)[C_INT + 4 * kq + 1] * s;
         g0 = __shfl_sync(FULL, s, 26);
         g1 = __shfl_sync(FULL, s, 27);
         g2 = __shfl_sync(FULL, s, 28);
@@ -1290,21 +1290,12 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     } else {
 #pragma unroll 1
       for (int i = NT - 1; i > m; --i) {
-        float u = r_of(i, first);
-        if (i < NT - 1) {  // - rho V_i g'_{i+1}
-          const float* cf = sm.C(i);
-          if (lane < 9) {
-            u -= rho * cf[C_INT + 4 * lane + 1] * gint;
-          } else if (lane < NV) {
-            u -= rho * (cf[C_DYNV + lane - 9] * g0 + cf[C_DYNV + 20 + lane - 9] * g1 +
-                        cf[C_DYNV + 40 + lane - 9] * g2);
-          }
-        }
+        const float u = r_of(i, first) - bot_corr(sm.C(i), gint, g0, g1, g2);
         const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
         store_s(i, s);
         const float* cp = sm.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
         const float sq = __shfl_down_sync(FULL, s, 9);
-        gint = lane < 9 ? cp[C_INT + 4 * lane] * s + cp[C_INT + 4 * lane + 2] * sq : 0.f;
+        gint = f_q * (cp[C_INT + 4 * kq] * s + cp[C_INT + 4 * kq + 2] * sq);
         g0 = __shfl_sync(FULL, s, 26);
         g1 = __shfl_sync(FULL, s, 27);
         g2 = __shfl_sync(FULL, s, 28);
@@ -1315,29 +1306,10 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     __syncthreads();
     // ---------------------------------------------------------------- middle
     if (warp == 0) {
-      float u = r_of(m, first);
-      if (m > 0) {
-        const float* cp = sm.C(m - 1);
-        const float gk = __shfl_sync(FULL, gint, lane >= 9 && lane < 18 ? lane - 9 : 0);
-        if (lane < 9) {
-          u -= rho * cp[C_INT + 4 * lane] * gint;
-        } else if (lane < 18) {
-          const int k = lane - 9;
-          u -= rho * (cp[C_INT + 4 * k + 2] * gk + cp[C_DYNU + k] * g0 + cp[C_DYNU + 12 + k] * g1 +
-                      cp[C_DYNU + 24 + k] * g2);
-        }
-      }
-      if (m + 1 < NT) {
-        const float* cf = sm.C(m);
-        if (lane < 9) {
-          u -= rho * cf[C_INT + 4 * lane + 1] * gb[lane];
-        } else if (lane < NV) {
-          u -= rho * (cf[C_DYNV + lane - 9] * gb[9] + cf[C_DYNV + 20 + lane - 9] * gb[10] +
-                      cf[C_DYNV + 40 + lane - 9] * gb[11]);
-        }
-      }
+      float u = r_of(m, first) - top_corr(sm.C(m - 1), gint, g0, g1, g2);
+      if (m + 1 < NT) u -= bot_corr(sm.C(m), gb[kq], gb[9], gb[10], gb[11]);
       const float x = ext_mv(sm.Sinv(m), lane, ubuf, u);
-      if (lane < NV) sm.V(m, V_S)[lane] = x;
+      if (is_var) sm.V(m, V_S)[lane] = x;
       bad = bad || !isfinite(x);
     }
     __syncthreads();
@@ -1349,58 +1321,41 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float* cf = sm.C(i);
         float* vs = sm.V(i, V_S);
         const float* xn = sm.V(i + 1, V_S);
-        float dl = 0.f, xi = 0.f;
-        if (lane < 9) {
-          dl = cf[C_INT + 4 * lane] * xn[lane] + cf[C_INT + 4 * lane + 2] * xn[NQ + lane];
-          xi = cf[C_INT + 4 * lane + 1] * dl;
-        } else if (lane < 12) {
-          const float* ub = cf + C_DYNU + 12 * (lane - 9);
-          float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
-          a0 = fmaf(ub[3], xn[NQ + 3], a0);
-          a1 = fmaf(ub[4], xn[NQ + 4], a1);
-          a2 = fmaf(ub[5], xn[NQ + 5], a2);
-          a0 = fmaf(ub[6], xn[NQ + 6], a0);
-          a1 = fmaf(ub[7], xn[NQ + 7], a1);
-          a2 = fmaf(ub[8], xn[NQ + 8], a2);
-          xi = a0 + a1 + a2;
-        }
-        xib[lane] = xi;
+        // xi_k = a2_k (a1_k x[q_k] + a3_k x[qd_k]) (lanes 0..8), xi_b = u_b . x[qd] (9..11)
+        const float dl = cf[C_INT + 4 * kq] * xn[kq] + cf[C_INT + 4 * kq + 2] * xn[NQ + kq];
+        const float* ub = cf + C_DYNU + 12 * bw;
+        float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
+        a0 = fmaf(ub[3], xn[NQ + 3], a0);
+        a1 = fmaf(ub[4], xn[NQ + 4], a1);
+        a2 = fmaf(ub[5], xn[NQ + 5], a2);
+        a0 = fmaf(ub[6], xn[NQ + 6], a0);
+        a1 = fmaf(ub[7], xn[NQ + 7], a1);
+        a2 = fmaf(ub[8], xn[NQ + 8], a2);
+        const float xd = a0 + a1 + a2;
+        xib[lane] = is_q ? cf[C_INT + 4 * kq + 1] * dl : (lane < 12 ? xd : 0.f);
         __syncwarp();
+        // lanes < 26: row j of S^-1 (cols 0..8 = column j) and W_b[j];  26..28: W_b, G_b
         const float* Sd = sm.Sinv(i);
-        const int j = lane < SROWS ? lane : SROWS - 1;
-        const float* rw = Sd + j * SROW;  // lanes < 26: row j (= column j); 26..28: W_b
+        const float* rw = Sd + jr * SROW;
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; k += 2) {
           acc0 = fmaf(rw[k], xib[k], acc0);
           if (k + 1 < 9) acc1 = fmaf(rw[k + 1], xib[k + 1], acc1);
         }
-        if (lane < NV) {
+        const float* wsrc = lane < NV ? Sd + NV * SROW + jr : cf + C_G + 3 * bw;
+        const int wstride = lane < NV ? SROW : 1;
 #pragma unroll
-          for (int b = 0; b < 3; ++b) acc1 = fmaf(Sd[(NV + b) * SROW + j], xib[9 + b], acc1);
-        } else {
-          const int b = j - NV;
-#pragma unroll
-          for (int b2 = 0; b2 < 3; ++b2) acc1 = fmaf(cf[C_G + 3 * b + b2], xib[9 + b2], acc1);
-        }
+        for (int b = 0; b < 3; ++b) acc1 = fmaf(wsrc[b * wstride], xib[9 + b], acc1);
         const float acc = acc0 + acc1;
-        float zt = 0.f, xt = 0.f;
-        int slot = -1;
-        if (lane < NV) {
-          xt = vs[lane] - rho * acc;
-          vs[lane] = xt;
-          bad = bad || !isfinite(xt);
-          if (lane < 9) {  // z~ of integration row k: a2 x~_i[q_k] + (a1, a3) . x~_{i+1}
-            zt = fmaf(cf[C_INT + 4 * lane + 1], xt, dl);
-            slot = lane;
-          }
-        } else if (lane < SROWS) {  // z~ of dynamics row b: v_b.x~_i + u_b.x~_{i+1}
-          const int b = lane - NV;
-          const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
-          zt = gam - rho * acc + xib[9 + b];
-          slot = 9 + b;
-        }
-        if (slot >= 0) bad = !row_update(sm.R(i) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        const float xt = is_var ? vs[lane] - rho * acc : 0.f;
+        if (is_var) vs[lane] = xt;
+        bad = bad || !isfinite(xt);
+        // z~: integration row k (lane k) = a2 x~_i[q_k] + dl ; dynamics row b (lane 26+b) =
+        // v_b.x~_i + u_b.x~_{i+1} = g_b - rho acc + xi_b
+        const float zt = is_q ? fmaf(cf[C_INT + 4 * kq + 1], xt, dl) : gamma_of(i) - rho * acc + xib[9 + bw];
+        const int slot = is_q ? kq : 9 + bw;
+        bad = !row_update(sm.R(i) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
         __syncwarp();
         bad = finish_node(i) || bad;
       }
@@ -1410,61 +1365,46 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float* cp = sm.C(i - 1);  // interval i-1 couples nodes i-1 and i
         const float* xp = sm.V(i - 1, V_S);
         float* vs = sm.V(i, V_S);
-        float xiv = 0.f;  // xi'_k = a2_k x_{i-1}[q_k];  xi'_b = v_b . x_{i-1}
-        if (lane < 9) {
-          xiv = cp[C_INT + 4 * lane + 1] * xp[lane];
-          xib[lane] = cp[C_INT + 4 * lane] * xiv;
-          xib[9 + lane] = cp[C_INT + 4 * lane + 2] * xiv;
-        } else if (lane < 12) {
-          const float* vb = cp + C_DYNV + 20 * (lane - 9);
-          float a0 = 0.f, a1 = 0.f, a2 = 0.f;
+        // xi'_k = a2_k x_{i-1}[q_k] (lanes 0..8, published as a1 xi', a3 xi'); xi'_b = v_b . x_{i-1}
+        const float xiv = cp[C_INT + 4 * kq + 1] * xp[kq];
+        const float* vb = cp + C_DYNV + 20 * bw;
+        float a0 = 0.f, a1 = 0.f, a2 = 0.f;
 #pragma unroll
-          for (int k = 0; k < 17; k += 3) {
-            a0 = fmaf(vb[k], xp[9 + k], a0);
-            if (k + 1 < 17) a1 = fmaf(vb[k + 1], xp[10 + k], a1);
-            if (k + 2 < 17) a2 = fmaf(vb[k + 2], xp[11 + k], a2);
-          }
-          xiv = a0 + a1 + a2;
-          xib[18 + lane - 9] = xiv;
+        for (int k = 0; k < 17; k += 3) {
+          a0 = fmaf(vb[k], xp[9 + k], a0);
+          if (k + 1 < 17) a1 = fmaf(vb[k + 1], xp[10 + k], a1);
+          if (k + 2 < 17) a2 = fmaf(vb[k + 2], xp[11 + k], a2);
         }
+        const float xd = a0 + a1 + a2;
+        if (is_q) {
+          xib[lane] = cp[C_INT + 4 * kq] * xiv;
+          xib[9 + lane] = cp[C_INT + 4 * kq + 2] * xiv;
+        }
+        if (lane >= 9 && lane < 12) xib[18 + bw] = xd;
         __syncwarp();
         const float* Sd = sm.Sinv(i);
-        const int j = lane < SROWS ? lane : SROWS - 1;
-        const float* rw = Sd + j * SROW;  // lanes < 26: row j of T^-1; 26..28: W'_b
+        const float* rw = Sd + jr * SROW;  // lanes < 26: row j of T^-1; 26..28: W'_b
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
           acc0 = fmaf(rw[k], xib[k], acc0);
           acc1 = fmaf(rw[NQ + k], xib[9 + k], acc1);
         }
-        if (lane < NV) {
+        const float* wsrc = lane < NV ? Sd + NV * SROW + jr : cp + C_G + 3 * bw;
+        const int wstride = lane < NV ? SROW : 1;
 #pragma unroll
-          for (int b = 0; b < 3; ++b) acc0 = fmaf(Sd[(NV + b) * SROW + j], xib[18 + b], acc0);
-        } else {
-          const int b = j - NV;
-#pragma unroll
-          for (int b2 = 0; b2 < 3; ++b2) acc0 = fmaf(cp[C_G + 3 * b + b2], xib[18 + b2], acc0);
-        }
+        for (int b = 0; b < 3; ++b) acc0 = fmaf(wsrc[b * wstride], xib[18 + b], acc0);
         const float acc = acc0 + acc1;
-        float xt = 0.f;
-        if (lane < NV) {
-          xt = vs[lane] - rho * acc;
-          vs[lane] = xt;
-          bad = bad || !isfinite(xt);
-        }
+        const float xt = is_var ? vs[lane] - rho * acc : 0.f;
+        if (is_var) vs[lane] = xt;
+        bad = bad || !isfinite(xt);
         const float xq = __shfl_down_sync(FULL, xt, 9);  // lane k: x_i[qd_k]
-        float zt = 0.f;
-        int slot = -1;
-        if (lane < 9) {  // z~ of integration row k of interval i-1
-          zt = xiv + cp[C_INT + 4 * lane] * xt + cp[C_INT + 4 * lane + 2] * xq;
-          slot = lane;
-        } else if (lane >= NV && lane < SROWS) {  // z~ of dynamics row b: v_b.x_{i-1} + u_b.x_i
-          const int b = lane - NV;
-          const float gam = b < 2 ? vs[NV + b] : sm.V(i, V_X)[NV];
-          zt = xib[18 + b] + gam - rho * acc;
-          slot = 9 + b;
-        }
-        if (slot >= 0) bad = !row_update(sm.R(i - 1) + slot, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        // z~: integration row k = xi'_k + a1 x_i[q_k] + a3 x_i[qd_k];
+        //     dynamics row b = v_b.x_{i-1} + u_b.x_i = xi'_b + g'_b - rho acc
+        const float zt = is_q ? xiv + cp[C_INT + 4 * kq] * xt + cp[C_INT + 4 * kq + 2] * xq
+                              : xib[18 + bw] + gamma_of(i) - rho * acc;
+        const int slot = is_q ? kq : 9 + bw;
+        bad = !row_update(sm.R(i - 1) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
         __syncwarp();
         bad = finish_node(i) || bad;
       }

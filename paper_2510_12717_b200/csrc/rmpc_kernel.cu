@@ -202,8 +202,10 @@ __device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, c
 
 // ------------------------------------------------------------------------- full row view
 // out_r = Op_j(A_rj, v_j) for the 40 slots of node i (lane l: slot l in o0, slot 32+l in
-// o1) and, at node 0, the 18 initial-state rows (lane l < 18 in o2).  Used by Ruiz and the
-// residuals; the ADMM loop gets the integration/dynamics rows from the recurrences instead.
+// o1) and the 18 initial-state rows (lane l < 18 in o2; C_INIT is zero unless i == 0).  Used
+// by Ruiz and the residuals; the ADMM loop gets the integration/dynamics rows from the
+// recurrences instead.  Branch-free: every lane runs the same instructions with clamped
+// indices and zero coefficients (C_ZERO) where its slot has no term.
 template <class Op>
 __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int which, float& o0,
                                          float& o1, float& o2) {
@@ -211,75 +213,51 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
   const float* vi = sm.V(i, which);
   const float* vn = (i + 1 < sm.NT) ? sm.V(i + 1, which) : vi;  // coefficients are 0 then
   const uint32_t bits = sm.flags[i];
-  o0 = Op::id();
-  o1 = Op::id();
-  o2 = Op::id();
-  if (lane < 9) {
-    const float4 a = *reinterpret_cast<const float4*>(cf + C_INT + 4 * lane);
-    o0 = Op::comb(o0, a.x, vn[lane]);
-    o0 = Op::comb(o0, a.y, vi[lane]);
-    o0 = Op::comb(o0, a.z, vn[NQ + lane]);
-  } else if (lane >= 12 && lane < 28) {
-    const int c = (lane - 12) >> 2, t = (lane - 12) & 3;
-    if (t < 2) {
-      o0 = Op::comb(o0, cf[C_FORCE + 4 * c + 2 * t], vi[18 + 2 * c]);
-      o0 = Op::comb(o0, cf[C_FORCE + 4 * c + 2 * t + 1], vi[19 + 2 * c]);
-    }
-  } else if (lane >= 28) {
-    o0 = Op::comb(o0, cf[C_BOX + lane - 28], vi[3 + lane - 28]);
-  }
-  if (lane < 8) {
-    const int m = 4 + lane;
-    o1 = Op::comb(o1, cf[C_BOX + m], vi[m < 6 ? 3 + m : NQ + 3 + (m - 6)]);
-  }
-  if (i == 0 && lane < NINIT) o2 = Op::comb(o2, cf[C_INIT + lane], vi[lane]);
-  {  // dynamics rows: lane = support entry (qd_{i+1}: 0..8, node-i vars 9..25)
-    float p0 = Op::id(), p1 = Op::id(), p2 = Op::id();
-    if (lane < 9) {
-      const float v = vn[NQ + lane];
-      p0 = Op::comb(p0, cf[C_DYNU + lane], v);
-      p1 = Op::comb(p1, cf[C_DYNU + 12 + lane], v);
-      p2 = Op::comb(p2, cf[C_DYNU + 24 + lane], v);
-    } else if (lane < NV) {
-      const float v = vi[lane];
-      p0 = Op::comb(p0, cf[C_DYNV + lane - 9], v);
-      p1 = Op::comb(p1, cf[C_DYNV + 20 + lane - 9], v);
-      p2 = Op::comb(p2, cf[C_DYNV + 40 + lane - 9], v);
-    }
+  // own terms: integration (lanes 0..8), force cones (12..27, t < 2), boxes (28..31)
+  const bool li = lane < 9, lb = lane >= 28;
+  const int cq = (lane - 12) >> 2, tq = (lane - 12) & 3;
+  const bool lf = lane >= 12 && lane < 28 && tq < 2;
+  const int c1 = li ? C_INT + 4 * lane : (lf ? C_FORCE + 4 * cq + 2 * tq : (lb ? C_BOX + lane - 28 : C_ZERO));
+  const int c2 = li ? C_INT + 4 * lane + 1 : (lf ? C_FORCE + 4 * cq + 2 * tq + 1 : C_ZERO);
+  const int c3 = li ? C_INT + 4 * lane + 2 : C_ZERO;
+  const float* v1 = li ? vn + lane : vi + (lf ? 18 + 2 * cq : (lb ? lane - 25 : 0));
+  const float* v2 = vi + (li ? lane : (lf ? 19 + 2 * cq : 0));
+  const float* v3 = vn + (li ? NQ + lane : 0);
+  o0 = Op::comb(Op::comb(Op::comb(Op::id(), cf[c1], *v1), cf[c2], *v2), cf[c3], *v3);
+  const int m4 = 4 + lane;  // slot 32 + lane: boxes 4..11
+  o1 = Op::comb(Op::id(), cf[lane < 8 ? C_BOX + m4 : C_ZERO],
+                vi[lane < 8 ? (m4 < 6 ? 3 + m4 : NQ + m4 - 3) : 0]);
+  o2 = Op::comb(Op::id(), cf[lane < NINIT ? C_INIT + lane : C_ZERO], vi[lane < NINIT ? lane : 0]);
+  // dynamics rows 9..11: lane = support entry (qd_{i+1}: 0..8, node-i vars 9..25)
+  const bool du = lane < 9, dv = lane >= 9 && lane < NV;
+  const int dc = du ? C_DYNU + lane : (dv ? C_DYNV + lane - 9 : C_ZERO);
+  const int ds = du ? 12 : (dv ? 20 : 0);
+  const float dval = du ? vn[NQ + lane] : vi[dv ? lane : 0];
+  const float p0 = Op::comb(Op::id(), cf[dc], dval), p1 = Op::comb(Op::id(), cf[dc + ds], dval),
+              p2 = Op::comb(Op::id(), cf[dc + 2 * ds], dval), p3 = Op::id();
+  // contact Jacobian rows t2, t3: 8-lane group per contact
+  const int c = lane >> 3, s = lane & 7;
+  const int col = chain_col(c, s < 6 ? s : 0);
+  const float vd = vi[NQ + col];
+  const float vt = ((bits >> c) & 1u) ? vd : vi[col];
+  const float pa = Op::comb(Op::id(), cf[s < 6 ? C_JA + 9 * c + col : C_ZERO], vt);
+  const float pb = Op::comb(Op::id(), cf[s < 6 ? C_JB + 9 * c + col : C_ZERO], vd);
+  // Transposed butterflies: 4 dynamics partials -> row (lane >> 3) in 6 shuffles; the
+  // (pa, pb) pair -> pa in lanes 8c..8c+3, pb in 8c+4..8c+7 in 3 shuffles.
+  const bool h = lane & 16, g = lane & 8, e = lane & 4;
+  float k0 = h ? p2 : p0, k1 = h ? p3 : p1;
+  k0 = Op::red(k0, __shfl_xor_sync(FULL, h ? p0 : p2, 16));
+  k1 = Op::red(k1, __shfl_xor_sync(FULL, h ? p1 : p3, 16));
+  float kd = Op::red(g ? k1 : k0, __shfl_xor_sync(FULL, g ? k0 : k1, 8));
+  float kc = Op::red(e ? pb : pa, __shfl_xor_sync(FULL, e ? pa : pb, 4));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      p0 = Op::red(p0, __shfl_xor_sync(FULL, p0, o));
-      p1 = Op::red(p1, __shfl_xor_sync(FULL, p1, o));
-      p2 = Op::red(p2, __shfl_xor_sync(FULL, p2, o));
-    }
-    if (lane == 9) o0 = p0;
-    else if (lane == 10) o0 = p1;
-    else if (lane == 11) o0 = p2;
-  }
-  {  // contact Jacobian rows t2, t3: 8-lane group per contact
-    const int c = lane >> 3, s = lane & 7;
-    float pa = Op::id(), pb = Op::id();
-    if (s < 6) {
-      const int col = chain_col(c, s);
-      const float vd = vi[NQ + col];
-      const float vt = ((bits >> c) & 1u) ? vd : vi[col];
-      pa = Op::comb(pa, cf[C_JA + 9 * c + col], vt);
-      pb = Op::comb(pb, cf[C_JB + 9 * c + col], vd);
-    }
+  for (int o = 4; o > 0; o >>= 1) kd = Op::red(kd, __shfl_xor_sync(FULL, kd, o));
 #pragma unroll
-    for (int o = 4; o > 0; o >>= 1) {
-      pa = Op::red(pa, __shfl_xor_sync(FULL, pa, o));
-      pb = Op::red(pb, __shfl_xor_sync(FULL, pb, o));
-    }
-    const bool mine = lane >= 12 && lane < 28;
-    const int src = mine ? ((lane - 12) >> 2) << 3 : 0;
-    const float ga = __shfl_sync(FULL, pa, src), gb = __shfl_sync(FULL, pb, src);
-    if (mine) {
-      const int t = (lane - 12) & 3;
-      if (t == 2) o0 = ga;
-      else if (t == 3) o0 = gb;
-    }
-  }
+  for (int o = 2; o > 0; o >>= 1) kc = Op::red(kc, __shfl_xor_sync(FULL, kc, o));
+  const bool ld = lane >= 9 && lane < 12, lc = lane >= 12 && lane < 28 && tq >= 2;
+  const float rd = __shfl_sync(FULL, kd, ld ? 8 * (lane - 9) : 0);
+  const float rc = __shfl_sync(FULL, kc, lc ? 8 * cq + 4 * (tq - 2) : 0);
+  o0 = ld ? rd : (lc ? rc : o0);
 }
 
 // ------------------------------------------------------------------------- FP64 kinematics
@@ -693,46 +671,45 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
   build_terms(lane, T);
   TermBytes B;
   term_bytes<TV_D>(T, B);
+  // Double-buffered scales: pass p reads (d, e) from one copy and writes d delta, e delta to
+  // the other, so one barrier per pass suffices.  The second d lives in the S^-1 region (free
+  // until the factorization), the second e in V_S.
+  const int nd = (NT + 1) * NSLOT;
+  for (int r = lane + 32 * warp; r < nd; r += 64) sm.sinv[r] = sm.dsc[r];
+  __syncthreads();
+  auto inv_sqrt1 = [](float nrm) { return nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f; };
 #pragma unroll 1
   for (int pass = 0; pass < P.ruiz_iters; ++pass) {
+    const bool odd = pass & 1;
+    Sm src = sm;
+    src.dsc = odd ? sm.sinv : sm.dsc;
+    float* dst = odd ? sm.dsc : sm.sinv;
+    const int es = odd ? V_S : V_E, ed = odd ? V_E : V_S;
 #pragma unroll 1
     for (int i = warp; i < NT; i += 2) {  // nodes are independent within a pass
       float o0, o1, o2;
-      row_view<OpMax>(sm, i, lane, V_E, o0, o1, o2);
-      const float* d = sm.D(i);
-      const float cv = col_view<OpMax, TV_D>(sm, i, T, B);
-      float4* rw = sm.R(i);
-      auto stash = [](float4* r, const float* dp, float o) {
-        const float nrm = *dp * o;
-        r->z = nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f;
-      };
-      stash(rw + lane, d + lane, o0);
-      if (lane < 8) stash(rw + 32 + lane, d + 32 + lane, o1);
-      if (i == 0 && lane < NINIT) stash(sm.R(-1) + INIT0 + lane, sm.D(-1) + INIT0 + lane, o2);
-      if (lane < NV) {
-        const float e = sm.V(i, V_E)[lane];
-        const float pd = (float)wcost(P, lane) * (float)P.dt[i];
-        const float nrm = e * fmaxf(fabsf(pd) * e, cv);
-        sm.V(i, V_S)[lane] = nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f;
-      }
-    }
-    __syncthreads();  // every norm of this pass uses the scales of the previous pass
-#pragma unroll 1
-    for (int i = warp; i < NT; i += 2) {
-      float4* rw = sm.R(i);
-      float* d = sm.D(i);
-      d[lane] *= rw[lane].z;
-      rw[lane].z = 0.f;
-      if (lane < 8) {
-        d[32 + lane] *= rw[32 + lane].z;
-        rw[32 + lane].z = 0.f;
-      }
+      row_view<OpMax>(src, i, lane, es, o0, o1, o2);
+      const float cv = col_view<OpMax, TV_D>(src, i, T, B);
+      const float* d = src.D(i);
+      float* dn = dst + (i + 1) * NSLOT;
+      dn[lane] = d[lane] * inv_sqrt1(d[lane] * o0);
+      if (lane < 8) dn[32 + lane] = d[32 + lane] * inv_sqrt1(d[32 + lane] * o1);
       if (i == 0 && lane < NINIT) {
-        sm.D(-1)[INIT0 + lane] *= sm.R(-1)[INIT0 + lane].z;
-        sm.R(-1)[INIT0 + lane].z = 0.f;
+        const float* d0 = src.D(-1) + INIT0;
+        dst[INIT0 + lane] = d0[lane] * inv_sqrt1(d0[lane] * o2);
       }
-      if (lane < NV) sm.V(i, V_E)[lane] *= sm.V(i, V_S)[lane];
+      if (lane < NV) {
+        const float e = sm.V(i, es)[lane];
+        const float pd = (float)wcost(P, lane) * (float)P.dt[i];
+        sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, cv));
+      }
     }
+    __syncthreads();  // every norm of the next pass uses the scales of this one
+  }
+  if (P.ruiz_iters & 1) {  // the last pass wrote the second copies
+    for (int r = lane + 32 * warp; r < nd; r += 64) sm.dsc[r] = sm.sinv[r];
+    for (int i = warp; i < NT; i += 2)
+      if (lane < NV) sm.V(i, V_E)[lane] = sm.V(i, V_S)[lane];
     __syncthreads();
   }
 }

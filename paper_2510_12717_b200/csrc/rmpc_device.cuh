@@ -5,7 +5,9 @@
 // by sparse LDL^T, ldl.cpp:123-192) is replaced by its mathematically identical reduced form
 //     (P^ + sigma I + rho A^T A) x~ = sigma x - q^ + A^T (rho z - y),   z~ = A^ x~,
 // which is block tridiagonal over horizon nodes (26 x 26 blocks) and is solved by block
-// elimination with explicit Schur-complement inverses S_i^-1 kept in shared memory.
+// elimination with explicit Schur-complement inverses S_i^-1 kept in tensor memory (TMEM):
+// TMEM lane j holds row j of every block the warp owns, so a row is one tcgen05.ld and the
+// per-agent shared memory drops to the QP data (~27 KB at T = 10, six agents per SM).
 // See DESIGN.md for the derivation and the HBM / shared-memory budget.
 #pragma once
 
@@ -17,8 +19,9 @@ namespace rmpc_dev {
 
 constexpr int NV = 26, NQ = 9, NF = 8, NC = 4, NJ = 6;
 constexpr int MAXT = RMPC_MAX_HORIZON;
-constexpr int SROW = 26;      // row stride of the S^-1 block (LDS.64 rows, conflict-free)
-constexpr int SROWS = 29;     // 26 rows of S_i^-1, then W_b = S_i^-1 v_b (b = 0..2)
+constexpr int SROWS = 29;     // TMEM lanes of a node block: 26 rows of S_i^-1, then W_b^T
+constexpr int TCOLS = 32;     // TMEM columns per node block: S_i^-1 row j, then W_b[j] (26..28)
+constexpr int MAX_AGENTS = 6; // agents (warp pairs) per CTA: 384 threads, <= 168 registers
 constexpr int NSLOT = 40;     // constraint-row slots per node block
 constexpr int NINIT = 18;     // initial-state rows
 constexpr int INIT0 = 12;     // initial-state rows live in block -1, slots [12, 30)
@@ -58,10 +61,12 @@ constexpr int V_E = 2;    // Ruiz column scale e
 constexpr int V_S = 3;    // r_i -> s_i -> x~_i -> next r_i
 constexpr int V_NUM = 4;
 constexpr int V_STRIDE = 28;
+constexpr int G_SCR = 160;    // 12 x 13 G block (+ pad) of the factorization
 
 struct KParams {
   int32_t NT, n_qp, ruiz_iters, warm_start;
   int32_t n_agents, profile;
+  int32_t agents_per_cta, cols_per_warp, tmem_cols, pad_;
   double dt[MAXT];
   double wq[NQ], wqd[NQ], wf[NF];
   double z_swing, v_to, v_td;
@@ -81,9 +86,9 @@ struct KParams {
   unsigned long long* prof;  // [RMPC_NUM_STAGES] cycle accumulators (profile only)
 };
 
-// Shared-memory footprint of one warp (one agent) in floats, every region 16-byte aligned.
+// Shared-memory footprint of one agent (warp pair) in floats, every region 16-byte aligned.
 struct Layout {
-  int sinv, coef, vec, row, dsc, bc, flags, total;
+  int scr, coef, vec, row, dsc, bc, flags, total;
 };
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
@@ -91,7 +96,9 @@ __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 __host__ __device__ inline Layout make_layout(int NT) {
   Layout L;
   int o = 0;
-  L.sinv = o;  o += align4(NT * SROWS * SROW);
+  // scratch: Ruiz's second d, the two 12 x 13 G blocks of the factorization, z* rows (FP64)
+  const int nscr = (NT + 1) * NSLOT > 2 * G_SCR ? (NT + 1) * NSLOT : 2 * G_SCR;
+  L.scr = o;   o += align4(nscr);
   L.coef = o;  o += (NT + 1) * C_SIZE;              // block -1 first
   L.vec = o;   o += NT * V_NUM * V_STRIDE;
   L.row = o;   o += 4 * (NT + 1) * NSLOT;           // float4 {lo, hi, z, t = rho z - y}
@@ -103,6 +110,33 @@ __host__ __device__ inline Layout make_layout(int NT) {
 }
 
 inline int smem_bytes(int NT) { return make_layout(NT).total * 4; }
+
+// Nodes owned by one warp (top: [0, m], bottom: (m, T)), i.e. TMEM blocks per warp.
+__host__ __device__ inline int nodes_per_warp(int NT) {
+  const int m = mid_node(NT), a = m + 1, b = NT - 1 - m;
+  return a > b ? a : b;
+}
+
+// CTA shape: A agents = 2A warps; warp w uses TMEM lanes [32 (w % 4), +32) and columns
+// [(w / 4) * cols_per_warp, +cols_per_warp), so A is bounded by TMEM (512 columns), by the
+// 227 KB of shared memory and by MAX_AGENTS.
+struct CtaShape {
+  int agents, cols_per_warp, tmem_cols, smem_bytes;
+};
+inline CtaShape cta_shape(int NT) {
+  CtaShape c;
+  c.cols_per_warp = TCOLS * nodes_per_warp(NT);
+  const int per = smem_bytes(NT);
+  int A = MAX_AGENTS;
+  while (A > 1 && (((2 * A + 3) / 4) * c.cols_per_warp > 512 || A * per > 227 * 1024 - 128)) --A;
+  c.agents = A;
+  const int need = ((2 * A + 3) / 4) * c.cols_per_warp;
+  int cols = 32;
+  while (cols < need) cols *= 2;
+  c.tmem_cols = cols;
+  c.smem_bytes = A * per;
+  return c;
+}
 
 }  // namespace rmpc_dev
 

@@ -34,7 +34,7 @@ namespace rmpc_dev {
 
 // ------------------------------------------------------------------------- helpers
 struct Sm {
-  float* sinv;
+  float* scr;   // scratch (Ruiz d copy, factorization G blocks, FP64 z* rows)
   float* coef;  // block -1 at coef, node i at coef + (i + 1) * C_SIZE
   float* vec;
   float4* row;  // block -1 at row, node i at row + (i + 1) * NSLOT
@@ -42,14 +42,76 @@ struct Sm {
   float* bc;
   uint32_t* flags;
   int NT;
+  int mid;      // middle node: the top warp owns [0, mid], the bottom warp (mid, NT)
+  uint32_t tm;  // TMEM address of this warp's first node block (lane quarter | column)
+  int bar;      // named barrier of the agent's warp pair
   __device__ __forceinline__ float* C(int i) const { return coef + (i + 1) * C_SIZE; }
   __device__ __forceinline__ float4* R(int i) const { return row + (i + 1) * NSLOT; }
   __device__ __forceinline__ float* D(int i) const { return dsc + (i + 1) * NSLOT; }
   __device__ __forceinline__ float* V(int i, int which) const {
     return vec + (i * V_NUM + which) * V_STRIDE;
   }
-  __device__ __forceinline__ float* Sinv(int i) const { return sinv + i * SROWS * SROW; }
+  // TMEM block of node i (only meaningful in the warp that owns node i)
+  __device__ __forceinline__ uint32_t Tm(int i) const {
+    return tm + (uint32_t)(TCOLS * (i <= mid ? i : i - mid - 1));
+  }
 };
+
+// ------------------------------------------------------------------------- sync / TMEM
+// The two warps of an agent synchronise on their own named barrier (64 threads); barrier 0
+// is the CTA-wide one used only around TMEM allocation.
+__device__ __forceinline__ void pair_sync(const Sm& sm) {
+  asm volatile("bar.sync %0, 64;" ::"r"(sm.bar) : "memory");
+}
+__device__ __forceinline__ bool pair_or(const Sm& sm, bool v) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbar.red.or.pred q, %2, 64, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((int)v), "r"(sm.bar)
+      : "memory");
+  return r != 0;
+}
+__device__ __forceinline__ bool pair_and(const Sm& sm, bool v) {
+  int r;
+  asm volatile(
+      "{\n\t.reg .pred p, q;\n\tsetp.ne.s32 p, %1, 0;\n\tbar.red.and.pred q, %2, 64, p;\n\t"
+      "selp.s32 %0, 1, 0, q;\n\t}"
+      : "=r"(r)
+      : "r"((int)v), "r"(sm.bar)
+      : "memory");
+  return r != 0;
+}
+
+#define RMPC_X32(F, v)                                                                        \
+  F(v[0]), F(v[1]), F(v[2]), F(v[3]), F(v[4]), F(v[5]), F(v[6]), F(v[7]), F(v[8]), F(v[9]),  \
+      F(v[10]), F(v[11]), F(v[12]), F(v[13]), F(v[14]), F(v[15]), F(v[16]), F(v[17]),         \
+      F(v[18]), F(v[19]), F(v[20]), F(v[21]), F(v[22]), F(v[23]), F(v[24]), F(v[25]),         \
+      F(v[26]), F(v[27]), F(v[28]), F(v[29]), F(v[30]), F(v[31])
+#define RMPC_OUT(x) "=f"(x)
+#define RMPC_IN(x) "f"(x)
+#define RMPC_OPS32                                                                              \
+  "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24," \
+  "%25,%26,%27,%28,%29,%30,%31}"
+#define RMPC_OPS32_1                                                                           \
+  "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25," \
+  "%26,%27,%28,%29,%30,%31,%32}"
+
+// Lane l of the warp reads / writes its TMEM row (lane quarter of the warp) at columns
+// [a, a + 32): one 32x32b.x32 access moves a whole 26-float block row plus its W entries.
+__device__ __forceinline__ void tm_load(uint32_t a, float v[TCOLS]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " RMPC_OPS32 ", [%32];"
+               : RMPC_X32(RMPC_OUT, v)
+               : "r"(a));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void tm_store(uint32_t a, const float v[TCOLS]) {
+  asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " RMPC_OPS32_1 ";"
+               ::"r"(a), RMPC_X32(RMPC_IN, v)
+               : "memory");
+  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+}
 
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
@@ -672,18 +734,18 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
   TermBytes B;
   term_bytes<TV_D>(T, B);
   // Double-buffered scales: pass p reads (d, e) from one copy and writes d delta, e delta to
-  // the other, so one barrier per pass suffices.  The second d lives in the S^-1 region (free
-  // until the factorization), the second e in V_S.
+  // the other, so one barrier per pass suffices.  The second d lives in the scratch region,
+  // the second e in V_S.
   const int nd = (NT + 1) * NSLOT;
-  for (int r = lane + 32 * warp; r < nd; r += 64) sm.sinv[r] = sm.dsc[r];
-  __syncthreads();
+  for (int r = lane + 32 * warp; r < nd; r += 64) sm.scr[r] = sm.dsc[r];
+  pair_sync(sm);
   auto inv_sqrt1 = [](float nrm) { return nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f; };
 #pragma unroll 1
   for (int pass = 0; pass < P.ruiz_iters; ++pass) {
     const bool odd = pass & 1;
     Sm src = sm;
-    src.dsc = odd ? sm.sinv : sm.dsc;
-    float* dst = odd ? sm.dsc : sm.sinv;
+    src.dsc = odd ? sm.scr : sm.dsc;
+    float* dst = odd ? sm.dsc : sm.scr;
     const int es = odd ? V_S : V_E, ed = odd ? V_E : V_S;
 #pragma unroll 1
     for (int i = warp; i < NT; i += 2) {  // nodes are independent within a pass
@@ -704,13 +766,13 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
         sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, cv));
       }
     }
-    __syncthreads();  // every norm of the next pass uses the scales of this one
+    pair_sync(sm);  // every norm of the next pass uses the scales of this one
   }
   if (P.ruiz_iters & 1) {  // the last pass wrote the second copies
-    for (int r = lane + 32 * warp; r < nd; r += 64) sm.dsc[r] = sm.sinv[r];
+    for (int r = lane + 32 * warp; r < nd; r += 64) sm.dsc[r] = sm.scr[r];
     for (int i = warp; i < NT; i += 2)
       if (lane < NV) sm.V(i, V_E)[lane] = sm.V(i, V_S)[lane];
-    __syncthreads();
+    pair_sync(sm);
   }
 }
 
@@ -756,7 +818,7 @@ __device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp
     rd.y *= dr;
     sm.row[r] = rd;
   }
-  __syncthreads();
+  pair_sync(sm);
 }
 
 // ------------------------------------------------------------------------- stage: factor
@@ -876,21 +938,33 @@ __device__ __forceinline__ bool gauss_jordan(int j, float S[NV], float* bc) {
   return good;
 }
 
-__device__ __forceinline__ void store_inverse(float* Sd, int j, const float S[NV]) {
-  if (j < NV) {
-    float2* dst = reinterpret_cast<float2*>(Sd + j * SROW);
+// Node block in TMEM (TCOLS columns of the owning warp's lane quarter): lane j < 26 holds row
+// j of the inverse in columns 0..25 and W_b[j] in columns 26..28; lanes 26..28 hold W_b^T in
+// columns 0..25 (transposed through `tr`, >= 96 floats of the warp's scratch).
+__device__ __forceinline__ void store_block(uint32_t a, int j, const float S[NV], const float W[3], float* tr) {
 #pragma unroll
-    for (int q = 0; q < 13; ++q) dst[q] = make_float2(S[2 * q], S[2 * q + 1]);
-  }
+  for (int b = 0; b < 3; ++b) tr[32 * b + j] = W[b];
+  __syncwarp();
+  const bool wrow = j >= NV && j < SROWS;
+  const float* src = tr + 32 * (wrow ? j - NV : 0);
+  float v[TCOLS];
+#pragma unroll
+  for (int k = 0; k < NV; ++k) v[k] = wrow ? src[k] : S[k];
+#pragma unroll
+  for (int b = 0; b < 3; ++b) v[NV + b] = wrow ? 0.f : W[b];
+#pragma unroll
+  for (int k = SROWS; k < TCOLS; ++k) v[k] = 0.f;
+  tm_store(a, v);
+  __syncwarp();  // tr is reused by the caller
 }
 
-// Top Schur step after S_i^-1 (rows in S): W_b = S^-1 v_b -> rows 26..28, G_dd -> C(i)[C_G],
-// and the update Yp (rows j < 18, cols < 18) of node i+1: rho^2 U_i G_i U_i^T.
+// Top Schur step after S_i^-1 (rows in S): W_b = S^-1 v_b, the node block into TMEM, G_dd ->
+// C(i)[C_G], and the update Yp (rows j < 18, cols < 18) of node i+1: rho^2 U_i G_i U_i^T.
 __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i, int j, const float S[NV],
                                           float Yp[18]) {
   const float rho = (float)P.rho;
   const float* cf = sm.C(i);
-  float* Sd = sm.Sinv(i);
+  float* G = sm.scr;  // the top warp's 12 x 13 G block
   float W[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {
@@ -899,9 +973,8 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
 #pragma unroll
     for (int l = 9; l < NV; ++l) acc = fmaf(S[l], vb[l - 9], acc);
     W[b] = j < NV ? acc : 0.f;
-    if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
   }
-  float* G = sm.Sinv(i + 1);  // node i+1's block is free until it is factorized: 12 x 13
+  store_block(sm.Tm(i), j, S, W, G);
   if (j < 9) {
     const float a2 = cf[C_INT + 4 * j + 1];
 #pragma unroll
@@ -956,14 +1029,40 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
   __syncwarp();
 }
 
+// Update of node `iv` (the upper node of interval iv) from the bottom half: row j of
+// rho^2 V_iv G'_iv V_iv^T, G' (12 x 13) in G.
+__device__ __forceinline__ void bottom_update(const KParams& P, const Sm& sm, int iv, int j, const float* G,
+                                              float Yb[NV]) {
+  const float* cp = sm.C(iv);
+  float Z[12];  // Z[j][s] = sum_r V[j][r] G'[r][s]
+  if (j < 9) {
+    const float a2 = cp[C_INT + 4 * j + 1];
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = a2 * G[j * 13 + s];
+  } else if (j < NV) {
+    const float v0 = cp[C_DYNV + j - 9], v1 = cp[C_DYNV + 20 + j - 9], v2 = cp[C_DYNV + 40 + j - 9];
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = v0 * G[9 * 13 + s] + v1 * G[10 * 13 + s] + v2 * G[11 * 13 + s];
+  } else {
+#pragma unroll
+    for (int s = 0; s < 12; ++s) Z[s] = 0.f;
+  }
+  const float r2 = (float)P.rho * (float)P.rho;
+#pragma unroll
+  for (int l = 0; l < 9; ++l) Yb[l] = r2 * Z[l] * cp[C_INT + 4 * l + 1];
+#pragma unroll
+  for (int l = 9; l < NV; ++l)
+    Yb[l] = r2 * (Z[9] * cp[C_DYNV + l - 9] + Z[10] * cp[C_DYNV + 20 + l - 9] + Z[11] * cp[C_DYNV + 40 + l - 9]);
+}
+
 // Bottom Schur step after T_i^-1 (rows in S), interval i-1 couples nodes i-1 and i:
-// W'_b = T^-1 u_b -> rows 26..28, G'_dd -> C(i-1)[C_G], and the full update Yb of node i-1:
-// rho^2 V_{i-1} G'_{i-1} V_{i-1}^T with G' = U^T T^-1 U (12 x 12).
+// W'_b = T^-1 u_b, the node block into TMEM, G'_dd -> C(i-1)[C_G], G' = U^T T^-1 U (12 x 12)
+// into the bottom warp's scratch (read by the top warp at the middle) and the update Yb of
+// node i-1.
 __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int i, int j, const float S[NV],
                                              float Yb[NV]) {
-  const float rho = (float)P.rho;
   const float* cp = sm.C(i - 1);
-  float* Sd = sm.Sinv(i);
+  float* G = sm.scr + G_SCR;
   float W[3];
 #pragma unroll
   for (int b = 0; b < 3; ++b) {  // W'_b[j] = sum_k T^-1[j][9+k] u_b[k]
@@ -972,15 +1071,12 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
 #pragma unroll
     for (int k = 0; k < 9; ++k) acc = fmaf(S[NQ + k], ub[k], acc);
     W[b] = j < NV ? acc : 0.f;
-    if (j < NV) Sd[(NV + b) * SROW + j] = W[b];
   }
+  store_block(sm.Tm(i), j, S, W, G);
   // int-int / int-dyn parts: lane k (row k) and lane 9+k (row 9+k) of T^-1
   float Pk[9];
 #pragma unroll
   for (int l = 0; l < 9; ++l) Pk[l] = cp[C_INT + 4 * l] * S[l] + cp[C_INT + 4 * l + 2] * S[NQ + l];
-  // node i-1's block is free until it is factorized (offset 200: at the middle node the top
-  // warp may be using [0, 156) of the same block concurrently): 12 x 13
-  float* G = sm.Sinv(i - 1) + 200;
   const float a1 = j < 9 ? cp[C_INT + 4 * j] : 0.f, a3 = j < 9 ? cp[C_INT + 4 * j + 2] : 0.f;
 #pragma unroll
   for (int l = 0; l < 9; ++l) {
@@ -1014,32 +1110,14 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
       }
   }
   __syncwarp();
-  float Z[12];  // Z[j][s] = sum_r V[j][r] G'[r][s]
-  if (j < 9) {
-    const float a2 = cp[C_INT + 4 * j + 1];
-#pragma unroll
-    for (int s = 0; s < 12; ++s) Z[s] = a2 * G[j * 13 + s];
-  } else if (j < NV) {
-    const float v0 = cp[C_DYNV + j - 9], v1 = cp[C_DYNV + 20 + j - 9], v2 = cp[C_DYNV + 40 + j - 9];
-#pragma unroll
-    for (int s = 0; s < 12; ++s) Z[s] = v0 * G[9 * 13 + s] + v1 * G[10 * 13 + s] + v2 * G[11 * 13 + s];
-  } else {
-#pragma unroll
-    for (int s = 0; s < 12; ++s) Z[s] = 0.f;
-  }
-  const float r2 = rho * rho;
-#pragma unroll
-  for (int l = 0; l < 9; ++l) Yb[l] = r2 * Z[l] * cp[C_INT + 4 * l + 1];
-#pragma unroll
-  for (int l = 9; l < NV; ++l)
-    Yb[l] = r2 * (Z[9] * cp[C_DYNV + l - 9] + Z[10] * cp[C_DYNV + 20 + l - 9] + Z[11] * cp[C_DYNV + 40 + l - 9]);
-  __syncwarp();
+  bottom_update(P, sm, i - 1, j, G, Yb);
 }
 
-// Returns false (CTA-uniform) on a non-positive pivot (SingularityError, ldl.cpp:155-160).
+// Returns false (pair-uniform) on a non-positive pivot (SingularityError, ldl.cpp:155-160).
 // Both warps run the same loop (one Gauss-Jordan / assembly instance in the code): step t
 // factorizes node t (warp 0, top) or node T-1-t (warp 1, bottom); warp 0's last step is the
-// middle node, whose bottom update warp 1 hands over through the middle block.
+// middle node, whose bottom update it rebuilds from the G' block the bottom warp left in its
+// scratch.
 __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
   const int NT = P.NT;
   const int m = mid_node(NT);
@@ -1055,13 +1133,7 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
   for (int t = 0; t < steps; ++t) {
     const bool middle = t == steps - 1;
     if (middle) {
-      __syncthreads();  // both halves are done with their scratch in the middle block
-      if (warp == 1 && j < NV) {
-        float* dst = sm.Sinv(m) + j * SROW;
-#pragma unroll
-        for (int l = 0; l < NV; ++l) dst[l] = Y[l];
-      }
-      __syncthreads();
+      pair_sync(sm);  // the bottom half's G' of interval m is complete
       if (warp == 1) break;
     }
     const int i = warp == 0 ? (middle ? m : t) : NT - 1 - t;
@@ -1069,21 +1141,19 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
     if (!active) continue;  // the shorter half waits at the middle
     float S[NV];
     assemble_diag(P, sm, i, j, S);
-    if (middle && j < NV) {
-      const float* yb = sm.Sinv(m) + j * SROW;
+    if (middle && m + 1 < NT) {
+      float Yb[NV];
+      bottom_update(P, sm, m, j, sm.scr + G_SCR, Yb);
 #pragma unroll
-      for (int l = 0; l < NV; ++l) S[l] -= yb[l];
+      for (int l = 0; l < NV; ++l) S[l] -= Yb[l];
     }
 #pragma unroll
     for (int l = 0; l < NV; ++l) S[l] -= Y[l];
     __syncwarp();
     good = gauss_jordan(j, S, bc) && good;
-    store_inverse(sm.Sinv(i), j, S);
     if (middle) {
-      if (j < NV) {
-#pragma unroll
-        for (int b = 0; b < 3; ++b) sm.Sinv(m)[(NV + b) * SROW + j] = 0.f;
-      }
+      const float W0[3] = {0.f, 0.f, 0.f};
+      store_block(sm.Tm(i), j, S, W0, sm.scr);
     } else if (warp == 0) {
       float Yp[18];
       top_schur(P, sm, i, j, S, Yp);
@@ -1093,7 +1163,7 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
       bottom_schur(P, sm, i, j, S, Y);
     }
   }
-  return __syncthreads_and(good);
+  return pair_and(sm, good);
 }
 
 // ------------------------------------------------------------------------- stage: ADMM
@@ -1113,30 +1183,28 @@ __device__ __forceinline__ bool row_update(float4* r, bool active, float zt, flo
   return !active || isfinite(zt);
 }
 
-// [S_i^-1 ; W_i^T] u for lanes 0..28 (u published through buf).
-__device__ __forceinline__ float ext_mv(const float* Sd, int lane, float* buf, float u) {
+// [S_i^-1 ; W_i^T] u for lanes 0..28 (u published through buf, the block row from TMEM).
+__device__ __forceinline__ float ext_mv(uint32_t a, int lane, float* buf, float u) {
   buf[lane] = lane < NV ? u : 0.f;
+  float v[TCOLS];
+  tm_load(a, v);
   __syncwarp();
-  const int j = lane < SROWS ? lane : SROWS - 1;
-  const float2* rw = reinterpret_cast<const float2*>(Sd + j * SROW);
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
 #pragma unroll
   for (int q = 0; q < 6; ++q) {
     const float4 bb = b4[q];
-    const float2 r0 = rw[2 * q], r1 = rw[2 * q + 1];
-    a0 = fmaf(r0.x, bb.x, a0);
-    a1 = fmaf(r0.y, bb.y, a1);
-    a2 = fmaf(r1.x, bb.z, a2);
-    a3 = fmaf(r1.y, bb.w, a3);
+    a0 = fmaf(v[4 * q], bb.x, a0);
+    a1 = fmaf(v[4 * q + 1], bb.y, a1);
+    a2 = fmaf(v[4 * q + 2], bb.z, a2);
+    a3 = fmaf(v[4 * q + 3], bb.w, a3);
   }
   {
     const float2 bb = reinterpret_cast<const float2*>(buf)[12];
-    const float2 r = rw[12];
-    a0 = fmaf(r.x, bb.x, a0);
-    a1 = fmaf(r.y, bb.y, a1);
+    a0 = fmaf(v[24], bb.x, a0);
+    a1 = fmaf(v[25], bb.y, a1);
   }
-  return (a0 + a1) + (a2 + a3);
+  return lane < SROWS ? (a0 + a1) + (a2 + a3) : 0.f;
 }
 
 struct AdmmConst {
@@ -1213,7 +1281,6 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   const int kq = is_q ? lane : (is_qd ? lane - 9 : 0);    // k of q_k / qd_k
   const int jv = is_dv ? lane - 9 : 0;                     // index into v_b (node vars 9..25)
   const int bw = is_w ? lane - NV : (lane >= 9 && lane < 12 ? lane - 9 : 0);
-  const int jr = lane < SROWS ? lane : SROWS - 1;          // row of the 29-row block
   const float f_q = is_q ? 1.f : 0.f, f_qd = is_qd ? 1.f : 0.f, f_dv = is_dv ? 1.f : 0.f;
   auto r_of = [&](int i, bool first) {  // (sigma x - q^ + A^T(rho z - y)) restricted to node i
     const float cv = first ? 0.f : col_view<OpSum, TV_T>(sm, i, T, B);
@@ -1256,7 +1323,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
 #pragma unroll 1
       for (int i = 0; i < m; ++i) {
         const float u = r_of(i, first) - top_corr(sm.C(i - 1), gint, g0, g1, g2);
-        const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
+        const float s = ext_mv(sm.Tm(i), lane, ubuf, u);
         store_s(i, s);
         gint = f_q * sm.C(i)[C_INT + 4 * kq + 1] * s;
         g0 = __shfl_sync(FULL, s, 26);
@@ -1268,7 +1335,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
 #pragma unroll 1
       for (int i = NT - 1; i > m; --i) {
         const float u = r_of(i, first) - bot_corr(sm.C(i), gint, g0, g1, g2);
-        const float s = ext_mv(sm.Sinv(i), lane, ubuf, u);
+        const float s = ext_mv(sm.Tm(i), lane, ubuf, u);
         store_s(i, s);
         const float* cp = sm.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
         const float sq = __shfl_down_sync(FULL, s, 9);
@@ -1280,16 +1347,16 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
       }
       gb[lane] = lane < 9 ? gint : (lane == 9 ? g0 : (lane == 10 ? g1 : (lane == 11 ? g2 : 0.f)));
     }
-    __syncthreads();
+    pair_sync(sm);
     // ---------------------------------------------------------------- middle
     if (warp == 0) {
       float u = r_of(m, first) - top_corr(sm.C(m - 1), gint, g0, g1, g2);
       if (m + 1 < NT) u -= bot_corr(sm.C(m), gb[kq], gb[9], gb[10], gb[11]);
-      const float x = ext_mv(sm.Sinv(m), lane, ubuf, u);
+      const float x = ext_mv(sm.Tm(m), lane, ubuf, u);
       if (is_var) sm.V(m, V_S)[lane] = x;
       bad = bad || !isfinite(x);
     }
-    __syncthreads();
+    pair_sync(sm);
     // ---------------------------------------------------------------- backward
     if (warp == 0) {
       bad = finish_node(m) || bad;
@@ -1312,18 +1379,16 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         xib[lane] = is_q ? cf[C_INT + 4 * kq + 1] * dl : (lane < 12 ? xd : 0.f);
         __syncwarp();
         // lanes < 26: row j of S^-1 (cols 0..8 = column j) and W_b[j];  26..28: W_b, G_b
-        const float* Sd = sm.Sinv(i);
-        const float* rw = Sd + jr * SROW;
+        float v[TCOLS];
+        tm_load(sm.Tm(i), v);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; k += 2) {
-          acc0 = fmaf(rw[k], xib[k], acc0);
-          if (k + 1 < 9) acc1 = fmaf(rw[k + 1], xib[k + 1], acc1);
+          acc0 = fmaf(v[k], xib[k], acc0);
+          if (k + 1 < 9) acc1 = fmaf(v[k + 1], xib[k + 1], acc1);
         }
-        const float* wsrc = lane < NV ? Sd + NV * SROW + jr : cf + C_G + 3 * bw;
-        const int wstride = lane < NV ? SROW : 1;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) acc1 = fmaf(wsrc[b * wstride], xib[9 + b], acc1);
+        for (int b = 0; b < 3; ++b) acc1 = fmaf(lane < NV ? v[NV + b] : cf[C_G + 3 * bw + b], xib[9 + b], acc1);
         const float acc = acc0 + acc1;
         const float xt = is_var ? vs[lane] - rho * acc : 0.f;
         if (is_var) vs[lane] = xt;
@@ -1359,18 +1424,16 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         }
         if (lane >= 9 && lane < 12) xib[18 + bw] = xd;
         __syncwarp();
-        const float* Sd = sm.Sinv(i);
-        const float* rw = Sd + jr * SROW;  // lanes < 26: row j of T^-1; 26..28: W'_b
+        float v[TCOLS];  // lanes < 26: row j of T^-1 and W'_b[j]; 26..28: W'_b, G'_b
+        tm_load(sm.Tm(i), v);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-          acc0 = fmaf(rw[k], xib[k], acc0);
-          acc1 = fmaf(rw[NQ + k], xib[9 + k], acc1);
+          acc0 = fmaf(v[k], xib[k], acc0);
+          acc1 = fmaf(v[NQ + k], xib[9 + k], acc1);
         }
-        const float* wsrc = lane < NV ? Sd + NV * SROW + jr : cp + C_G + 3 * bw;
-        const int wstride = lane < NV ? SROW : 1;
 #pragma unroll
-        for (int b = 0; b < 3; ++b) acc0 = fmaf(wsrc[b * wstride], xib[18 + b], acc0);
+        for (int b = 0; b < 3; ++b) acc0 = fmaf(lane < NV ? v[NV + b] : cp[C_G + 3 * bw + b], xib[18 + b], acc0);
         const float acc = acc0 + acc1;
         const float xt = is_var ? vs[lane] - rho * acc : 0.f;
         if (is_var) vs[lane] = xt;
@@ -1386,7 +1449,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         bad = finish_node(i) || bad;
       }
     }
-    if (__syncthreads_or(bad)) return it;
+    if (pair_or(sm, bad)) return it;
   }
   return -1;
 }
@@ -1400,34 +1463,35 @@ __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage,
   }
 }
 
-__global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
-  extern __shared__ __align__(16) float smem[];
-  const int agent = blockIdx.x;
-  if (agent >= P.n_agents) return;
-  const int lane = threadIdx.x & 31;
-  const int warp = threadIdx.x >> 5;
+// One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
+// blocks at `tm`, named barrier `bar`.
+__device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int bar, int agent,
+                                            int lane, int warp) {
   const int NT = P.NT;
   const Layout L = make_layout(NT);
   Sm sm;
-  sm.sinv = smem + L.sinv;
-  sm.coef = smem + L.coef;
-  sm.vec = smem + L.vec;
-  sm.row = reinterpret_cast<float4*>(smem + L.row);
-  sm.dsc = smem + L.dsc;
-  sm.bc = smem + L.bc;
-  sm.flags = reinterpret_cast<uint32_t*>(smem + L.flags);
+  sm.scr = base + L.scr;
+  sm.coef = base + L.coef;
+  sm.vec = base + L.vec;
+  sm.row = reinterpret_cast<float4*>(base + L.row);
+  sm.dsc = base + L.dsc;
+  sm.bc = base + L.bc;
+  sm.flags = reinterpret_cast<uint32_t*>(base + L.flags);
   sm.NT = NT;
+  sm.mid = mid_node(NT);
+  sm.tm = tm;
+  sm.bar = bar;
+  const int tid = warp * 32 + lane;
   long long t0 = P.profile ? clock64() : 0;
 
   // zero coefficients (incl. block -1), rows, vectors; d = e = 1
-  const int tid = threadIdx.x;
   for (int k = tid; k < (NT + 1) * C_SIZE; k += 64) sm.coef[k] = 0.f;
   for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
     sm.row[r] = make_float4(0.f, 0.f, 0.f, 0.f);
     sm.dsc[r] = 1.f;
   }
   for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;
-  __syncthreads();
+  pair_sync(sm);
   for (int i = warp; i < NT; i += 2)
     if (lane < NV) sm.V(i, V_E)[lane] = 1.f;
   sm.bc[tid] = 0.f;
@@ -1449,26 +1513,26 @@ __global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
   bool st_ok = true;
 #pragma unroll
   for (int k = 0; k < 9; ++k) st_ok = st_ok && isfinite(st.q[k]) && isfinite(st.qd[k]);
-  prof_mark(P, threadIdx.x, 0, t0);
-  __syncthreads();
+  prof_mark(P, tid, 0, t0);
+  pair_sync(sm);
 
   int ok = 1;
   if (warp == 0) ok = setup_nodes(P, sm, lane, st, cmd, gait, warm, pz) && st_ok;
-  ok = __syncthreads_and(ok);
-  prof_mark(P, threadIdx.x, 2, t0);
+  ok = pair_and(sm, ok);
+  prof_mark(P, tid, 2, t0);
   if (!ok) {
     out.status = RMPC_STATUS_NONFINITE_INPUT;
   } else {
     if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
     apply_scaling(P, sm, lane, warp);
-    prof_mark(P, threadIdx.x, 3, t0);
+    prof_mark(P, tid, 3, t0);
     const int good = factorize(P, sm, lane, warp);
     if (!good) {
       out.status = RMPC_STATUS_SINGULAR;
     } else {
-      prof_mark(P, threadIdx.x, 4, t0);
+      prof_mark(P, tid, 4, t0);
       const int bad_it = admm(P, sm, lane, warp);
-      prof_mark(P, threadIdx.x, 5, t0);
+      prof_mark(P, tid, 5, t0);
       if (bad_it >= 0) {
         out.status = RMPC_STATUS_DIVERGED;
         out.fail_iter = bad_it;
@@ -1510,7 +1574,7 @@ __global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
         dinf = fmaxf(dinf, fabsf(e * x));
         const double zv = g + dz;  // z* = guess + dz (mpc.cpp:308-314)
         if (P.z_out) P.z_out[((size_t)agent * NT + i) * NV + lane] = (float)zv;
-        if (i < 2) reinterpret_cast<double*>(sm.sinv)[i * 32 + lane] = zv;  // S^-1 is dead
+        if (i < 2) reinterpret_cast<double*>(sm.scr)[i * 32 + lane] = zv;
       }
     }
     prim = wmax(prim);
@@ -1523,7 +1587,7 @@ __global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
     out.v_mpc = (float)obj;
     __syncwarp();
     if (lane == 0) {  // inverse dynamics at node 0 (mpc.cpp:320-330), FP64
-      const double* z0 = reinterpret_cast<const double*>(sm.sinv);
+      const double* z0 = reinterpret_cast<const double*>(sm.scr);
       const double* z1 = z0 + 32;
       double q[9], qd[9], qdd[9], F[8], gen[9];
       const double dt0 = P.dt[0];
@@ -1549,16 +1613,51 @@ __global__ void __launch_bounds__(64) rti_kernel(const KParams P) {
   if (lane == 0) P.out[agent] = out;
 }
 
+// CTA = P.agents_per_cta warp pairs.  Warp w uses TMEM lanes [32 (w % 4), +32) (the quarter
+// tcgen05.ld/st of warp w can reach) and columns [(w / 4) cols_per_warp, +cols_per_warp).
+__global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ uint32_t tmem_base;
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = tmem_base;
+  const int pair = w >> 1;
+  const int agent = blockIdx.x * P.agents_per_cta + pair;
+  if (agent < P.n_agents) {
+    const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * P.cols_per_warp);
+    solve_agent(P, smem + pair * make_layout(P.NT).total, tm, 1 + pair, agent, lane, w & 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(P.tmem_cols) : "memory");
+}
+
 }  // namespace rmpc_dev
 
-int rmpc_kernel_setup(int NT) {
-  const int bytes = rmpc_dev::smem_bytes(NT);
-  return (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+int rmpc_kernel_setup(int) {
+  return (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   227 * 1024 - 128);  // static smem: the TMEM base
 }
 
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   if (params.n_agents <= 0) return 0;
-  const int bytes = rmpc_dev::smem_bytes(params.NT);
-  rmpc_dev::rti_kernel<<<params.n_agents, 64, bytes, (cudaStream_t)stream>>>(params);
+  const rmpc_dev::CtaShape c = rmpc_dev::cta_shape(params.NT);
+  rmpc_dev::KParams P = params;
+  P.agents_per_cta = c.agents;
+  P.cols_per_warp = c.cols_per_warp;
+  P.tmem_cols = c.tmem_cols;
+  const int grid = (P.n_agents + c.agents - 1) / c.agents;
+  rmpc_dev::rti_kernel<<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
   return (int)cudaGetLastError();
 }

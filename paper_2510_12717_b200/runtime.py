@@ -19,7 +19,7 @@ from .abi import (NV, RMPC_ERR_STRUCTURAL, SOLUTION_DTYPE, STAGE_NAMES, Model, S
                   default_model, default_settings)
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "lib", "librmpc_b200.so")
+LIB_PATH = os.environ.get("RMPC_B200_LIB") or os.path.join(_HERE, "lib", "librmpc_b200.so")
 _lib = None
 
 _VP = C.c_void_p

@@ -1,3 +1,7 @@
+// Microtest (run once on a B200): a 12-warp CTA allocates 512 TMEM columns; warp w owns lane
+// quarter w % 4 and column block (w / 4) * 160 -- the layout rti_kernel uses.  Checks that each
+// warp reads back exactly what it stored and times tcgen05.ld.32x32b.x32.
+// nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/tq tools/micro/tmem_quarters.cu
 // TMEM microtest: 12-warp CTA, 512 columns, warp w -> lane quarter w%4, column block (w/4)*160.
 #include <cstdio>
 #include <cstdint>

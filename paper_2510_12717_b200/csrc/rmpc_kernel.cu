@@ -210,12 +210,11 @@ __device__ __forceinline__ void build_terms(int lane, Terms& T) {
 }
 
 // Multipliers of terms 2..5 at a node with stance bits `bits`.
+// m = m0 + m1 * stance with (m0, m1) = (1, -1) on q, (0, 1) on qd, (1, 0) otherwise.
 __device__ __forceinline__ void ja_masks(const Terms& T, uint32_t bits, float m[4]) {
+  const float m0 = T.kind == 1 ? 0.f : 1.f, m1 = T.kind == 0 ? -1.f : (T.kind == 1 ? 1.f : 0.f);
 #pragma unroll
-  for (int c = 0; c < 4; ++c) {
-    const bool st = (bits >> c) & 1u;
-    m[c] = T.kind == 0 ? (st ? 0.f : 1.f) : (T.kind == 1 ? (st ? 1.f : 0.f) : 1.f);
-  }
+  for (int c = 0; c < 4; ++c) m[c] = fmaf(m1, (float)((bits >> c) & 1u), m0);
 }
 
 // Byte offsets of the 17 terms: coefficients relative to C(i), row values relative to R(i)
@@ -327,11 +326,9 @@ struct Fr {
   double px, pz, vx, vz;
 };
 
-// Point attached to `f` at offset (x, z) in the frame rotated by `ang`, spinning at `w`
-// (robot.cpp:39-43).
-__device__ __forceinline__ Fr attach(const Fr& f, double ang, double w, double x, double z) {
-  double s, c;
-  sincos(ang, &s, &c);
+// Point attached to `f` at offset (x, z) in the frame rotated by an angle with sine/cosine
+// (s, c), spinning at `w` (robot.cpp:39-43).
+__device__ __forceinline__ Fr attach(const Fr& f, double s, double c, double w, double x, double z) {
   const double rx = c * x - s * z, rz = s * x + c * z;
   Fr o;
   o.px = f.px + rx;
@@ -356,6 +353,7 @@ struct Frames {
   Fr con[4];
 };
 
+// Each of the 7 absolute angles (pitch, then hip/knee/ankle of each leg) gets one sincos.
 __device__ void fk_frames(const KParams& P, const double* q, const double* qd, Frames& F) {
   Fr base;
   base.px = 0.0;
@@ -363,7 +361,9 @@ __device__ void fk_frames(const KParams& P, const double* q, const double* qd, F
   base.vx = qd[0];
   base.vz = qd[1];
   const double th = q[2];
-  const Fr hip = attach(base, th, qd[2], 0.0, -0.5 * P.torso_len);
+  double s0, c0;
+  sincos(th, &s0, &c0);
+  const Fr hip = attach(base, s0, c0, qd[2], 0.0, -0.5 * P.torso_len);
   F.piv[2] = base;
   F.piv[3] = hip;
   F.piv[6] = hip;
@@ -373,16 +373,20 @@ __device__ void fk_frames(const KParams& P, const double* q, const double* qd, F
     const int h = 3 + 3 * leg;
     const double a1 = th + q[h], a2 = a1 + q[h + 1], a3 = a2 + q[h + 2];
     const double w1 = qd[2] + qd[h], w2 = w1 + qd[h + 1], w3 = w2 + qd[h + 2];
-    const Fr knee = attach(hip, a1, w1, 0.0, -P.thigh_len);
-    const Fr ankle = attach(knee, a2, w2, 0.0, -P.shank_len);
+    double s1, c1, s2, c2, s3, c3;
+    sincos(a1, &s1, &c1);
+    sincos(a2, &s2, &c2);
+    sincos(a3, &s3, &c3);
+    const Fr knee = attach(hip, s1, c1, w1, 0.0, -P.thigh_len);
+    const Fr ankle = attach(knee, s2, c2, w2, 0.0, -P.shank_len);
     F.piv[h + 1] = knee;
     F.piv[h + 2] = ankle;
-    F.com[1 + 3 * leg] = attach(hip, a1, w1, 0.0, -0.5 * P.thigh_len);
-    F.com[2 + 3 * leg] = attach(knee, a2, w2, 0.0, -0.5 * P.shank_len);
-    F.com[3 + 3 * leg] = attach(ankle, a3, w3, 0.0, -P.ankle_drop);
-    const int c0 = leg == 0 ? 2 : 0;  // contacts (R toe, R heel, L toe, L heel)
-    F.con[c0] = attach(ankle, a3, w3, P.foot_half, -P.ankle_drop);
-    F.con[c0 + 1] = attach(ankle, a3, w3, -P.foot_half, -P.ankle_drop);
+    F.com[1 + 3 * leg] = attach(hip, s1, c1, w1, 0.0, -0.5 * P.thigh_len);
+    F.com[2 + 3 * leg] = attach(knee, s2, c2, w2, 0.0, -0.5 * P.shank_len);
+    F.com[3 + 3 * leg] = attach(ankle, s3, c3, w3, 0.0, -P.ankle_drop);
+    const int k0 = leg == 0 ? 2 : 0;  // contacts (R toe, R heel, L toe, L heel)
+    F.con[k0] = attach(ankle, s3, c3, w3, P.foot_half, -P.ankle_drop);
+    F.con[k0 + 1] = attach(ankle, s3, c3, w3, -P.foot_half, -P.ankle_drop);
   }
 }
 
@@ -739,7 +743,8 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
   const int nd = (NT + 1) * NSLOT;
   for (int r = lane + 32 * warp; r < nd; r += 64) sm.scr[r] = sm.dsc[r];
   pair_sync(sm);
-  auto inv_sqrt1 = [](float nrm) { return nrm > 0.f ? 1.f / sqrtf(nrm) : 1.f; };
+  const float wl = lane < NV ? (float)wcost(P, lane) : 0.f;
+  auto inv_sqrt1 = [](float nrm) { return nrm > 0.f ? rsqrtf(nrm) : 1.f; };  // MUFU.RSQ
 #pragma unroll 1
   for (int pass = 0; pass < P.ruiz_iters; ++pass) {
     const bool odd = pass & 1;
@@ -762,7 +767,7 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
       }
       if (lane < NV) {
         const float e = sm.V(i, es)[lane];
-        const float pd = (float)wcost(P, lane) * (float)P.dt[i];
+        const float pd = wl * (float)P.dt[i];
         sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, cv));
       }
     }
@@ -926,7 +931,7 @@ __device__ __forceinline__ bool gauss_jordan(int j, float S[NV], float* bc) {
     }
     const float p = R[k];
     good = good && (p > 0.f);
-    const float pinv = 1.f / p;
+    const float pinv = __frcp_rn(p);  // == 1.f / p
     const float f = S[k];
     const bool me = (j == k);
     const float keep = me ? 0.f : 1.f;
@@ -1539,9 +1544,8 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
       }
     }
   }
-  if (warp != 0) return;  // residuals, z* and inverse dynamics on the solver warp
-
-  if (out.status == RMPC_STATUS_OK) {
+  if (out.status == RMPC_STATUS_OK) {  // (pair-uniform) residuals, objective, z*: nodes split
+                                       // between the warps; inverse dynamics on warp 0
     // unscaled residuals (qp.cpp:192-200): prim = |A^x - z| / d, dual = |P^x + q^ + A^T y| / e
     Terms T;
     build_terms(lane, T);
@@ -1551,7 +1555,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
     double obj = 0.0;
     const float rho = (float)P.rho;
 #pragma unroll 1
-    for (int i = 0; i < NT; ++i) {
+    for (int i = warp; i < NT; i += 2) {
       float o0, o1, o2;
       row_view<OpSum>(sm, i, lane, V_X, o0, o1, o2);
       const float4* rw = sm.R(i);
@@ -1581,6 +1585,18 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
     dual = wmax(dual);
     dinf = wmax(dinf);
     obj = wsumd(obj);
+    if (warp == 1 && lane == 0) {
+      sm.bc[0] = prim;
+      sm.bc[1] = dual;
+      sm.bc[2] = dinf;
+      reinterpret_cast<double*>(sm.bc)[2] = obj;
+    }
+    pair_sync(sm);
+    if (warp != 0) return;
+    prim = fmaxf(prim, sm.bc[0]);
+    dual = fmaxf(dual, sm.bc[1]);
+    dinf = fmaxf(dinf, sm.bc[2]);
+    obj += reinterpret_cast<const double*>(sm.bc)[2];
     out.prim_res = prim;
     out.dual_res = dual;
     out.delta_inf_norm = dinf;
@@ -1606,8 +1622,10 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
       }
       for (int k = 0; k < 8; ++k) out.f0[k] = (float)F[k];
     }
-  } else if (P.z_out != nullptr) {
-    for (int k = lane; k < NT * NV; k += 32) P.z_out[(size_t)agent * NT * NV + k] = 0.f;
+  } else {
+    if (warp != 0) return;
+    if (P.z_out != nullptr)
+      for (int k = lane; k < NT * NV; k += 32) P.z_out[(size_t)agent * NT * NV + k] = 0.f;
   }
   prof_mark(P, lane, 6, t0);
   if (lane == 0) P.out[agent] = out;

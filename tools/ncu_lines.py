@@ -1,0 +1,74 @@
+"""Attribute an ncu SASS source page (per-instruction stall samples) to CUDA source lines.
+
+python tools/ncu_lines.py <report.ncu-rep> [top]   (run here, not on the GPU box)
+
+The line table comes from `nvdisasm --print-line-info` of the in-tree library's cubin (built
+with -lineinfo); instruction i of the ncu page is instruction i of the disassembly.
+"""
+import collections
+import csv
+import io
+import os
+import re
+import subprocess
+import sys
+import tempfile
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+LIB = os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
+FUNC = "_ZN8rmpc_dev10rti_kernelENS_7KParamsE"
+
+
+def line_table():
+    with tempfile.TemporaryDirectory() as d:
+        subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=d, check=True, capture_output=True)
+        cub = [f for f in os.listdir(d) if f.startswith("rmpc_kernel.") and f.endswith(".cubin")][0]
+        txt = subprocess.run(["nvdisasm", "--print-line-info", os.path.join(d, cub)],
+                             check=True, capture_output=True, text=True).stdout
+    cur, out, inside = None, [], False
+    for ln in txt.splitlines():
+        if ln.startswith(".text."):
+            inside = ln.startswith(".text." + FUNC + ":")
+            continue
+        if not inside:
+            continue
+        m = re.search(r'File "([^"]+)", line (\d+)', ln)
+        if m:
+            cur = (os.path.basename(m.group(1)), int(m.group(2)))
+        elif re.match(r"\s*/\*[0-9a-f]{4,}\*/", ln):
+            out.append(cur)
+    return out
+
+
+def main():
+    rep = sys.argv[1]
+    top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+    page = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source", "sass"],
+                          check=True, capture_output=True, text=True).stdout
+    rows = list(csv.reader(io.StringIO(page)))
+    hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
+    h = rows[hi]
+    cs, ci = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+    ins = [r for r in rows[hi + 1:] if len(r) > ci]
+    lines = line_table()
+    if len(lines) != len(ins):
+        print(f"warning: {len(ins)} ncu instructions vs {len(lines)} disassembled", file=sys.stderr)
+    samp, inst = collections.Counter(), collections.Counter()
+    for k, r in enumerate(ins):
+        key = lines[k] if k < len(lines) else ("?", 0)
+        samp[key] += float(r[cs] or 0)
+        inst[key] += float(r[ci] or 0)
+    ts, ti = sum(samp.values()), sum(inst.values())
+    src = {}
+    print(f"total samples {ts:.0f}, warp-instructions {ti:.0f}")
+    for key, s in samp.most_common(top):
+        f, n = key
+        if f not in src:
+            p = os.path.join(ROOT, "paper_2510_12717_b200", "csrc", f)
+            src[f] = open(p).read().splitlines() if os.path.exists(p) else []
+        text = src[f][n - 1].strip()[:90] if 0 < n <= len(src[f]) else ""
+        print(f"{100 * s / ts:5.1f}% samp {100 * inst[key] / ti:5.1f}% inst  {f}:{n}  {text}")
+
+
+if __name__ == "__main__":
+    main()

@@ -934,10 +934,10 @@ __device__ __forceinline__ bool gauss_jordan(int j, float S[NV], float* bc) {
     const float pinv = __frcp_rn(p);  // == 1.f / p
     const float f = S[k];
     const bool me = (j == k);
-    const float keep = me ? 0.f : 1.f;
-    const float alpha = me ? pinv : -f * pinv;
+    // the pivot row holds S == R: (pinv - 1) R + R scales it by pinv in the same FMA
+    const float alpha = me ? pinv - 1.f : -f * pinv;
 #pragma unroll
-    for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], keep * S[l]);
+    for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], S[l]);
     S[k] = me ? pinv : -f * pinv;
   }
   return good;

@@ -40,6 +40,28 @@ def line_table():
     return out
 
 
+def functions(path):
+    """(first line, name) of every function / lambda-holding definition in a source file."""
+    out = []
+    for n, ln in enumerate(open(path).read().splitlines(), 1):
+        m = re.match(r"(?:template <[^>]*>\s*)?(?:__global__|__device__|__host__)[^(]*?\b(\w+)\(", ln)
+        if m:
+            out.append((n, m.group(1)))
+        m = re.match(r"\s+auto (\w+) = \[", ln)
+        if m:
+            out.append((n, "lambda:" + m.group(1)))
+    return out
+
+
+def func_of(table, n):
+    name = "?"
+    for first, f in table:
+        if first > n:
+            break
+        name = f
+    return name
+
+
 def main():
     rep = sys.argv[1]
     top = int(sys.argv[2]) if len(sys.argv) > 2 else 40
@@ -59,6 +81,16 @@ def main():
         samp[key] += float(r[cs] or 0)
         inst[key] += float(r[ci] or 0)
     ts, ti = sum(samp.values()), sum(inst.values())
+    kern = os.path.join(ROOT, "paper_2510_12717_b200", "csrc", "rmpc_kernel.cu")
+    table = functions(kern)
+    fs, fi = collections.Counter(), collections.Counter()
+    for (f, n), v in samp.items():
+        key = func_of(table, n) if f == "rmpc_kernel.cu" else f
+        fs[key] += v
+        fi[key] += inst[(f, n)]
+    print("by function (innermost source function after inlining):")
+    for key, v in fs.most_common(30):
+        print(f"{100 * v / ts:5.1f}% samp {100 * fi[key] / ti:5.1f}% inst  {key}")
     src = {}
     print(f"total samples {ts:.0f}, warp-instructions {ti:.0f}")
     for key, s in samp.most_common(top):

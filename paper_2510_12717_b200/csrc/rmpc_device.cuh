@@ -42,12 +42,13 @@ constexpr int C_INT = 0;      // [9][4]: a1 (on q_{i+1,k}), a2 (on q_{i,k}), a3 
 constexpr int C_DYNV = 36;    // [3][20]: dynamics row b on node-i vars 9..25 (index j - 9)
 constexpr int C_DYNU = 96;    // [3][12]: dynamics row b on qd_{i+1,k}
 constexpr int C_FORCE = 132;  // [4][4]: contact c rows t0 (Fx,Fz), t1 (Fx,Fz)
-constexpr int C_JA = 148;     // [4][9]: row t2: on qd_k (stance) or q_k (swing height)
+constexpr int C_JA = 148;     // [4][9]: row t2 on qd_k (stance velocity; zero for swing)
 constexpr int C_JB = 184;     // [4][9]: row t3 on qd_k (stance; zero for swing)
 constexpr int C_BOX = 220;    // [12]: joint q boxes (6) then qd boxes (6)
 constexpr int C_INIT = 232;   // [18]: initial-state rows (node 0 only, rows in block -1)
 constexpr int C_G = 250;      // [9]: G_bb' = v_b^T S_i^-1 v_b' (dynamics rows)
-constexpr int C_SIZE = 260;
+constexpr int C_JAQ = 260;    // [4][9]: row t2 on q_k (swing height; zero for stance)
+constexpr int C_SIZE = 296;
 constexpr int C_ZERO = C_INT + 3;  // an entry that is always 0
 
 // Split of the horizon for the two-sided (twisted) elimination: warp 0 owns nodes [0, m)

@@ -177,7 +177,7 @@ __device__ __forceinline__ void build_terms(int lane, Terms& T) {
     T.co[0] = C_INT + 4 * k + 1;        T.to[0] = k;
     T.co[1] = -CS + C_INT + 4 * k;      T.to[1] = -NSLOT + k;
 #pragma unroll
-    for (int c = 0; c < 4; ++c) { T.co[2 + c] = C_JA + 9 * c + k; T.to[2 + c] = 14 + 4 * c; }
+    for (int c = 0; c < 4; ++c) { T.co[2 + c] = C_JAQ + 9 * c + k; T.to[2 + c] = 14 + 4 * c; }
     if (k >= 3) { T.co[6] = C_BOX + k - 3; T.to[6] = 28 + k - 3; }
     T.co[7] = C_INIT + k;               T.to[7] = -NSLOT + INIT0 + k;
   } else if (lane < 18) {
@@ -209,14 +209,6 @@ __device__ __forceinline__ void build_terms(int lane, Terms& T) {
   }
 }
 
-// Multipliers of terms 2..5 at a node with stance bits `bits`.
-// m = m0 + m1 * stance with (m0, m1) = (1, -1) on q, (0, 1) on qd, (1, 0) otherwise.
-__device__ __forceinline__ void ja_masks(const Terms& T, uint32_t bits, float m[4]) {
-  const float m0 = T.kind == 1 ? 0.f : 1.f, m1 = T.kind == 0 ? -1.f : (T.kind == 1 ? 1.f : 0.f);
-#pragma unroll
-  for (int c = 0; c < 4; ++c) m[c] = fmaf(m1, (float)((bits >> c) & 1u), m0);
-}
-
 // Byte offsets of the 17 terms: coefficients relative to C(i), row values relative to R(i)
 // (+12 = t, +8 = {z, t}) or to D(i).
 struct TermBytes {
@@ -241,13 +233,10 @@ __device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, c
   const char* cb = reinterpret_cast<const char*>(sm.C(i));
   const char* tb = MODE == TV_D ? reinterpret_cast<const char*>(sm.D(i))
                                 : reinterpret_cast<const char*>(sm.R(i));
-  float m[4];
-  ja_masks(T, sm.flags[i], m);
   float acc0 = Op::id(), acc1 = Op::id();
 #pragma unroll
   for (int k = 0; k < 17; ++k) {
-    float c = *reinterpret_cast<const float*>(cb + B.cb[k]);
-    if (k >= 2 && k <= 5) c *= m[k - 2];
+    const float c = *reinterpret_cast<const float*>(cb + B.cb[k]);
     float v;
     if (MODE == TV_Y) {
       const float2 zt = *reinterpret_cast<const float2*>(tb + B.tb[k]);
@@ -273,7 +262,6 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
   const float* cf = sm.C(i);
   const float* vi = sm.V(i, which);
   const float* vn = (i + 1 < sm.NT) ? sm.V(i + 1, which) : vi;  // coefficients are 0 then
-  const uint32_t bits = sm.flags[i];
   // own terms: integration (lanes 0..8), force cones (12..27, t < 2), boxes (28..31)
   const bool li = lane < 9, lb = lane >= 28;
   const int cq = (lane - 12) >> 2, tq = (lane - 12) & 3;
@@ -300,8 +288,8 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
   const int c = lane >> 3, s = lane & 7;
   const int col = chain_col(c, s < 6 ? s : 0);
   const float vd = vi[NQ + col];
-  const float vt = ((bits >> c) & 1u) ? vd : vi[col];
-  const float pa = Op::comb(Op::id(), cf[s < 6 ? C_JA + 9 * c + col : C_ZERO], vt);
+  const float pa = Op::comb(Op::comb(Op::id(), cf[s < 6 ? C_JAQ + 9 * c + col : C_ZERO], vi[col]),
+                            cf[s < 6 ? C_JA + 9 * c + col : C_ZERO], vd);
   const float pb = Op::comb(Op::id(), cf[s < 6 ? C_JB + 9 * c + col : C_ZERO], vd);
   // Transposed butterflies: 4 dynamics partials -> row (lane >> 3) in 6 shuffles; the
   // (pa, pb) pair -> pa in lanes 8c..8c+3, pb in 8c+4..8c+7 in 3 shuffles.
@@ -698,7 +686,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
           const double h = bezier_height(swt[c], P.z_swing, P.v_to, P.v_td);
           const double r = h - F.con[c].pz;
 #pragma unroll
-          for (int k = 0; k < 9; ++k) cf[C_JA + 9 * c + k] = to_f(Jz[c][k]);
+          for (int k = 0; k < 9; ++k) cf[C_JAQ + 9 * c + k] = to_f(Jz[c][k]);
           set_row(r0 + 2, r, r);
         }
       }
@@ -790,7 +778,6 @@ __device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp
     const float* ei = sm.V(i, V_E);
     const float* en = i + 1 < NT ? sm.V(i + 1, V_E) : ei;
     const float* d = sm.D(i);
-    const uint32_t bits = sm.flags[i];
     if (lane < 9) {
       const float dr = d[lane];
       cf[C_INT + 4 * lane + 0] *= dr * en[lane];
@@ -808,8 +795,8 @@ __device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp
     }
     for (int idx = lane; idx < 36; idx += 32) {
       const int c = idx / 9, k = idx % 9;
-      const bool st = (bits >> c) & 1u;
-      cf[C_JA + idx] *= d[14 + 4 * c] * ei[st ? NQ + k : k];
+      cf[C_JA + idx] *= d[14 + 4 * c] * ei[NQ + k];
+      cf[C_JAQ + idx] *= d[14 + 4 * c] * ei[k];
       cf[C_JB + idx] *= d[15 + 4 * c] * ei[NQ + k];
     }
     if (lane < 12) cf[C_BOX + lane] *= d[28 + lane] * ei[lane < 6 ? 3 + lane : NQ + 3 + (lane - 6)];
@@ -841,7 +828,6 @@ __device__ __forceinline__ void assemble_diag(const KParams& P, const Sm& sm, in
   const float rho = (float)P.rho, sigma = (float)P.sigma;
   const float* cf = sm.C(i);
   const float* cp = sm.C(i - 1);  // block -1 is zero for i == 0
-  const uint32_t bits = sm.flags[i];
   float dg = 0.f, pt = 0.f;
   int pidx = -1;
   if (j < NV) dg = phat(P, sm, i, j) + sigma;
@@ -888,17 +874,14 @@ __device__ __forceinline__ void assemble_diag(const KParams& P, const Sm& sm, in
   }
 #pragma unroll
   for (int c = 0; c < 4; ++c) {  // contact rows t2/t3: velocity on qd (stance), height on q
-    const float* ja = cf + C_JA + 9 * c;
-    if ((bits >> c) & 1u) {
-      const float* jb = cf + C_JB + 9 * c;
-      const bool mine = j >= 9 && j < 18;
-      const float s0 = mine ? rho * ja[j - 9] : 0.f, s1 = mine ? rho * jb[j - 9] : 0.f;
+    const float *ja = cf + C_JA + 9 * c, *jb = cf + C_JB + 9 * c, *jq = cf + C_JAQ + 9 * c;
+    const bool mine = j >= 9 && j < 18;
+    const float s0 = mine ? rho * ja[j - 9] : 0.f, s1 = mine ? rho * jb[j - 9] : 0.f;
+    const float sq = j < 9 ? rho * jq[j] : 0.f;
 #pragma unroll
-      for (int m = 0; m < 9; ++m) S[NQ + m] = fmaf(s0, ja[m], fmaf(s1, jb[m], S[NQ + m]));
-    } else {
-      const float s = j < 9 ? rho * ja[j] : 0.f;
-#pragma unroll
-      for (int m = 0; m < 9; ++m) S[m] = fmaf(s, ja[m], S[m]);
+    for (int m = 0; m < 9; ++m) {
+      S[NQ + m] = fmaf(s0, ja[m], fmaf(s1, jb[m], S[NQ + m]));
+      S[m] = fmaf(sq, jq[m], S[m]);
     }
   }
 }
@@ -1225,12 +1208,10 @@ __device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const f
                                           const AdmmConst& K) {
   const int c = lane >> 3, s = lane & 7;
   const float* cf = sm.C(i);
-  const bool st = (sm.flags[i] >> c) & 1u;
   const int col = chain_col(c, s < 6 ? s : 0);
   const float vd = xs[NQ + col];
-  const float vt = st ? vd : xs[col];
   const float on = s < 6 ? 1.f : 0.f;
-  float pa = on * cf[C_JA + 9 * c + col] * vt;
+  float pa = on * (cf[C_JAQ + 9 * c + col] * xs[col] + cf[C_JA + 9 * c + col] * vd);
   float pb = on * cf[C_JB + 9 * c + col] * vd;
 #pragma unroll
   for (int o = 4; o > 0; o >>= 1) {

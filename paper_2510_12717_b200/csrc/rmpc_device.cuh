@@ -38,7 +38,9 @@ constexpr int INIT0 = 12;     // initial-state rows live in block -1, slots [12,
 // slots [12, 30); node 0 sees it as its "previous node", so every node has the same pattern.
 
 // Per-node coefficient block (floats).  Unscaled A values during setup/Ruiz, scaled A^ after.
-constexpr int C_INT = 0;      // [9][4]: a1 (on q_{i+1,k}), a2 (on q_{i,k}), a3 (on qd_{i+1,k}), 0
+constexpr int C_A1 = 0;       // [9]: integration row k on q_{i+1,k}
+constexpr int C_A2 = 9;       // [9]: ... on q_{i,k}
+constexpr int C_A3 = 18;      // [9]: ... on qd_{i+1,k};  [27, 36) stays zero
 constexpr int C_DYNV = 36;    // [3][20]: dynamics row b on node-i vars 9..25 (index j - 9)
 constexpr int C_DYNU = 96;    // [3][12]: dynamics row b on qd_{i+1,k}
 constexpr int C_FORCE = 132;  // [4][4]: contact c rows t0 (Fx,Fz), t1 (Fx,Fz)
@@ -49,7 +51,7 @@ constexpr int C_INIT = 232;   // [18]: initial-state rows (node 0 only, rows in 
 constexpr int C_G = 250;      // [9]: G_bb' = v_b^T S_i^-1 v_b' (dynamics rows)
 constexpr int C_JAQ = 260;    // [4][9]: row t2 on q_k (swing height; zero for stance)
 constexpr int C_SIZE = 296;
-constexpr int C_ZERO = C_INT + 3;  // an entry that is always 0
+constexpr int C_ZERO = 27;    // an entry that is always 0
 
 // Split of the horizon for the two-sided (twisted) elimination: warp 0 owns nodes [0, m)
 // eliminated top-down plus the middle node m, warp 1 owns (m, T) eliminated bottom-up.
@@ -89,7 +91,7 @@ struct KParams {
 
 // Shared-memory footprint of one agent (warp pair) in floats, every region 16-byte aligned.
 struct Layout {
-  int scr, coef, vec, row, dsc, bc, flags, total;
+  int scr, coef, vec, row, tt, dsc, bc, flags, total;
 };
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
@@ -103,6 +105,7 @@ __host__ __device__ inline Layout make_layout(int NT) {
   L.coef = o;  o += (NT + 1) * C_SIZE;              // block -1 first
   L.vec = o;   o += NT * V_NUM * V_STRIDE;
   L.row = o;   o += 4 * (NT + 1) * NSLOT;           // float4 {lo, hi, z, t = rho z - y}
+  L.tt = o;    o += (NT + 1) * NSLOT;               // t of every row again, unit stride (column view)
   L.dsc = o;   o += (NT + 1) * NSLOT;               // Ruiz row scale d
   L.bc = o;    o += 128;                            // per warp: 2 x 32 broadcast buffers
   L.flags = o; o += align4(NT);

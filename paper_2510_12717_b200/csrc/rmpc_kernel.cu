@@ -38,6 +38,7 @@ struct Sm {
   float* coef;  // block -1 at coef, node i at coef + (i + 1) * C_SIZE
   float* vec;
   float4* row;  // block -1 at row, node i at row + (i + 1) * NSLOT
+  float* tt;    // rows[.].t again, one float per slot: conflict-free column-view gathers
   float* dsc;
   float* bc;
   uint32_t* flags;
@@ -48,6 +49,7 @@ struct Sm {
   __device__ __forceinline__ float* C(int i) const { return coef + (i + 1) * C_SIZE; }
   __device__ __forceinline__ float4* R(int i) const { return row + (i + 1) * NSLOT; }
   __device__ __forceinline__ float* D(int i) const { return dsc + (i + 1) * NSLOT; }
+  __device__ __forceinline__ float* T(int i) const { return tt + (i + 1) * NSLOT; }
   __device__ __forceinline__ float* V(int i, int which) const {
     return vec + (i * V_NUM + which) * V_STRIDE;
   }
@@ -174,8 +176,8 @@ __device__ __forceinline__ void build_terms(int lane, Terms& T) {
   if (lane < 9) {
     const int k = lane;
     T.kind = 0;
-    T.co[0] = C_INT + 4 * k + 1;        T.to[0] = k;
-    T.co[1] = -CS + C_INT + 4 * k;      T.to[1] = -NSLOT + k;
+    T.co[0] = C_A2 + k;        T.to[0] = k;
+    T.co[1] = -CS + C_A1 + k;      T.to[1] = -NSLOT + k;
 #pragma unroll
     for (int c = 0; c < 4; ++c) { T.co[2 + c] = C_JAQ + 9 * c + k; T.to[2 + c] = 14 + 4 * c; }
     if (k >= 3) { T.co[6] = C_BOX + k - 3; T.to[6] = 28 + k - 3; }
@@ -183,7 +185,7 @@ __device__ __forceinline__ void build_terms(int lane, Terms& T) {
   } else if (lane < 18) {
     const int k = lane - 9;
     T.kind = 1;
-    T.co[0] = -CS + C_INT + 4 * k + 2;  T.to[0] = -NSLOT + k;
+    T.co[0] = -CS + C_A3 + k;  T.to[0] = -NSLOT + k;
     T.co[1] = -CS + C_DYNU + k;         T.to[1] = -NSLOT + 9;
 #pragma unroll
     for (int c = 0; c < 4; ++c) {
@@ -221,7 +223,7 @@ __device__ __forceinline__ void term_bytes(const Terms& T, TermBytes& B) {
 #pragma unroll
   for (int k = 0; k < 17; ++k) {
     B.cb[k] = T.co[k] * 4;
-    B.tb[k] = MODE == TV_D ? T.to[k] * 4 : T.to[k] * 16 + (MODE == TV_T ? 12 : 8);
+    B.tb[k] = MODE == TV_Y ? T.to[k] * 16 + 8 : T.to[k] * 4;
   }
 }
 
@@ -232,7 +234,8 @@ __device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, c
                                           float rho = 0.f) {
   const char* cb = reinterpret_cast<const char*>(sm.C(i));
   const char* tb = MODE == TV_D ? reinterpret_cast<const char*>(sm.D(i))
-                                : reinterpret_cast<const char*>(sm.R(i));
+                   : (MODE == TV_T ? reinterpret_cast<const char*>(sm.T(i))
+                                   : reinterpret_cast<const char*>(sm.R(i)));
   float acc0 = Op::id(), acc1 = Op::id();
 #pragma unroll
   for (int k = 0; k < 17; ++k) {
@@ -266,9 +269,9 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
   const bool li = lane < 9, lb = lane >= 28;
   const int cq = (lane - 12) >> 2, tq = (lane - 12) & 3;
   const bool lf = lane >= 12 && lane < 28 && tq < 2;
-  const int c1 = li ? C_INT + 4 * lane : (lf ? C_FORCE + 4 * cq + 2 * tq : (lb ? C_BOX + lane - 28 : C_ZERO));
-  const int c2 = li ? C_INT + 4 * lane + 1 : (lf ? C_FORCE + 4 * cq + 2 * tq + 1 : C_ZERO);
-  const int c3 = li ? C_INT + 4 * lane + 2 : C_ZERO;
+  const int c1 = li ? C_A1 + lane : (lf ? C_FORCE + 4 * cq + 2 * tq : (lb ? C_BOX + lane - 28 : C_ZERO));
+  const int c2 = li ? C_A2 + lane : (lf ? C_FORCE + 4 * cq + 2 * tq + 1 : C_ZERO);
+  const int c3 = li ? C_A3 + lane : C_ZERO;
   const float* v1 = li ? vn + lane : vi + (lf ? 18 + 2 * cq : (lb ? lane - 25 : 0));
   const float* v2 = vi + (li ? lane : (lf ? 19 + 2 * cq : 0));
   const float* v3 = vn + (li ? NQ + lane : 0);
@@ -622,9 +625,9 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
     if (i + 1 < NT) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) {  // integration (mpc.cpp:138-148)
-        cf[C_INT + 4 * k + 0] = 1.f;
-        cf[C_INT + 4 * k + 1] = -1.f;
-        cf[C_INT + 4 * k + 2] = to_f(-dt);
+        cf[C_A1 + k] = 1.f;
+        cf[C_A2 + k] = -1.f;
+        cf[C_A3 + k] = to_f(-dt);
         const double r = -(nq[k] - gq[k] - dt * nqd[k]);
         set_row(rw + k, r, r);
       }
@@ -780,9 +783,9 @@ __device__ void apply_scaling(const KParams& P, const Sm& sm, int lane, int warp
     const float* d = sm.D(i);
     if (lane < 9) {
       const float dr = d[lane];
-      cf[C_INT + 4 * lane + 0] *= dr * en[lane];
-      cf[C_INT + 4 * lane + 1] *= dr * ei[lane];
-      cf[C_INT + 4 * lane + 2] *= dr * en[NQ + lane];
+      cf[C_A1 + lane] *= dr * en[lane];
+      cf[C_A2 + lane] *= dr * ei[lane];
+      cf[C_A3 + lane] *= dr * en[NQ + lane];
 #pragma unroll
       for (int b = 0; b < 3; ++b) cf[C_DYNU + 12 * b + lane] *= d[9 + b] * en[NQ + lane];
     } else if (lane < NV) {
@@ -832,14 +835,14 @@ __device__ __forceinline__ void assemble_diag(const KParams& P, const Sm& sm, in
   int pidx = -1;
   if (j < NV) dg = phat(P, sm, i, j) + sigma;
   if (j < 9) {
-    const float a2 = cf[C_INT + 4 * j + 1], a1 = cp[C_INT + 4 * j], a3 = cp[C_INT + 4 * j + 2];
+    const float a2 = cf[C_A2 + j], a1 = cp[C_A1 + j], a3 = cp[C_A3 + j];
     const float bx = j >= 3 ? cf[C_BOX + j - 3] : 0.f, bi = cf[C_INIT + j];
     dg += rho * (a2 * a2 + a1 * a1 + bx * bx + bi * bi);
     pt = rho * a1 * a3;
     pidx = NQ + j;
   } else if (j < 18) {
     const int k = j - 9;
-    const float a1 = cp[C_INT + 4 * k], a3 = cp[C_INT + 4 * k + 2];
+    const float a1 = cp[C_A1 + k], a3 = cp[C_A3 + k];
     const float bx = k >= 3 ? cf[C_BOX + 6 + k - 3] : 0.f, bi = cf[C_INIT + j];
     dg += rho * (a3 * a3 + bx * bx + bi * bi);
     pt = rho * a1 * a3;
@@ -964,9 +967,9 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
   }
   store_block(sm.Tm(i), j, S, W, G);
   if (j < 9) {
-    const float a2 = cf[C_INT + 4 * j + 1];
+    const float a2 = cf[C_A2 + j];
 #pragma unroll
-    for (int k = 0; k < 9; ++k) G[j * 13 + k] = a2 * S[k] * cf[C_INT + 4 * k + 1];
+    for (int k = 0; k < 9; ++k) G[j * 13 + k] = a2 * S[k] * cf[C_A2 + k];
 #pragma unroll
     for (int b = 0; b < 3; ++b) {
       G[j * 13 + 9 + b] = a2 * W[b];
@@ -993,12 +996,12 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
   __syncwarp();
   float Z[12];
   if (j < 9) {
-    const float a1 = cf[C_INT + 4 * j];
+    const float a1 = cf[C_A1 + j];
 #pragma unroll
     for (int s = 0; s < 12; ++s) Z[s] = a1 * G[j * 13 + s];
   } else if (j < 18) {
     const int k = j - 9;
-    const float a3 = cf[C_INT + 4 * k + 2];
+    const float a3 = cf[C_A3 + k];
     const float u0 = cf[C_DYNU + k], u1 = cf[C_DYNU + 12 + k], u2 = cf[C_DYNU + 24 + k];
 #pragma unroll
     for (int s = 0; s < 12; ++s)
@@ -1009,10 +1012,10 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
   }
   const float r2 = rho * rho;
 #pragma unroll
-  for (int m = 0; m < 9; ++m) Yp[m] = r2 * Z[m] * cf[C_INT + 4 * m];
+  for (int m = 0; m < 9; ++m) Yp[m] = r2 * Z[m] * cf[C_A1 + m];
 #pragma unroll
   for (int k = 0; k < 9; ++k)
-    Yp[NQ + k] = r2 * (Z[k] * cf[C_INT + 4 * k + 2] + Z[9] * cf[C_DYNU + k] + Z[10] * cf[C_DYNU + 12 + k] +
+    Yp[NQ + k] = r2 * (Z[k] * cf[C_A3 + k] + Z[9] * cf[C_DYNU + k] + Z[10] * cf[C_DYNU + 12 + k] +
                        Z[11] * cf[C_DYNU + 24 + k]);
   __syncwarp();
 }
@@ -1024,7 +1027,7 @@ __device__ __forceinline__ void bottom_update(const KParams& P, const Sm& sm, in
   const float* cp = sm.C(iv);
   float Z[12];  // Z[j][s] = sum_r V[j][r] G'[r][s]
   if (j < 9) {
-    const float a2 = cp[C_INT + 4 * j + 1];
+    const float a2 = cp[C_A2 + j];
 #pragma unroll
     for (int s = 0; s < 12; ++s) Z[s] = a2 * G[j * 13 + s];
   } else if (j < NV) {
@@ -1037,7 +1040,7 @@ __device__ __forceinline__ void bottom_update(const KParams& P, const Sm& sm, in
   }
   const float r2 = (float)P.rho * (float)P.rho;
 #pragma unroll
-  for (int l = 0; l < 9; ++l) Yb[l] = r2 * Z[l] * cp[C_INT + 4 * l + 1];
+  for (int l = 0; l < 9; ++l) Yb[l] = r2 * Z[l] * cp[C_A2 + l];
 #pragma unroll
   for (int l = 9; l < NV; ++l)
     Yb[l] = r2 * (Z[9] * cp[C_DYNV + l - 9] + Z[10] * cp[C_DYNV + 20 + l - 9] + Z[11] * cp[C_DYNV + 40 + l - 9]);
@@ -1064,8 +1067,8 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
   // int-int / int-dyn parts: lane k (row k) and lane 9+k (row 9+k) of T^-1
   float Pk[9];
 #pragma unroll
-  for (int l = 0; l < 9; ++l) Pk[l] = cp[C_INT + 4 * l] * S[l] + cp[C_INT + 4 * l + 2] * S[NQ + l];
-  const float a1 = j < 9 ? cp[C_INT + 4 * j] : 0.f, a3 = j < 9 ? cp[C_INT + 4 * j + 2] : 0.f;
+  for (int l = 0; l < 9; ++l) Pk[l] = cp[C_A1 + l] * S[l] + cp[C_A3 + l] * S[NQ + l];
+  const float a1 = j < 9 ? cp[C_A1 + j] : 0.f, a3 = j < 9 ? cp[C_A3 + j] : 0.f;
 #pragma unroll
   for (int l = 0; l < 9; ++l) {
     const float q = __shfl_down_sync(FULL, Pk[l], 9);
@@ -1158,8 +1161,8 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
 // One constraint-row update (qp.cpp:163-170) on the stored {lo, hi, z, t = rho z - y}; the
 // store is predicated on `active` (r must point at a valid row either way).  Returns false
 // on a non-finite z~ of an active row.
-__device__ __forceinline__ bool row_update(float4* r, bool active, float zt, float alpha, float oma,
-                                           float rho, float rho_inv) {
+__device__ __forceinline__ bool row_update(float4* r, float* tr, bool active, float zt, float alpha,
+                                           float oma, float rho, float rho_inv) {
   float4 rd = *r;
   const float y = fmaf(rho, rd.z, -rd.w);
   const float w = alpha * zt + oma * rd.z;
@@ -1167,7 +1170,10 @@ __device__ __forceinline__ bool row_update(float4* r, bool active, float zt, flo
   const float yn = y + rho * (w - zn);
   rd.z = zn;
   rd.w = fmaf(rho, zn, -yn);
-  if (active) *r = rd;
+  if (active) {
+    *r = rd;
+    *tr = rd.w;
+  }
   return !active || isfinite(zt);
 }
 
@@ -1224,10 +1230,10 @@ __device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const f
   const float zb = cf[C_BOX + mb] * xs[mb < 6 ? 3 + mb : NQ + 3 + (mb - 6)];
   const float zt = s == 0 ? pa : (s == 1 ? pb : (s >= 6 ? zf : zb));
   const int slot = s == 0 ? 14 + 4 * c : (s == 1 ? 15 + 4 * c : (s >= 6 ? 12 + 4 * c + t : 28 + mb));
-  bool ok = row_update(sm.R(i) + slot, s != 5, zt, K.alpha, K.oma, K.rho, K.rho_inv);
+  bool ok = row_update(sm.R(i) + slot, sm.T(i) + slot, s != 5, zt, K.alpha, K.oma, K.rho, K.rho_inv);
   if (i == 0) {
     const int l = lane < NINIT ? lane : 0;
-    ok = row_update(sm.R(-1) + INIT0 + l, lane < NINIT, cf[C_INIT + l] * xs[l], K.alpha, K.oma, K.rho,
+    ok = row_update(sm.R(-1) + INIT0 + l, sm.T(-1) + INIT0 + l, lane < NINIT, cf[C_INIT + l] * xs[l], K.alpha, K.oma, K.rho,
                     K.rho_inv) && ok;
   }
   return !ok;
@@ -1290,13 +1296,13 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
   // - rho U g : top correction of node i from node i-1 (coefficients of interval i-1)
   auto top_corr = [&](const float* cp, float gint, float g0, float g1, float g2) {
     const float gk = __shfl_sync(FULL, gint, kq);
-    const float ci = cp[C_INT + 4 * kq + (is_q ? 0 : 2)];
+    const float ci = cp[(is_q ? C_A1 : C_A3) + kq];
     return rho * ((f_q + f_qd) * ci * gk +
                   f_qd * (cp[C_DYNU + kq] * g0 + cp[C_DYNU + 12 + kq] * g1 + cp[C_DYNU + 24 + kq] * g2));
   };
   // - rho V g' : bottom correction of node i from node i+1 (coefficients of interval i)
   auto bot_corr = [&](const float* cf, float gint, float g0, float g1, float g2) {
-    return rho * (f_q * cf[C_INT + 4 * kq + 1] * gint +
+    return rho * (f_q * cf[C_A2 + kq] * gint +
                   f_dv * (cf[C_DYNV + jv] * g0 + cf[C_DYNV + 20 + jv] * g1 + cf[C_DYNV + 40 + jv] * g2));
   };
 #pragma unroll 1
@@ -1311,7 +1317,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float u = r_of(i, first) - top_corr(sm.C(i - 1), gint, g0, g1, g2);
         const float s = ext_mv(sm.Tm(i), lane, ubuf, u);
         store_s(i, s);
-        gint = f_q * sm.C(i)[C_INT + 4 * kq + 1] * s;
+        gint = f_q * sm.C(i)[C_A2 + kq] * s;
         g0 = __shfl_sync(FULL, s, 26);
         g1 = __shfl_sync(FULL, s, 27);
         g2 = __shfl_sync(FULL, s, 28);
@@ -1325,7 +1331,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         store_s(i, s);
         const float* cp = sm.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
         const float sq = __shfl_down_sync(FULL, s, 9);
-        gint = f_q * (cp[C_INT + 4 * kq] * s + cp[C_INT + 4 * kq + 2] * sq);
+        gint = f_q * (cp[C_A1 + kq] * s + cp[C_A3 + kq] * sq);
         g0 = __shfl_sync(FULL, s, 26);
         g1 = __shfl_sync(FULL, s, 27);
         g2 = __shfl_sync(FULL, s, 28);
@@ -1352,7 +1358,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         float* vs = sm.V(i, V_S);
         const float* xn = sm.V(i + 1, V_S);
         // xi_k = a2_k (a1_k x[q_k] + a3_k x[qd_k]) (lanes 0..8), xi_b = u_b . x[qd] (9..11)
-        const float dl = cf[C_INT + 4 * kq] * xn[kq] + cf[C_INT + 4 * kq + 2] * xn[NQ + kq];
+        const float dl = cf[C_A1 + kq] * xn[kq] + cf[C_A3 + kq] * xn[NQ + kq];
         const float* ub = cf + C_DYNU + 12 * bw;
         float a0 = ub[0] * xn[NQ], a1 = ub[1] * xn[NQ + 1], a2 = ub[2] * xn[NQ + 2];
         a0 = fmaf(ub[3], xn[NQ + 3], a0);
@@ -1362,7 +1368,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         a1 = fmaf(ub[7], xn[NQ + 7], a1);
         a2 = fmaf(ub[8], xn[NQ + 8], a2);
         const float xd = a0 + a1 + a2;
-        xib[lane] = is_q ? cf[C_INT + 4 * kq + 1] * dl : (lane < 12 ? xd : 0.f);
+        xib[lane] = is_q ? cf[C_A2 + kq] * dl : (lane < 12 ? xd : 0.f);
         __syncwarp();
         // lanes < 26: row j of S^-1 (cols 0..8 = column j) and W_b[j];  26..28: W_b, G_b
         float v[TCOLS];
@@ -1381,9 +1387,9 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         bad = bad || !isfinite(xt);
         // z~: integration row k (lane k) = a2 x~_i[q_k] + dl ; dynamics row b (lane 26+b) =
         // v_b.x~_i + u_b.x~_{i+1} = g_b - rho acc + xi_b
-        const float zt = is_q ? fmaf(cf[C_INT + 4 * kq + 1], xt, dl) : gamma_of(i) - rho * acc + xib[9 + bw];
+        const float zt = is_q ? fmaf(cf[C_A2 + kq], xt, dl) : gamma_of(i) - rho * acc + xib[9 + bw];
         const int slot = is_q ? kq : 9 + bw;
-        bad = !row_update(sm.R(i) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        bad = !row_update(sm.R(i) + slot, sm.T(i) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
         __syncwarp();
         bad = finish_node(i) || bad;
       }
@@ -1394,7 +1400,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float* xp = sm.V(i - 1, V_S);
         float* vs = sm.V(i, V_S);
         // xi'_k = a2_k x_{i-1}[q_k] (lanes 0..8, published as a1 xi', a3 xi'); xi'_b = v_b . x_{i-1}
-        const float xiv = cp[C_INT + 4 * kq + 1] * xp[kq];
+        const float xiv = cp[C_A2 + kq] * xp[kq];
         const float* vb = cp + C_DYNV + 20 * bw;
         float a0 = 0.f, a1 = 0.f, a2 = 0.f;
 #pragma unroll
@@ -1405,8 +1411,8 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         }
         const float xd = a0 + a1 + a2;
         if (is_q) {
-          xib[lane] = cp[C_INT + 4 * kq] * xiv;
-          xib[9 + lane] = cp[C_INT + 4 * kq + 2] * xiv;
+          xib[lane] = cp[C_A1 + kq] * xiv;
+          xib[9 + lane] = cp[C_A3 + kq] * xiv;
         }
         if (lane >= 9 && lane < 12) xib[18 + bw] = xd;
         __syncwarp();
@@ -1427,10 +1433,10 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float xq = __shfl_down_sync(FULL, xt, 9);  // lane k: x_i[qd_k]
         // z~: integration row k = xi'_k + a1 x_i[q_k] + a3 x_i[qd_k];
         //     dynamics row b = v_b.x_{i-1} + u_b.x_i = xi'_b + g'_b - rho acc
-        const float zt = is_q ? xiv + cp[C_INT + 4 * kq] * xt + cp[C_INT + 4 * kq + 2] * xq
+        const float zt = is_q ? xiv + cp[C_A1 + kq] * xt + cp[C_A3 + kq] * xq
                               : xib[18 + bw] + gamma_of(i) - rho * acc;
         const int slot = is_q ? kq : 9 + bw;
-        bad = !row_update(sm.R(i - 1) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
+        bad = !row_update(sm.R(i - 1) + slot, sm.T(i - 1) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
         __syncwarp();
         bad = finish_node(i) || bad;
       }
@@ -1460,6 +1466,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   sm.coef = base + L.coef;
   sm.vec = base + L.vec;
   sm.row = reinterpret_cast<float4*>(base + L.row);
+  sm.tt = base + L.tt;
   sm.dsc = base + L.dsc;
   sm.bc = base + L.bc;
   sm.flags = reinterpret_cast<uint32_t*>(base + L.flags);
@@ -1474,6 +1481,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   for (int k = tid; k < (NT + 1) * C_SIZE; k += 64) sm.coef[k] = 0.f;
   for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
     sm.row[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sm.tt[r] = 0.f;
     sm.dsc[r] = 1.f;
   }
   for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;

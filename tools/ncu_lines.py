@@ -15,7 +15,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
+LIB = os.environ.get("RMPC_B200_LIB") or os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
 FUNC = "_ZN8rmpc_dev10rti_kernelENS_7KParamsE"
 
 
@@ -71,15 +71,19 @@ def main():
     hi = next(i for i, r in enumerate(rows) if r and r[0] == "Address")
     h = rows[hi]
     cs, ci = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
+    cw, cx = h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Excessive")
     ins = [r for r in rows[hi + 1:] if len(r) > ci]
     lines = line_table()
     if len(lines) != len(ins):
         print(f"warning: {len(ins)} ncu instructions vs {len(lines)} disassembled", file=sys.stderr)
     samp, inst = collections.Counter(), collections.Counter()
+    wav, wex = collections.Counter(), collections.Counter()
     for k, r in enumerate(ins):
         key = lines[k] if k < len(lines) else ("?", 0)
         samp[key] += float(r[cs] or 0)
         inst[key] += float(r[ci] or 0)
+        wav[key] += float(r[cw] or 0)
+        wex[key] += float(r[cx] or 0)
     ts, ti = sum(samp.values()), sum(inst.values())
     kern = os.path.join(ROOT, "paper_2510_12717_b200", "csrc", "rmpc_kernel.cu")
     table = functions(kern)
@@ -92,6 +96,11 @@ def main():
     for key, v in fs.most_common(30):
         print(f"{100 * v / ts:5.1f}% samp {100 * fi[key] / ti:5.1f}% inst  {key}")
     src = {}
+    tw, tx = sum(wav.values()), sum(wex.values())
+    print(f"shared wavefronts {tw:.0f}, excessive {tx:.0f} ({100 * tx / max(tw, 1):.1f}%); top lines by excess:")
+    for key, v in wex.most_common(12):
+        f, n = key
+        print(f"  {100 * v / max(tx, 1):5.1f}% of excess, {wav[key]:.0f} wavefronts  {f}:{n}")
     print(f"total samples {ts:.0f}, warp-instructions {ti:.0f}")
     for key, s in samp.most_common(top):
         f, n = key

@@ -1,0 +1,95 @@
+/*
+ * rmpc_b200_env.h — C ABI of the closed-loop step that follows the batched solve
+ * (SURVEY.md §8(f) rows 1-2), device-resident and asynchronous on a CUDA stream:
+ *
+ *   rmpc_physics_step_device   physics_step      (/root/reference/proj/src/env.cpp:38-68):
+ *                              penalty contacts on the terrain, `substeps` semi-implicit
+ *                              Euler steps with qdd = M^-1 (tau - h + J^T F) (LLT), then
+ *                              advance_phase (gait.cpp:31-35)
+ *   rmpc_control_step_device   mpc_torque + blend + physics_step fused in one kernel
+ *                              (mpc.cpp:340-344, policy.cpp:133-157, ppo.cpp:345-349): the
+ *                              torque a failed solution yields is zero, as in Trainer::train
+ *   rmpc_observe_device        observe (policy.cpp:104-122): the 23-entry policy input
+ *
+ * The environment owns the reference's EnvConfig physics/terrain part (env.hpp:52-63) and the
+ * heightfield (Terrain, env.cpp:8-27, drawn from Rng(seed, 0x7e22) like the reference).  Each
+ * agent carries its randomize_model draw (env.cpp:196-208) as rmpc_body {mu, mass_scale};
+ * a NULL body array means the base model.  All arithmetic is FP64 (the simulator's state
+ * integrates over thousands of steps).  Per-agent blow-ups never abort the batch: status 1
+ * replaces the reference's SimBlowupError.
+ */
+#ifndef RMPC_B200_ENV_H_
+#define RMPC_B200_ENV_H_
+
+#include "rmpc_b200.h"
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define RMPC_OBS_DIM 23
+
+/* EnvConfig (env.hpp:52-63) and TerrainConfig (env.hpp:16-23). */
+typedef struct rmpc_env_config {
+  double control_dt;     /* 0.01 s (100 Hz control) */
+  int32_t substeps;      /* 4 (400 Hz physics) */
+  int32_t terrain_kind;  /* 0 flat, 1 heightfield */
+  double k_n, c_n, v_slip;           /* penalty contact: 5e4, 500, 0.05 */
+  double amplitude, cell, extent;    /* heightfield: 0.04, 0.3, 80 */
+  uint64_t terrain_seed;             /* 0 */
+} rmpc_env_config;
+
+/* randomize_model (env.cpp:196-208): friction and one common mass/inertia scale. */
+typedef struct rmpc_body {
+  double mu;
+  double mass_scale;
+} rmpc_body;
+
+/* BlendStrategy (policy.hpp): joint-joint, joint-torque, torque-torque (policy.cpp:133-157). */
+enum {
+  RMPC_BLEND_JOINT_JOINT = 0,
+  RMPC_BLEND_JOINT_TORQUE = 1,
+  RMPC_BLEND_TORQUE_TORQUE = 2
+};
+
+/* Simulation outcome per agent. */
+enum { RMPC_SIM_OK = 0, RMPC_SIM_BLOWUP = 1 };
+
+typedef struct rmpc_env rmpc_env;
+
+void rmpc_env_config_default(rmpc_env_config* cfg);
+/* Builds the terrain on the host and uploads it with the base model to `device`. */
+int32_t rmpc_env_create(const rmpc_model* base, const rmpc_env_config* cfg, int32_t device,
+                        rmpc_env** out);
+void rmpc_env_destroy(rmpc_env* env);
+/* Terrain::height_at (env.cpp:17-27) on the host copy, for tests and callers. */
+int32_t rmpc_env_height_at(const rmpc_env* env, double x, double* h);
+
+/* One control period for n agents.  states/gaits are updated in place; tau is n x 6 (FP64);
+ * sim_status (n, may be NULL) receives RMPC_SIM_*.  stream 0 = the legacy default stream. */
+int32_t rmpc_physics_step_device(rmpc_env* env, int32_t n, rmpc_state* d_states,
+                                 rmpc_gait* d_gaits, const rmpc_body* d_bodies,
+                                 const double* d_tau, int32_t* d_sim_status, void* stream);
+
+/* tau = blend(mpc_torque(sol), ...) (zero for a failed solution), then the physics step.
+ * d_action (n x 6) may be NULL (zero action); d_tau_out (n x 6) may be NULL. */
+int32_t rmpc_control_step_device(rmpc_env* env, int32_t n, const rmpc_solution* d_sol,
+                                 const double* d_action, int32_t strategy, double lambda,
+                                 rmpc_state* d_states, rmpc_gait* d_gaits,
+                                 const rmpc_body* d_bodies, double* d_tau_out,
+                                 int32_t* d_sim_status, void* stream);
+
+/* observe(state, solution) -> n x RMPC_OBS_DIM FP64 (ObsSettings: v_mpc_scale 1e-2,
+ * v_mpc_sentinel 10 for a failed solution). */
+int32_t rmpc_observe_device(int32_t n, const rmpc_state* d_states, const rmpc_gait* d_gaits,
+                            const rmpc_solution* d_sol, double v_mpc_scale,
+                            double v_mpc_sentinel, double* d_obs, void* stream);
+
+/* sizeof of the env ABI structs (0 config, 1 body) for binding-side layout checks. */
+int32_t rmpc_env_sizeof(int32_t which);
+
+#ifdef __cplusplus
+}  /* extern "C" */
+#endif
+
+#endif  /* RMPC_B200_ENV_H_ */

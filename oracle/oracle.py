@@ -264,3 +264,69 @@ def admm(P, q, A, lo, hi, *, sigma=1e-6, rho=0.1, alpha=1.6, iters=25, ruiz_iter
     if rc != 0:
         raise ValueError("admm: structural error")
     return dict(x=x, y=y, z=z, prim=info[0], dual=info[1], obj=info[2], iters=int(info[3]))
+
+
+# ---------------------------------------------------------------- closed-loop step (env.cpp)
+def _env_lib():
+    L = lib()
+    if not getattr(L, "_env_bound", False):
+        L.oracle_terrain_height_at.restype = C.c_double
+        L.oracle_terrain_height_at.argtypes = [C.c_void_p, C.c_double]
+        L.oracle_control_step_batch.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                                C.c_int32, C.c_double] + [C.c_void_p] * 5
+        L.oracle_observe_batch.argtypes = [C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_double,
+                                           C.c_double, C.c_void_p]
+        L._env_bound = True
+    return L
+
+
+def env_config_default():
+    from paper_2510_12717_b200.env import EnvConfig
+    c = EnvConfig()
+    _env_lib().oracle_env_config_default(C.byref(c))
+    return c
+
+
+def terrain_height_at(cfg, x: float) -> float:
+    return _env_lib().oracle_terrain_height_at(C.byref(cfg), float(x))
+
+
+def physics_step_batch(model: Model, cfg, states, gaits, tau, bodies=None):
+    """physics_step + advance_phase for every agent: returns (states, gaits, status)."""
+    st, ga = _f64(states).copy().reshape(-1, 18), _f64(gaits).copy().reshape(-1, 7)
+    n = st.shape[0]
+    tau = _f64(tau, (n, 6))
+    bo = None if bodies is None else _f64(bodies, (n, 2))
+    status = np.zeros(n, np.int32)
+    _env_lib().oracle_physics_step_batch(C.byref(model), C.byref(cfg), C.c_int32(n), ptr(st), ptr(ga),
+                                         ptr(bo), ptr(tau), status.ctypes.data_as(C.POINTER(C.c_int32)))
+    return st, ga, status
+
+
+def control_step_batch(model: Model, cfg, solutions, states, gaits, action=None, strategy=0, lam=0.0,
+                       bodies=None):
+    """Trainer::train's control (zero torque on failure, else blend(mpc_torque)) + physics:
+    returns (states, gaits, tau, status).  `solutions` is the device's SOLUTION_DTYPE array."""
+    st, ga = _f64(states).copy().reshape(-1, 18), _f64(gaits).copy().reshape(-1, 7)
+    n = st.shape[0]
+    sols = np.ascontiguousarray(solutions)
+    act = None if action is None else _f64(action, (n, 6))
+    bo = None if bodies is None else _f64(bodies, (n, 2))
+    tau = np.zeros((n, 6))
+    status = np.zeros(n, np.int32)
+    _env_lib().oracle_control_step_batch(C.byref(model), C.byref(cfg), n, sols.ctypes.data,
+                                         None if act is None else act.ctypes.data, int(strategy), float(lam),
+                                         st.ctypes.data, ga.ctypes.data,
+                                         None if bo is None else bo.ctypes.data, tau.ctypes.data,
+                                         status.ctypes.data)
+    return st, ga, tau, status
+
+
+def observe_batch(states, gaits, solutions, scale=1e-2, sentinel=10.0):
+    st, ga = _f64(states).reshape(-1, 18), _f64(gaits).reshape(-1, 7)
+    n = st.shape[0]
+    sols = np.ascontiguousarray(solutions)
+    obs = np.zeros((n, 23))
+    _env_lib().oracle_observe_batch(n, st.ctypes.data, ga.ctypes.data, sols.ctypes.data, scale, sentinel,
+                                    obs.ctypes.data)
+    return obs

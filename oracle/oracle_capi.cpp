@@ -6,6 +6,8 @@
 #include <thread>
 
 #include "rmpc_oracle.hpp"
+#include "rmpc_oracle_env.hpp"
+#include "rmpc_oracle_rng.hpp"
 #include "oracle_flops.hpp"
 
 using namespace oracle;
@@ -111,36 +113,6 @@ int32_t oracle_flops(const rmpc_model* model, const rmpc_settings* st, const rmp
   }
   return s.status;
 }
-
-// xoshiro256++ with splitmix64 seeding, restated from rng.hpp:15-75 (stream constructor
-// Rng(seed, stream)).  out[n] = uniform() draws of one stream.
-namespace {
-struct Rng {
-  uint64_t s[4];
-  static uint64_t splitmix(uint64_t x) {
-    x += 0x9e3779b97f4a7c15ULL;
-    x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
-    x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
-    return x ^ (x >> 31);
-  }
-  static uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
-  Rng(uint64_t seed, uint64_t stream) {
-    uint64_t x = seed ^ splitmix(stream + 0x9e3779b97f4a7c15ULL);
-    for (auto& w : s) {
-      x += 0x9e3779b97f4a7c15ULL;
-      w = splitmix(x);
-    }
-  }
-  uint64_t next() {
-    const uint64_t r = rotl(s[0] + s[3], 23) + s[0];
-    const uint64_t t = s[1] << 17;
-    s[2] ^= s[0]; s[3] ^= s[1]; s[1] ^= s[2]; s[0] ^= s[3]; s[2] ^= t;
-    s[3] = rotl(s[3], 45);
-    return r;
-  }
-  double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
-};
-}  // namespace
 
 void oracle_rng_uniform(uint64_t seed, uint64_t stream, int32_t n, double* out) {
   Rng r(seed, stream);
@@ -381,6 +353,38 @@ int32_t oracle_admm_dense(int32_t n, int32_t m, const double* P, const double* q
   } catch (const std::exception&) {
     return RMPC_ERR_STRUCTURAL;
   }
+}
+
+// ---------------------------------------------------------------- closed-loop step (env.cpp)
+void oracle_env_config_default(rmpc_env_config* c) { env_config_default(c); }
+
+double oracle_terrain_height_at(const rmpc_env_config* c, double x) { return Terrain(*c).height_at(x); }
+
+void oracle_physics_step_batch(const rmpc_model* base, const rmpc_env_config* cfg, int32_t n,
+                               rmpc_state* states, rmpc_gait* gaits, const rmpc_body* bodies,
+                               const double* tau, int32_t* status) {
+  const Terrain ter(*cfg);
+  for (int a = 0; a < n; ++a) {
+    const rmpc_model m = randomized(*base, bodies ? bodies + a : nullptr);
+    status[a] = physics_step(m, *cfg, ter, states[a], gaits[a], tau + 6 * a);
+  }
+}
+
+void oracle_control_step_batch(const rmpc_model* base, const rmpc_env_config* cfg, int32_t n,
+                               const rmpc_solution* sols, const double* action, int32_t strategy,
+                               double lambda, rmpc_state* states, rmpc_gait* gaits,
+                               const rmpc_body* bodies, double* tau_out, int32_t* status) {
+  const Terrain ter(*cfg);
+  for (int a = 0; a < n; ++a) {
+    const rmpc_model m = randomized(*base, bodies ? bodies + a : nullptr);
+    status[a] = control_step(m, *cfg, ter, sols[a], action ? action + 6 * a : nullptr, strategy,
+                             lambda, states[a], gaits[a], tau_out + 6 * a);
+  }
+}
+
+void oracle_observe_batch(int32_t n, const rmpc_state* states, const rmpc_gait* gaits,
+                          const rmpc_solution* sols, double scale, double sentinel, double* obs) {
+  for (int a = 0; a < n; ++a) observe(states[a], gaits[a], sols[a], scale, sentinel, obs + RMPC_OBS_DIM * a);
 }
 
 }  // extern "C"

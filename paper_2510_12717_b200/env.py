@@ -1,0 +1,124 @@
+"""Closed-loop step after the solve over include/rmpc_b200_env.h:
+physics_step (env.cpp:38-68), the fused mpc_torque + blend + physics control step
+(mpc.cpp:340-344, policy.cpp:133-157, ppo.cpp:340-349) and observe (policy.cpp:104-122), all
+device-resident on CUDA tensors.  Layouts: states (n, 18) f64 = rmpc_state, gaits (n, 7) f64 =
+rmpc_gait, bodies (n, 2) f64 = rmpc_body {mu, mass_scale}, tau / action (n, 6) f64,
+solutions SOLUTION_DTYPE bytes, observations (n, 23) f64."""
+from __future__ import annotations
+
+import ctypes as C
+
+from .abi import Model, default_model
+from .runtime import RmpcError, library
+
+OBS_DIM = 23
+BLEND = {"joint-joint": 0, "joint-torque": 1, "torque-torque": 2}
+SIM_OK, SIM_BLOWUP = 0, 1
+
+_VP, _I, _D = C.c_void_p, C.c_int32, C.c_double
+
+
+class EnvConfig(C.Structure):
+    """EnvConfig physics + TerrainConfig (env.hpp:16-63)."""
+    _fields_ = [("control_dt", _D), ("substeps", _I), ("terrain_kind", _I), ("k_n", _D),
+                ("c_n", _D), ("v_slip", _D), ("amplitude", _D), ("cell", _D), ("extent", _D),
+                ("terrain_seed", C.c_uint64)]
+
+
+def _bind(L):
+    if getattr(L, "_env_bound", False):
+        return L
+    L.rmpc_env_config_default.argtypes = [_VP]
+    L.rmpc_env_config_default.restype = None
+    L.rmpc_env_create.argtypes = [_VP, _VP, _I, C.POINTER(_VP)]
+    L.rmpc_env_create.restype = _I
+    L.rmpc_env_destroy.argtypes = [_VP]
+    L.rmpc_env_destroy.restype = None
+    L.rmpc_env_height_at.argtypes = [_VP, _D, C.POINTER(_D)]
+    L.rmpc_env_height_at.restype = _I
+    L.rmpc_physics_step_device.argtypes = [_VP, _I, _VP, _VP, _VP, _VP, _VP, _VP]
+    L.rmpc_physics_step_device.restype = _I
+    L.rmpc_control_step_device.argtypes = [_VP, _I, _VP, _VP, _I, _D, _VP, _VP, _VP, _VP, _VP, _VP]
+    L.rmpc_control_step_device.restype = _I
+    L.rmpc_observe_device.argtypes = [_I, _VP, _VP, _VP, _D, _D, _VP, _VP]
+    L.rmpc_observe_device.restype = _I
+    L.rmpc_env_sizeof.argtypes = [_I]
+    L.rmpc_env_sizeof.restype = _I
+    L._env_bound = True
+    return L
+
+
+def default_env_config(**overrides) -> EnvConfig:
+    c = EnvConfig()
+    _bind(library()).rmpc_env_config_default(C.byref(c))
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+def _p(t):
+    if t is None:
+        return None
+    return t if isinstance(t, int) else t.data_ptr()
+
+
+def _s(stream):
+    if stream is None:
+        return None
+    s = stream if isinstance(stream, int) else stream.cuda_stream
+    return 1 if s == 0 else s  # cudaStreamLegacy
+
+
+class Env:
+    """The reference's per-env simulator step, batched on one GPU (device `device`)."""
+
+    def __init__(self, model: Model | None = None, config: EnvConfig | None = None, device: int = 0):
+        self._lib = _bind(library())
+        self.model = model if model is not None else default_model()
+        self.config = config if config is not None else default_env_config()
+        h = _VP()
+        rc = self._lib.rmpc_env_create(C.byref(self.model), C.byref(self.config), device, C.byref(h))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_env_create failed")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.rmpc_env_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def height_at(self, x: float) -> float:
+        v = _D()
+        self._lib.rmpc_env_height_at(self._h, float(x), C.byref(v))
+        return v.value
+
+    def physics_step(self, states, gaits, tau, bodies=None, sim_status=None, stream=None):
+        n = states.shape[0]
+        rc = self._lib.rmpc_physics_step_device(self._h, n, _p(states), _p(gaits), _p(bodies), _p(tau),
+                                                _p(sim_status), _s(stream))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_physics_step_device failed")
+
+    def control_step(self, solutions, states, gaits, action=None, strategy: str | int = "joint-joint",
+                     lam: float = 0.0, bodies=None, tau_out=None, sim_status=None, stream=None):
+        n = states.shape[0]
+        st = BLEND[strategy] if isinstance(strategy, str) else int(strategy)
+        rc = self._lib.rmpc_control_step_device(self._h, n, _p(solutions), _p(action), st, float(lam),
+                                                _p(states), _p(gaits), _p(bodies), _p(tau_out),
+                                                _p(sim_status), _s(stream))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_control_step_device failed")
+
+    def observe(self, states, gaits, solutions, obs, v_mpc_scale: float = 1e-2,
+                v_mpc_sentinel: float = 10.0, stream=None):
+        n = states.shape[0]
+        rc = self._lib.rmpc_observe_device(n, _p(states), _p(gaits), _p(solutions), v_mpc_scale,
+                                           v_mpc_sentinel, _p(obs), _s(stream))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_observe_device failed")

@@ -11,20 +11,22 @@ import pytest
 import paper_2510_12717_b200 as R
 from paper_2510_12717_b200 import abi, runtime
 
-HEADER = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include",
-                      "rmpc_b200.h")
+INCLUDE = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "include")
+HEADERS = [os.path.join(INCLUDE, h) for h in ("rmpc_b200.h", "rmpc_b200_env.h")]
 
 
 def declared_functions():
-    src = open(HEADER).read()
-    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
-    return sorted(set(re.findall(r"\b(rmpc_[a-z_0-9]+)\s*\(", src)))
+    names = set()
+    for h in HEADERS:
+        src = re.sub(r"/\*.*?\*/", "", open(h).read(), flags=re.S)
+        names |= set(re.findall(r"\b(rmpc_[a-z_0-9]+)\s*\(", src))
+    return sorted(names)
 
 
 def test_library_exports_every_declared_symbol():
     L = R.library()
     names = declared_functions()
-    assert len(names) >= 18
+    assert len(names) >= 27
     for n in names:
         assert hasattr(L, n), n
 
@@ -35,6 +37,17 @@ def test_struct_sizes_match_header():
              abi.SOLUTION_DTYPE.itemsize, C.sizeof(abi.Timing)]
     assert [L.rmpc_sizeof(i) for i in range(7)] == sizes
     assert L.rmpc_sizeof(99) == -1
+    from paper_2510_12717_b200.env import EnvConfig, _bind
+    _bind(L)
+    assert [L.rmpc_env_sizeof(i) for i in range(2)] == [C.sizeof(EnvConfig), 16]
+    assert L.rmpc_env_sizeof(2) == -1
+
+
+def test_env_config_defaults_and_terrain_match_oracle(oracle):
+    from paper_2510_12717_b200.env import default_env_config
+    c = default_env_config()
+    assert bytes(c) == bytes(oracle.env_config_default())
+    assert (c.control_dt, c.substeps, c.k_n, c.c_n, c.v_slip) == (0.01, 4, 5e4, 500.0, 0.05)
 
 
 def test_defaults_match_library_defaults():

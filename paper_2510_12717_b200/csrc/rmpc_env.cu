@@ -66,7 +66,7 @@ __device__ int physics(const EnvParams& E, double mu, double mscale, rmpc_state&
 #pragma unroll 1
   for (int sub = 0; sub < E.substeps; ++sub) {
     Frames F;
-    fk_frames(E.geo, s.q, s.qd, F);  // base x taken as 0: Jacobians use differences only
+    fk_frames(E.geo, s.q, s.qd, F, s.q[0]);  // absolute x, as the terrain lookup needs
     double L[NQ * (NQ + 1) / 2];     // lower triangle of M, row-major, then its Cholesky factor
     double gen[NQ];
 #pragma unroll
@@ -114,7 +114,7 @@ __device__ int physics(const EnvParams& E, double mu, double mscale, rmpc_state&
     // penalty contacts (env.cpp:49-56)
 #pragma unroll
     for (int c = 0; c < NC; ++c) {
-      const double ground = height_at(E, F.con[c].px + s.q[0]);
+      const double ground = height_at(E, F.con[c].px);
       const double pen = ground - F.con[c].pz;
       if (pen > 0.0) {
         const double fz = fmax(0.0, E.k_n * pen - E.c_n * F.con[c].vz);

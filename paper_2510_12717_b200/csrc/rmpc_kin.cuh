@@ -38,9 +38,9 @@ struct Frames {
 
 // Each of the 7 absolute angles (pitch, then hip/knee/ankle of each leg) gets one sincos.
 template <class Geo>  // torso_len, thigh_len, shank_len, foot_half, ankle_drop
-__device__ void fk_frames(const Geo& P, const double* q, const double* qd, Frames& F) {
+__device__ void fk_frames(const Geo& P, const double* q, const double* qd, Frames& F, double base_x = 0.0) {
   Fr base;
-  base.px = 0.0;
+  base.px = base_x;  // 0 for the solve: Jacobians use position differences only
   base.pz = q[1];
   base.vx = qd[0];
   base.vz = qd[1];

@@ -45,6 +45,9 @@ def parse():
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=4096, help="agents in the CPU baseline sample")
+    p.add_argument("--cl-agents", type=int, default=8192,
+                   help="C5 closed-loop agents per GPU (65 536 over 8 B200); 0 disables")
+    p.add_argument("--cl-ticks", type=int, default=100, help="C5 closed-loop ticks")
     return p.parse_args()
 
 
@@ -195,6 +198,54 @@ def run_reference_arm(args):
     print(json.dumps(line), flush=True)
 
 
+def closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier):
+    """C5: args.cl_agents per GPU, mixed gaits (phase_switch 0.4/0.5/0.65/1.0), args.cl_ticks
+    ticks of [solve -> state <- (q*[1], qd*[1]), phase += 0.01 s], per-tick CUDA events."""
+    import torch
+    from paper_2510_12717_b200.abi import SOLUTION_DTYPE
+    from paper_2510_12717_b200.env import plan_feedback
+    from paper_2510_12717_b200.sharding import shard_range
+    n, T = args.cl_agents, args.horizon
+    s = R.default_settings(T)
+    st, cm, ga = R.synthetic_batch(n * world, "mixed", seed=5, model=m, settings=s)
+    lo, hi = shard_range(rank, world, n * world)
+    br = R.BatchRunner(n, m, s, devices=[dev.index])
+    stream = torch.cuda.Stream(device=dev)
+    with torch.cuda.stream(stream):
+        d_st, d_cm, d_ga = (torch.from_numpy(a[lo:hi].copy()).to(dev) for a in (st, cm, ga))
+        d_out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        d_z = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
+
+    def tick():
+        br.solve_device(d_st, d_cm, d_ga, d_out, z_out=d_z, stream=stream)
+        plan_feedback(d_z, d_out, d_st, d_ga, T, 0.01, stream=stream)
+
+    for _ in range(3):
+        tick()
+    ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+          for _ in range(args.cl_ticks)]
+    barrier()
+    torch.cuda.synchronize()
+    with torch.cuda.stream(stream):
+        for k in range(args.cl_ticks):
+            ev[k][0].record(stream)
+            tick()
+            ev[k][1].record(stream)
+    stream.synchronize()
+    barrier()
+    tick_ms = max_over_ranks([a.elapsed_time(b) for a, b in ev])
+    sol = d_out.cpu().numpy().view(SOLUTION_DTYPE)
+    ok = int(max_over_ranks([float((sol["status"] != 0).sum())])[0])
+    br.close()
+    return {"config": "C5: %d agents per GPU x %d GPU, N=%d, mixed gaits, %d ticks, state <- plan node 1, "
+                      "phase += 10 ms" % (n, world, T, args.cl_ticks),
+            "agents_total": n * world, "ticks": args.cl_ticks,
+            "p50_tick_ms": float(np.median(tick_ms)), "p99_tick_ms": float(np.percentile(tick_ms, 99)),
+            "solves_per_s": n * world / (float(np.mean(tick_ms)) * 1e-3),
+            "tick_budget_ms": 10.0, "failed_solves_last_tick_max_rank": ok,
+            "gpu_launches_per_tick": 2}
+
+
 def main():
     args = parse()
     if args.impl == "reference":
@@ -301,6 +352,12 @@ def main():
                 "the tensor roofline applies; FLOP_alg is the reference algorithm's count",
     }
 
+    # ---- C5 closed loop: varied gaits, every tick replans from the previous
+    #      plan's node 1 with the phase advanced 10 ms; solve + plan feedback stay on the device
+    closed = None
+    if args.cl_agents > 0:
+        closed = closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier)
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -333,6 +390,7 @@ def main():
             "roofline": roofline,
             "gpu_launches": args.steps,
             "status_ok": ok, "clocks": clk, "cpu_baseline": cpu,
+            "closed_loop": closed,
         }
         print(json.dumps(line), flush=True)
     br.close()

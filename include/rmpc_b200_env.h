@@ -85,6 +85,14 @@ int32_t rmpc_observe_device(int32_t n, const rmpc_state* d_states, const rmpc_ga
                             const rmpc_solution* d_sol, double v_mpc_scale,
                             double v_mpc_sentinel, double* d_obs, void* stream);
 
+/* Plan feedback for open-loop replanning benchmarks: state <- node 1 of
+ * the previous plan z* (q*[1], qd*[1]; n x horizon x 26 FP32 as rmpc_solve writes it), gait
+ * phase advanced by dt (advance_phase, gait.cpp:31-35).  Agents whose solve failed keep their
+ * state and only advance the phase. */
+int32_t rmpc_plan_feedback_device(int32_t n, int32_t horizon, const float* d_z,
+                                  const rmpc_solution* d_sol, rmpc_state* d_states,
+                                  rmpc_gait* d_gaits, double dt, void* stream);
+
 /* sizeof of the env ABI structs (0 config, 1 body) for binding-side layout checks. */
 int32_t rmpc_env_sizeof(int32_t which);
 

@@ -258,6 +258,21 @@ __global__ void __launch_bounds__(128) observe_kernel(int n, const rmpc_state* s
   o[22] = sols[a].status == RMPC_STATUS_OK ? scale * (double)sols[a].v_mpc : sentinel;
 }
 
+__global__ void __launch_bounds__(128) plan_feedback_kernel(int n, int T, const float* z, const rmpc_solution* sols,
+                                                            rmpc_state* states, rmpc_gait* gaits, double dt) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  if (sols[a].status == RMPC_STATUS_OK && T > 1) {
+    const float* z1 = z + ((size_t)a * T + 1) * 26;
+#pragma unroll
+    for (int k = 0; k < NQ; ++k) {
+      states[a].q[k] = (double)z1[k];
+      states[a].qd[k] = (double)z1[NQ + k];
+    }
+  }
+  gaits[a].phase = wrap01(gaits[a].phase + dt / gaits[a].period);
+}
+
 // xoshiro256++ stream Rng(seed, stream) (rng.hpp:15-41), for the heightfield draw.
 struct HostRng {
   uint64_t s[4];
@@ -432,6 +447,15 @@ int32_t rmpc_observe_device(int32_t n, const rmpc_state* states, const rmpc_gait
   if (n == 0) return RMPC_OK;
   rmpc_env_dev::observe_kernel<<<(n + 127) / 128, 128, 0, env_stream(stream)>>>(n, states, gaits, sols, scale,
                                                                                sentinel, obs);
+  return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+}
+
+int32_t rmpc_plan_feedback_device(int32_t n, int32_t horizon, const float* z, const rmpc_solution* sols,
+                                  rmpc_state* states, rmpc_gait* gaits, double dt, void* stream) {
+  if (n < 0 || horizon < 1 || (n > 0 && (!z || !sols || !states || !gaits))) return RMPC_ERR_INVALID_ARG;
+  if (n == 0) return RMPC_OK;
+  rmpc_env_dev::plan_feedback_kernel<<<(n + 127) / 128, 128, 0, env_stream(stream)>>>(n, horizon, z, sols, states,
+                                                                                     gaits, dt);
   return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
 }
 

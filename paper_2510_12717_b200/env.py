@@ -42,6 +42,8 @@ def _bind(L):
     L.rmpc_control_step_device.restype = _I
     L.rmpc_observe_device.argtypes = [_I, _VP, _VP, _VP, _D, _D, _VP, _VP]
     L.rmpc_observe_device.restype = _I
+    L.rmpc_plan_feedback_device.argtypes = [_I, _I, _VP, _VP, _VP, _VP, _D, _VP]
+    L.rmpc_plan_feedback_device.restype = _I
     L.rmpc_env_sizeof.argtypes = [_I]
     L.rmpc_env_sizeof.restype = _I
     L._env_bound = True
@@ -122,3 +124,12 @@ class Env:
                                            v_mpc_sentinel, _p(obs), _s(stream))
         if rc != 0:
             raise RmpcError(rc, "rmpc_observe_device failed")
+
+
+def plan_feedback(z, solutions, states, gaits, horizon: int, dt: float = 0.01, stream=None):
+    """C5 open-loop replanning: state <- (q*[1], qd*[1]) of the last plan, phase += dt/period."""
+    L = _bind(library())
+    rc = L.rmpc_plan_feedback_device(states.shape[0], horizon, _p(z), _p(solutions), _p(states), _p(gaits),
+                                     float(dt), _s(stream))
+    if rc != 0:
+        raise RmpcError(rc, "rmpc_plan_feedback_device failed")

@@ -10,6 +10,7 @@
  *                              (mpc.cpp:340-344, policy.cpp:133-157, ppo.cpp:345-349): the
  *                              torque a failed solution yields is zero, as in Trainer::train
  *   rmpc_observe_device        observe (policy.cpp:104-122): the 23-entry policy input
+ *   rmpc_policy_forward_device policy_forward (policy.cpp:85-102): the residual MLPs
  *
  * The environment owns the reference's EnvConfig physics/terrain part (env.hpp:52-63) and the
  * heightfield (Terrain, env.cpp:8-27, drawn from Rng(seed, 0x7e22) like the reference).  Each
@@ -92,6 +93,19 @@ int32_t rmpc_observe_device(int32_t n, const rmpc_state* d_states, const rmpc_ga
 int32_t rmpc_plan_feedback_device(int32_t n, int32_t horizon, const float* d_z,
                                   const rmpc_solution* d_sol, rmpc_state* d_states,
                                   rmpc_gait* d_gaits, double dt, void* stream);
+
+/* Residual policy forward: policy_forward (policy.cpp:85-102) for n
+ * agents, FP64 like the reference: two 4-layer ELU MLPs (obs -> hidden -> hidden -> hidden ->
+ * act / 1).  `params` is MlpParams::flatten_into order (policy.cpp:40-47) of pi then value --
+ * per layer W (out x in, column-major as Eigen stores it) then b -- then log_std (act_dim):
+ * n_params = pi.num_params() + value.num_params() + act_dim (PolicyParams::num_params). */
+typedef struct rmpc_policy rmpc_policy;
+int32_t rmpc_policy_create(int32_t obs_dim, int32_t act_dim, int32_t hidden, const double* params,
+                           int32_t n_params, int32_t device, rmpc_policy** out);
+void rmpc_policy_destroy(rmpc_policy* policy);
+/* mean (n x act_dim) and value (n); either output may be NULL. */
+int32_t rmpc_policy_forward_device(rmpc_policy* policy, int32_t n, const double* d_obs,
+                                   double* d_mean, double* d_value, void* stream);
 
 /* sizeof of the env ABI structs (0 config, 1 body) for binding-side layout checks. */
 int32_t rmpc_env_sizeof(int32_t which);

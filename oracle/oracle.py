@@ -330,3 +330,22 @@ def observe_batch(states, gaits, solutions, scale=1e-2, sentinel=10.0):
     _env_lib().oracle_observe_batch(n, st.ctypes.data, ga.ctypes.data, sols.ctypes.data, scale, sentinel,
                                     obs.ctypes.data)
     return obs
+
+
+def init_policy(obs=23, act=6, hidden=64, seed=0, zero_final=True) -> np.ndarray:
+    """init_policy (policy.cpp:57-83) in flatten_into order: pi, value, log_std."""
+    L = lib()
+    L.oracle_init_policy.restype = C.c_int32
+    n = L.oracle_init_policy(obs, act, hidden, C.c_uint64(seed), int(zero_final), None, 0)
+    out = np.zeros(n)
+    L.oracle_init_policy(obs, act, hidden, C.c_uint64(seed), int(zero_final), ptr(out), n)
+    return out
+
+
+def policy_forward(params, obs, act=6, hidden=64):
+    o = _f64(obs)
+    o = o.reshape(-1, o.shape[-1])
+    n, od = o.shape
+    mean, value = np.zeros((n, act)), np.zeros(n)
+    lib().oracle_policy_forward_batch(ptr(_f64(params)), od, act, hidden, n, ptr(o), ptr(mean), ptr(value))
+    return mean, value

@@ -387,4 +387,17 @@ void oracle_observe_batch(int32_t n, const rmpc_state* states, const rmpc_gait* 
   for (int a = 0; a < n; ++a) observe(states[a], gaits[a], sols[a], scale, sentinel, obs + RMPC_OBS_DIM * a);
 }
 
+int32_t oracle_init_policy(int32_t obs, int32_t act, int32_t hidden, uint64_t seed, int32_t zero_final,
+                           double* out, int32_t cap) {
+  const std::vector<double> p = init_policy_flat(obs, act, hidden, seed, zero_final != 0);
+  if (out && cap >= (int32_t)p.size()) std::copy(p.begin(), p.end(), out);
+  return (int32_t)p.size();
+}
+
+void oracle_policy_forward_batch(const double* params, int32_t obs, int32_t act, int32_t hidden, int32_t n,
+                                 const double* o, double* mean, double* value) {
+  for (int a = 0; a < n; ++a)
+    policy_forward_flat(params, obs, act, hidden, o + (size_t)obs * a, mean + (size_t)act * a, value + a);
+}
+
 }  // extern "C"

@@ -8,6 +8,8 @@
 //   randomize_model                   env.cpp:196-208
 //   advance_phase, contact_phase      gait.cpp:14,31-35
 //   mpc_torque, blend, observe        mpc.cpp:340-344, policy.cpp:104-157
+//   init_policy, mlp_forward,         policy.cpp:15-31, 40-102 (flatten_into order)
+//   policy_forward
 #pragma once
 
 #include <cmath>
@@ -185,6 +187,63 @@ inline void observe(const rmpc_state& st, const rmpc_gait& g, const rmpc_solutio
   o[20] = std::sin(kTwoPi * pl);
   o[21] = std::cos(kTwoPi * pl);
   o[22] = sol.status == 0 ? v_mpc_scale * (double)sol.v_mpc : sentinel;
+}
+
+// init_policy (policy.cpp:57-83) flattened as MlpParams::flatten_into (policy.cpp:40-47): per
+// layer W (out x in) column-major, then b; pi, then value, then log_std.  zero_final = the
+// reference's zero-initialised last policy layer (tests pass false to exercise it).
+inline std::vector<double> init_policy_flat(int obs, int act, int hidden, uint64_t seed, bool zero_final) {
+  Rng rng(seed, 0xB0117);
+  std::vector<double> out;
+  auto build = [&](int out_dim, bool zero_last) {
+    const int sizes[5] = {obs, hidden, hidden, hidden, out_dim};
+    for (int l = 0; l < 4; ++l) {
+      const int rows = sizes[l + 1], cols = sizes[l];
+      const double limit = std::sqrt(6.0 / (rows + cols));
+      std::vector<double> W(static_cast<size_t>(rows) * cols);
+      for (int i = 0; i < rows; ++i)
+        for (int j = 0; j < cols; ++j) W[static_cast<size_t>(j) * rows + i] = rng.uniform(-limit, limit);
+      if (zero_last && l == 3) std::fill(W.begin(), W.end(), 0.0);
+      out.insert(out.end(), W.begin(), W.end());
+      out.insert(out.end(), rows, 0.0);
+    }
+  };
+  build(act, zero_final);
+  build(1, false);
+  out.insert(out.end(), act, std::log(0.5));
+  return out;
+}
+
+// mlp_forward (policy.cpp:15-31) on a flattened trunk starting at p; returns the end offset.
+inline size_t mlp_forward_flat(const double* p, int obs, int hidden, int out_dim, const double* in,
+                               double* out) {
+  const int sizes[5] = {obs, hidden, hidden, hidden, out_dim};
+  std::vector<double> h(in, in + obs), z;
+  size_t off = 0;
+  for (int l = 0; l < 4; ++l) {
+    const int rows = sizes[l + 1], cols = sizes[l];
+    const double* W = p + off;
+    const double* b = W + static_cast<size_t>(rows) * cols;
+    z.assign(rows, 0.0);
+    for (int i = 0; i < rows; ++i) {
+      double acc = 0.0;
+      for (int j = 0; j < cols; ++j) acc += W[static_cast<size_t>(j) * rows + i] * h[j];
+      z[i] = acc + b[i];
+    }
+    off += static_cast<size_t>(rows) * cols + rows;
+    if (l < 3)
+      for (double& v : z) v = v > 0.0 ? v : std::expm1(v);
+    h = z;
+  }
+  for (int i = 0; i < out_dim; ++i) out[i] = h[i];
+  return off;
+}
+
+// policy_forward (policy.cpp:85-102) without the cache.
+inline void policy_forward_flat(const double* params, int obs, int act, int hidden, const double* o,
+                                double* mean, double* value) {
+  const size_t off = mlp_forward_flat(params, obs, hidden, act, o, mean);
+  mlp_forward_flat(params + off, obs, hidden, 1, o, value);
 }
 
 }  // namespace oracle

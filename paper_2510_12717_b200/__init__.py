@@ -13,8 +13,8 @@ from .abi import (NC, NF, NJ, NQ, NV, SOLUTION_DTYPE, STAGE_NAMES, STATUS_DIVERG
                   default_model, default_settings, gait_row, standing_gait_row)
 from .runtime import BatchRunner, RmpcError, library, load_library  # noqa: F401
 from .synthetic import synthetic_batch  # noqa: F401
-from .env import Env, EnvConfig, default_env_config  # noqa: F401
+from .env import Env, EnvConfig, Policy, default_env_config  # noqa: F401
 
 __all__ = ["BatchRunner", "RmpcError", "Model", "Settings", "Timing", "default_model",
            "default_settings", "gait_row", "standing_gait_row", "synthetic_batch",
-           "SOLUTION_DTYPE", "load_library", "library", "Env", "EnvConfig", "default_env_config"]
+           "SOLUTION_DTYPE", "load_library", "library", "Env", "EnvConfig", "Policy", "default_env_config"]

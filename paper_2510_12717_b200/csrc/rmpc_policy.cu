@@ -1,0 +1,173 @@
+// rmpc_policy.cu — the residual policy forward on sm_100a:
+// policy_forward (/root/reference/proj/src/policy.cpp:85-102) = mlp_forward (policy.cpp:15-31)
+// of the pi and value trunks, FP64 like the reference.
+//
+// Why CUDA cores, not tcgen05: per agent the two trunks are 4 layers of at most 64 x 64 (about
+// 40 kFLOP), so 16 k agents are 0.7 GFLOP per tick (~20 us of FP64 CUDA-core time); TF32/BF16
+// tensor-core GEMMs would miss the FP64 reference by 1e-3 and save microseconds.  Layout: one
+// warp per agent, lane j owns output neurons j and j + 32 of every layer, all weights of both
+// trunks resident in shared memory as Eigen stores them (column-major, so a layer's column is
+// 64 consecutive doubles: conflict-free 8-byte loads across the warp), the layer input staged
+// per warp in shared memory and broadcast.  Persistent CTAs of 8 warps stride over the agents.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <new>
+#include <vector>
+
+#include "../../include/rmpc_b200_env.h"
+
+namespace rmpc_policy_dev {
+
+constexpr int WARPS = 8, MAXH = 64, MAXIO = 64;
+
+struct Net {
+  int in[4], out[4];   // layer shapes
+  int w[4], b[4];      // offsets (doubles) into the shared weight block
+};
+
+struct PolicyParams {
+  int obs, act, hidden, total;  // total doubles of both trunks (log_std excluded)
+  Net pi, vf;
+};
+
+// One trunk for the agent held by this warp; x (per-warp smem, MAXIO) holds the input and is
+// overwritten layer by layer.  Returns, in lane j, outputs j (o0) and j + 32 (o1).
+__device__ __forceinline__ void trunk(const Net& N, const double* W, double* x, int lane, double& o0,
+                                      double& o1) {
+#pragma unroll 1
+  for (int l = 0; l < 4; ++l) {
+    const int ni = N.in[l], no = N.out[l];
+    const double* Wl = W + N.w[l];
+    double a0 = lane < no ? W[N.b[l] + lane] : 0.0;
+    double a1 = lane + 32 < no ? W[N.b[l] + lane + 32] : 0.0;
+    const int j0 = lane < no ? lane : 0, j1 = lane + 32 < no ? lane + 32 : 0;
+#pragma unroll 4
+    for (int k = 0; k < ni; ++k) {  // column k of W (column-major, out rows)
+      const double xk = x[k];
+      a0 = fma(Wl[k * no + j0], xk, a0);
+      a1 = fma(Wl[k * no + j1], xk, a1);
+    }
+    if (l < 3) {  // ELU on the hidden layers (policy.cpp:13)
+      a0 = a0 > 0.0 ? a0 : expm1(a0);
+      a1 = a1 > 0.0 ? a1 : expm1(a1);
+    }
+    __syncwarp();
+    if (lane < no) x[lane] = a0;
+    if (lane + 32 < no) x[lane + 32] = a1;
+    __syncwarp();
+    o0 = a0;
+    o1 = a1;
+  }
+}
+
+__global__ void __launch_bounds__(32 * WARPS) forward_kernel(const PolicyParams P, const double* __restrict__ gw,
+                                                             int n, const double* __restrict__ obs,
+                                                             double* mean, double* value) {
+  extern __shared__ __align__(16) double sw[];
+  double* W = sw;                        // both trunks, P.total doubles
+  double* xs = sw + P.total;             // per warp: MAXIO input staging
+  for (int k = threadIdx.x; k < P.total; k += blockDim.x) W[k] = gw[k];
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* x = xs + warp * MAXIO;
+  for (int a = blockIdx.x * WARPS + warp; a < n; a += gridDim.x * WARPS) {
+    const double* o = obs + (size_t)a * P.obs;
+    double o0, o1;
+    if (mean) {
+      for (int k = lane; k < P.obs; k += 32) x[k] = o[k];
+      __syncwarp();
+      trunk(P.pi, W, x, lane, o0, o1);
+      if (lane < P.act) mean[(size_t)a * P.act + lane] = o0;
+    }
+    if (value) {
+      __syncwarp();
+      for (int k = lane; k < P.obs; k += 32) x[k] = o[k];
+      __syncwarp();
+      trunk(P.vf, W, x, lane, o0, o1);
+      if (lane == 0) value[a] = o0;
+    }
+    __syncwarp();
+  }
+}
+
+}  // namespace rmpc_policy_dev
+
+struct rmpc_policy {
+  int device = 0;
+  rmpc_policy_dev::PolicyParams P{};
+  double* d_w = nullptr;
+  int smem = 0, grid = 0;
+};
+
+extern "C" {
+
+int32_t rmpc_policy_create(int32_t obs_dim, int32_t act_dim, int32_t hidden, const double* params,
+                           int32_t n_params, int32_t device, rmpc_policy** out) {
+  using namespace rmpc_policy_dev;
+  if (!out || !params) return RMPC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (obs_dim < 1 || obs_dim > MAXIO || act_dim < 1 || act_dim > MAXH || hidden < 1 || hidden > MAXH)
+    return RMPC_ERR_STRUCTURAL;
+  rmpc_policy_dev::PolicyParams P{};
+  P.obs = obs_dim;
+  P.act = act_dim;
+  P.hidden = hidden;
+  int off = 0;
+  auto net = [&](Net& N, int out_dim) {
+    const int sizes[5] = {obs_dim, hidden, hidden, hidden, out_dim};  // init_policy, policy.cpp:69-76
+    for (int l = 0; l < 4; ++l) {
+      N.in[l] = sizes[l];
+      N.out[l] = sizes[l + 1];
+      N.w[l] = off;
+      off += sizes[l] * sizes[l + 1];
+      N.b[l] = off;
+      off += sizes[l + 1];
+    }
+  };
+  net(P.pi, act_dim);
+  net(P.vf, 1);
+  P.total = off;
+  if (n_params != off + act_dim) return RMPC_ERR_STRUCTURAL;  // + log_std
+  if (cudaSetDevice(device) != cudaSuccess) return RMPC_ERR_CUDA;
+  rmpc_policy* p = new (std::nothrow) rmpc_policy;
+  if (!p) return RMPC_ERR_CUDA;
+  p->device = device;
+  p->P = P;
+  p->smem = (P.total + WARPS * MAXIO) * (int)sizeof(double);
+  int sms = 148;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  p->grid = sms;
+  if (cudaMalloc(&p->d_w, P.total * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(p->d_w, params, P.total * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+      cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem) !=
+          cudaSuccess) {
+    cudaFree(p->d_w);
+    delete p;
+    return RMPC_ERR_CUDA;
+  }
+  *out = p;
+  return RMPC_OK;
+}
+
+void rmpc_policy_destroy(rmpc_policy* p) {
+  if (!p) return;
+  cudaSetDevice(p->device);
+  cudaFree(p->d_w);
+  delete p;
+}
+
+int32_t rmpc_policy_forward_device(rmpc_policy* p, int32_t n, const double* obs, double* mean, double* value,
+                                   void* stream) {
+  if (!p || n < 0 || (n > 0 && !obs)) return RMPC_ERR_INVALID_ARG;
+  if (n == 0 || (!mean && !value)) return RMPC_OK;
+  if (cudaSetDevice(p->device) != cudaSuccess) return RMPC_ERR_CUDA;
+  const int need = (n + rmpc_policy_dev::WARPS - 1) / rmpc_policy_dev::WARPS;
+  rmpc_policy_dev::forward_kernel<<<need < p->grid ? need : p->grid, 32 * rmpc_policy_dev::WARPS, p->smem,
+                                    stream ? (cudaStream_t)stream : cudaStreamLegacy>>>(p->P, p->d_w, n, obs,
+                                                                                         mean, value);
+  return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+}
+
+}  // extern "C"

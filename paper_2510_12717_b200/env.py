@@ -44,6 +44,12 @@ def _bind(L):
     L.rmpc_observe_device.restype = _I
     L.rmpc_plan_feedback_device.argtypes = [_I, _I, _VP, _VP, _VP, _VP, _D, _VP]
     L.rmpc_plan_feedback_device.restype = _I
+    L.rmpc_policy_create.argtypes = [_I, _I, _I, _VP, _I, _I, C.POINTER(_VP)]
+    L.rmpc_policy_create.restype = _I
+    L.rmpc_policy_destroy.argtypes = [_VP]
+    L.rmpc_policy_destroy.restype = None
+    L.rmpc_policy_forward_device.argtypes = [_VP, _I, _VP, _VP, _VP, _VP]
+    L.rmpc_policy_forward_device.restype = _I
     L.rmpc_env_sizeof.argtypes = [_I]
     L.rmpc_env_sizeof.restype = _I
     L._env_bound = True
@@ -133,3 +139,36 @@ def plan_feedback(z, solutions, states, gaits, horizon: int, dt: float = 0.01, s
                                      float(dt), _s(stream))
     if rc != 0:
         raise RmpcError(rc, "rmpc_plan_feedback_device failed")
+
+
+class Policy:
+    """Residual policy (policy_forward, policy.cpp:85-102) on the device, FP64.  `params` is the
+    flat PolicyParams vector in MlpParams::flatten_into order (pi, value, log_std)."""
+
+    def __init__(self, params, obs_dim: int = OBS_DIM, act_dim: int = 6, hidden: int = 64, device: int = 0):
+        import numpy as np
+        self._lib = _bind(library())
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        self.obs_dim, self.act_dim, self.hidden = obs_dim, act_dim, hidden
+        self.log_std = p[-act_dim:].copy()
+        h = _VP()
+        rc = self._lib.rmpc_policy_create(obs_dim, act_dim, hidden, p.ctypes.data, p.size, device, C.byref(h))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_policy_create failed (parameter count or dims)")
+        self._h = h
+
+    def close(self):
+        if getattr(self, "_h", None):
+            self._lib.rmpc_policy_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def forward(self, obs, mean=None, value=None, stream=None):
+        rc = self._lib.rmpc_policy_forward_device(self._h, obs.shape[0], _p(obs), _p(mean), _p(value), _s(stream))
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_policy_forward_device failed")

@@ -143,3 +143,19 @@ def test_closed_loop_on_device(oracle):
     assert ((sim == 1) == ~fin).all()
     assert (sol["status"][~fin] == R.STATUS_NONFINITE_INPUT).all()
     assert fin.mean() > 0.5
+
+
+def test_policy_forward_parity(oracle):
+    from paper_2510_12717_b200.env import Policy
+    params = oracle.init_policy(seed=3, zero_final=False)
+    n = 4096
+    obs = np.random.default_rng(10).uniform(-2, 2, (n, 23))
+    pol = Policy(params)
+    mean = torch.zeros((n, 6), dtype=torch.float64, device=DEV)
+    value = torch.zeros(n, dtype=torch.float64, device=DEV)
+    pol.forward(dev(obs), mean, value)
+    torch.cuda.synchronize()
+    rm, rv = oracle.policy_forward(params, obs)
+    np.testing.assert_allclose(mean.cpu().numpy(), rm, rtol=1e-12, atol=1e-13)
+    np.testing.assert_allclose(value.cpu().numpy(), rv, rtol=1e-12, atol=1e-13)
+    np.testing.assert_array_equal(pol.log_std, np.log(0.5))

@@ -166,3 +166,36 @@ def test_observe_layout(oracle):
     np.testing.assert_allclose(o[:, 20], np.sin(2 * np.pi * 0.3))
     np.testing.assert_allclose(o[:2, 22], 1e-2 * sols["v_mpc"][:2].astype(np.float64))
     assert o[2, 22] == 10.0
+
+
+def test_policy_init_and_forward(oracle):
+    """init_policy (policy.cpp:57-83): num_params, zero-initialised last policy layer (the
+    residual action is exactly zero at the start), log_std = log 0.5; mlp_forward restated
+    against a numpy evaluation of the same flattened (column-major) weights."""
+    p = oracle.init_policy()
+    sizes = [23, 64, 64, 64]
+    n_pi = sum(a * b + b for a, b in zip(sizes, sizes[1:] + [6]))
+    n_v = sum(a * b + b for a, b in zip(sizes, sizes[1:] + [1]))
+    assert p.size == n_pi + n_v + 6
+    np.testing.assert_array_equal(p[-6:], np.log(0.5))
+    obs = np.random.default_rng(0).uniform(-1, 1, (5, 23))
+    mean, value = oracle.policy_forward(p, obs)
+    assert not mean.any() and value.any()
+    q = oracle.init_policy(zero_final=False)
+    mean, value = oracle.policy_forward(q, obs)
+
+    def mlp(w, x, outs):
+        off = 0
+        for l, (i, o) in enumerate(zip(sizes, sizes[1:] + [outs])):
+            W = w[off:off + i * o].reshape(i, o).T  # column-major (out x in)
+            b = w[off + i * o:off + i * o + o]
+            off += i * o + o
+            x = W @ x + b
+            if l < 3:
+                x = np.where(x > 0, x, np.expm1(x))
+        return x, off
+    for k in range(5):
+        m_np, off = mlp(q, obs[k], 6)
+        v_np, _ = mlp(q[off:], obs[k], 1)
+        np.testing.assert_allclose(mean[k], m_np, rtol=1e-12, atol=1e-14)
+        np.testing.assert_allclose(value[k], v_np[0], rtol=1e-12, atol=1e-14)

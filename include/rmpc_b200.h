@@ -169,8 +169,11 @@ const char* rmpc_build_info(void);
 /* Measured FP32 FMA throughput of `device` (TFLOP/s): the CUDA-core roofline denominator. */
 int32_t rmpc_fma_peak(int32_t device, double* tflops);
 
-/* Dynamic shared memory one agent (one CTA) needs at `horizon` nodes. */
+/* Dynamic shared memory one agent (one warp pair) needs at `horizon` nodes. */
 int32_t rmpc_smem_bytes(int32_t horizon);
+/* Agents per CTA (= per SM: one CTA per SM) at `horizon` nodes, bounded by the 512 TMEM columns
+ * that hold the factor, the 227 KB of shared memory and 6 warp pairs (384 threads). */
+int32_t rmpc_agents_per_cta(int32_t horizon);
 /* sizeof of the ABI structs (0 model, 1 settings, 2 state, 3 command, 4 gait, 5 solution,
  * 6 timing) for binding-side layout checks. */
 int32_t rmpc_sizeof(int32_t which);

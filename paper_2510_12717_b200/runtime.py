@@ -29,7 +29,7 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_solve", "rmpc_solve_device", "rmpc_size", "rmpc_workers", "rmpc_horizon",
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
-           "rmpc_smem_bytes", "rmpc_sizeof", "rmpc_fma_peak")
+           "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak")
 
 
 class RmpcError(RuntimeError):

@@ -72,11 +72,18 @@ def test_stage_names_and_status_messages():
     assert b"sm_100a" in L.rmpc_build_info()
 
 
-def test_smem_budget_allows_four_agents_per_sm_at_n10():
-    """4 CTAs x (dynamic smem + 1 KB reserved) must fit the 228 KB SM carve-out at N=10."""
+def test_cta_shape_six_agents_per_sm_at_n10():
+    """T=10: 6 warp pairs per CTA (TMEM: 3 warps x 160 columns per lane quarter), their shared
+    memory within 227 KB; every horizon up to 32 gets at least one agent pair's worth."""
     L = R.library()
-    assert 4 * (L.rmpc_smem_bytes(10) + 1024) <= 228 * 1024
-    assert L.rmpc_smem_bytes(32) <= 227 * 1024
+    L.rmpc_agents_per_cta.argtypes = [C.c_int32]
+    assert L.rmpc_agents_per_cta(10) == 6
+    assert 6 * L.rmpc_smem_bytes(10) <= 227 * 1024 - 128
+    assert L.rmpc_agents_per_cta(20) == 2 and L.rmpc_agents_per_cta(32) == 2
+    for T in range(2, 33):
+        A = L.rmpc_agents_per_cta(T)
+        assert 1 <= A <= 6 and A * L.rmpc_smem_bytes(T) <= 227 * 1024 - 128
+    assert L.rmpc_agents_per_cta(0) == -1 and L.rmpc_agents_per_cta(33) == -1
 
 
 def test_mpc_torque_matches_oracle_pd(oracle):

@@ -22,7 +22,9 @@ def run_both(oracle, kind, T, n, seed=1, workers=16):
 
 @pytest.mark.parametrize("kind,T,n", [("standing", 10, 1), ("standing", 12, 8), ("random", 10, 4096),
                                       ("random", 5, 2048), ("random", 20, 1024),
-                                      ("mixed", 10, 2048), ("random", 12, 512)])
+                                      ("mixed", 10, 2048), ("random", 12, 512),
+                                      ("random", 2, 256), ("mixed", 3, 256), ("random", 31, 64),
+                                      ("mixed", 32, 64), ("random", 10, 7)])
 def test_parity_with_oracle(oracle, kind, T, n):
     sol, z, ref, zr, _ = run_both(oracle, kind, T, n)
     c = compare(sol, ref, z, zr)

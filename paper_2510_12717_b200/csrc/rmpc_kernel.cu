@@ -504,7 +504,9 @@ __device__ __forceinline__ void set_row(float4* r, double lo, double hi) {
 // Lane i < NT builds node i of the QP (build_qp, mpc.cpp:64-238) in FP64 and stores the
 // unscaled coefficients, bounds and q in shared memory.  Returns false if the linearization
 // point is non-finite (StructuralError, mpc.cpp:70-72).
-__device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc_state& st,
+// The two warps split a node's work (both recompute the schedule, guess and FK frames):
+// warp 1 the base-dynamics rows (the 7-link M/h sums) and q^, warp 0 everything else.
+__device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, const rmpc_state& st,
                             const rmpc_command& cmd, const rmpc_gait& gait, bool warm,
                             const float* pz) {
   const int NT = P.NT;
@@ -521,7 +523,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
     for (int k = 0; k < 9; ++k) ok = ok && isfinite(gq[k]) && isfinite(gqd[k]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) ok = ok && isfinite(gF[k]);
-    sm.flags[i] = bits;
+    if (warp == 0) sm.flags[i] = bits;
     float* cf = sm.C(i);
     float4* rw = sm.R(i);
     const double dt = P.dt[i];
@@ -532,7 +534,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
 #pragma unroll
     for (int c = 0; c < 4; ++c) contact_jac(F, c, Jx[c], Jz[c]);
 
-    {  // q = w dt (guess - desired)  (mpc.cpp:81-103)
+    if (warp == 1) {  // q = w dt (guess - desired)  (mpc.cpp:81-103)
       float* qh = sm.V(i, V_QH);
 #pragma unroll 1
       for (int j = 0; j < NV; ++j) {
@@ -541,7 +543,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
         qh[j] = to_f(wcost(P, j) * dt * (g - des));
       }
     }
-    if (i + 1 < NT) {
+    if (warp == 0 && i + 1 < NT) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) {  // integration (mpc.cpp:138-148)
         cf[C_A1 + k] = 1.f;
@@ -550,6 +552,8 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
         const double r = -(nq[k] - gq[k] - dt * nqd[k]);
         set_row(rw + k, r, r);
       }
+    }
+    if (warp == 1 && i + 1 < NT) {
       double Mb[3][9], hb[3];  // base dynamics with qdd eliminated (mpc.cpp:150-175)
       base_dynamics(P, gqd, F, Mb, hb);
       const double dt_inv = 1.0 / dt;
@@ -576,6 +580,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
         set_row(rw + 9 + b, -resid, -resid);
       }
     }
+    if (warp == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {  // contacts (mpc.cpp:181-218)
       const double fx = gF[2 * c], fz = gF[2 * c + 1];
@@ -632,6 +637,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc
         set_row(ri + 9 + k, rqd, rqd);
       }
     }
+    }  // warp 0
   }
   return __all_sync(FULL, ok);
 }
@@ -1430,7 +1436,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   pair_sync(sm);
 
   int ok = 1;
-  if (warp == 0) ok = setup_nodes(P, sm, lane, st, cmd, gait, warm, pz) && st_ok;
+  ok = setup_nodes(P, sm, lane, warp, st, cmd, gait, warm, pz) && st_ok;
   ok = pair_and(sm, ok);
   prof_mark(P, tid, 2, t0);
   if (!ok) {

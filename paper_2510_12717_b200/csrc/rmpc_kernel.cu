@@ -316,15 +316,13 @@ __device__ __forceinline__ void row_view(const Sm& sm, int i, int lane, int whic
 // ------------------------------------------------------------------------- FP64 kinematics
 // Fr, attach, kchain, Frames, fk_frames, contact_jac: rmpc_kin.cuh (shared with rmpc_env.cu).
 
-// Top three rows of M (robot.cpp:169-178) and of h (robot.cpp:184-195).
-__device__ void base_dynamics(const KParams& P, const double* qd, const Frames& F,
-                              double Mb[3][9], double hb[3]) {
+
+// Row b (< 3) of M (robot.cpp:169-178) and h (robot.cpp:184-195): one lane per (node, row).
+__device__ void base_dynamics_row(const KParams& P, const double* qd, const Frames& F, int b,
+                                  double Mr[9], double& hr) {
+  hr = 0.0;
 #pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    hb[b] = 0.0;
-#pragma unroll
-    for (int k = 0; k < 9; ++k) Mb[b][k] = 0.0;
-  }
+  for (int k = 0; k < 9; ++k) Mr[k] = 0.0;
 #pragma unroll
   for (int l = 0; l < 7; ++l) {
     double Jx[9], Jz[9];
@@ -344,16 +342,17 @@ __device__ void base_dynamics(const KParams& P, const double* qd, const Frames& 
       }
     }
     const double m = P.m_link[l];
+    const double jxb = b == 0 ? Jx[0] : (b == 1 ? Jx[1] : Jx[2]);
+    const double jzb = b == 0 ? Jz[0] : (b == 1 ? Jz[1] : Jz[2]);
 #pragma unroll
-    for (int b = 0; b < 3; ++b) {
+    for (int k = 0; k < 9; ++k) Mr[k] += m * (jxb * Jx[k] + jzb * Jz[k]);
+    hr += m * (jxb * ax + jzb * (az + P.gravity));
+    if (b == 2) {  // rotational part: coordinate 2 is in every chain
 #pragma unroll
-      for (int k = 0; k < 9; ++k) Mb[b][k] += m * (Jx[b] * Jx[k] + Jz[b] * Jz[k]);
-      hb[b] += m * (Jx[b] * ax + Jz[b] * (az + P.gravity));
-    }
-#pragma unroll
-    for (int s = 0; s < 4; ++s) {  // rotational part: coordinate 2 is in every chain
-      const int a = kchain(l, s);
-      if (a >= 0) Mb[2][a] += P.I_link[l];
+      for (int s = 0; s < 4; ++s) {
+        const int a = kchain(l, s);
+        if (a >= 0) Mr[a] += P.I_link[l];
+      }
     }
   }
 }
@@ -504,9 +503,9 @@ __device__ __forceinline__ void set_row(float4* r, double lo, double hi) {
 // Lane i < NT builds node i of the QP (build_qp, mpc.cpp:64-238) in FP64 and stores the
 // unscaled coefficients, bounds and q in shared memory.  Returns false if the linearization
 // point is non-finite (StructuralError, mpc.cpp:70-72).
-// The two warps split a node's work (both recompute the schedule, guess and FK frames):
-// warp 1 the base-dynamics rows (the 7-link M/h sums) and q^, warp 0 everything else.
-__device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, const rmpc_state& st,
+// Warp 0's share: lane i < NT builds node i's integration, contact, box and initial-state rows
+// (setup_dynamics below builds the base-dynamics rows and q^ on warp 1).
+__device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, const rmpc_state& st,
                             const rmpc_command& cmd, const rmpc_gait& gait, bool warm,
                             const float* pz) {
   const int NT = P.NT;
@@ -523,7 +522,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, 
     for (int k = 0; k < 9; ++k) ok = ok && isfinite(gq[k]) && isfinite(gqd[k]);
 #pragma unroll
     for (int k = 0; k < 8; ++k) ok = ok && isfinite(gF[k]);
-    if (warp == 0) sm.flags[i] = bits;
+    sm.flags[i] = bits;
     float* cf = sm.C(i);
     float4* rw = sm.R(i);
     const double dt = P.dt[i];
@@ -534,16 +533,7 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, 
 #pragma unroll
     for (int c = 0; c < 4; ++c) contact_jac(F, c, Jx[c], Jz[c]);
 
-    if (warp == 1) {  // q = w dt (guess - desired)  (mpc.cpp:81-103)
-      float* qh = sm.V(i, V_QH);
-#pragma unroll 1
-      for (int j = 0; j < NV; ++j) {
-        double g, des;
-        guess_and_target(P, i, j, warm, pz, st, cmd, bits, g, des);
-        qh[j] = to_f(wcost(P, j) * dt * (g - des));
-      }
-    }
-    if (warp == 0 && i + 1 < NT) {
+    if (i + 1 < NT) {
 #pragma unroll
       for (int k = 0; k < 9; ++k) {  // integration (mpc.cpp:138-148)
         cf[C_A1 + k] = 1.f;
@@ -553,34 +543,6 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, 
         set_row(rw + k, r, r);
       }
     }
-    if (warp == 1 && i + 1 < NT) {
-      double Mb[3][9], hb[3];  // base dynamics with qdd eliminated (mpc.cpp:150-175)
-      base_dynamics(P, gqd, F, Mb, hb);
-      const double dt_inv = 1.0 / dt;
-#pragma unroll
-      for (int b = 0; b < 3; ++b) {
-        double mq = 0.0;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) mq += Mb[b][k] * (nqd[k] - gqd[k]);
-        double jbf = 0.0;
-#pragma unroll
-        for (int c = 0; c < 4; ++c) jbf += Jx[c][b] * gF[2 * c] + Jz[c][b] * gF[2 * c + 1];
-        const double resid = mq * dt_inv + hb[b] - jbf;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          const double mv = Mb[b][k] * dt_inv;
-          cf[C_DYNU + 12 * b + k] = to_f(mv);
-          cf[C_DYNV + 20 * b + k] = to_f(-mv);
-        }
-#pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          cf[C_DYNV + 20 * b + 9 + 2 * c] = to_f(-Jx[c][b]);
-          cf[C_DYNV + 20 * b + 10 + 2 * c] = to_f(-Jz[c][b]);
-        }
-        set_row(rw + 9 + b, -resid, -resid);
-      }
-    }
-    if (warp == 0) {
 #pragma unroll
     for (int c = 0; c < 4; ++c) {  // contacts (mpc.cpp:181-218)
       const double fx = gF[2 * c], fz = gF[2 * c + 1];
@@ -637,7 +599,79 @@ __device__ bool setup_nodes(const KParams& P, const Sm& sm, int lane, int warp, 
         set_row(ri + 9 + k, rqd, rqd);
       }
     }
-    }  // warp 0
+  }
+  return __all_sync(FULL, ok);
+}
+
+// Warp 1's share of the setup: the base-dynamics rows of every interval with qdd eliminated
+// (mpc.cpp:150-175), one lane per (node, row b), and q^ = w dt (guess - desired)
+// (mpc.cpp:81-103), one lane per node.
+__device__ bool setup_dynamics(const KParams& P, const Sm& sm, int lane, const rmpc_state& st,
+                               const rmpc_command& cmd, const rmpc_gait& gait, bool warm,
+                               const float* pz) {
+  const int NT = P.NT;
+  bool ok = true;
+  uint32_t* bits_of = reinterpret_cast<uint32_t*>(sm.scr);  // scratch is free until Ruiz
+  for (int i = lane; i < NT; i += 32) {
+    double swt[4];
+    bits_of[i] = node_schedule(P, gait, i, swt);
+  }
+  __syncwarp();
+  // one lane per (node, row) while that fits the warp, else one lane per node (FK once)
+  const bool split = 3 * (NT - 1) <= 32;
+#pragma unroll 1
+  for (int t = lane; t < (split ? 3 : 1) * (NT - 1); t += 32) {
+    const int i = t % (NT - 1);
+    const int b0 = split ? t / (NT - 1) : 0, b1 = split ? b0 + 1 : 3;
+    const uint32_t bits = bits_of[i], bits_n = bits_of[i + 1];
+    double gq[9], gqd[9], gF[8], nq[9], nqd[9], nF[8];
+    node_guess(P, i, warm, pz, st, bits, gq, gqd, gF);
+    node_guess(P, i + 1, warm, pz, st, bits_n, nq, nqd, nF);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) ok = ok && isfinite(gq[k]) && isfinite(gqd[k]);
+    Frames F;
+    fk_frames(P, gq, gqd, F);
+    const double dt_inv = 1.0 / P.dt[i];
+#pragma unroll 1
+    for (int b = b0; b < b1; ++b) {
+    double Mr[9], hr;
+    base_dynamics_row(P, gqd, F, b, Mr, hr);
+    double mq = 0.0;
+#pragma unroll
+    for (int k = 0; k < 9; ++k) mq += Mr[k] * (nqd[k] - gqd[k]);
+    // column b of the contact Jacobians: b = 0, 1 base translation, b = 2 pitch (robot.cpp:98)
+    double jbf = 0.0, jx[4], jz[4];
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      jx[c] = b == 0 ? 1.0 : (b == 1 ? 0.0 : -(F.con[c].pz - F.piv[2].pz));
+      jz[c] = b == 0 ? 0.0 : (b == 1 ? 1.0 : F.con[c].px - F.piv[2].px);
+      jbf += jx[c] * gF[2 * c] + jz[c] * gF[2 * c + 1];
+    }
+    const double resid = mq * dt_inv + hr - jbf;
+    float* cf = sm.C(i);
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      const double mv = Mr[k] * dt_inv;
+      cf[C_DYNU + 12 * b + k] = to_f(mv);
+      cf[C_DYNV + 20 * b + k] = to_f(-mv);
+    }
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      cf[C_DYNV + 20 * b + 9 + 2 * c] = to_f(-jx[c]);
+      cf[C_DYNV + 20 * b + 10 + 2 * c] = to_f(-jz[c]);
+    }
+    set_row(sm.R(i) + 9 + b, -resid, -resid);
+    }
+  }
+#pragma unroll 1
+  for (int i = lane; i < NT; i += 32) {
+    float* qh = sm.V(i, V_QH);
+#pragma unroll 1
+    for (int j = 0; j < NV; ++j) {
+      double g, des;
+      guess_and_target(P, i, j, warm, pz, st, cmd, bits_of[i], g, des);
+      qh[j] = to_f(wcost(P, j) * P.dt[i] * (g - des));
+    }
   }
   return __all_sync(FULL, ok);
 }
@@ -1436,7 +1470,8 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   pair_sync(sm);
 
   int ok = 1;
-  ok = setup_nodes(P, sm, lane, warp, st, cmd, gait, warm, pz) && st_ok;
+  ok = (warp == 0 ? setup_nodes(P, sm, lane, st, cmd, gait, warm, pz)
+                  : setup_dynamics(P, sm, lane, st, cmd, gait, warm, pz)) && st_ok;
   ok = pair_and(sm, ok);
   prof_mark(P, tid, 2, t0);
   if (!ok) {

@@ -1199,7 +1199,7 @@ __device__ __forceinline__ bool node_rows(const Sm& sm, int lane, int i, const f
 }
 
 // AdmmSolver::run (qp.cpp:156-190): exactly n_qp iterations from x = y = z = 0.  Returns the
-// first iteration with a non-finite iterate, or -1 (CTA-uniform).
+// first iteration with a non-finite iterate, or -1 (pair-uniform).
 //
 // Two-sided solve of H x~ = r (factorize): warp 0 owns nodes [0, m) and the middle node m,
 // warp 1 owns (m, T); each warp also does the node-local work of its nodes (r_i from the
@@ -1264,6 +1264,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     return rho * (f_q * cf[C_A2 + kq] * gint +
                   f_dv * (cf[C_DYNV + jv] * g0 + cf[C_DYNV + 20 + jv] * g1 + cf[C_DYNV + 40 + jv] * g2));
   };
+  int first_bad = 0x7fffffff;  // this lane's first iteration with a non-finite value
 #pragma unroll 1
   for (int it = 0; it < P.n_qp; ++it) {
     const bool first = it == 0;  // x = y = z = 0: r = -q^
@@ -1400,9 +1401,18 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         bad = finish_node(i) || bad;
       }
     }
-    if (pair_or(sm, bad)) return it;
+    // no barrier between iterations: the halves exchange data only at the middle (the two
+    // barriers above order every cross-half access), so a non-finite iterate is recorded here
+    // and the pair agrees on the first one after the loop (qp.cpp:159-161 reports the first).
+    if (bad && first_bad > it) first_bad = it;
   }
-  return -1;
+  const int wfirst = __reduce_min_sync(FULL, first_bad);
+  int* fb = reinterpret_cast<int*>(sm.bc);  // the broadcast buffers are free after the loop
+  pair_sync(sm);
+  if (lane == 0) fb[warp] = wfirst;
+  pair_sync(sm);
+  const int f = fb[0] < fb[1] ? fb[0] : fb[1];
+  return f == 0x7fffffff ? -1 : f;
 }
 
 // ------------------------------------------------------------------------- kernel

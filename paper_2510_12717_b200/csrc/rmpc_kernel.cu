@@ -1311,7 +1311,8 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     pair_sync(sm);
     // ---------------------------------------------------------------- backward
     if (warp == 0) {
-      bad = finish_node(m) || bad;
+      // software-pipelined: step i's TMEM row and xi are loaded before node i+1's own rows
+      // (finish_node, independent of step i) are updated, and consumed after
 #pragma unroll 1
       for (int i = m - 1; i >= 0; --i) {
         const float* cf = sm.C(i);
@@ -1333,26 +1334,35 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         // lanes < 26: row j of S^-1 (cols 0..8 = column j) and W_b[j];  26..28: W_b, G_b
         float v[TCOLS];
         tm_load(sm.Tm(i), v);
+        float xi[12];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) xi[k] = xib[k];
+        float wg[3];
+#pragma unroll
+        for (int b = 0; b < 3; ++b) wg[b] = lane < NV ? v[NV + b] : cf[C_G + 3 * bw + b];
+        const float vsl = vs[lane < NV ? lane : 0], gam = gamma_of(i);
+        bad = finish_node(i + 1) || bad;
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; k += 2) {
-          acc0 = fmaf(v[k], xib[k], acc0);
-          if (k + 1 < 9) acc1 = fmaf(v[k + 1], xib[k + 1], acc1);
+          acc0 = fmaf(v[k], xi[k], acc0);
+          if (k + 1 < 9) acc1 = fmaf(v[k + 1], xi[k + 1], acc1);
         }
 #pragma unroll
-        for (int b = 0; b < 3; ++b) acc1 = fmaf(lane < NV ? v[NV + b] : cf[C_G + 3 * bw + b], xib[9 + b], acc1);
+        for (int b = 0; b < 3; ++b) acc1 = fmaf(wg[b], xi[9 + b], acc1);
         const float acc = acc0 + acc1;
-        const float xt = is_var ? vs[lane] - rho * acc : 0.f;
+        const float xt = is_var ? vsl - rho * acc : 0.f;
         if (is_var) vs[lane] = xt;
         bad = bad || !isfinite(xt);
         // z~: integration row k (lane k) = a2 x~_i[q_k] + dl ; dynamics row b (lane 26+b) =
         // v_b.x~_i + u_b.x~_{i+1} = g_b - rho acc + xi_b
-        const float zt = is_q ? fmaf(cf[C_A2 + kq], xt, dl) : gamma_of(i) - rho * acc + xib[9 + bw];
+        const float xib_b = bw == 0 ? xi[9] : (bw == 1 ? xi[10] : xi[11]);
+        const float zt = is_q ? fmaf(cf[C_A2 + kq], xt, dl) : gam - rho * acc + xib_b;
         const int slot = is_q ? kq : 9 + bw;
         bad = !row_update(sm.R(i) + slot, sm.T(i) + slot, is_q || is_w, zt, K.alpha, K.oma, K.rho, K.rho_inv) || bad;
         __syncwarp();
-        bad = finish_node(i) || bad;
       }
+      bad = finish_node(0) || bad;  // nodes m..1 were finished inside the loop
     } else {
 #pragma unroll 1
       for (int i = m + 1; i < NT; ++i) {

@@ -109,6 +109,17 @@ __device__ __forceinline__ void tm_load(uint32_t a, float v[TCOLS]) {
                : "r"(a));
   asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 }
+// Split form: issue the load, do independent work, then wait (v is tied to the wait so the
+// compiler cannot consume it earlier).
+__device__ __forceinline__ void tm_load_issue(uint32_t a, float v[TCOLS]) {
+  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " RMPC_OPS32 ", [%32];"
+               : RMPC_X32(RMPC_OUT, v)
+               : "r"(a));
+}
+#define RMPC_INOUT(x) "+f"(x)
+__device__ __forceinline__ void tm_load_wait(float v[TCOLS]) {
+  asm volatile("tcgen05.wait::ld.sync.aligned;" : RMPC_X32(RMPC_INOUT, v)::"memory");
+}
 __device__ __forceinline__ void tm_store(uint32_t a, const float v[TCOLS]) {
   asm volatile("tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], " RMPC_OPS32_1 ";"
                ::"r"(a), RMPC_X32(RMPC_IN, v)
@@ -1160,6 +1171,24 @@ __device__ __forceinline__ float ext_mv(uint32_t a, int lane, float* buf, float 
   return lane < SROWS ? (a0 + a1) + (a2 + a3) : 0.f;
 }
 
+// The matvec half of ext_mv on an already loaded block row v (u published in buf).
+__device__ __forceinline__ float block_row_dot(const float v[TCOLS], const float* buf, int lane) {
+  const float4* b4 = reinterpret_cast<const float4*>(buf);
+  float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
+#pragma unroll
+  for (int q = 0; q < 6; ++q) {
+    const float4 bb = b4[q];
+    a0 = fmaf(v[4 * q], bb.x, a0);
+    a1 = fmaf(v[4 * q + 1], bb.y, a1);
+    a2 = fmaf(v[4 * q + 2], bb.z, a2);
+    a3 = fmaf(v[4 * q + 3], bb.w, a3);
+  }
+  const float2 bb = reinterpret_cast<const float2*>(buf)[12];
+  a0 = fmaf(v[24], bb.x, a0);
+  a1 = fmaf(v[25], bb.y, a1);
+  return lane < SROWS ? (a0 + a1) + (a2 + a3) : 0.f;
+}
+
 struct AdmmConst {
   float rho, sigma, alpha, oma, rho_inv;
 };
@@ -1271,11 +1300,21 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     bool bad = false;
     // ---------------------------------------------------------------- forward
     float gint = 0.f, g0 = 0.f, g1 = 0.f, g2 = 0.f;  // g of the last eliminated node
+    // software-pipelined: r of the next node is gathered while this node's TMEM row loads
+    // (the middle's r waits for the barrier: the bottom half's previous backward writes the
+    // interval-m rows it reads)
+    float rc = warp == 0 ? (m > 0 ? r_of(0, first) : 0.f) : (NT - 1 > m ? r_of(NT - 1, first) : 0.f);
     if (warp == 0) {
 #pragma unroll 1
       for (int i = 0; i < m; ++i) {
-        const float u = r_of(i, first) - top_corr(sm.C(i - 1), gint, g0, g1, g2);
-        const float s = ext_mv(sm.Tm(i), lane, ubuf, u);
+        const float u = rc - top_corr(sm.C(i - 1), gint, g0, g1, g2);
+        ubuf[lane] = lane < NV ? u : 0.f;
+        float v[TCOLS];
+        tm_load_issue(sm.Tm(i), v);
+        if (i + 1 < m) rc = r_of(i + 1, first);
+        tm_load_wait(v);
+        __syncwarp();
+        const float s = block_row_dot(v, ubuf, lane);
         store_s(i, s);
         gint = f_q * sm.C(i)[C_A2 + kq] * s;
         g0 = __shfl_sync(FULL, s, 26);
@@ -1286,8 +1325,14 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     } else {
 #pragma unroll 1
       for (int i = NT - 1; i > m; --i) {
-        const float u = r_of(i, first) - bot_corr(sm.C(i), gint, g0, g1, g2);
-        const float s = ext_mv(sm.Tm(i), lane, ubuf, u);
+        const float u = rc - bot_corr(sm.C(i), gint, g0, g1, g2);
+        ubuf[lane] = lane < NV ? u : 0.f;
+        float v[TCOLS];
+        tm_load_issue(sm.Tm(i), v);
+        if (i - 1 > m) rc = r_of(i - 1, first);
+        tm_load_wait(v);
+        __syncwarp();
+        const float s = block_row_dot(v, ubuf, lane);
         store_s(i, s);
         const float* cp = sm.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
         const float sq = __shfl_down_sync(FULL, s, 9);

@@ -859,49 +859,61 @@ __device__ __forceinline__ void assemble_diag(const KParams& P, const Sm& sm, in
   }
 }
 
-// In-place Gauss-Jordan inverse of the SPD block held row-wise by the warp (lane j: row j);
-// pivot rows are exchanged through `bc` (2 x 32 floats).  Returns false on a pivot <= 0.
-__device__ __forceinline__ bool gauss_jordan(int j, float S[NV], float* bc) {
+// In-place Gauss-Jordan inverse of the SPD block held row-wise by the warp (lane j: row j),
+// pivot rows exchanged through shared memory.  Returns false on a non-positive pivot.
+// 2 x 2 pivot blocks: 13 elimination steps instead of 26 (the step's
+// latency -- pivot rows through shared memory, one reciprocal -- is what bounds the
+// factorization).  Pivot rows k, k+1 go through `buf` (>= 112 floats, the warp's G scratch,
+// double-buffered).  Block GJ on [[a, b], [c, d]] = S[k:k+2, k:k+2] with P = its inverse:
+//   rows j != k, k+1:  S_j -= (f P) [R_k; R_k+1],  S_j[k:k+2] = -(f P),   f = S_j[k:k+2]
+//   rows k, k+1:       [R_k; R_k+1] <- P [R_k; R_k+1],  S[k:k+2, k:k+2] = P
+// written as one FMA pair per element for every lane (the pivot rows hold S_j = R_k / R_k+1).
+// A 2 x 2 pivot block of an SPD matrix is PD: a > 0 and det > 0 (both LDL^T pivots positive,
+// the reference's SingularityError test, ldl.cpp:155-160).
+__device__ __forceinline__ bool gauss_jordan2(int j, float S[NV], float* buf) {
   bool good = true;
 #pragma unroll
-  for (int k = 0; k < NV; ++k) {
-    float* buf = bc + 32 * (k & 1);
-    if (j == k) {
-      float4* b4 = reinterpret_cast<float4*>(buf);
+  for (int p = 0; p < NV / 2; ++p) {
+    const int k = 2 * p;
+    float* bb = buf + 56 * (p & 1);
+    if (j == k || j == k + 1) {
+      float4* b4 = reinterpret_cast<float4*>(bb + 28 * (j - k));
 #pragma unroll
       for (int q = 0; q < 6; ++q) b4[q] = make_float4(S[4 * q], S[4 * q + 1], S[4 * q + 2], S[4 * q + 3]);
-      reinterpret_cast<float2*>(buf)[12] = make_float2(S[24], S[25]);
+      reinterpret_cast<float2*>(bb + 28 * (j - k))[12] = make_float2(S[24], S[25]);
     }
     __syncwarp();
-    float R[NV];
-    {
-      const float4* b4 = reinterpret_cast<const float4*>(buf);
+    float R0[NV], R1[NV];
+#pragma unroll
+    for (int r = 0; r < 2; ++r) {
+      const float4* b4 = reinterpret_cast<const float4*>(bb + 28 * r);
+      float* R = r == 0 ? R0 : R1;
 #pragma unroll
       for (int q = 0; q < 6; ++q) {
         const float4 w = b4[q];
         R[4 * q] = w.x; R[4 * q + 1] = w.y; R[4 * q + 2] = w.z; R[4 * q + 3] = w.w;
       }
-      const float2 w = reinterpret_cast<const float2*>(buf)[12];
+      const float2 w = reinterpret_cast<const float2*>(bb + 28 * r)[12];
       R[24] = w.x;
       R[25] = w.y;
     }
-    const float p = R[k];
-    good = good && (p > 0.f);
-    const float pinv = __frcp_rn(p);  // == 1.f / p
-    const float f = S[k];
-    const bool me = (j == k);
-    // the pivot row holds S == R: (pinv - 1) R + R scales it by pinv in the same FMA
-    const float alpha = me ? pinv - 1.f : -f * pinv;
+    const float a = R0[k], b = R0[k + 1], c = R1[k], d = R1[k + 1];
+    const float det = fmaf(a, d, -b * c);
+    good = good && a > 0.f && det > 0.f;
+    const float idet = __frcp_rn(det);
+    const float p00 = d * idet, p01 = -b * idet, p10 = -c * idet, p11 = a * idet;
+    const float f0 = S[k], f1 = S[k + 1];
+    const bool m0 = j == k, m1 = j == k + 1;
+    const float al0 = m0 ? 1.f - p00 : (m1 ? -p10 : fmaf(f0, p00, f1 * p10));
+    const float al1 = m0 ? -p01 : (m1 ? 1.f - p11 : fmaf(f0, p01, f1 * p11));
 #pragma unroll
-    for (int l = 0; l < NV; ++l) S[l] = fmaf(alpha, R[l], S[l]);
-    S[k] = me ? pinv : -f * pinv;
+    for (int l = 0; l < NV; ++l) S[l] = fmaf(-al0, R0[l], fmaf(-al1, R1[l], S[l]));
+    S[k] = m0 ? p00 : (m1 ? p10 : -al0);
+    S[k + 1] = m0 ? p01 : (m1 ? p11 : -al1);
   }
   return good;
 }
 
-// Node block in TMEM (TCOLS columns of the owning warp's lane quarter): lane j < 26 holds row
-// j of the inverse in columns 0..25 and W_b[j] in columns 26..28; lanes 26..28 hold W_b^T in
-// columns 0..25 (transposed through `tr`, >= 96 floats of the warp's scratch).
 __device__ __forceinline__ void store_block(uint32_t a, int j, const float S[NV], const float W[3], float* tr) {
 #pragma unroll
   for (int b = 0; b < 3; ++b) tr[32 * b + j] = W[b];
@@ -1111,7 +1123,7 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
 #pragma unroll
     for (int l = 0; l < NV; ++l) S[l] -= Y[l];
     __syncwarp();
-    good = gauss_jordan(j, S, bc) && good;
+    good = gauss_jordan2(j, S, sm.scr + G_SCR * warp) && good;
     if (middle) {
       const float W0[3] = {0.f, 0.f, 0.f};
       store_block(sm.Tm(i), j, S, W0, sm.scr);

@@ -948,6 +948,17 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
     W[b] = j < NV ? acc : 0.f;
   }
   store_block(sm.Tm(i), j, S, W, G);
+  // G_dd[b][b2] = v_b . W_b2 over node vars 9..25, lane 3 b + b2 < 9, from W^T still in G
+  const int gb = j < 9 ? j / 3 : 0, gb2 = j < 9 ? j % 3 : 0;
+  float gacc0 = 0.f, gacc1 = 0.f;
+#pragma unroll
+  for (int l = 0; l < 17; l += 2) {
+    gacc0 = fmaf(cf[C_DYNV + 20 * gb + l], G[32 * gb2 + 9 + l], gacc0);
+    if (l + 1 < 17) gacc1 = fmaf(cf[C_DYNV + 20 * gb + l + 1], G[32 * gb2 + 10 + l], gacc1);
+  }
+  const float gacc = gacc0 + gacc1;
+  const float gv = 0.5f * (gacc + __shfl_sync(FULL, gacc, 3 * gb2 + gb));
+  __syncwarp();  // W^T read before G overwrites it
   if (j < 9) {
     const float a2 = cf[C_A2 + j];
 #pragma unroll
@@ -958,22 +969,9 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
       G[(9 + b) * 13 + j] = a2 * W[b];
     }
   }
-  float gdd[3][3];
-#pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    const float vb = (j >= 9 && j < NV) ? cf[C_DYNV + 20 * b + j - 9] : 0.f;
-#pragma unroll
-    for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(vb * W[b2]);
-  }
-  if (j == 0) {
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-      for (int b2 = 0; b2 < 3; ++b2) {
-        const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
-        G[(9 + b) * 13 + 9 + b2] = gv;
-        sm.C(i)[C_G + 3 * b + b2] = gv;
-      }
+  if (j < 9) {
+    G[(9 + gb) * 13 + 9 + gb2] = gv;
+    sm.C(i)[C_G + 3 * gb + gb2] = gv;
   }
   __syncwarp();
   float Z[12];
@@ -1046,6 +1044,17 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
     W[b] = j < NV ? acc : 0.f;
   }
   store_block(sm.Tm(i), j, S, W, G);
+  // G'_dd[b][b2] = u_b . W'_b2 over qd (node vars 9..17), lane 3 b + b2 < 9
+  const int gb = j < 9 ? j / 3 : 0, gb2 = j < 9 ? j % 3 : 0;
+  float gacc0 = 0.f, gacc1 = 0.f;
+#pragma unroll
+  for (int l = 0; l < 9; l += 2) {
+    gacc0 = fmaf(cp[C_DYNU + 12 * gb + l], G[32 * gb2 + 9 + l], gacc0);
+    if (l + 1 < 9) gacc1 = fmaf(cp[C_DYNU + 12 * gb + l + 1], G[32 * gb2 + 10 + l], gacc1);
+  }
+  const float gacc = gacc0 + gacc1;
+  const float gv = 0.5f * (gacc + __shfl_sync(FULL, gacc, 3 * gb2 + gb));
+  __syncwarp();  // W'^T read before G overwrites it
   // int-int / int-dyn parts: lane k (row k) and lane 9+k (row 9+k) of T^-1
   float Pk[9];
 #pragma unroll
@@ -1065,22 +1074,9 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
       G[(9 + b) * 13 + j] = g;
     }
   }
-  float gdd[3][3];
-#pragma unroll
-  for (int b = 0; b < 3; ++b) {
-    const float ub = (j >= 9 && j < 18) ? cp[C_DYNU + 12 * b + j - 9] : 0.f;
-#pragma unroll
-    for (int b2 = 0; b2 < 3; ++b2) gdd[b][b2] = wsum(ub * W[b2]);
-  }
-  if (j == 0) {
-#pragma unroll
-    for (int b = 0; b < 3; ++b)
-#pragma unroll
-      for (int b2 = 0; b2 < 3; ++b2) {
-        const float gv = 0.5f * (gdd[b][b2] + gdd[b2][b]);
-        G[(9 + b) * 13 + 9 + b2] = gv;
-        sm.C(i - 1)[C_G + 3 * b + b2] = gv;
-      }
+  if (j < 9) {
+    G[(9 + gb) * 13 + 9 + gb2] = gv;
+    sm.C(i - 1)[C_G + 3 * gb + gb2] = gv;
   }
   __syncwarp();
   bottom_update(P, sm, i - 1, j, G, Yb);

@@ -713,25 +713,39 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
     src.dsc = odd ? sm.scr : sm.dsc;
     float* dst = odd ? sm.dsc : sm.scr;
     const int es = odd ? V_S : V_E, ed = odd ? V_E : V_S;
-#pragma unroll 1
-    for (int i = warp; i < NT; i += 2) {  // nodes are independent within a pass
-      float o0, o1, o2;
-      row_view<OpMax>(src, i, lane, es, o0, o1, o2);
-      const float cv = col_view<OpMax, TV_D>(src, i, T, B);
+    struct Norms {
+      float o0, o1, o2, cv;
+    };
+    auto norms = [&](int i) {  // reads only the source copies
+      Norms n;
+      row_view<OpMax>(src, i, lane, es, n.o0, n.o1, n.o2);
+      n.cv = col_view<OpMax, TV_D>(src, i, T, B);
+      return n;
+    };
+    auto update = [&](int i, const Norms& n) {  // writes only the destination copies
       const float* d = src.D(i);
       float* dn = dst + (i + 1) * NSLOT;
-      dn[lane] = d[lane] * inv_sqrt1(d[lane] * o0);
-      if (lane < 8) dn[32 + lane] = d[32 + lane] * inv_sqrt1(d[32 + lane] * o1);
+      dn[lane] = d[lane] * inv_sqrt1(d[lane] * n.o0);
+      if (lane < 8) dn[32 + lane] = d[32 + lane] * inv_sqrt1(d[32 + lane] * n.o1);
       if (i == 0 && lane < NINIT) {
         const float* d0 = src.D(-1) + INIT0;
-        dst[INIT0 + lane] = d0[lane] * inv_sqrt1(d0[lane] * o2);
+        dst[INIT0 + lane] = d0[lane] * inv_sqrt1(d0[lane] * n.o2);
       }
       if (lane < NV) {
         const float e = sm.V(i, es)[lane];
         const float pd = wl * (float)P.dt[i];
-        sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, cv));
+        sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, n.cv));
       }
+    };
+    // nodes are independent within a pass: two per iteration, all loads ahead of the stores
+    int i = warp;
+#pragma unroll 1
+    for (; i + 2 < NT; i += 4) {
+      const Norms a = norms(i), b = norms(i + 2);
+      update(i, a);
+      update(i + 2, b);
     }
+    if (i < NT) update(i, norms(i));
     pair_sync(sm);  // every norm of the next pass uses the scales of this one
   }
   if (P.ruiz_iters & 1) {  // the last pass wrote the second copies

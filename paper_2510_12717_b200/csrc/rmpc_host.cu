@@ -498,7 +498,7 @@ int32_t rmpc_set_stage_profiling(rmpc_handle* h, int32_t enabled) {
 }
 
 const char* rmpc_build_info(void) {
-  return "rmpc_b200 sm_100a fused warp-per-agent RTI kernel (reduced SPD block-tridiagonal ADMM, FP32 + FP64 linearization)";
+  return "rmpc_b200 sm_100a fused warp-pair-per-agent RTI kernel (reduced SPD block-tridiagonal ADMM, factor in TMEM, FP32 + FP64 linearization)";
 }
 
 int32_t rmpc_fma_peak(int32_t device, double* tflops) {

@@ -1,6 +1,6 @@
-// rmpc_kernel.cu — fused warp-per-agent RTI-MPC solve for sm_100a.
+// rmpc_kernel.cu — fused warp-pair-per-agent RTI-MPC solve for sm_100a.
 //
-// One warp runs MpcController::rti_step (/root/reference/proj/src/mpc.cpp:248-338) for one
+// One warp pair runs MpcController::rti_step (/root/reference/proj/src/mpc.cpp:248-338) for one
 // agent: gait schedule and cold/warm guess (f_init, gait.cpp:37-99), FP64 linearization of
 // the floating-base dynamics and contacts (robot.cpp:29-195), QP rows (build_qp,
 // mpc.cpp:64-238), Ruiz passes (ruiz.cpp:7-36 via qp.cpp:64-95), factorization, exactly n_qp
@@ -14,11 +14,14 @@
 // block tridiagonal over horizon nodes; its off-diagonal blocks C_i = rho U_i V_i^T have rank
 // 12 (the 9 integration + 3 dynamics rows of interval i).  Block elimination keeps
 //     S_0 = H_00,  S_{i+1} = H_{i+1,i+1} - rho^2 U_i (V_i^T S_i^-1 V_i) U_i^T
-// with S_i^-1 and W_i = S_i^-1 V_i(dyn) in shared memory, so each iteration is
+// with S_i^-1 and W_i = S_i^-1 V_i(dyn) in tensor memory, so each iteration is
 //     forward:  u_i = r_i - rho U_{i-1} gamma_{i-1},  s_i = S_i^-1 u_i,  gamma_i = V_i^T s_i
 //     backward: x~_i = s_i - rho [S_i^-1 | W_i] xi_i,   xi_i = diag(a2, 1) U_i^T x~_{i+1}
 // where gamma comes out of the same 29-row matvec as s (rows 26..28 = W^T) and the backward
-// step is a 12-column update: no warp reductions on either recurrence.
+// step is a 12-column update: no warp reductions on either recurrence.  The elimination is
+// two-sided: warp 0 of the agent's pair runs nodes [0, m) top-down and the middle node m, warp 1
+// runs (m, T) bottom-up (mirrored recurrences with T_i = D_i - rho^2 V_i G'_i V_i^T); the pair
+// meets at the middle node only.  Six agents (warp pairs) share a CTA / SM.
 //
 // Precision: gait, guess, linearization, constraint right-hand sides, the objective and the
 // inverse dynamics in FP64; Ruiz, H, S^-1 and the ADMM iterations in FP32.

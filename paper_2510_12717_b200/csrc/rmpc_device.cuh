@@ -70,6 +70,9 @@ struct KParams {
   int32_t NT, n_qp, ruiz_iters, warm_start;
   int32_t n_agents, profile;
   int32_t agents_per_cta, cols_per_warp, tmem_cols, pad_;
+  // launch shape: full_ctas CTAs of agents_per_cta agents, then CTAs of tail_agents (the
+  // last, partial wave spread over every SM at fewer agents per CTA)
+  int32_t full_ctas, tail_agents;
   double dt[MAXT];
   double wq[NQ], wqd[NQ], wf[NF];
   double z_swing, v_to, v_td;

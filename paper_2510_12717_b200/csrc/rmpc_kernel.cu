@@ -1688,7 +1688,11 @@ __global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
   const int pair = w >> 1;
-  const int agent = blockIdx.x * P.agents_per_cta + pair;
+  const int b = blockIdx.x;
+  const int agent = b < P.full_ctas ? b * P.agents_per_cta + pair
+                                    : (pair < P.tail_agents ? P.full_ctas * P.agents_per_cta +
+                                                                   (b - P.full_ctas) * P.tail_agents + pair
+                                                             : P.n_agents);
   if (agent < P.n_agents) {
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * P.cols_per_warp);
     solve_agent(P, smem + pair * make_layout(P.NT).total, tm, 1 + pair, agent, lane, w & 1);
@@ -1714,7 +1718,25 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   P.agents_per_cta = c.agents;
   P.cols_per_warp = c.cols_per_warp;
   P.tmem_cols = c.tmem_cols;
-  const int grid = (P.n_agents + c.agents - 1) / c.agents;
+  // Whole waves of full CTAs (one CTA per SM), then the remainder spread over the SMs at
+  // ceil(R / SMs) agents per CTA: a partial wave of fewer agents per SM runs faster than a
+  // partial wave of full CTAs on a subset of the SMs.
+  static int sms[64] = {0};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
+  const int nsm = dev < 64 && sms[dev] > 0 ? sms[dev] : 148;
+  const int wave = nsm * c.agents;
+  const int full_waves = P.n_agents / wave;
+  const int rem = P.n_agents - full_waves * wave;
+  int tail = 0, tail_ctas = 0;
+  if (rem > 0) {
+    tail = (rem + nsm - 1) / nsm;
+    tail_ctas = (rem + tail - 1) / tail;
+  }
+  P.full_ctas = full_waves * nsm;
+  P.tail_agents = tail;
+  const int grid = P.full_ctas + tail_ctas;
   rmpc_dev::rti_kernel<<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
   return (int)cudaGetLastError();
 }

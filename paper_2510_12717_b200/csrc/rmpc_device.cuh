@@ -69,7 +69,7 @@ constexpr int G_SCR = 160;    // 12 x 13 G block (+ pad) of the factorization
 struct KParams {
   int32_t NT, n_qp, ruiz_iters, warm_start;
   int32_t n_agents, profile;
-  int32_t agents_per_cta, cols_per_warp, tmem_cols, pad_;
+  int32_t agents_per_cta, spill_nodes, tmem_cols, pad_;
   // launch shape: full_ctas CTAs of agents_per_cta agents, then CTAs of tail_agents (the
   // last, partial wave spread over every SM at fewer agents per CTA)
   int32_t full_ctas, tail_agents;
@@ -94,12 +94,15 @@ struct KParams {
 
 // Shared-memory footprint of one agent (warp pair) in floats, every region 16-byte aligned.
 struct Layout {
-  int scr, coef, vec, row, tt, dsc, bc, flags, total;
+  int scr, coef, vec, row, tt, dsc, bc, flags, spill, total;
 };
+constexpr int SPILL_BLK = 32 * TCOLS;  // a node block kept in shared memory (swizzled rows)
 
 __host__ __device__ inline int align4(int x) { return (x + 3) & ~3; }
 
-__host__ __device__ inline Layout make_layout(int NT) {
+// spill_nodes: node blocks per warp that do not fit the warp's TMEM share (both warps of the
+// agent get the same space).
+__host__ __device__ inline Layout make_layout(int NT, int spill_nodes = 0) {
   Layout L;
   int o = 0;
   // scratch: Ruiz's second d, the two 12 x 13 G blocks of the factorization, z* rows (FP64)
@@ -112,11 +115,12 @@ __host__ __device__ inline Layout make_layout(int NT) {
   L.dsc = o;   o += (NT + 1) * NSLOT;               // Ruiz row scale d
   L.bc = o;    o += 128;                            // per warp: 2 x 32 broadcast buffers
   L.flags = o; o += align4(NT);
+  L.spill = o; o += 2 * spill_nodes * SPILL_BLK;
   L.total = o;
   return L;
 }
 
-inline int smem_bytes(int NT) { return make_layout(NT).total * 4; }
+inline int smem_bytes(int NT, int spill_nodes = 0) { return make_layout(NT, spill_nodes).total * 4; }
 
 // Nodes owned by one warp (top: [0, m], bottom: (m, T)), i.e. TMEM blocks per warp.
 __host__ __device__ inline int nodes_per_warp(int NT) {
@@ -124,24 +128,32 @@ __host__ __device__ inline int nodes_per_warp(int NT) {
   return a > b ? a : b;
 }
 
-// CTA shape: A agents = 2A warps; warp w uses TMEM lanes [32 (w % 4), +32) and columns
-// [(w / 4) * cols_per_warp, +cols_per_warp), so A is bounded by TMEM (512 columns), by the
-// 227 KB of shared memory and by MAX_AGENTS.
+// CTA shape: A agents = 2A warps; warp w can address only TMEM lane quarter w % 4, whose 512
+// columns (16 node blocks of 32) are split evenly between the warps of that quarter.  A warp's
+// first `tm_nodes(quarter)` node blocks live in TMEM, the rest ("spill") in shared memory.  A
+// is the largest count (<= MAX_AGENTS) whose shared memory, spill included, fits 227 KB.
+__host__ __device__ inline int warps_in_quarter(int A, int q) { return (2 * A - q + 3) / 4; }
+__host__ __device__ inline int tm_nodes(int NT, int A, int q) {
+  const int nw = nodes_per_warp(NT), cap = 16 / warps_in_quarter(A, q);
+  return nw < cap ? nw : cap;
+}
 struct CtaShape {
-  int agents, cols_per_warp, tmem_cols, smem_bytes;
+  int agents, spill_nodes, tmem_cols, smem_bytes;
 };
 inline CtaShape cta_shape(int NT) {
   CtaShape c;
-  c.cols_per_warp = TCOLS * nodes_per_warp(NT);
-  const int per = smem_bytes(NT);
+  const int nw = nodes_per_warp(NT);
   int A = MAX_AGENTS;
-  while (A > 1 && (((2 * A + 3) / 4) * c.cols_per_warp > 512 || A * per > 227 * 1024 - 128)) --A;
+  for (;; --A) {
+    c.spill_nodes = nw - tm_nodes(NT, A, 0);  // quarter 0 holds the most warps
+    if (A == 1 || A * smem_bytes(NT, c.spill_nodes) <= 227 * 1024 - 128) break;
+  }
   c.agents = A;
-  const int need = ((2 * A + 3) / 4) * c.cols_per_warp;
+  const int need = warps_in_quarter(A, 0) * tm_nodes(NT, A, 0) * TCOLS;
   int cols = 32;
   while (cols < need) cols *= 2;
   c.tmem_cols = cols;
-  c.smem_bytes = A * per;
+  c.smem_bytes = A * smem_bytes(NT, c.spill_nodes);
   return c;
 }
 

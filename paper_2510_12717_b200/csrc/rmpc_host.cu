@@ -532,7 +532,10 @@ int32_t rmpc_fma_peak(int32_t device, double* tflops) {
   return e == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
 }
 
-int32_t rmpc_smem_bytes(int32_t horizon) { return rmpc_dev::smem_bytes(horizon); }
+int32_t rmpc_smem_bytes(int32_t horizon) {
+  if (horizon < 1 || horizon > rmpc_dev::MAXT) return -1;
+  return rmpc_dev::cta_shape(horizon).smem_bytes / rmpc_dev::cta_shape(horizon).agents;
+}
 int32_t rmpc_agents_per_cta(int32_t horizon) {
   if (horizon < 1 || horizon > rmpc_dev::MAXT) return -1;
   return rmpc_dev::cta_shape(horizon).agents;

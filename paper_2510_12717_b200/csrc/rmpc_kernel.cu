@@ -49,6 +49,9 @@ struct Sm {
   int NT;
   int mid;      // middle node: the top warp owns [0, mid], the bottom warp (mid, NT)
   uint32_t tm;  // TMEM address of this warp's first node block (lane quarter | column)
+  int tmn;      // node blocks of this warp in TMEM; the rest are in `spill` (shared memory)
+  float* spill;
+  bool spills;  // compile-time constant per kernel instantiation (folds the TMEM-only path)
   int bar;      // named barrier of the agent's warp pair
   __device__ __forceinline__ float* C(int i) const { return coef + (i + 1) * C_SIZE; }
   __device__ __forceinline__ float4* R(int i) const { return row + (i + 1) * NSLOT; }
@@ -57,10 +60,8 @@ struct Sm {
   __device__ __forceinline__ float* V(int i, int which) const {
     return vec + (i * V_NUM + which) * V_STRIDE;
   }
-  // TMEM block of node i (only meaningful in the warp that owns node i)
-  __device__ __forceinline__ uint32_t Tm(int i) const {
-    return tm + (uint32_t)(TCOLS * (i <= mid ? i : i - mid - 1));
-  }
+  // index of node i among the blocks of the warp that owns it
+  __device__ __forceinline__ int blk(int i) const { return i <= mid ? i : i - mid - 1; }
 };
 
 // ------------------------------------------------------------------------- sync / TMEM
@@ -129,6 +130,44 @@ __device__ __forceinline__ void tm_store(uint32_t a, const float v[TCOLS]) {
                : "memory");
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
+
+// Node block rows: TMEM for the warp's first `tmn` blocks, else a shared-memory copy whose
+// rows (32 floats per lane) have their float4 chunks XOR-swizzled by lane & 7 so eight
+// consecutive lanes' LDS.128 hit distinct banks.  The branch is warp-uniform.
+__device__ __forceinline__ const float4* spill_row(const Sm& sm, int b, int lane) {
+  return reinterpret_cast<const float4*>(sm.spill + (b - sm.tmn) * SPILL_BLK + lane * TCOLS);
+}
+__device__ __forceinline__ void blk_load_issue(const Sm& sm, int i, int lane, float v[TCOLS]) {
+  const int b = sm.blk(i);
+  if (!sm.spills || b < sm.tmn) {
+    tm_load_issue(sm.tm + (uint32_t)(TCOLS * b), v);
+  } else {
+    const float4* r = spill_row(sm, b, lane);
+#pragma unroll
+    for (int c = 0; c < TCOLS / 4; ++c) {
+      const float4 w = r[c ^ (lane & 7)];
+      v[4 * c] = w.x; v[4 * c + 1] = w.y; v[4 * c + 2] = w.z; v[4 * c + 3] = w.w;
+    }
+  }
+}
+__device__ __forceinline__ void blk_load_wait(const Sm& sm, int i, float v[TCOLS]) {
+  if (!sm.spills || sm.blk(i) < sm.tmn) tm_load_wait(v);
+}
+__device__ __forceinline__ void blk_load(const Sm& sm, int i, int lane, float v[TCOLS]) {
+  blk_load_issue(sm, i, lane, v);
+  blk_load_wait(sm, i, v);
+}
+__device__ __forceinline__ void blk_store(const Sm& sm, int i, int lane, const float v[TCOLS]) {
+  const int b = sm.blk(i);
+  if (!sm.spills || b < sm.tmn) {
+    tm_store(sm.tm + (uint32_t)(TCOLS * b), v);
+  } else {
+    float4* r = const_cast<float4*>(spill_row(sm, b, lane));
+#pragma unroll
+    for (int c = 0; c < TCOLS / 4; ++c) r[c ^ (lane & 7)] = make_float4(v[4 * c], v[4 * c + 1], v[4 * c + 2], v[4 * c + 3]);
+  }
+}
+
 
 __device__ __forceinline__ float wsum(float v) {
 #pragma unroll
@@ -931,7 +970,8 @@ __device__ __forceinline__ bool gauss_jordan2(int j, float S[NV], float* buf) {
   return good;
 }
 
-__device__ __forceinline__ void store_block(uint32_t a, int j, const float S[NV], const float W[3], float* tr) {
+__device__ __forceinline__ void store_block(const Sm& sm, int i, int j, const float S[NV], const float W[3],
+                                            float* tr) {
 #pragma unroll
   for (int b = 0; b < 3; ++b) tr[32 * b + j] = W[b];
   __syncwarp();
@@ -944,7 +984,7 @@ __device__ __forceinline__ void store_block(uint32_t a, int j, const float S[NV]
   for (int b = 0; b < 3; ++b) v[NV + b] = wrow ? 0.f : W[b];
 #pragma unroll
   for (int k = SROWS; k < TCOLS; ++k) v[k] = 0.f;
-  tm_store(a, v);
+  blk_store(sm, i, j, v);
   __syncwarp();  // tr is reused by the caller
 }
 
@@ -964,7 +1004,7 @@ __device__ __forceinline__ void top_schur(const KParams& P, const Sm& sm, int i,
     for (int l = 9; l < NV; ++l) acc = fmaf(S[l], vb[l - 9], acc);
     W[b] = j < NV ? acc : 0.f;
   }
-  store_block(sm.Tm(i), j, S, W, G);
+  store_block(sm, i, j, S, W, G);
   // G_dd[b][b2] = v_b . W_b2 over node vars 9..25, lane 3 b + b2 < 9, from W^T still in G
   const int gb = j < 9 ? j / 3 : 0, gb2 = j < 9 ? j % 3 : 0;
   float gacc0 = 0.f, gacc1 = 0.f;
@@ -1060,7 +1100,7 @@ __device__ __forceinline__ void bottom_schur(const KParams& P, const Sm& sm, int
     for (int k = 0; k < 9; ++k) acc = fmaf(S[NQ + k], ub[k], acc);
     W[b] = j < NV ? acc : 0.f;
   }
-  store_block(sm.Tm(i), j, S, W, G);
+  store_block(sm, i, j, S, W, G);
   // G'_dd[b][b2] = u_b . W'_b2 over qd (node vars 9..17), lane 3 b + b2 < 9
   const int gb = j < 9 ? j / 3 : 0, gb2 = j < 9 ? j % 3 : 0;
   float gacc0 = 0.f, gacc1 = 0.f;
@@ -1139,7 +1179,7 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
     good = gauss_jordan2(j, S, sm.scr + G_SCR * warp) && good;
     if (middle) {
       const float W0[3] = {0.f, 0.f, 0.f};
-      store_block(sm.Tm(i), j, S, W0, sm.scr);
+      store_block(sm, i, j, S, W0, sm.scr);
     } else if (warp == 0) {
       float Yp[18];
       top_schur(P, sm, i, j, S, Yp);
@@ -1173,10 +1213,10 @@ __device__ __forceinline__ bool row_update(float4* r, float* tr, bool active, fl
 }
 
 // [S_i^-1 ; W_i^T] u for lanes 0..28 (u published through buf, the block row from TMEM).
-__device__ __forceinline__ float ext_mv(uint32_t a, int lane, float* buf, float u) {
+__device__ __forceinline__ float ext_mv(const Sm& sm, int i, int lane, float* buf, float u) {
   buf[lane] = lane < NV ? u : 0.f;
   float v[TCOLS];
-  tm_load(a, v);
+  blk_load(sm, i, lane, v);
   __syncwarp();
   const float4* b4 = reinterpret_cast<const float4*>(buf);
   float a0 = 0.f, a1 = 0.f, a2 = 0.f, a3 = 0.f;
@@ -1335,9 +1375,9 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float u = rc - top_corr(sm.C(i - 1), gint, g0, g1, g2);
         ubuf[lane] = lane < NV ? u : 0.f;
         float v[TCOLS];
-        tm_load_issue(sm.Tm(i), v);
+        blk_load_issue(sm, i, lane, v);
         if (i + 1 < m) rc = r_of(i + 1, first);
-        tm_load_wait(v);
+        blk_load_wait(sm, i, v);
         __syncwarp();
         const float s = block_row_dot(v, ubuf, lane);
         store_s(i, s);
@@ -1353,9 +1393,9 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         const float u = rc - bot_corr(sm.C(i), gint, g0, g1, g2);
         ubuf[lane] = lane < NV ? u : 0.f;
         float v[TCOLS];
-        tm_load_issue(sm.Tm(i), v);
+        blk_load_issue(sm, i, lane, v);
         if (i - 1 > m) rc = r_of(i - 1, first);
-        tm_load_wait(v);
+        blk_load_wait(sm, i, v);
         __syncwarp();
         const float s = block_row_dot(v, ubuf, lane);
         store_s(i, s);
@@ -1374,7 +1414,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
     if (warp == 0) {
       float u = r_of(m, first) - top_corr(sm.C(m - 1), gint, g0, g1, g2);
       if (m + 1 < NT) u -= bot_corr(sm.C(m), gb[kq], gb[9], gb[10], gb[11]);
-      const float x = ext_mv(sm.Tm(m), lane, ubuf, u);
+      const float x = ext_mv(sm, m, lane, ubuf, u);
       if (is_var) sm.V(m, V_S)[lane] = x;
       bad = bad || !isfinite(x);
     }
@@ -1403,7 +1443,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         __syncwarp();
         // lanes < 26: row j of S^-1 (cols 0..8 = column j) and W_b[j];  26..28: W_b, G_b
         float v[TCOLS];
-        tm_load(sm.Tm(i), v);
+        blk_load(sm, i, lane, v);
         float xi[12];
 #pragma unroll
         for (int k = 0; k < 12; ++k) xi[k] = xib[k];
@@ -1457,7 +1497,7 @@ __device__ int admm(const KParams& P, const Sm& sm, int lane, int warp) {
         if (lane >= 9 && lane < 12) xib[18 + bw] = xd;
         __syncwarp();
         float v[TCOLS];  // lanes < 26: row j of T^-1 and W'_b[j]; 26..28: W'_b, G'_b
-        tm_load(sm.Tm(i), v);
+        blk_load(sm, i, lane, v);
         float acc0 = 0.f, acc1 = 0.f;
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
@@ -1506,10 +1546,11 @@ __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage,
 
 // One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
 // blocks at `tm`, named barrier `bar`.
-__device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int bar, int agent,
-                                            int lane, int warp) {
+template <bool SPILL>
+__device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int tmn, int bar,
+                                            int agent, int lane, int warp) {
   const int NT = P.NT;
-  const Layout L = make_layout(NT);
+  const Layout L = make_layout(NT, P.spill_nodes);
   Sm sm;
   sm.scr = base + L.scr;
   sm.coef = base + L.coef;
@@ -1522,6 +1563,9 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   sm.NT = NT;
   sm.mid = mid_node(NT);
   sm.tm = tm;
+  sm.tmn = tmn;
+  sm.spills = SPILL;
+  sm.spill = base + L.spill + warp * P.spill_nodes * SPILL_BLK;
   sm.bar = bar;
   const int tid = warp * 32 + lane;
   long long t0 = P.profile ? clock64() : 0;
@@ -1671,7 +1715,9 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
 }
 
 // CTA = P.agents_per_cta warp pairs.  Warp w uses TMEM lanes [32 (w % 4), +32) (the quarter
-// tcgen05.ld/st of warp w can reach) and columns [(w / 4) cols_per_warp, +cols_per_warp).
+// tcgen05.ld/st of warp w can reach) and columns [(w / 4) tmn 32, +tmn 32), tmn = the node
+// blocks its quarter's share holds (tm_nodes); further blocks go to its shared-memory spill.
+template <bool SPILL>
 __global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P) {
   extern __shared__ __align__(16) float smem[];
   __shared__ uint32_t tmem_base;
@@ -1694,8 +1740,10 @@ __global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P
                                                                    (b - P.full_ctas) * P.tail_agents + pair
                                                              : P.n_agents);
   if (agent < P.n_agents) {
-    const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * P.cols_per_warp);
-    solve_agent(P, smem + pair * make_layout(P.NT).total, tm, 1 + pair, agent, lane, w & 1);
+    const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
+    const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
+    solve_agent<SPILL>(P, smem + pair * make_layout(P.NT, P.spill_nodes).total, tm, tmn, 1 + pair, agent, lane,
+                       w & 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -1707,8 +1755,11 @@ __global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P
 }  // namespace rmpc_dev
 
 int rmpc_kernel_setup(int) {
-  return (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   227 * 1024 - 128);  // static smem: the TMEM base
+  const int bytes = 227 * 1024 - 128;  // static smem: the TMEM base
+  int rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  if (rc == 0)
+    rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  return rc;
 }
 
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
@@ -1716,7 +1767,7 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   const rmpc_dev::CtaShape c = rmpc_dev::cta_shape(params.NT);
   rmpc_dev::KParams P = params;
   P.agents_per_cta = c.agents;
-  P.cols_per_warp = c.cols_per_warp;
+  P.spill_nodes = c.spill_nodes;
   P.tmem_cols = c.tmem_cols;
   // Whole waves of full CTAs (one CTA per SM), then the remainder spread over the SMs at
   // ceil(R / SMs) agents per CTA: a partial wave of fewer agents per SM runs faster than a
@@ -1737,6 +1788,9 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   P.full_ctas = full_waves * nsm;
   P.tail_agents = tail;
   const int grid = P.full_ctas + tail_ctas;
-  rmpc_dev::rti_kernel<<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
+  if (c.spill_nodes > 0)
+    rmpc_dev::rti_kernel<true><<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
+  else
+    rmpc_dev::rti_kernel<false><<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
   return (int)cudaGetLastError();
 }

@@ -74,12 +74,15 @@ def test_stage_names_and_status_messages():
 
 def test_cta_shape_six_agents_per_sm_at_n10():
     """T=10: 6 warp pairs per CTA (TMEM: 3 warps x 160 columns per lane quarter), their shared
-    memory within 227 KB; every horizon up to 32 gets at least one agent pair's worth."""
+    memory within 227 KB; longer horizons keep the node blocks that exceed a warp's TMEM share
+    in shared memory; every horizon up to 32 gets at least two agents per CTA."""
     L = R.library()
     L.rmpc_agents_per_cta.argtypes = [C.c_int32]
     assert L.rmpc_agents_per_cta(10) == 6
     assert 6 * L.rmpc_smem_bytes(10) <= 227 * 1024 - 128
-    assert L.rmpc_agents_per_cta(20) == 2 and L.rmpc_agents_per_cta(32) == 2
+    # T = 12: 5 agents (one node block per warp in shared memory); T = 20: 3 (two per warp)
+    assert L.rmpc_agents_per_cta(12) == 5 and L.rmpc_agents_per_cta(20) == 3
+    assert L.rmpc_agents_per_cta(32) == 2
     for T in range(2, 33):
         A = L.rmpc_agents_per_cta(T)
         assert 1 <= A <= 6 and A * L.rmpc_smem_bytes(T) <= 227 * 1024 - 128

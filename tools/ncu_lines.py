@@ -16,7 +16,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.environ.get("RMPC_B200_LIB") or os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
-FUNC = "_ZN8rmpc_dev10rti_kernelENS_7KParamsE"
+FUNC = os.environ.get("RMPC_NCU_FUNC", "_ZN8rmpc_dev10rti_kernelILb0EEEvNS_7KParamsE")  # the TMEM-only instantiation (T <= 10)
 
 
 def line_table():

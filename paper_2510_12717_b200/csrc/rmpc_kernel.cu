@@ -107,12 +107,6 @@ __device__ __forceinline__ bool pair_and(const Sm& sm, bool v) {
 
 // Lane l of the warp reads / writes its TMEM row (lane quarter of the warp) at columns
 // [a, a + 32): one 32x32b.x32 access moves a whole 26-float block row plus its W entries.
-__device__ __forceinline__ void tm_load(uint32_t a, float v[TCOLS]) {
-  asm volatile("tcgen05.ld.sync.aligned.32x32b.x32.b32 " RMPC_OPS32 ", [%32];"
-               : RMPC_X32(RMPC_OUT, v)
-               : "r"(a));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
-}
 // Split form: issue the load, do independent work, then wait (v is tied to the wait so the
 // compiler cannot consume it earlier).
 __device__ __forceinline__ void tm_load_issue(uint32_t a, float v[TCOLS]) {
@@ -169,11 +163,6 @@ __device__ __forceinline__ void blk_store(const Sm& sm, int i, int lane, const f
 }
 
 
-__device__ __forceinline__ float wsum(float v) {
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
-  return v;
-}
 __device__ __forceinline__ float wmax(float v) {
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(FULL, v, o));

@@ -16,7 +16,7 @@ SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rmpc_kernel.cu", "rmpc_host.
 HEADERS = [os.path.join(HERE, "csrc", h) for h in ("rmpc_device.cuh", "rmpc_kin.cuh")] + \
     [os.path.join(ROOT, "include", h) for h in ("rmpc_b200.h", "rmpc_b200_env.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-              "-Xcompiler", "-fPIC", "-shared", "-Xptxas", "-v"]
+              "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 
 
 def nvcc() -> str:
@@ -38,13 +38,26 @@ def build(force: bool = False, verbose: bool = False) -> str:
         return LIB_PATH
     os.makedirs(LIB_DIR, exist_ok=True)
     tmp = LIB_PATH + ".tmp"
-    cmd = [nvcc(), *NVCC_FLAGS, "-o", tmp, *SOURCES]
-    r = subprocess.run(cmd, capture_output=True, text=True)
+    # one nvcc per translation unit, in parallel (the solve kernel dominates), then one link
+    objs = [os.path.join(LIB_DIR, os.path.basename(src).replace(".cu", ".o")) for src in SOURCES]
+    procs = [subprocess.Popen([nvcc(), *NVCC_FLAGS, "-c", "-o", o, src], stdout=subprocess.PIPE,
+                              stderr=subprocess.PIPE, text=True) for src, o in zip(SOURCES, objs)]
+    logs = []
+    for pr in procs:
+        out, err = pr.communicate()
+        logs.append(out + err)
+        if pr.returncode != 0:
+            sys.stderr.write(out + err)
+            raise RuntimeError("nvcc failed building librmpc_b200.so")
+    r = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
+                       capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
-        raise RuntimeError("nvcc failed building librmpc_b200.so")
+        raise RuntimeError("nvcc failed linking librmpc_b200.so")
     if verbose:
-        sys.stderr.write(r.stderr)
+        sys.stderr.write("".join(logs))
+    for o in objs:
+        os.remove(o)
     os.replace(tmp, LIB_PATH)
     return LIB_PATH
 

@@ -159,6 +159,16 @@ void rmpc_nominal_pose(const rmpc_model* model, double q_out[RMPC_NQ]);
 int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol,
                         const rmpc_state* state, double tau_out[RMPC_NJ]);
 
+/* rmpc_solve_device plus the active set of the final ADMM iterate (the north star's parity
+ * criterion): d_active receives n x (horizon + 1) x 40 bytes on the solver's padded row grid
+ * (block -1 = the 18 initial-state rows at slots 12..29, then per node: 0..8 integration,
+ * 9..11 base dynamics, 12 + 4c + t contact c row t, 28..39 joint boxes), each 0 inactive,
+ * 1 at the lower bound, 2 at the upper bound, 3 equality row or no row (all 3 for a failed
+ * agent).  Cold start, no z*. */
+int32_t rmpc_solve_device_active_set(rmpc_handle* handle, const rmpc_state* d_states,
+                                     const rmpc_command* d_cmds, const rmpc_gait* d_gaits,
+                                     rmpc_solution* d_out, uint8_t* d_active, void* stream);
+
 /* Stage-profiling switch: when on, the kernel samples the SM clock at the reference's stage
  * boundaries and rmpc_last_timing() reports the per-stage split of kernel_ms. */
 int32_t rmpc_set_stage_profiling(rmpc_handle* handle, int32_t enabled);

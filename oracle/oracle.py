@@ -349,3 +349,17 @@ def policy_forward(params, obs, act=6, hidden=64):
     mean, value = np.zeros((n, act)), np.zeros(n)
     lib().oracle_policy_forward_batch(ptr(_f64(params)), od, act, hidden, n, ptr(o), ptr(mean), ptr(value))
     return mean, value
+
+
+def active_set_batch(model: Model, settings: Settings, states, cmds, gaits, workers=0):
+    """Final-iterate active set on the device's (node + 1, slot) grid: codes (n, T+1, 40) int8
+    (0 inactive, 1 at lo, 2 at hi, 3 equality / no row) and the scaled-space margin."""
+    st, cm, ga = _f64(states).reshape(-1, 18), _f64(cmds).reshape(-1, 3), _f64(gaits).reshape(-1, 7)
+    n, T = st.shape[0], settings.horizon
+    act = np.zeros((n, T + 1, 40), np.int8)
+    margin = np.zeros((n, T + 1, 40))
+    rc = lib().oracle_active_set_batch(C.byref(model), C.byref(settings), C.c_int32(n), ptr(st), ptr(cm),
+                                       ptr(ga), C.c_int32(workers), act.ctypes.data_as(C.c_void_p), ptr(margin))
+    if rc != 0:
+        raise ValueError(f"oracle_active_set_batch: {rc}")
+    return act, margin

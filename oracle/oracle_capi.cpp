@@ -400,4 +400,32 @@ void oracle_policy_forward_batch(const double* params, int32_t obs, int32_t act,
     policy_forward_flat(params, obs, act, hidden, o + (size_t)obs * a, mean + (size_t)act * a, value + a);
 }
 
+// Active set of the final ADMM iterate per agent on the device's (node + 1, slot) grid:
+// act (n x (T+1) x 40 int8), margin (same shape, FP64, scaled space).  Cold start.
+int32_t oracle_active_set_batch(const rmpc_model* model, const rmpc_settings* st, int32_t n,
+                                const rmpc_state* states, const rmpc_command* cmds, const rmpc_gait* gaits,
+                                int32_t workers, int8_t* act, double* margin) {
+  if (n < 1 || st->horizon < 2 || st->horizon > RMPC_MAX_HORIZON) return RMPC_ERR_STRUCTURAL;
+  double nominal[kNq];
+  nominal_pose(*model, nominal);
+  const size_t W = (size_t)(st->horizon + 1) * 40;
+  std::atomic<int> cursor{0};
+  auto work = [&]() {
+    for (;;) {
+      const int i = cursor.fetch_add(1);
+      if (i >= n) break;
+      const Solution s = rti_step<double>(*model, *st, nominal, states[i], cmds[i], gaits[i], nullptr, false, false);
+      for (size_t k = 0; k < W; ++k) {
+        act[i * W + k] = s.act.empty() ? 3 : s.act[k];
+        margin[i * W + k] = s.act_margin.empty() ? 0.0 : s.act_margin[k];
+      }
+    }
+  };
+  const int nw = std::max(1, std::min(workers > 0 ? workers : (int)std::thread::hardware_concurrency(), (int)n));
+  std::vector<std::thread> pool;
+  for (int w = 0; w < nw; ++w) pool.emplace_back(work);
+  for (auto& t : pool) t.join();
+  return 0;
+}
+
 }  // extern "C"

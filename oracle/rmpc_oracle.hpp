@@ -722,6 +722,7 @@ struct Qp {
   std::vector<T> q;
   Csc<T> A;  // m x n
   std::vector<T> lo, hi;
+  std::vector<int> tag;  // per row: (node + 1) * 40 + slot of the device's padded layout
   int n() const { return P.ncols; }
   int m() const { return A.nrows; }
 };
@@ -735,6 +736,10 @@ struct AdmmSettings {  // qp.hpp:29-36
 template <class T>
 struct QpResult {
   std::vector<T> x, y, z;
+  // final iterate per row: 1 at lo, 2 at hi, 0 between (scaled space, where the clamp acts),
+  // 3 for an equality row; margin = distance of the unclamped value to the nearer bound
+  std::vector<int8_t> act;
+  std::vector<T> margin;
   T prim = T(0.0), dual = T(0.0), obj = T(0.0), obj_quad = T(0.0), obj_lin = T(0.0);
   int iters_run = 0;
   int ldl_nnz = 0;
@@ -857,9 +862,18 @@ QpResult<T> admm_solve(const Qp<T>& qp, const AdmmSettings& st, const std::vecto
         throw DivergenceError("admm: non-finite iterate at iteration " + std::to_string(it), it);
     for (int i = 0; i < m; ++i) zt[i] = z[i] + rho_inv * (b[n + i] - y[i]);
     for (int i = 0; i < n; ++i) x[i] = alpha * b[i] + (T(1.0) - alpha) * x[i];
+    const bool last = it + 1 == st.iters;
+    if (last) {
+      res.act.assign(m, 0);
+      res.margin.assign(m, T(0.0));
+    }
     for (int i = 0; i < m; ++i) {
       const T wv = alpha * zt[i] + (T(1.0) - alpha) * z[i];
       T zn = wv + rho_inv * y[i];
+      if (last) {
+        res.act[i] = los[i] == his[i] ? 3 : (zn <= los[i] ? 1 : (zn >= his[i] ? 2 : 0));
+        res.margin[i] = std::min(abs(zn - los[i]), abs(zn - his[i]));
+      }
       zn = std::min(std::max(zn, los[i]), his[i]);
       z[i] = zn;
       y[i] += rho * (wv - zn);
@@ -1011,16 +1025,20 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
   std::vector<Trip<T>> at;
   std::vector<T> lo, hi;
   int row = 0;
-  auto bound = [&](T l, T h) { lo.push_back(l); hi.push_back(h); ++row; };
+  std::vector<int> tag;
+  int cur_tag = 0;  // set before each bound(); slots as in the device layout (rmpc_device.cuh)
+  auto bound = [&](T l, T h) { lo.push_back(l); hi.push_back(h); tag.push_back(cur_tag); ++row; };
   const T inf = T(kInf);
   for (int k = 0; k < kNq; ++k) {  // initial state (mpc.cpp:126-136)
     at.push_back({row, vq(0, k), T(1.0)});
     const T r = T(state.q[k]) - g.q[k];
+    cur_tag = 12 + k;
     bound(r, r);
   }
   for (int k = 0; k < kNq; ++k) {
     at.push_back({row, vqd(0, k), T(1.0)});
     const T r = T(state.qd[k]) - g.qd[k];
+    cur_tag = 21 + k;
     bound(r, r);
   }
   for (int i = 0; i + 1 < NT; ++i) {  // integration (mpc.cpp:138-148)
@@ -1030,6 +1048,7 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
       at.push_back({row, vq(i, k), T(-1.0)});
       at.push_back({row, vqd(i + 1, k), -dt});
       const T r = -(g.q[(i + 1) * kNq + k] - g.q[i * kNq + k] - dt * g.qd[(i + 1) * kNq + k]);
+      cur_tag = (i + 1) * 40 + k;
       bound(r, r);
     }
   }
@@ -1056,6 +1075,7 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
         at.push_back({row, vf(i, 2 * c), -kin[i].c_jac[c][0][b]});
         at.push_back({row, vf(i, 2 * c + 1), -kin[i].c_jac[c][1][b]});
       }
+      cur_tag = (i + 1) * 40 + 9 + b;
       bound(-res[b], -res[b]);
     }
   }
@@ -1063,12 +1083,16 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
   for (int i = 0; i < NT; ++i) {  // contacts (mpc.cpp:181-218)
     for (int c = 0; c < kNc; ++c) {
       const T fx = g.F[i * kNf + 2 * c], fz = g.F[i * kNf + 2 * c + 1];
+      int t_ = 0;
+      auto ctag = [&]() { cur_tag = (i + 1) * 40 + 12 + 4 * c + t_++; };
       if (ref.stance[i][c]) {
         at.push_back({row, vf(i, 2 * c), T(1.0)});
         at.push_back({row, vf(i, 2 * c + 1), -mu});
+        ctag();
         bound(-inf, -(fx - mu * fz));
         at.push_back({row, vf(i, 2 * c), T(-1.0)});
         at.push_back({row, vf(i, 2 * c + 1), -mu});
+        ctag();
         bound(-inf, -(-fx - mu * fz));
         if (i == 0) continue;
         for (int ax = 0; ax < 2; ++ax) {
@@ -1079,12 +1103,15 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
             const T j = kin[i].c_jac[c][ax][k];
             if (j != T(0.0)) at.push_back({row, vqd(i, k), j});
           }
+          ctag();
           bound(r, r);
         }
       } else {
         at.push_back({row, vf(i, 2 * c), T(1.0)});
+        ctag();
         bound(-fx, -fx);
         at.push_back({row, vf(i, 2 * c + 1), T(1.0)});
+        ctag();
         bound(-fz, -fz);
         if (i == 0) continue;
         const T r = T(ref.swing_height[i][c]) - kin[i].c[c].pz;
@@ -1092,6 +1119,7 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
           const T j = kin[i].c_jac[c][1][k];
           if (j != T(0.0)) at.push_back({row, vq(i, k), j});
         }
+        ctag();
         bound(r, r);
       }
     }
@@ -1099,16 +1127,19 @@ Qp<T> build_qp(const rmpc_state& state, const Traj<T>& g, const Reference& ref,
   for (int i = 1; i < NT; ++i) {  // joint boxes (mpc.cpp:220-232)
     for (int k = 0; k < kNj; ++k) {
       at.push_back({row, vq(i, 3 + k), T(1.0)});
+      cur_tag = (i + 1) * 40 + 28 + k;
       bound(T(model.joint_lo[k]) - g.q[i * kNq + 3 + k], T(model.joint_hi[k]) - g.q[i * kNq + 3 + k]);
     }
     for (int k = 0; k < kNj; ++k) {
       at.push_back({row, vqd(i, 3 + k), T(1.0)});
+      cur_tag = (i + 1) * 40 + 34 + k;
       bound(T(-model.qd_limit[k]) - g.qd[i * kNq + 3 + k], T(model.qd_limit[k]) - g.qd[i * kNq + 3 + k]);
     }
   }
   qp.A = csc_from_triplets(at, row, n);
   qp.lo = lo;
   qp.hi = hi;
+  qp.tag = tag;
   return qp;
 }
 
@@ -1123,6 +1154,10 @@ struct Solution {
   double v_quad = 0, v_lin = 0;
   double stage_s[kNumStages] = {0};
   int m = 0, n = 0, ldl_nnz = 0;
+  // active set of the final iterate on the device's (node + 1, slot) grid ((T+1) x 40):
+  // 0 inactive, 1 at lo, 2 at hi, 3 equality row or no row; margin as in QpResult
+  std::vector<int8_t> act;
+  std::vector<double> act_margin;
 };
 
 // MpcController::rti_step (mpc.cpp:248-338).  `prev_z` (T x 26) is read only when

@@ -75,6 +75,12 @@ Solution rti_step(const rmpc_model& model, const rmpc_settings& st, const double
     as.ruiz_iters = st.ruiz_iters;
     const QpResult<T> r = admm_solve<T>(qp, as, nullptr, nullptr, true, timed ? sol.stage_s : nullptr);
     sol.ldl_nnz = r.ldl_nnz;
+    sol.act.assign((size_t)(NT + 1) * 40, 3);
+    sol.act_margin.assign((size_t)(NT + 1) * 40, 0.0);
+    for (int k = 0; k < qp.m(); ++k) {
+      sol.act[qp.tag[k]] = r.act[k];
+      sol.act_margin[qp.tag[k]] = (double)r.margin[k];
+    }
 
     // full step + inverse dynamics at node 0 (mpc.cpp:305-330)
     g_stage = kRnea;

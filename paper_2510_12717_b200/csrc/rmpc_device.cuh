@@ -89,6 +89,7 @@ struct KParams {
   const float* prev_z;
   rmpc_solution* out;
   float* z_out;
+  uint8_t* act_out;  // optional: final active set, (T+1) x NSLOT codes per agent
   unsigned long long* prof;  // [RMPC_NUM_STAGES] cycle accumulators (profile only)
 };
 

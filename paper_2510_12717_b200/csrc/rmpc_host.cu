@@ -451,6 +451,31 @@ int32_t rmpc_solve_device(rmpc_handle* h, const rmpc_state* d_states, const rmpc
   return RMPC_OK;
 }
 
+int32_t rmpc_solve_device_active_set(rmpc_handle* h, const rmpc_state* d_states, const rmpc_command* d_cmds,
+                                     const rmpc_gait* d_gaits, rmpc_solution* d_out, uint8_t* d_active,
+                                     void* stream) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (h->shards.size() != 1) { h->err = "rmpc_solve_device_active_set: single-device handles only"; return RMPC_ERR_INVALID_ARG; }
+  if (!d_states || !d_cmds || !d_gaits || !d_out || !d_active) { h->err = "rmpc_solve_device_active_set: NULL array"; return RMPC_ERR_STRUCTURAL; }
+  Shard& sh = h->shards[0];
+  cudaSetDevice(sh.device);
+  rmpc_dev::KParams P = make_params(*h);
+  P.n_agents = h->n;
+  P.states = d_states;
+  P.cmds = d_cmds;
+  P.gaits = d_gaits;
+  P.out = d_out;
+  P.act_out = d_active;
+  P.prof = sh.d_prof;
+  P.warm_start = 0;
+  const int rc = rmpc_launch_rti(P, stream ? stream : (void*)sh.stream);
+  if (rc != 0) {
+    h->err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+  }
+  return RMPC_OK;
+}
+
 int32_t rmpc_size(const rmpc_handle* h) { return h ? h->n : 0; }
 int32_t rmpc_workers(const rmpc_handle* h) { return h ? (int32_t)h->shards.size() : 0; }
 int32_t rmpc_horizon(const rmpc_handle* h) { return h ? h->NT : 0; }

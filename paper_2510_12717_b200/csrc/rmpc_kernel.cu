@@ -1636,6 +1636,14 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
       if (lane < 8) prim = fmaxf(prim, fabsf(o1 - rw[32 + lane].z) / d[32 + lane]);
       if (i == 0 && lane < NINIT)
         prim = fmaxf(prim, fabsf(o2 - sm.R(-1)[INIT0 + lane].z) / sm.D(-1)[INIT0 + lane]);
+      if (P.act_out) {  // active set of the final iterate (scaled space, where the clamp acts)
+        uint8_t* ao = P.act_out + (size_t)agent * (NT + 1) * NSLOT;
+        auto code = [](float4 r) -> uint8_t { return r.x == r.y ? 3 : (r.z == r.x ? 1 : (r.z == r.y ? 2 : 0)); };
+        ao[(i + 1) * NSLOT + lane] = code(rw[lane]);
+        if (lane < 8) ao[(i + 1) * NSLOT + 32 + lane] = code(rw[32 + lane]);
+        if (i == 0 && lane < NSLOT) ao[lane] = code(sm.R(-1)[lane < NSLOT ? lane : 0]);
+        if (i == 0 && lane < NSLOT - 32) ao[32 + lane] = code(sm.R(-1)[32 + lane]);
+      }
       const float aty = col_view<OpSum, TV_Y>(sm, i, T, B, rho);
       const uint32_t bits = sm.flags[i];
       if (lane < NV) {
@@ -1698,6 +1706,8 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
     if (warp != 0) return;
     if (P.z_out != nullptr)
       for (int k = lane; k < NT * NV; k += 32) P.z_out[(size_t)agent * NT * NV + k] = 0.f;
+    if (P.act_out != nullptr)
+      for (int k = lane; k < (NT + 1) * NSLOT; k += 32) P.act_out[(size_t)agent * (NT + 1) * NSLOT + k] = 3;
   }
   prof_mark(P, lane, 6, t0);
   if (lane == 0) P.out[agent] = out;

@@ -26,7 +26,7 @@ _VP = C.c_void_p
 _I = C.c_int32
 
 EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_destroy",
-           "rmpc_solve", "rmpc_solve_device", "rmpc_size", "rmpc_workers", "rmpc_horizon",
+           "rmpc_solve", "rmpc_solve_device", "rmpc_solve_device_active_set", "rmpc_size", "rmpc_workers", "rmpc_horizon",
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
            "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak")
@@ -55,6 +55,8 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_solve.restype = _I
     L.rmpc_solve_device.argtypes = [_VP] * 9
     L.rmpc_solve_device.restype = _I
+    L.rmpc_solve_device_active_set.argtypes = [_VP] * 7
+    L.rmpc_solve_device_active_set.restype = _I
     for f in ("rmpc_size", "rmpc_workers", "rmpc_horizon"):
         getattr(L, f).argtypes = [_VP]
         getattr(L, f).restype = _I
@@ -197,6 +199,20 @@ class BatchRunner:
                 s = 1  # cudaStreamLegacy: NULL would select the runner's own stream
         rc = self._lib.rmpc_solve_device(self._h, p(states), p(cmds), p(gaits), p(prev), p(prev_z),
                                          p(out), p(z_out), s)
+        if rc != 0:
+            self._err(rc)
+
+    def solve_device_active_set(self, states, cmds, gaits, out, active, stream=None):
+        """rmpc_solve_device plus the final iterate's active set: `active` is a uint8 CUDA
+        tensor of n x (T+1) x 40 codes (0 inactive, 1 at lo, 2 at hi, 3 equality / no row)."""
+        def p(t):
+            return t if isinstance(t, int) else t.data_ptr()
+        s = None
+        if stream is not None:
+            s = stream if isinstance(stream, int) else stream.cuda_stream
+            if s == 0:
+                s = 1
+        rc = self._lib.rmpc_solve_device_active_set(self._h, p(states), p(cmds), p(gaits), p(out), p(active), s)
         if rc != 0:
             self._err(rc)
 

@@ -197,3 +197,39 @@ def test_repeated_solves_are_bit_identical(T):
     for _ in range(4):
         sol, z = br.solve(st, cm, ga, want_z=True)
         assert sol.tobytes() == first.tobytes() and z.tobytes() == z0.tobytes()
+
+
+@pytest.mark.parametrize("kind,T,n", [("random", 10, 2048), ("mixed", 10, 2048), ("random", 20, 256)])
+def test_active_set_matches_oracle(oracle, kind, T, n):
+    """The north star's active-set criterion: which inequality rows (friction cones, joint boxes)
+    sit at a bound at the final iterate, compared row by row on the device's slot grid.  A row
+    may differ only where the FP64 oracle's unclamped value is within 1e-4 (scaled space) of a
+    bound -- FP32 rounding decides those -- and the equality / absent pattern is identical."""
+    import torch
+    m, s = default_model(), default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, kind, seed=21, model=m, settings=s)
+    if kind == "random":  # push joints toward their limits, fast joints, fast commands:
+        rng = np.random.default_rng(22)  # joint boxes and friction cones become active
+        st[:, 3:9] += rng.uniform(-0.8, 0.8, (n, 6))
+        st[:, 12:18] = rng.uniform(-15.0, 15.0, (n, 6))
+        cm[:, 1] *= 2.5
+    br = R.BatchRunner(n, m, s)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(np.ascontiguousarray(a)).to(dev) for a in (st, cm, ga)]
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    act = torch.zeros(n * (T + 1) * 40, dtype=torch.uint8, device=dev)
+    br.solve_device_active_set(*d, out, act, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    g = act.cpu().numpy().reshape(n, T + 1, 40).astype(np.int8)
+    r, margin = oracle.active_set_batch(m, s, st, cm, ga, workers=16)
+    sol = out.cpu().numpy().view(SOLUTION_DTYPE)
+    assert (sol["status"] == 0).all()
+    assert ((g == 3) == (r == 3)).all()  # same equality / absent rows
+    ineq = r != 3
+    mism = (g != r) & ineq
+    active = ((r == 1) | (r == 2)) & ineq
+    print(kind, T, "inequality rows", int(ineq.sum()), "active", int(active.sum()),
+          "mismatches", int(mism.sum()), "max margin at a mismatch",
+          float(margin[mism].max()) if mism.any() else 0.0)
+    assert active.sum() > 0
+    assert (margin[mism] <= 1e-4).all()

@@ -270,3 +270,22 @@ def test_fp64_flop_count_stable(oracle, model):
                            standing_gait_row())
     assert 0.5e6 < by.sum() < 1.5e6
     assert np.argmax(by) == 5  # admm_iters dominates, as in the reference
+
+
+def test_active_set_grid_of_the_restated_qp(oracle):
+    """The oracle's final-iterate active set on the device's slot grid: integration / dynamics /
+    initial-state / swing zero-force rows are equalities (3), friction cones (stance, one-sided)
+    and joint boxes (nodes >= 1) are inequalities (0/1/2), node 0 has no boxes or velocity
+    rows, and the last node has no interval rows."""
+    import numpy as np
+    import paper_2510_12717_b200 as R
+    m, s = R.default_model(), R.default_settings(10)
+    st, cm, ga = R.synthetic_batch(16, "mixed", seed=4, model=m, settings=s)
+    act, margin = oracle.active_set_batch(m, s, st, cm, ga, workers=4)
+    assert act.shape == (16, 11, 40) and set(np.unique(act)) <= {0, 1, 2, 3}
+    assert (act[:, 0, 12:30] == 3).all()            # initial-state rows
+    assert (act[:, 1:10, 0:12] == 3).all()          # integration + dynamics (intervals 0..8)
+    assert (act[:, 10, 0:12] == 3).all()            # last node: no interval rows (absent)
+    assert (act[:, 2:11, 28:40] != 3).all()         # joint boxes from node 1 on
+    assert (act[:, 1, 28:40] == 3).all()            # node 0: no boxes
+    assert (margin >= 0).all()

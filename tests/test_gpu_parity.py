@@ -233,3 +233,8 @@ def test_active_set_matches_oracle(oracle, kind, T, n):
           float(margin[mism].max()) if mism.any() else 0.0)
     assert active.sum() > 0
     assert (margin[mism] <= 1e-4).all()
+    # and the solution itself on these harder (constraint-active) states
+    ref, _, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=16)
+    c = compare(sol, ref)
+    assert c["status_equal"]
+    assert c["tau"].max() <= TOL and c["f0"].max() <= TOL and c["v"].max() <= TOL

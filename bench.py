@@ -336,6 +336,16 @@ def main():
     e2e_ms = float(max_over_ranks([(t1 - t0) * 1e3 / args.steps])[0])
     tm = br.last_timing()
     ok = int(np.sum(h_out["status"] == 0))
+    # the full MpcSolution equivalent: the records plus the whole planned trajectory z*
+    h_z = torch.zeros((n, T, 26), dtype=torch.float32).pin_memory().numpy()
+    br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z)
+    t1 = time.perf_counter()
+    barrier()
+    e2e_z_ms = float(max_over_ranks([(t1 - t0) * 1e3 / args.steps])[0])
 
     # ---- roofline: FP32 CUDA-core bound
     peak = fma_peak_tflops(local)
@@ -385,6 +395,10 @@ def main():
             "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "solves/s",
                     "h2d_bytes_per_step": n * (144 + 24 + 56), "d2h_bytes_per_step": n * 140,
                     "ms_per_step": e2e_ms, "api": "rmpc_solve (C ABI), pinned host buffers",
+                    "with_z_star": {"value": n * world / (e2e_z_ms * 1e-3), "ms_per_step": e2e_z_ms,
+                                    "d2h_bytes_per_step": n * (140 + T * 26 * 4),
+                                    "note": "also returns the planned trajectory z* (T x 26 FP32), "
+                                            "everything the reference's MpcSolution carries"},
                     "last_timing_ms": {"h2d": tm["h2d_ms"], "kernel": tm["kernel_ms"], "d2h": tm["d2h_ms"],
                                        "total": tm["total_ms"]}},
             "roofline": roofline,

@@ -158,7 +158,10 @@ def cpu_baseline_run(args, n_sample, steps=1):
     for _ in range(steps):
         _, _, _, wall = O.solve_batch(m, s, st, cm, ga, workers=cores, want_z=False)
         walls.append(wall)
-    return n_sample * steps / (sum(walls) * 1e-3), cores, walls
+    # and the 1-worker figure (BatchRunner with workers = 1) on a smaller slice
+    k = min(256, n_sample)
+    _, _, _, wall1 = O.solve_batch(m, s, st[:k], cm[:k], ga[:k], workers=1, want_z=False)
+    return n_sample * steps / (sum(walls) * 1e-3), cores, walls, k / (wall1 * 1e-3)
 
 
 def run_reference_arm(args):
@@ -371,8 +374,9 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, walls = cpu_baseline_run(args, min(args.cpu_sample, n), steps=2)
+            v, cores, walls, v1 = cpu_baseline_run(args, min(args.cpu_sample, n), steps=2)
             cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": "port",
+                   "single_thread_value": v1,
                    "sample": f"2 ticks x {min(args.cpu_sample, n)} agents of the same workload, "
                              f"{cores} host threads ({cpu_model()}); FP64 oracle restating the "
                              f"reference algorithm incl. per-solve ordering + LDL^T"}

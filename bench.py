@@ -359,6 +359,8 @@ def main():
         "bound": "fp32", "achieved": achieved, "peak": peak, "unit": "TFLOP/s",
         "frac": (achieved / peak) if (achieved and peak) else None,
         "traffic": traffic.get("dram_bytes_per_launch") if traffic else None,
+        "ncu_executed_fp32_tflops": traffic.get("executed_fp32_tflops") if traffic else None,
+        "ncu_executed_fp32_frac": traffic.get("executed_fp32_frac_of_peak") if traffic else None,
         "peak_source": "measured FP32 FMA loop on this GPU (rmpc_fma_peak), of measured",
         "flop_alg_per_solve": fl,
         "note": "CUDA-core FP32 kernel (no GEMM, HBM traffic ~0.4 KB/agent): neither the HBM nor "

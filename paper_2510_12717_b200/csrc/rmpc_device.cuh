@@ -55,7 +55,10 @@ constexpr int C_ZERO = 27;    // an entry that is always 0
 
 // Split of the horizon for the two-sided (twisted) elimination: warp 0 owns nodes [0, m)
 // eliminated top-down plus the middle node m, warp 1 owns (m, T) eliminated bottom-up.
-__host__ __device__ inline int mid_node(int NT) { return NT >= 2 ? (NT - 2) / 2 : 0; }
+// m = (T-1)/2 balances the two chains: even T (10): the top eliminates T/2-1 nodes plus the
+// middle, the bottom T/2 (forward 5 | 5, backward 4 | 5); odd T (5): (T-1)/2 each plus the
+// middle.  Both halves hold at most ceil(T/2) node blocks either way.
+__host__ __device__ inline int mid_node(int NT) { return NT >= 2 ? (NT - 1) / 2 : 0; }
 
 // Per-node vectors, V_STRIDE floats each; [26, 28) are spare (gamma of the forward sweep).
 constexpr int V_X = 0;    // ADMM x (scaled space)

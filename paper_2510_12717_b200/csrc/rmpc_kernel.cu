@@ -753,7 +753,7 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
       n.cv = col_view<OpMax, TV_D>(src, i, T, B);
       return n;
     };
-    auto update = [&](int i, const Norms& n) {  // writes only the destination copies
+    auto update_rows = [&](int i, const Norms& n) {  // writes only the destination copies
       const float* d = src.D(i);
       float* dn = dst + (i + 1) * NSLOT;
       dn[lane] = d[lane] * inv_sqrt1(d[lane] * n.o0);
@@ -762,21 +762,39 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
         const float* d0 = src.D(-1) + INIT0;
         dst[INIT0 + lane] = d0[lane] * inv_sqrt1(d0[lane] * n.o2);
       }
+    };
+    auto update_cols = [&](int i, const Norms& n) {
       if (lane < NV) {
         const float e = sm.V(i, es)[lane];
         const float pd = wl * (float)P.dt[i];
         sm.V(i, ed)[lane] = e * inv_sqrt1(e * fmaxf(fabsf(pd) * e, n.cv));
       }
     };
-    // nodes are independent within a pass: two per iteration, all loads ahead of the stores
+    auto update = [&](int i, const Norms& n) {
+      update_rows(i, n);
+      update_cols(i, n);
+    };
+    // nodes are independent within a pass: two per iteration, all loads ahead of the stores;
+    // for odd T the last node is split: warp 0 its row scales, warp 1 its column scales
+    const int ne = NT & ~1;
     int i = warp;
 #pragma unroll 1
-    for (; i + 2 < NT; i += 4) {
+    for (; i + 2 < ne; i += 4) {
       const Norms a = norms(i), b = norms(i + 2);
       update(i, a);
       update(i + 2, b);
     }
-    if (i < NT) update(i, norms(i));
+    if (i < ne) update(i, norms(i));
+    if (NT & 1) {
+      Norms n;
+      if (warp == 0) {
+        row_view<OpMax>(src, NT - 1, lane, es, n.o0, n.o1, n.o2);
+        update_rows(NT - 1, n);
+      } else {
+        n.cv = col_view<OpMax, TV_D>(src, NT - 1, T, B);
+        update_cols(NT - 1, n);
+      }
+    }
     pair_sync(sm);  // every norm of the next pass uses the scales of this one
   }
   if (P.ruiz_iters & 1) {  // the last pass wrote the second copies
@@ -1139,7 +1157,6 @@ __device__ bool factorize(const KParams& P, const Sm& sm, int lane, int warp) {
   const int nbot = NT - 1 - m;
   const int steps = (m > nbot ? m : nbot) + 1;
   const int j = lane;
-  float* bc = sm.bc + 64 * warp;
   bool good = true;
   float Y[NV];  // update of the next node to eliminate (top: rows/cols < 18 non-zero)
 #pragma unroll

@@ -238,3 +238,24 @@ def test_active_set_matches_oracle(oracle, kind, T, n):
     c = compare(sol, ref)
     assert c["status_equal"]
     assert c["tau"].max() <= TOL and c["f0"].max() <= TOL and c["v"].max() <= TOL
+
+
+SWEEP = [(k, T, seed) for seed, (k, T) in enumerate(
+    [("random", 4), ("mixed", 6), ("standing", 7), ("random", 8), ("mixed", 9), ("random", 11),
+     ("mixed", 13), ("standing", 14), ("random", 15), ("mixed", 16), ("random", 17), ("mixed", 18),
+     ("random", 22), ("mixed", 24), ("random", 26), ("mixed", 28), ("standing", 30)])]
+
+
+@pytest.mark.parametrize("kind,T,seed", SWEEP)
+def test_parity_sweep_over_horizons(oracle, kind, T, seed):
+    """Every horizon shape the CTA planner distinguishes (TMEM-only, one or two spilled node
+    blocks per warp, 2 to 6 agents per CTA, odd/even middle split) against the oracle."""
+    n = 96
+    m, s = default_model(), default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, kind, seed=100 + seed, model=m, settings=s)
+    sol, z = R.BatchRunner(n, m, s).solve(st, cm, ga, want_z=True)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=16)
+    c = compare(sol, ref, z, zr)
+    assert c["status_equal"] and c["n_ok"] == n
+    assert c["tau"].max() <= TOL and c["f0"].max() <= TOL and c["v"].max() <= TOL
+    assert c["z"].max() <= 1e-3

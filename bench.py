@@ -82,6 +82,75 @@ def ncu_traffic():
         return None
 
 
+class NvmlClockSampler:
+    """SM clock and clocks-event (throttle) reasons polled through NVML every ~1 ms on a host
+    thread for exactly the timed region (nvidia-smi's 200 ms period would see one or two
+    samples of a ~30 ms region).  Falls back to ClockSampler when NVML is unavailable."""
+
+    REASONS = (("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake", "nvmlClocksEventReasonHwPowerBrakeSlowdown"))
+
+    def __init__(self, device):
+        import threading
+        import pynvml as N
+        self.N = N
+        N.nvmlInit()
+        # torch's device index is the CUDA ordinal; NVML enumerates every GPU of the box in PCI
+        # order -> match the CUDA device's PCI bus / device numbers
+        import torch
+        props = torch.cuda.get_device_properties(device)
+        bus, dev = getattr(props, "pci_bus_id", None), getattr(props, "pci_device_id", None)
+        self.h = None
+        if bus is not None:
+            for k in range(N.nvmlDeviceGetCount()):
+                h = N.nvmlDeviceGetHandleByIndex(k)
+                pi = N.nvmlDeviceGetPciInfo(h)
+                if pi.bus == bus and (dev is None or pi.device == dev):
+                    self.h = h
+                    break
+        if self.h is None:
+            self.h = N.nvmlDeviceGetHandleByIndex(device)
+        self.samples = []
+        self.stop_ev = threading.Event()
+        self.t = threading.Thread(target=self._run, daemon=True)
+
+    def _run(self):
+        N = self.N
+        while not self.stop_ev.is_set():
+            try:
+                sm = N.nvmlDeviceGetClockInfo(self.h, N.NVML_CLOCK_SM)
+                rs = N.nvmlDeviceGetCurrentClocksEventReasons(self.h)
+                self.samples.append((sm, rs))
+            except Exception:
+                pass
+            time.sleep(0.001)
+
+    def start(self):
+        self.t.start()
+
+    def stop(self):
+        self.stop_ev.set()
+        self.t.join()
+        N = self.N
+        if not self.samples:
+            return None
+        try:
+            mx = N.nvmlDeviceGetMaxClockInfo(self.h, N.NVML_CLOCK_SM)
+        except Exception:
+            mx = max(sm for sm, _ in self.samples)
+        reasons = set()
+        for _, rs in self.samples:
+            for name, attr in self.REASONS:
+                bit = getattr(N, attr, 0)
+                if bit and rs & bit:
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm for sm, _ in self.samples), "sm_max_mhz": float(mx),
+                "reasons": sorted(reasons), "samples": len(self.samples), "source": "nvml, ~1 ms, timed region only"}
+
+
 class ClockSampler:
     """nvidia-smi clocks / throttle reasons sampled every 200 ms during the timed region."""
 
@@ -302,13 +371,15 @@ def main():
 
     # ---- device-resident timed region: K steps, CUDA events on the launching stream, L2
     #      flushed between steps (outside the per-step events)
-    clocks = ClockSampler(local)
+    try:
+        clocks = NvmlClockSampler(local)
+    except Exception:
+        clocks = ClockSampler(local)
     ev = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
           for _ in range(args.steps)]
     barrier()
     torch.cuda.synchronize()
     clocks.start()
-    time.sleep(0.3)
     with torch.cuda.stream(stream):
         for k in range(args.steps):
             flush.zero_()

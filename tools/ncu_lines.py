@@ -85,11 +85,11 @@ def main():
         wav[key] += float(r[cw] or 0)
         wex[key] += float(r[cx] or 0)
     ts, ti = sum(samp.values()), sum(inst.values())
-    kern = os.path.join(ROOT, "paper_2510_12717_b200", "csrc", "rmpc_kernel.cu")
-    table = functions(kern)
+    csrc = os.path.join(ROOT, "paper_2510_12717_b200", "csrc")
+    tables = {f: functions(os.path.join(csrc, f)) for f in os.listdir(csrc) if f.endswith((".cu", ".cuh"))}
     fs, fi = collections.Counter(), collections.Counter()
     for (f, n), v in samp.items():
-        key = func_of(table, n) if f == "rmpc_kernel.cu" else f
+        key = f"{f}:{func_of(tables[f], n)}" if f in tables else f
         fs[key] += v
         fi[key] += inst[(f, n)]
     print("by function (innermost source function after inlining):")

@@ -91,7 +91,7 @@ __device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, c
   const char* tb = MODE == TV_D ? reinterpret_cast<const char*>(sm.D(i))
                    : (MODE == TV_T ? reinterpret_cast<const char*>(sm.T(i))
                                    : reinterpret_cast<const char*>(sm.R(i)));
-  float acc0 = Op::id(), acc1 = Op::id();
+  float acc[4] = {Op::id(), Op::id(), Op::id(), Op::id()};  // four chains: 5 deep instead of 9
 #pragma unroll
   for (int k = 0; k < 17; ++k) {
     const float c = *reinterpret_cast<const float*>(cb + B.cb[k]);
@@ -102,10 +102,9 @@ __device__ __forceinline__ float col_view(const Sm& sm, int i, const Terms& T, c
     } else {
       v = *reinterpret_cast<const float*>(tb + B.tb[k]);
     }
-    if (k & 1) acc1 = Op::comb(acc1, c, v);
-    else acc0 = Op::comb(acc0, c, v);
+    acc[k & 3] = Op::comb(acc[k & 3], c, v);
   }
-  return Op::red(acc0, acc1);
+  return Op::red(Op::red(acc[0], acc[1]), Op::red(acc[2], acc[3]));
 }
 
 // ------------------------------------------------------------------------- full row view

@@ -107,7 +107,68 @@ void rmpc_policy_destroy(rmpc_policy* policy);
 int32_t rmpc_policy_forward_device(rmpc_policy* policy, int32_t n, const double* d_obs,
                                    double* d_mean, double* d_value, void* stream);
 
-/* sizeof of the env ABI structs (0 config, 1 body) for binding-side layout checks. */
+/* Parameter count (pi + value + log_std, PolicyParams::num_params) and host copies of the
+ * device parameters in flatten_policy order (ppo.cpp:144-162). */
+int32_t rmpc_policy_num_params(const rmpc_policy* policy);
+int32_t rmpc_policy_get_params(rmpc_policy* policy, double* params, int32_t n_params);
+int32_t rmpc_policy_set_params(rmpc_policy* policy, const double* params, int32_t n_params);
+
+/* ---- PPO batch (/root/reference/proj/src/ppo.cpp:28-276), FP64. ---- */
+
+/* PpoConfig (ppo.hpp:14-24), the update part. */
+typedef struct rmpc_ppo_config {
+  double gamma, lam_gae, clip_eps;   /* 0.99, 0.95, 0.2 */
+  int32_t epochs, minibatches;       /* 4, 4 */
+  double lr, entropy_coef, value_coef, max_grad_norm;  /* 3e-4, 0, 0.5, 1 */
+} rmpc_ppo_config;
+/* PpoLossInfo (ppo.hpp:70-75) and PpoUpdateStats (ppo.hpp:103-108). */
+typedef struct rmpc_ppo_loss_info {
+  double total, surrogate, value_loss, entropy;
+} rmpc_ppo_loss_info;
+typedef struct rmpc_ppo_update_stats {
+  double loss, surrogate, value_loss, entropy;
+} rmpc_ppo_update_stats;
+
+void rmpc_ppo_config_default(rmpc_ppo_config* cfg);
+
+/* ppo_loss (ppo.cpp:79-135) over n samples (obs n x obs_dim, actions n x act_dim, old_logp /
+ * advantages / returns n; device pointers): the loss terms into d_info (device, one struct) and,
+ * if d_grads is non-NULL, the gradient of every parameter in flatten_grads order
+ * (rmpc_policy_num_params doubles, overwritten).  Deterministic: a fixed-order reduction. */
+int32_t rmpc_ppo_loss_device(rmpc_policy* policy, int32_t n, const double* d_obs,
+                             const double* d_actions, const double* d_old_logp,
+                             const double* d_advantages, const double* d_returns,
+                             const rmpc_ppo_config* cfg, double* d_grads,
+                             rmpc_ppo_loss_info* d_info, void* stream);
+
+/* gae_advantages (ppo.cpp:28-45): steps x envs row-major, raw (unnormalised) advantages and
+ * returns. */
+int32_t rmpc_gae_device(int32_t steps, int32_t envs, const double* d_rewards, const double* d_values,
+                        const double* d_dones, const double* d_bootstrap, double gamma, double lam,
+                        double* d_advantages, double* d_returns, void* stream);
+
+/* AdamOptimizer(num_params, lr) (ppo.cpp:181-191, betas 0.9 / 0.999, eps 1e-8) bound to a
+ * policy: its moment vectors live on the policy's device. */
+typedef struct rmpc_adam rmpc_adam;
+int32_t rmpc_adam_create(rmpc_policy* policy, double lr, rmpc_adam** out);
+void rmpc_adam_destroy(rmpc_adam* adam);
+
+/* Rng(seed, stream) (rng.hpp:15-25) as its four xoshiro256++ words, for rmpc_ppo_update_device. */
+void rmpc_rng_seed(uint64_t seed, uint64_t stream, uint64_t state[4]);
+
+/* ppo_update (ppo.cpp:193-276) on the policy's device parameters: GAE, advantage
+ * normalisation, then epochs x minibatches of {shuffle (Fisher-Yates on rng_state, advanced
+ * exactly like the reference's update_rng), ppo_loss + gradient, clip to max_grad_norm, Adam}.
+ * The rollout is device-resident, steps x envs (obs steps x envs x obs_dim, actions
+ * steps x envs x act_dim).  Blocks until done; stats on the host. */
+int32_t rmpc_ppo_update_device(rmpc_policy* policy, rmpc_adam* adam, int32_t steps, int32_t envs,
+                               const double* d_obs, const double* d_actions, const double* d_logp,
+                               const double* d_values, const double* d_rewards, const double* d_dones,
+                               const double* d_bootstrap, const rmpc_ppo_config* cfg,
+                               uint64_t rng_state[4], rmpc_ppo_update_stats* stats, void* stream);
+
+/* sizeof of the env ABI structs (0 config, 1 body, 2 ppo config, 3 loss info, 4 update stats)
+ * for binding-side layout checks. */
 int32_t rmpc_env_sizeof(int32_t which);
 
 #ifdef __cplusplus

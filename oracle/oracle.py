@@ -363,3 +363,78 @@ def active_set_batch(model: Model, settings: Settings, states, cmds, gaits, work
     if rc != 0:
         raise ValueError(f"oracle_active_set_batch: {rc}")
     return act, margin
+
+
+# ---------------------------------------------------------------- PPO batch (ppo.cpp:28-276)
+class PpoConfig(C.Structure):
+    _fields_ = [("gamma", C.c_double), ("lam_gae", C.c_double), ("clip_eps", C.c_double), ("epochs", C.c_int32),
+                ("minibatches", C.c_int32), ("lr", C.c_double), ("entropy_coef", C.c_double),
+                ("value_coef", C.c_double), ("max_grad_norm", C.c_double)]
+
+
+def ppo_config(**overrides) -> PpoConfig:
+    c = PpoConfig()
+    lib().oracle_ppo_config_default(C.byref(c))
+    for k, v in overrides.items():
+        setattr(c, k, v)
+    return c
+
+
+def ppo_loss(params, obs, actions, old_logp, adv, ret, cfg=None, act=6, hidden=64, grads=True):
+    """ppo_loss: ((total, surrogate, value_loss, entropy), flatten_grads vector or None)."""
+    p = _f64(params)
+    o, a = _f64(obs), _f64(actions)
+    n, od = o.shape
+    cfg = cfg or ppo_config()
+    info = (C.c_double * 4)()
+    g = np.zeros(p.size) if grads else None
+    lib().oracle_ppo_loss(ptr(p), od, act, hidden, n, ptr(o), ptr(a), ptr(_f64(old_logp)), ptr(_f64(adv)),
+                          ptr(_f64(ret)), C.byref(cfg), ptr(g) if g is not None else None, p.size, info)
+    return tuple(info), g
+
+
+def gae(rewards, values, dones, bootstrap, gamma=0.99, lam=0.95):
+    r, v, d, b = _f64(rewards), _f64(values), _f64(dones), _f64(bootstrap)
+    T, E = r.shape
+    adv, ret = np.zeros((T, E)), np.zeros((T, E))
+    lib().oracle_gae(T, E, ptr(r), ptr(v), ptr(d), ptr(b), C.c_double(gamma), C.c_double(lam), ptr(adv), ptr(ret))
+    return adv, ret
+
+
+class AdamState:
+    def __init__(self, n_params):
+        self.m, self.v, self.t = np.zeros(n_params), np.zeros(n_params), C.c_int32(0)
+
+
+def rng_words(seed, stream):
+    """Rng(seed, stream)'s xoshiro256++ state (rng.hpp:15-25)."""
+    mask = (1 << 64) - 1
+
+    def splitmix(x):
+        x = (x + 0x9E3779B97F4A7C15) & mask
+        x = ((x ^ (x >> 30)) * 0xBF58476D1CE4E5B9) & mask
+        x = ((x ^ (x >> 27)) * 0x94D049BB133111EB) & mask
+        return x ^ (x >> 31)
+
+    x = seed ^ splitmix((stream + 0x9E3779B97F4A7C15) & mask)
+    out = (C.c_uint64 * 4)()
+    for k in range(4):
+        x = (x + 0x9E3779B97F4A7C15) & mask
+        out[k] = splitmix(x)
+    return out
+
+
+def ppo_update(params, adam: AdamState, obs, actions, logp, values, rewards, dones, bootstrap, cfg=None, rng=None,
+               act=6, hidden=64):
+    """ppo_update in place on params (float64 array) / adam / rng; returns (loss, surrogate,
+    value_loss, entropy)."""
+    assert params.dtype == np.float64 and params.flags["C_CONTIGUOUS"]
+    o, a = _f64(obs), _f64(actions)
+    T, E = _f64(rewards).shape
+    cfg = cfg or ppo_config()
+    rng = rng if rng is not None else rng_words(0, 0x0272)
+    st = (C.c_double * 4)()
+    lib().oracle_ppo_update(ptr(params), o.shape[-1], act, hidden, T, E, ptr(o), ptr(a), ptr(_f64(logp)),
+                            ptr(_f64(values)), ptr(_f64(rewards)), ptr(_f64(dones)), ptr(_f64(bootstrap)),
+                            C.byref(cfg), ptr(adam.m), ptr(adam.v), C.byref(adam.t), params.size, rng, st)
+    return tuple(st)

@@ -7,6 +7,7 @@
 
 #include "rmpc_oracle.hpp"
 #include "rmpc_oracle_env.hpp"
+#include "rmpc_oracle_ppo.hpp"
 #include "rmpc_oracle_rng.hpp"
 #include "oracle_flops.hpp"
 
@@ -399,6 +400,41 @@ void oracle_policy_forward_batch(const double* params, int32_t obs, int32_t act,
   for (int a = 0; a < n; ++a)
     policy_forward_flat(params, obs, act, hidden, o + (size_t)obs * a, mean + (size_t)act * a, value + a);
 }
+
+// ppo_loss (ppo.cpp:79-135); grads (num_params) is zeroed here and may be null.
+void oracle_ppo_loss(const double* params, int32_t obs, int32_t act, int32_t hidden, int32_t n, const double* o,
+                     const double* a, const double* old_logp, const double* adv, const double* ret,
+                     const rmpc_ppo_config* cfg, double* grads, int32_t n_params, rmpc_ppo_loss_info* info) {
+  if (grads) std::fill(grads, grads + n_params, 0.0);
+  *info = ppo_loss(params, obs, act, hidden, n, o, a, old_logp, adv, ret, *cfg, grads);
+}
+
+void oracle_gae(int32_t T, int32_t E, const double* rew, const double* val, const double* done, const double* boot,
+                double gamma, double lam, double* adv, double* ret) {
+  gae(T, E, rew, val, done, boot, gamma, lam, adv, ret);
+}
+
+// ppo_update (ppo.cpp:193-276) with the Adam state (m, v, t) and the update Rng words carried
+// by the caller across calls.
+void oracle_ppo_update(double* params, int32_t obs, int32_t act, int32_t hidden, int32_t T, int32_t E,
+                       const double* o, const double* a, const double* logp, const double* values,
+                       const double* rewards, const double* dones, const double* boot, const rmpc_ppo_config* cfg,
+                       double* adam_m, double* adam_v, int32_t* adam_t, int32_t n_params, uint64_t rng_state[4],
+                       rmpc_ppo_update_stats* stats) {
+  Adam adam(n_params, cfg->lr);
+  std::copy(adam_m, adam_m + n_params, adam.m.begin());
+  std::copy(adam_v, adam_v + n_params, adam.v.begin());
+  adam.t = *adam_t;
+  Rng rng(0, 0);
+  for (int k = 0; k < 4; ++k) rng.s[k] = rng_state[k];
+  *stats = ppo_update(params, obs, act, hidden, T, E, o, a, logp, values, rewards, dones, boot, *cfg, adam, rng);
+  std::copy(adam.m.begin(), adam.m.end(), adam_m);
+  std::copy(adam.v.begin(), adam.v.end(), adam_v);
+  *adam_t = adam.t;
+  for (int k = 0; k < 4; ++k) rng_state[k] = rng.s[k];
+}
+
+void oracle_ppo_config_default(rmpc_ppo_config* c) { ppo_config_default(c); }
 
 // Active set of the final ADMM iterate per agent on the device's (node + 1, slot) grid:
 // act (n x (T+1) x 40 int8), margin (same shape, FP64, scaled space).  Cold start.

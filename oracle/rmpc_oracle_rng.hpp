@@ -32,6 +32,7 @@ struct Rng {
   }
   double uniform() { return static_cast<double>(next() >> 11) * 0x1.0p-53; }
   double uniform(double lo, double hi) { return lo + (hi - lo) * uniform(); }  // rng.hpp:41
+  int uniform_int(int n) { return static_cast<int>(next() % static_cast<uint64_t>(n)); }  // rng.hpp:43
 };
 
 

@@ -12,10 +12,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "librmpc_b200.so")
-SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rmpc_kernel.cu", "rmpc_host.cu", "rmpc_env.cu", "rmpc_policy.cu")]
+SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rmpc_kernel.cu", "rmpc_host.cu", "rmpc_env.cu", "rmpc_policy.cu",
+                                                       "rmpc_ppo.cu")]
 HEADERS = [os.path.join(HERE, "csrc", h) for h in ("rmpc_device.cuh", "rmpc_kin.cuh", "rmpc_sm.cuh",
                                                    "rmpc_views.cuh", "rmpc_model.cuh", "rmpc_setup.cuh",
-                                                   "rmpc_ruiz.cuh", "rmpc_factor.cuh", "rmpc_admm.cuh")] + \
+                                                   "rmpc_ruiz.cuh", "rmpc_factor.cuh", "rmpc_admm.cuh",
+                                                   "rmpc_policy.cuh")] + \
     [os.path.join(ROOT, "include", h) for h in ("rmpc_b200.h", "rmpc_b200_env.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]

@@ -463,6 +463,9 @@ int32_t rmpc_env_sizeof(int32_t which) {
   switch (which) {
     case 0: return (int32_t)sizeof(rmpc_env_config);
     case 1: return (int32_t)sizeof(rmpc_body);
+    case 2: return (int32_t)sizeof(rmpc_ppo_config);
+    case 3: return (int32_t)sizeof(rmpc_ppo_loss_info);
+    case 4: return (int32_t)sizeof(rmpc_ppo_update_stats);
     default: return -1;
   }
 }

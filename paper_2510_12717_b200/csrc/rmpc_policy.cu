@@ -16,21 +16,11 @@
 #include <new>
 #include <vector>
 
-#include "../../include/rmpc_b200_env.h"
+#include "rmpc_policy.cuh"
 
 namespace rmpc_policy_dev {
 
-constexpr int WARPS = 8, MAXH = 64, MAXIO = 64;
-
-struct Net {
-  int in[4], out[4];   // layer shapes
-  int w[4], b[4];      // offsets (doubles) into the shared weight block
-};
-
-struct PolicyParams {
-  int obs, act, hidden, total;  // total doubles of both trunks (log_std excluded)
-  Net pi, vf;
-};
+constexpr int WARPS = 8;
 
 // One trunk for the agent held by this warp; x (per-warp smem, MAXIO) holds the input and is
 // overwritten layer by layer.  Returns, in lane j, outputs j (o0) and j + 32 (o1).
@@ -94,13 +84,6 @@ __global__ void __launch_bounds__(32 * WARPS) forward_kernel(const PolicyParams 
 
 }  // namespace rmpc_policy_dev
 
-struct rmpc_policy {
-  int device = 0;
-  rmpc_policy_dev::PolicyParams P{};
-  double* d_w = nullptr;
-  int smem = 0, grid = 0;
-};
-
 extern "C" {
 
 int32_t rmpc_policy_create(int32_t obs_dim, int32_t act_dim, int32_t hidden, const double* params,
@@ -110,26 +93,8 @@ int32_t rmpc_policy_create(int32_t obs_dim, int32_t act_dim, int32_t hidden, con
   *out = nullptr;
   if (obs_dim < 1 || obs_dim > MAXIO || act_dim < 1 || act_dim > MAXH || hidden < 1 || hidden > MAXH)
     return RMPC_ERR_STRUCTURAL;
-  rmpc_policy_dev::PolicyParams P{};
-  P.obs = obs_dim;
-  P.act = act_dim;
-  P.hidden = hidden;
-  int off = 0;
-  auto net = [&](Net& N, int out_dim) {
-    const int sizes[5] = {obs_dim, hidden, hidden, hidden, out_dim};  // init_policy, policy.cpp:69-76
-    for (int l = 0; l < 4; ++l) {
-      N.in[l] = sizes[l];
-      N.out[l] = sizes[l + 1];
-      N.w[l] = off;
-      off += sizes[l] * sizes[l + 1];
-      N.b[l] = off;
-      off += sizes[l + 1];
-    }
-  };
-  net(P.pi, act_dim);
-  net(P.vf, 1);
-  P.total = off;
-  if (n_params != off + act_dim) return RMPC_ERR_STRUCTURAL;  // + log_std
+  const rmpc_policy_dev::PolicyParams P = rmpc_policy_dev::policy_shape(obs_dim, act_dim, hidden);
+  if (n_params != P.total + act_dim) return RMPC_ERR_STRUCTURAL;  // + log_std
   if (cudaSetDevice(device) != cudaSuccess) return RMPC_ERR_CUDA;
   rmpc_policy* p = new (std::nothrow) rmpc_policy;
   if (!p) return RMPC_ERR_CUDA;
@@ -139,8 +104,9 @@ int32_t rmpc_policy_create(int32_t obs_dim, int32_t act_dim, int32_t hidden, con
   int sms = 148;
   cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
   p->grid = sms;
-  if (cudaMalloc(&p->d_w, P.total * sizeof(double)) != cudaSuccess ||
-      cudaMemcpy(p->d_w, params, P.total * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
+  p->sms = sms;
+  if (cudaMalloc(&p->d_w, (P.total + act_dim) * sizeof(double)) != cudaSuccess ||
+      cudaMemcpy(p->d_w, params, (P.total + act_dim) * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess ||
       cudaFuncSetAttribute(forward_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, p->smem) !=
           cudaSuccess) {
     cudaFree(p->d_w);
@@ -155,7 +121,29 @@ void rmpc_policy_destroy(rmpc_policy* p) {
   if (!p) return;
   cudaSetDevice(p->device);
   cudaFree(p->d_w);
+  cudaFree(p->d_part);
+  cudaFree(p->d_grads);
   delete p;
+}
+
+int32_t rmpc_policy_num_params(const rmpc_policy* p) { return p ? p->P.total + p->P.act : -1; }
+
+int32_t rmpc_policy_get_params(rmpc_policy* p, double* params, int32_t n_params) {
+  if (!p || !params) return RMPC_ERR_INVALID_ARG;
+  if (n_params != p->P.total + p->P.act) return RMPC_ERR_STRUCTURAL;
+  if (cudaSetDevice(p->device) != cudaSuccess ||
+      cudaMemcpy(params, p->d_w, n_params * sizeof(double), cudaMemcpyDeviceToHost) != cudaSuccess)
+    return RMPC_ERR_CUDA;
+  return RMPC_OK;
+}
+
+int32_t rmpc_policy_set_params(rmpc_policy* p, const double* params, int32_t n_params) {
+  if (!p || !params) return RMPC_ERR_INVALID_ARG;
+  if (n_params != p->P.total + p->P.act) return RMPC_ERR_STRUCTURAL;
+  if (cudaSetDevice(p->device) != cudaSuccess ||
+      cudaMemcpy(p->d_w, params, n_params * sizeof(double), cudaMemcpyHostToDevice) != cudaSuccess)
+    return RMPC_ERR_CUDA;
+  return RMPC_OK;
 }
 
 int32_t rmpc_policy_forward_device(rmpc_policy* p, int32_t n, const double* obs, double* mean, double* value,

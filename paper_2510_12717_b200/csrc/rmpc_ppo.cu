@@ -1,0 +1,648 @@
+// rmpc_ppo.cu — the PPO batch on sm_100a (second half), FP64 like the
+// reference (/root/reference/proj/src/ppo.cpp):
+//
+//   rmpc_ppo_loss_device    ppo_loss (ppo.cpp:79-135): policy_forward with the cache
+//                           (policy.cpp:85-102), gaussian_log_prob (policy.cpp:168-176), the
+//                           clipped surrogate / value / entropy terms and mlp_backward
+//                           (ppo.cpp:64-77) summed over the batch
+//   rmpc_gae_device         gae_advantages (ppo.cpp:28-45)
+//   rmpc_ppo_update_device  ppo_update (ppo.cpp:193-276): GAE, advantage normalisation, epochs x
+//                           minibatches of {Fisher-Yates shuffle, ppo_loss, gradient-norm clip,
+//                           AdamOptimizer::step (ppo.cpp:181-191)}
+//
+// Loss kernel.  The batch gradient is a sum over samples of outer products delta_l post_l^T,
+// i.e. per layer a (out x n) . (n x in) product with a long reduction dimension: the kernel is
+// split-K over the samples.  Grid = (chunks, 2): blockIdx.y picks the trunk (pi / value, which
+// are independent given the batch), blockIdx.x a contiguous chunk of samples.  A block keeps its
+// trunk's weights in shared memory (column stride padded to an odd count, so the transposed
+// product W^T delta of the backward pass reads conflict-free) and walks its chunk in tiles of
+// 16 samples: forward (thread = neuron i x 2 samples, activations and ELU derivatives cached
+// in shared memory), the per-sample loss head (warp = sample), backward layer by layer, then
+// the gradient update.  Each thread owns fixed gradient entries (flat index t + 512 r) in
+// registers for the whole chunk, so the reduction over samples never leaves the SM; the
+// per-chunk partial gradients are summed in a fixed order by a second kernel (deterministic,
+// no atomics).  TF32/BF16 tensor cores would miss the FP64 reference by orders of magnitude;
+// the FP64 work is ~0.12 MFLOP per sample.
+#include <cuda_runtime.h>
+#include <math.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <new>
+#include <vector>
+
+#include "rmpc_policy.cuh"
+
+namespace rmpc_ppo_dev {
+
+using rmpc_policy_dev::MAXH;
+using rmpc_policy_dev::MAXIO;
+using rmpc_policy_dev::Net;
+using rmpc_policy_dev::PolicyParams;
+
+constexpr int THREADS = 512, TILE = 16, WARPS = THREADS / 32;
+constexpr double kLogSqrt2Pi = 0.91893853320467274178032973640562;
+
+struct TrunkSm {
+  int ld[4];        // padded column stride of W_l in shared memory (odd)
+  int w[4], b[4];   // shared-memory offsets of W_l and b_l
+  int wr[4], br[4]; // offsets of W_l and b_l relative to the trunk's first parameter
+  int wtotal;       // doubles of the shared weight region
+};
+
+struct LossParams {
+  PolicyParams P;
+  TrunkSm ts[2];
+  int n, chunk, nch;    // samples, samples per block, blocks per trunk
+  int pst, dst;         // per-sample strides of the activation / delta tiles
+  int part_stride;      // doubles per (trunk, chunk) partial
+  double clip_eps, value_coef, inv_n;
+  const double* w;      // parameters (flatten_policy order)
+  const double* obs;
+  const double* act;
+  const double* old_logp;
+  const double* adv;
+  const double* ret;
+  const int32_t* idx;   // optional gather: sample s of the batch is row idx[s]
+  double* part;
+};
+
+__device__ __forceinline__ double warp_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Tile layouts, per sample: activations [post_0 = obs | post_1 | post_2 | post_3 | 1] and
+// deltas [d_0 | d_1 | d_2 | d_3] (d_l holds ELU'(z_l) after the forward pass, then the delta).
+__device__ __forceinline__ int poff(const PolicyParams& P, int l) { return l == 0 ? 0 : P.obs + (l - 1) * P.hidden; }
+__device__ __forceinline__ int doff(const PolicyParams& P, int l) { return l * P.hidden; }
+
+template <int R>
+__global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double lstd[MAXIO];
+  __shared__ double wred[WARPS];
+  const int trunk = blockIdx.y, chunk = blockIdx.x;
+  const PolicyParams& P = L.P;
+  const Net& N = trunk == 0 ? P.pi : P.vf;
+  const TrunkSm& S = L.ts[trunk];
+  double* W = sm;
+  double* post = W + S.wtotal;
+  double* del = post + TILE * L.pst;
+  double* out = del + TILE * L.dst;  // TILE x MAXIO trunk outputs
+  double* red = out + TILE * MAXIO;  // WARPS x MAXIO log_std partials
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
+  const int one = P.obs + 3 * P.hidden;  // the constant-1 activation slot (bias gradients)
+
+  for (int l = 0; l < 4; ++l) {
+    const int rows = N.out[l], cols = N.in[l];
+    for (int e = t; e < rows * cols; e += THREADS) W[S.w[l] + (e / rows) * S.ld[l] + e % rows] = L.w[N.w[l] + e];
+    for (int i = t; i < rows; i += THREADS) W[S.b[l] + i] = L.w[N.b[l] + i];
+  }
+  if (t < P.act) lstd[t] = L.w[P.total + t];
+
+  // gradient entries of this thread: trunk-relative flat index t + THREADS r, as
+  // (delta slot | activation slot << 16), 0xffffffff past the trunk
+  uint32_t map[R];
+  double acc[R];
+#pragma unroll
+  for (int r = 0; r < R; ++r) {
+    const int e = t + THREADS * r;
+    acc[r] = 0.0;
+    map[r] = 0xffffffffu;
+    if (e < N.total) {
+      int l = 3;
+      while (l > 0 && e < S.wr[l]) --l;
+      const int rows = N.out[l];
+      uint32_t dix, pix;
+      if (e < S.br[l]) {
+        const int f = e - S.wr[l];
+        dix = doff(P, l) + f % rows;
+        pix = poff(P, l) + f / rows;
+      } else {
+        dix = doff(P, l) + (e - S.br[l]);
+        pix = one;
+      }
+      map[r] = dix | (pix << 16);
+    }
+  }
+  double lsg0 = 0.0, lsg1 = 0.0, lsum = 0.0;  // log_std gradient (lanes j, j + 32), loss term
+  const int c0 = chunk * L.chunk, c1 = min(L.n, c0 + L.chunk);
+  const int i = t & 63, sg = t >> 6;  // neuron / column and sample group of this thread
+  __syncthreads();
+
+  for (int base = c0; base < c1; base += TILE) {
+    // ---- load the tile (rows past the chunk are zero: zero delta, zero contribution)
+    for (int e = t; e < TILE * P.obs; e += THREADS) {
+      const int s = e / P.obs, k = e % P.obs, g = base + s;
+      double v = 0.0;
+      if (g < c1) v = L.obs[(size_t)(L.idx ? L.idx[g] : g) * P.obs + k];
+      post[s * L.pst + k] = v;
+    }
+    if (t < TILE) post[t * L.pst + one] = base + t < c1 ? 1.0 : 0.0;
+    __syncthreads();
+    // ---- forward (mlp_forward, policy.cpp:15-31): z = W h + b, ELU on the hidden layers
+    for (int l = 0; l < 4; ++l) {
+      const int rows = N.out[l], cols = N.in[l];
+      if (i < rows) {
+        const double* Wl = W + S.w[l];
+        const int ld = S.ld[l];
+        const double* x0 = post + sg * L.pst + poff(P, l);
+        const double* x1 = x0 + 8 * L.pst;
+        double a0 = 0.0, a1 = 0.0;
+#pragma unroll 4
+        for (int k = 0; k < cols; ++k) {
+          const double wk = Wl[k * ld + i];
+          a0 = fma(wk, x0[k], a0);
+          a1 = fma(wk, x1[k], a1);
+        }
+        const double z0 = a0 + W[S.b[l] + i], z1 = a1 + W[S.b[l] + i];
+        if (l < 3) {
+          post[sg * L.pst + poff(P, l + 1) + i] = z0 > 0.0 ? z0 : expm1(z0);
+          post[(sg + 8) * L.pst + poff(P, l + 1) + i] = z1 > 0.0 ? z1 : expm1(z1);
+          del[sg * L.dst + doff(P, l) + i] = z0 > 0.0 ? 1.0 : exp(z0);  // elu_grad, ppo.cpp:12
+          del[(sg + 8) * L.dst + doff(P, l) + i] = z1 > 0.0 ? 1.0 : exp(z1);
+        } else {
+          out[sg * MAXIO + i] = z0;
+          out[(sg + 8) * MAXIO + i] = z1;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- loss head (ppo.cpp:92-126), warp = sample
+    {
+      const int s = warp, g = base + s;
+      const bool valid = g < c1;
+      const size_t row = valid ? (size_t)(L.idx ? L.idx[g] : g) : 0;
+      double* d3 = del + s * L.dst + doff(P, 3);
+      if (trunk == 0) {
+        const int A = P.act;
+        double z0 = 0.0, z1 = 0.0, sd0 = 1.0, sd1 = 1.0, lp = 0.0;
+        if (lane < A) {
+          sd0 = exp(lstd[lane]);
+          z0 = (L.act[row * A + lane] - out[s * MAXIO + lane]) / sd0;
+          lp += -0.5 * z0 * z0 - lstd[lane] - kLogSqrt2Pi;
+        }
+        if (lane + 32 < A) {
+          sd1 = exp(lstd[lane + 32]);
+          z1 = (L.act[row * A + lane + 32] - out[s * MAXIO + lane + 32]) / sd1;
+          lp += -0.5 * z1 * z1 - lstd[lane + 32] - kLogSqrt2Pi;
+        }
+        lp = warp_sum(lp);
+        const double adv = valid ? L.adv[row] : 0.0;
+        const double ratio = exp(lp - (valid ? L.old_logp[row] : 0.0));
+        const double surr1 = ratio * adv;
+        const double clipped = fmin(fmax(ratio, 1.0 - L.clip_eps), 1.0 + L.clip_eps) * adv;
+        if (lane == 0 && valid) lsum += -fmin(surr1, clipped) * L.inv_n;
+        const double g_r = surr1 <= clipped ? -adv * L.inv_n : 0.0;
+        const bool on = valid && g_r != 0.0;
+        const double g_logp = g_r * ratio;
+        if (lane < A) {
+          d3[lane] = on ? g_logp * z0 / sd0 : 0.0;
+          if (on) lsg0 += g_logp * (z0 * z0 - 1.0);
+        }
+        if (lane + 32 < A) {
+          d3[lane + 32] = on ? g_logp * z1 / sd1 : 0.0;
+          if (on) lsg1 += g_logp * (z1 * z1 - 1.0);
+        }
+      } else if (lane == 0) {
+        const double verr = valid ? out[s * MAXIO] - L.ret[row] : 0.0;
+        if (valid) lsum += 0.5 * verr * verr * L.inv_n;
+        d3[0] = valid ? L.value_coef * verr * L.inv_n : 0.0;
+      }
+    }
+    __syncthreads();
+    // ---- backward (mlp_backward, ppo.cpp:64-77): delta_{l-1} = (W_l^T delta_l) .* ELU'(z_{l-1})
+    for (int l = 3; l > 0; --l) {
+      const int rows = N.out[l], cols = N.in[l];
+      if (i < cols) {
+        const double* Wl = W + S.w[l] + i * S.ld[l];
+        const double* e0 = del + sg * L.dst + doff(P, l);
+        const double* e1 = e0 + 8 * L.dst;
+        double b0 = 0.0, b1 = 0.0;
+#pragma unroll 4
+        for (int r = 0; r < rows; ++r) {
+          const double wk = Wl[r];
+          b0 = fma(wk, e0[r], b0);
+          b1 = fma(wk, e1[r], b1);
+        }
+        del[sg * L.dst + doff(P, l - 1) + i] *= b0;
+        del[(sg + 8) * L.dst + doff(P, l - 1) + i] *= b1;
+      }
+      __syncthreads();
+    }
+    // ---- gradient: W_l += delta_l post_l^T, b_l += delta_l over the tile
+#pragma unroll
+    for (int r = 0; r < R; ++r) {
+      if (map[r] != 0xffffffffu) {
+        const double* dp = del + (map[r] & 0xffffu);
+        const double* pp = post + (map[r] >> 16);
+        double a = acc[r];
+#pragma unroll
+        for (int s = 0; s < TILE; ++s) a = fma(dp[s * L.dst], pp[s * L.pst], a);
+        acc[r] = a;
+      }
+    }
+    __syncthreads();
+  }
+  // ---- per-chunk partials: gradient entries, log_std gradient (pi), loss term
+  double* part = L.part + (size_t)(trunk * L.nch + chunk) * L.part_stride;
+#pragma unroll
+  for (int r = 0; r < R; ++r)
+    if (map[r] != 0xffffffffu) part[t + THREADS * r] = acc[r];
+  if (trunk == 0) {
+    red[warp * MAXIO + lane] = lsg0;
+    red[warp * MAXIO + lane + 32] = lsg1;
+  }
+  if (lane == 0) wred[warp] = lsum;
+  __syncthreads();
+  if (trunk == 0 && t < P.act) {
+    double v = 0.0;
+    for (int w = 0; w < WARPS; ++w) v += red[w * MAXIO + t];
+    part[N.total + t] = v;
+  }
+  if (t == 0) {
+    double v = 0.0;
+    for (int w = 0; w < WARPS; ++w) v += wred[w];
+    part[N.total + MAXIO] = v;
+  }
+}
+
+// Fixed-order sum of the chunk partials into the flatten_grads vector and the loss info.
+__global__ void reduce_kernel(const PolicyParams P, int nch, int part_stride, const double* __restrict__ part,
+                              double entropy_coef, double value_coef, const double* __restrict__ w,
+                              double* grads, rmpc_ppo_loss_info* info) {
+  const int np = P.total + P.act;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < np; p += gridDim.x * blockDim.x) {
+    int tr = 0, e = p;
+    if (p >= P.pi.total && p < P.total) {
+      tr = 1;
+      e = p - P.pi.total;
+    } else if (p >= P.total) {
+      e = P.pi.total + (p - P.total);
+    }
+    double v = 0.0;
+    for (int c = 0; c < nch; ++c) v += part[(size_t)(tr * nch + c) * part_stride + e];
+    if (p >= P.total && entropy_coef != 0.0) v -= entropy_coef;
+    if (grads) grads[p] = v;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0 && info) {
+    double sur = 0.0, vl = 0.0, ent = 0.0;
+    for (int c = 0; c < nch; ++c) sur += part[(size_t)c * part_stride + P.pi.total + MAXIO];
+    for (int c = 0; c < nch; ++c) vl += part[(size_t)(nch + c) * part_stride + P.vf.total + MAXIO];
+    for (int j = 0; j < P.act; ++j) ent += w[P.total + j] + kLogSqrt2Pi + 0.5;
+    info->surrogate = sur;
+    info->value_loss = vl;
+    info->entropy = ent;
+    info->total = sur + value_coef * vl - entropy_coef * ent;
+  }
+}
+
+// gae_advantages (ppo.cpp:28-45): one thread per env, the backward recursion over the steps.
+__global__ void gae_kernel(int T, int E, const double* __restrict__ rew, const double* __restrict__ val,
+                           const double* __restrict__ done, const double* __restrict__ boot, double gamma,
+                           double lam, double* adv, double* ret) {
+  const int e = blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= E) return;
+  double running = 0.0;
+  for (int t = T - 1; t >= 0; --t) {
+    const size_t k = (size_t)t * E + e;
+    const double not_done = 1.0 - done[k];
+    const double next_value = t == T - 1 ? boot[e] : val[k + E];
+    const double delta = rew[k] + gamma * next_value * not_done - val[k];
+    running = delta + gamma * lam * not_done * running;
+    adv[k] = running;
+    ret[k] = running + val[k];
+  }
+}
+
+constexpr int RED_THREADS = 1024;
+
+// Fixed-order block sum (every thread gets the total).
+__device__ double block_sum(double v, double* sh) {
+  const int t = threadIdx.x;
+  sh[t] = v;
+  __syncthreads();
+  for (int o = RED_THREADS / 2; o > 0; o >>= 1) {
+    if (t < o) sh[t] += sh[t + o];
+    __syncthreads();
+  }
+  const double r = sh[0];
+  __syncthreads();
+  return r;
+}
+
+// Advantage normalisation of ppo_update (ppo.cpp:199-202), one block.
+__global__ void __launch_bounds__(RED_THREADS) normalize_kernel(int N, double* adv) {
+  __shared__ double sh[RED_THREADS];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < N; k += RED_THREADS) s += adv[k];
+  const double mean = block_sum(s, sh) / N;
+  double q = 0.0;
+  for (int k = threadIdx.x; k < N; k += RED_THREADS) q += (adv[k] - mean) * (adv[k] - mean);
+  const double var = block_sum(q, sh) / N;
+  const double inv_std = 1.0 / sqrt(var + 1e-8);
+  for (int k = threadIdx.x; k < N; k += RED_THREADS) adv[k] = (adv[k] - mean) * inv_std;
+}
+
+// Gradient-norm clip (ppo.cpp:255-257) + AdamOptimizer::step (ppo.cpp:181-191), one block.
+__global__ void __launch_bounds__(RED_THREADS) adam_kernel(int np, const double* __restrict__ g, double* m, double* v,
+                                                           double* w, double max_norm, double lr, double b1,
+                                                           double b2, double eps, double bc1, double bc2) {
+  __shared__ double sh[RED_THREADS];
+  double q = 0.0;
+  for (int k = threadIdx.x; k < np; k += RED_THREADS) q += g[k] * g[k];
+  const double norm = sqrt(block_sum(q, sh));
+  const bool clip = max_norm > 0.0 && norm > max_norm;
+  const double scale = clip ? max_norm / norm : 1.0;
+  for (int k = threadIdx.x; k < np; k += RED_THREADS) {
+    const double gk = clip ? g[k] * scale : g[k];
+    const double mk = b1 * m[k] + (1.0 - b1) * gk;
+    const double vk = b2 * v[k] + (1.0 - b2) * (gk * gk);
+    m[k] = mk;
+    v[k] = vk;
+    w[k] -= lr * (mk / bc1) / (sqrt(vk / bc2) + eps);
+  }
+}
+
+int rmax_for(int total) {
+  const int need = (total + THREADS - 1) / THREADS;
+  return need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 ? 24 : 33;
+}
+
+TrunkSm trunk_sm(const Net& N) {
+  TrunkSm S{};
+  int off = 0;
+  for (int l = 0; l < 4; ++l) {
+    S.ld[l] = N.out[l] | 1;
+    S.w[l] = off;
+    off += N.in[l] * S.ld[l];
+    S.b[l] = off;
+    off += N.out[l];
+    S.wr[l] = N.w[l] - N.w[0];
+    S.br[l] = N.b[l] - N.w[0];
+  }
+  S.wtotal = (off + 1) & ~1;
+  return S;
+}
+
+// One ppo_loss over n samples (optionally gathered through idx) into grads / info.
+int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, const double* old_logp,
+                const double* adv, const double* ret, const int32_t* idx, const rmpc_ppo_config& cfg, double* grads,
+                rmpc_ppo_loss_info* info, cudaStream_t st) {
+  const PolicyParams& P = p->P;
+  LossParams L{};
+  L.P = P;
+  L.ts[0] = trunk_sm(P.pi);
+  L.ts[1] = trunk_sm(P.vf);
+  L.n = n;
+  L.nch = std::max(1, std::min(p->sms / 2, (n + TILE - 1) / TILE));
+  L.chunk = (n + L.nch - 1) / L.nch;
+  L.pst = P.obs + 3 * P.hidden + 1;
+  L.dst = 3 * P.hidden + MAXIO;
+  L.part_stride = std::max(P.pi.total, P.vf.total) + 2 * MAXIO;
+  L.clip_eps = cfg.clip_eps;
+  L.value_coef = cfg.value_coef;
+  L.inv_n = 1.0 / n;
+  L.w = p->d_w;
+  L.obs = obs;
+  L.act = act;
+  L.old_logp = old_logp;
+  L.adv = adv;
+  L.ret = ret;
+  L.idx = idx;
+  const size_t need = (size_t)2 * L.nch * L.part_stride;
+  if (need > p->part_cap) {
+    cudaFree(p->d_part);
+    p->d_part = nullptr;
+    p->part_cap = 0;
+    if (cudaMalloc(&p->d_part, need * sizeof(double)) != cudaSuccess) return RMPC_ERR_CUDA;
+    p->part_cap = need;
+  }
+  L.part = p->d_part;
+  const int wmax = std::max(L.ts[0].wtotal, L.ts[1].wtotal);
+  const int smem = (int)sizeof(double) * (wmax + TILE * L.pst + TILE * L.dst + TILE * MAXIO + WARPS * MAXIO);
+  const int R = rmax_for(std::max(P.pi.total, P.vf.total));
+  auto go = [&](auto kern) {
+    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
+    kern<<<dim3(L.nch, 2), THREADS, smem, st>>>(L);
+    return true;
+  };
+  const bool ok = R == 8 ? go(loss_kernel<8>) : R == 16 ? go(loss_kernel<16>) : R == 24 ? go(loss_kernel<24>)
+                                                                                : go(loss_kernel<33>);
+  if (!ok) return RMPC_ERR_CUDA;
+  const int np = P.total + P.act;
+  reduce_kernel<<<(np + 255) / 256, 256, 0, st>>>(P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef,
+                                                 p->d_w, grads, info);
+  return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+}
+
+// xoshiro256++ (rng.hpp:15-43): seeding and uniform_int for the minibatch shuffles.
+uint64_t splitmix(uint64_t x) {
+  x += 0x9e3779b97f4a7c15ULL;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ULL;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebULL;
+  return x ^ (x >> 31);
+}
+uint64_t rotl(uint64_t x, int k) { return (x << k) | (x >> (64 - k)); }
+uint64_t next_u64(uint64_t s[4]) {
+  const uint64_t r = rotl(s[0] + s[3], 23) + s[0];
+  const uint64_t t = s[1] << 17;
+  s[2] ^= s[0];
+  s[3] ^= s[1];
+  s[1] ^= s[2];
+  s[0] ^= s[3];
+  s[2] ^= t;
+  s[3] = rotl(s[3], 45);
+  return r;
+}
+
+}  // namespace rmpc_ppo_dev
+
+struct rmpc_adam {
+  rmpc_policy* policy = nullptr;
+  double lr = 3e-4, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
+  int t = 0;
+  double* d_m = nullptr;
+  double* d_v = nullptr;
+  // ppo_update workspace
+  double* d_adv = nullptr;
+  double* d_ret = nullptr;
+  int32_t* d_order = nullptr;
+  rmpc_ppo_loss_info* d_info = nullptr;
+  int32_t* h_order = nullptr;  // pinned
+  size_t adv_cap = 0, ret_cap = 0, order_cap = 0, info_cap = 0;
+};
+
+extern "C" {
+
+void rmpc_ppo_config_default(rmpc_ppo_config* c) {  // PpoConfig, ppo.hpp:14-24
+  if (!c) return;
+  c->gamma = 0.99;
+  c->lam_gae = 0.95;
+  c->clip_eps = 0.2;
+  c->epochs = 4;
+  c->minibatches = 4;
+  c->lr = 3e-4;
+  c->entropy_coef = 0.0;
+  c->value_coef = 0.5;
+  c->max_grad_norm = 1.0;
+}
+
+void rmpc_rng_seed(uint64_t seed, uint64_t stream, uint64_t state[4]) {  // Rng(seed, stream)
+  uint64_t x = seed ^ rmpc_ppo_dev::splitmix(stream + 0x9e3779b97f4a7c15ULL);
+  for (int k = 0; k < 4; ++k) {
+    x += 0x9e3779b97f4a7c15ULL;
+    state[k] = rmpc_ppo_dev::splitmix(x);
+  }
+}
+
+int32_t rmpc_ppo_loss_device(rmpc_policy* p, int32_t n, const double* obs, const double* act, const double* old_logp,
+                             const double* adv, const double* ret, const rmpc_ppo_config* cfg, double* grads,
+                             rmpc_ppo_loss_info* info, void* stream) {
+  if (!p || !cfg || n < 0) return RMPC_ERR_INVALID_ARG;
+  if (n == 0) return RMPC_ERR_STRUCTURAL;  // ppo_loss: empty batch (ppo.cpp:82)
+  if (!obs || !act || !old_logp || !adv || !ret) return RMPC_ERR_INVALID_ARG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return RMPC_ERR_CUDA;
+  return rmpc_ppo_dev::launch_loss(p, n, obs, act, old_logp, adv, ret, nullptr, *cfg, grads, info,
+                                   stream ? (cudaStream_t)stream : cudaStreamLegacy);
+}
+
+int32_t rmpc_gae_device(int32_t T, int32_t E, const double* rew, const double* val, const double* done,
+                        const double* boot, double gamma, double lam, double* adv, double* ret, void* stream) {
+  if (T < 0 || E < 0 || ((size_t)T * E > 0 && (!rew || !val || !done || !boot || !adv || !ret)))
+    return RMPC_ERR_INVALID_ARG;
+  if ((size_t)T * E == 0) return RMPC_OK;
+  rmpc_ppo_dev::gae_kernel<<<(E + 127) / 128, 128, 0, stream ? (cudaStream_t)stream : cudaStreamLegacy>>>(
+      T, E, rew, val, done, boot, gamma, lam, adv, ret);
+  return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+}
+
+int32_t rmpc_adam_create(rmpc_policy* p, double lr, rmpc_adam** out) {
+  if (!p || !out) return RMPC_ERR_INVALID_ARG;
+  *out = nullptr;
+  if (cudaSetDevice(p->device) != cudaSuccess) return RMPC_ERR_CUDA;
+  rmpc_adam* a = new (std::nothrow) rmpc_adam;
+  if (!a) return RMPC_ERR_CUDA;
+  a->policy = p;
+  a->lr = lr;
+  const size_t np = (size_t)(p->P.total + p->P.act);
+  if (cudaMalloc(&a->d_m, np * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&a->d_v, np * sizeof(double)) != cudaSuccess ||
+      cudaMemset(a->d_m, 0, np * sizeof(double)) != cudaSuccess ||
+      cudaMemset(a->d_v, 0, np * sizeof(double)) != cudaSuccess) {
+    cudaFree(a->d_m);
+    cudaFree(a->d_v);
+    delete a;
+    return RMPC_ERR_CUDA;
+  }
+  *out = a;
+  return RMPC_OK;
+}
+
+void rmpc_adam_destroy(rmpc_adam* a) {
+  if (!a) return;
+  cudaSetDevice(a->policy->device);
+  cudaFree(a->d_m);
+  cudaFree(a->d_v);
+  cudaFree(a->d_adv);
+  cudaFree(a->d_ret);
+  cudaFree(a->d_order);
+  cudaFree(a->d_info);
+  cudaFreeHost(a->h_order);
+  delete a;
+}
+
+int32_t rmpc_ppo_update_device(rmpc_policy* p, rmpc_adam* a, int32_t T, int32_t E, const double* obs,
+                               const double* act, const double* logp, const double* values, const double* rewards,
+                               const double* dones, const double* boot, const rmpc_ppo_config* cfg,
+                               uint64_t rng[4], rmpc_ppo_update_stats* stats, void* stream) {
+  using namespace rmpc_ppo_dev;
+  if (!p || !a || a->policy != p || !cfg || !rng || !stats || T < 1 || E < 1) return RMPC_ERR_INVALID_ARG;
+  if (!obs || !act || !logp || !values || !rewards || !dones || !boot) return RMPC_ERR_INVALID_ARG;
+  if (cudaSetDevice(p->device) != cudaSuccess) return RMPC_ERR_CUDA;
+  const cudaStream_t st = stream ? (cudaStream_t)stream : cudaStreamLegacy;
+  const int N = T * E;
+  const int epochs = std::max(0, cfg->epochs), mbc = std::max(1, cfg->minibatches);
+  const int np = p->P.total + p->P.act;
+  auto grow = [](auto*& ptr, size_t& cap, size_t need, size_t elem) {
+    if (need <= cap) return true;
+    cudaFree(ptr);
+    ptr = nullptr;
+    cap = 0;
+    if (cudaMalloc(&ptr, need * elem) != cudaSuccess) return false;
+    cap = need;
+    return true;
+  };
+  if (!grow(a->d_adv, a->adv_cap, (size_t)N, sizeof(double)) || !grow(a->d_ret, a->ret_cap, (size_t)N, sizeof(double)))
+    return RMPC_ERR_CUDA;
+  const size_t norder = (size_t)std::max(epochs, 1) * N;
+  if (norder > a->order_cap) {
+    cudaFree(a->d_order);
+    cudaFreeHost(a->h_order);
+    a->d_order = nullptr;
+    a->h_order = nullptr;
+    a->order_cap = 0;
+    if (cudaMalloc(&a->d_order, norder * sizeof(int32_t)) != cudaSuccess ||
+        cudaMallocHost(&a->h_order, norder * sizeof(int32_t)) != cudaSuccess)
+      return RMPC_ERR_CUDA;
+    a->order_cap = norder;
+  }
+  if (!grow(a->d_info, a->info_cap, (size_t)std::max(epochs * mbc, 1), sizeof(rmpc_ppo_loss_info)))
+    return RMPC_ERR_CUDA;
+  if (!p->d_grads && cudaMalloc(&p->d_grads, np * sizeof(double)) != cudaSuccess) return RMPC_ERR_CUDA;
+  // every epoch's permutation up front (the Rng advances exactly as the reference's loop)
+  cudaStreamSynchronize(st);  // h_order may still feed a previous call's copy
+  std::vector<int32_t> order(N);
+  for (int k = 0; k < N; ++k) order[k] = k;
+  for (int ep = 0; ep < epochs; ++ep) {
+    for (int k = N - 1; k > 0; --k) std::swap(order[k], order[next_u64(rng) % (uint64_t)(k + 1)]);
+    std::copy(order.begin(), order.end(), a->h_order + (size_t)ep * N);
+  }
+  if (epochs > 0 &&
+      cudaMemcpyAsync(a->d_order, a->h_order, (size_t)epochs * N * sizeof(int32_t), cudaMemcpyHostToDevice, st) !=
+          cudaSuccess)
+    return RMPC_ERR_CUDA;
+  gae_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, E, rewards, values, dones, boot, cfg->gamma, cfg->lam_gae, a->d_adv,
+                                               a->d_ret);
+  normalize_kernel<<<1, RED_THREADS, 0, st>>>(N, a->d_adv);
+  const int mb = (N + mbc - 1) / mbc;
+  int count = 0;
+  for (int ep = 0; ep < epochs; ++ep) {
+    for (int b = 0; b < mbc; ++b) {
+      const int lo = b * mb, hi = std::min(N, lo + mb);
+      if (lo >= hi) continue;
+      const int rc = launch_loss(p, hi - lo, obs, act, logp, a->d_adv, a->d_ret, a->d_order + (size_t)ep * N + lo, *cfg,
+                                 p->d_grads, a->d_info + count, st);
+      if (rc != RMPC_OK) return rc;
+      ++a->t;
+      const double bc1 = 1.0 - std::pow(a->beta1, a->t), bc2 = 1.0 - std::pow(a->beta2, a->t);
+      adam_kernel<<<1, RED_THREADS, 0, st>>>(np, p->d_grads, a->d_m, a->d_v, p->d_w, cfg->max_grad_norm, a->lr,
+                                             a->beta1, a->beta2, a->eps, bc1, bc2);
+      ++count;
+    }
+  }
+  std::vector<rmpc_ppo_loss_info> infos(std::max(count, 1));
+  if (count > 0 && cudaMemcpyAsync(infos.data(), a->d_info, count * sizeof(rmpc_ppo_loss_info),
+                                   cudaMemcpyDeviceToHost, st) != cudaSuccess)
+    return RMPC_ERR_CUDA;
+  if (cudaStreamSynchronize(st) != cudaSuccess || cudaGetLastError() != cudaSuccess) return RMPC_ERR_CUDA;
+  rmpc_ppo_update_stats s{0.0, 0.0, 0.0, 0.0};
+  for (int k = 0; k < count; ++k) {
+    s.loss += infos[k].total;
+    s.surrogate += infos[k].surrogate;
+    s.value_loss += infos[k].value_loss;
+    s.entropy = infos[k].entropy;
+  }
+  if (count > 0) {
+    s.loss /= count;
+    s.surrogate /= count;
+    s.value_loss /= count;
+  }
+  *stats = s;
+  return RMPC_OK;
+}
+
+}  // extern "C"

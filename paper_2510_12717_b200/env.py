@@ -52,6 +52,12 @@ def _bind(L):
     L.rmpc_policy_forward_device.restype = _I
     L.rmpc_env_sizeof.argtypes = [_I]
     L.rmpc_env_sizeof.restype = _I
+    L.rmpc_policy_num_params.argtypes = [_VP]
+    L.rmpc_policy_num_params.restype = _I
+    L.rmpc_policy_get_params.argtypes = [_VP, _VP, _I]
+    L.rmpc_policy_get_params.restype = _I
+    L.rmpc_policy_set_params.argtypes = [_VP, _VP, _I]
+    L.rmpc_policy_set_params.restype = _I
     L._env_bound = True
     return L
 
@@ -150,7 +156,6 @@ class Policy:
         self._lib = _bind(library())
         p = np.ascontiguousarray(params, dtype=np.float64)
         self.obs_dim, self.act_dim, self.hidden = obs_dim, act_dim, hidden
-        self.log_std = p[-act_dim:].copy()
         h = _VP()
         rc = self._lib.rmpc_policy_create(obs_dim, act_dim, hidden, p.ctypes.data, p.size, device, C.byref(h))
         if rc != 0:
@@ -167,6 +172,31 @@ class Policy:
             self.close()
         except Exception:
             pass
+
+    @property
+    def num_params(self) -> int:
+        return int(self._lib.rmpc_policy_num_params(self._h))
+
+    def get_params(self):
+        """flatten_policy (ppo.cpp:144-153): a host copy of the device parameters."""
+        import numpy as np
+        out = np.zeros(self.num_params)
+        rc = self._lib.rmpc_policy_get_params(self._h, out.ctypes.data, out.size)
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_policy_get_params failed")
+        return out
+
+    def set_params(self, params):
+        """unflatten_policy (ppo.cpp:155-162) from a host vector."""
+        import numpy as np
+        p = np.ascontiguousarray(params, dtype=np.float64)
+        rc = self._lib.rmpc_policy_set_params(self._h, p.ctypes.data, p.size)
+        if rc != 0:
+            raise RmpcError(rc, "rmpc_policy_set_params failed (parameter count)")
+
+    @property
+    def log_std(self):
+        return self.get_params()[-self.act_dim:]
 
     def forward(self, obs, mean=None, value=None, stream=None):
         rc = self._lib.rmpc_policy_forward_device(self._h, obs.shape[0], _p(obs), _p(mean), _p(value), _s(stream))

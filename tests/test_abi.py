@@ -39,8 +39,19 @@ def test_struct_sizes_match_header():
     assert L.rmpc_sizeof(99) == -1
     from paper_2510_12717_b200.env import EnvConfig, _bind
     _bind(L)
-    assert [L.rmpc_env_sizeof(i) for i in range(2)] == [C.sizeof(EnvConfig), 16]
-    assert L.rmpc_env_sizeof(2) == -1
+    from paper_2510_12717_b200.ppo import LossInfo, PpoConfig, UpdateStats
+    assert [L.rmpc_env_sizeof(i) for i in range(5)] == [C.sizeof(EnvConfig), 16, C.sizeof(PpoConfig),
+                                                        C.sizeof(LossInfo), C.sizeof(UpdateStats)]
+    assert L.rmpc_env_sizeof(5) == -1
+
+
+def test_ppo_config_defaults_match_oracle(oracle):
+    from paper_2510_12717_b200.ppo import default_ppo_config, rng_state
+    c = default_ppo_config()
+    assert bytes(c) == bytes(oracle.ppo_config())
+    assert (c.gamma, c.lam_gae, c.clip_eps, c.epochs, c.minibatches, c.lr, c.value_coef, c.max_grad_norm) == \
+        (0.99, 0.95, 0.2, 4, 4, 3e-4, 0.5, 1.0)
+    assert list(rng_state(7, 0x0272)) == list(oracle.rng_words(7, 0x0272))
 
 
 def test_env_config_defaults_and_terrain_match_oracle(oracle):

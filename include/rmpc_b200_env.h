@@ -11,6 +11,9 @@
  *                              torque a failed solution yields is zero, as in Trainer::train
  *   rmpc_observe_device        observe (policy.cpp:104-122): the 23-entry policy input
  *   rmpc_policy_forward_device policy_forward (policy.cpp:85-102): the residual MLPs
+ *   rmpc_ppo_*, rmpc_gae_device, rmpc_adam_*
+ *                              the PPO batch (ppo.cpp:28-276): loss + gradient, GAE, Adam,
+ *                              whole ppo_update calls on a device-resident rollout
  *
  * The environment owns the reference's EnvConfig physics/terrain part (env.hpp:52-63) and the
  * heightfield (Terrain, env.cpp:8-27, drawn from Rng(seed, 0x7e22) like the reference).  Each
@@ -166,6 +169,9 @@ int32_t rmpc_ppo_update_device(rmpc_policy* policy, rmpc_adam* adam, int32_t ste
                                const double* d_values, const double* d_rewards, const double* d_dones,
                                const double* d_bootstrap, const rmpc_ppo_config* cfg,
                                uint64_t rng_state[4], rmpc_ppo_update_stats* stats, void* stream);
+
+/* Measured FP64 FMA throughput of `device` (TFLOP/s): the PPO batch's roofline denominator. */
+int32_t rmpc_fma_peak_f64(int32_t device, double* tflops);
 
 /* sizeof of the env ABI structs (0 config, 1 body, 2 ppo config, 3 loss info, 4 update stats)
  * for binding-side layout checks. */

@@ -296,20 +296,54 @@ void fill_timing(rmpc_handle& h, double total_ms) {
 
 }  // namespace
 
-// FP32 FMA throughput probe: 8 independent FMA chains per thread, enough resident warps to
-// saturate every SM.  The roofline denominator of bench.py ("of measured").
-__global__ void fma_peak_kernel(float* out, int iters, float a, float b) {
-  float x0 = threadIdx.x * 1e-7f, x1 = x0 + 1e-7f, x2 = x0 + 2e-7f, x3 = x0 + 3e-7f;
-  float x4 = x0 + 4e-7f, x5 = x0 + 5e-7f, x6 = x0 + 6e-7f, x7 = x0 + 7e-7f;
+// FMA throughput probe (FP32 for the solve, FP64 for the PPO batch): 8 independent FMA chains
+// per thread, enough resident warps to saturate every SM.  The roofline denominators
+// ("of measured").
+template <typename F>
+__global__ void fma_peak_kernel(F* out, int iters, F a, F b) {
+  F x0 = threadIdx.x * F(1e-7), x1 = x0 + F(1e-7), x2 = x0 + F(2e-7), x3 = x0 + F(3e-7);
+  F x4 = x0 + F(4e-7), x5 = x0 + F(5e-7), x6 = x0 + F(6e-7), x7 = x0 + F(7e-7);
   for (int i = 0; i < iters; ++i) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
-      x0 = fmaf(x0, a, b); x1 = fmaf(x1, a, b); x2 = fmaf(x2, a, b); x3 = fmaf(x3, a, b);
-      x4 = fmaf(x4, a, b); x5 = fmaf(x5, a, b); x6 = fmaf(x6, a, b); x7 = fmaf(x7, a, b);
+      x0 = fma(x0, a, b); x1 = fma(x1, a, b); x2 = fma(x2, a, b); x3 = fma(x3, a, b);
+      x4 = fma(x4, a, b); x5 = fma(x5, a, b); x6 = fma(x6, a, b); x7 = fma(x7, a, b);
     }
   }
-  const float r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
-  if (r == 1.2345f) out[0] = r;  // keep the chains alive
+  const F r = ((x0 + x1) + (x2 + x3)) + ((x4 + x5) + (x6 + x7));
+  if (r == F(1.2345)) out[0] = r;  // keep the chains alive
+}
+
+template <typename F>
+int32_t fma_peak(int32_t device, double* tflops) {
+  if (!tflops) return RMPC_ERR_INVALID_ARG;
+  if (cudaSetDevice(device) != cudaSuccess) return RMPC_ERR_CUDA;
+  int sms = 0;
+  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
+  F* d = nullptr;
+  cudaMalloc(&d, sizeof(F));
+  const int threads = 256, blocks = sms * 8, iters = sizeof(F) == 4 ? 4096 : 1024;
+  cudaEvent_t e0, e1;
+  cudaEventCreate(&e0);
+  cudaEventCreate(&e1);
+  fma_peak_kernel<F><<<blocks, threads>>>(d, 64, F(0.999), F(1e-6));  // warm-up
+  double best = 0.0;
+  for (int rep = 0; rep < 5; ++rep) {
+    cudaEventRecord(e0);
+    fma_peak_kernel<F><<<blocks, threads>>>(d, iters, F(0.999), F(1e-6));
+    cudaEventRecord(e1);
+    cudaEventSynchronize(e1);
+    float ms = 0.f;
+    cudaEventElapsedTime(&ms, e0, e1);
+    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
+    best = std::max(best, flops / (ms * 1e-3) / 1e12);
+  }
+  cudaEventDestroy(e0);
+  cudaEventDestroy(e1);
+  cudaFree(d);
+  const cudaError_t e = cudaGetLastError();
+  *tflops = best;
+  return e == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
 }
 
 extern "C" {
@@ -526,36 +560,9 @@ const char* rmpc_build_info(void) {
   return "rmpc_b200 sm_100a fused warp-pair-per-agent RTI kernel (reduced SPD block-tridiagonal ADMM, factor in TMEM, FP32 + FP64 linearization)";
 }
 
-int32_t rmpc_fma_peak(int32_t device, double* tflops) {
-  if (!tflops) return RMPC_ERR_INVALID_ARG;
-  if (cudaSetDevice(device) != cudaSuccess) return RMPC_ERR_CUDA;
-  int sms = 0;
-  cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, device);
-  float* d = nullptr;
-  cudaMalloc(&d, sizeof(float));
-  const int threads = 256, blocks = sms * 8, iters = 4096;
-  cudaEvent_t e0, e1;
-  cudaEventCreate(&e0);
-  cudaEventCreate(&e1);
-  fma_peak_kernel<<<blocks, threads>>>(d, 64, 0.999f, 1e-6f);  // warm-up
-  double best = 0.0;
-  for (int rep = 0; rep < 5; ++rep) {
-    cudaEventRecord(e0);
-    fma_peak_kernel<<<blocks, threads>>>(d, iters, 0.999f, 1e-6f);
-    cudaEventRecord(e1);
-    cudaEventSynchronize(e1);
-    float ms = 0.f;
-    cudaEventElapsedTime(&ms, e0, e1);
-    const double flops = 2.0 * 8 * 16 * (double)iters * threads * blocks;
-    best = std::max(best, flops / (ms * 1e-3) / 1e12);
-  }
-  cudaEventDestroy(e0);
-  cudaEventDestroy(e1);
-  cudaFree(d);
-  const cudaError_t e = cudaGetLastError();
-  *tflops = best;
-  return e == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
-}
+int32_t rmpc_fma_peak(int32_t device, double* tflops) { return fma_peak<float>(device, tflops); }
+
+int32_t rmpc_fma_peak_f64(int32_t device, double* tflops) { return fma_peak<double>(device, tflops); }
 
 int32_t rmpc_smem_bytes(int32_t horizon) {
   if (horizon < 1 || horizon > rmpc_dev::MAXT) return -1;

@@ -16,13 +16,14 @@
 // are independent given the batch), blockIdx.x a contiguous chunk of samples.  A block keeps its
 // trunk's weights in shared memory (column stride padded to an odd count, so the transposed
 // product W^T delta of the backward pass reads conflict-free) and walks its chunk in tiles of
-// 16 samples: forward (thread = neuron i x 2 samples, activations and ELU derivatives cached
+// 32 samples: forward (thread = neuron i x 4 samples, activations and ELU derivatives cached
 // in shared memory), the per-sample loss head (warp = sample), backward layer by layer, then
-// the gradient update.  Each thread owns fixed gradient entries (flat index t + 512 r) in
-// registers for the whole chunk, so the reduction over samples never leaves the SM; the
-// per-chunk partial gradients are summed in a fixed order by a second kernel (deterministic,
-// no atomics).  TF32/BF16 tensor cores would miss the FP64 reference by orders of magnitude;
-// the FP64 work is ~0.12 MFLOP per sample.
+// the gradient update.  Thread (i, kg) owns the gradient entries W_l(i, 8 kg .. 8 kg + 7) (and
+// b_l(i) for kg = 0) of every layer in registers for the whole chunk, so the reduction over
+// samples never leaves the SM; the per-chunk partial gradients are summed in a fixed order by a
+// second kernel (deterministic, no atomics).  Every phase is shared-memory bound: activation and
+// delta pairs are read as broadcast double2, weights as per-lane scalars.  TF32/BF16 tensor cores
+// would miss the FP64 reference by orders of magnitude; the FP64 work is ~0.11 MFLOP per sample.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -41,7 +42,7 @@ using rmpc_policy_dev::MAXIO;
 using rmpc_policy_dev::Net;
 using rmpc_policy_dev::PolicyParams;
 
-constexpr int THREADS = 512, TILE = 16, WARPS = THREADS / 32;
+constexpr int THREADS = 512, TILE = 32, WARPS = THREADS / 32, SPT = TILE / (THREADS / 64);
 constexpr double kLogSqrt2Pi = 0.91893853320467274178032973640562;
 
 struct TrunkSm {
@@ -55,7 +56,7 @@ struct LossParams {
   PolicyParams P;
   TrunkSm ts[2];
   int n, chunk, nch;    // samples, samples per block, blocks per trunk
-  int pst, dst;         // per-sample strides of the activation / delta tiles
+  int pst, dst, ost;    // per-sample strides of the activation / delta / output tiles
   int part_stride;      // doubles per (trunk, chunk) partial
   double clip_eps, value_coef, inv_n;
   const double* w;      // parameters (flatten_policy order)
@@ -74,12 +75,15 @@ __device__ __forceinline__ double warp_sum(double v) {
   return v;
 }
 
-// Tile layouts, per sample: activations [post_0 = obs | post_1 | post_2 | post_3 | 1] and
-// deltas [d_0 | d_1 | d_2 | d_3] (d_l holds ELU'(z_l) after the forward pass, then the delta).
-__device__ __forceinline__ int poff(const PolicyParams& P, int l) { return l == 0 ? 0 : P.obs + (l - 1) * P.hidden; }
-__device__ __forceinline__ int doff(const PolicyParams& P, int l) { return l * P.hidden; }
+// Tile layouts, per sample (every segment starts at an even offset, so pairs load as double2):
+// activations [post_0 = obs | post_1 | post_2 | post_3 | 1] and deltas [d_0 | d_1 | d_2 | d_3]
+// (d_l holds ELU'(z_l) after the forward pass, then the delta).
+__device__ __forceinline__ int even_up(int x) { return (x + 1) & ~1; }
+__device__ __forceinline__ int poff(const PolicyParams& P, int l) {
+  return l == 0 ? 0 : even_up(P.obs) + (l - 1) * even_up(P.hidden);
+}
+__device__ __forceinline__ int doff(const PolicyParams& P, int l) { return l * even_up(P.hidden); }
 
-template <int R>
 __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double lstd[MAXIO];
@@ -91,10 +95,9 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   double* W = sm;
   double* post = W + S.wtotal;
   double* del = post + TILE * L.pst;
-  double* out = del + TILE * L.dst;  // TILE x MAXIO trunk outputs
-  double* red = out + TILE * MAXIO;  // WARPS x MAXIO log_std partials
+  double* out = del + TILE * L.dst;  // TILE x ost trunk outputs
+  double* red = post;                // WARPS x MAXIO log_std partials (after the last tile)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
-  const int one = P.obs + 3 * P.hidden;  // the constant-1 activation slot (bias gradients)
 
   for (int l = 0; l < 4; ++l) {
     const int rows = N.out[l], cols = N.in[l];
@@ -102,35 +105,22 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
     for (int i = t; i < rows; i += THREADS) W[S.b[l] + i] = L.w[N.b[l] + i];
   }
   if (t < P.act) lstd[t] = L.w[P.total + t];
+  // pads stay zero (the paired loads read them)
+  for (int e = t; e < TILE * (L.pst + L.dst); e += THREADS) post[e] = 0.0;
 
-  // gradient entries of this thread: trunk-relative flat index t + THREADS r, as
-  // (delta slot | activation slot << 16), 0xffffffff past the trunk
-  uint32_t map[R];
-  double acc[R];
+  // Gradient ownership: thread (i, kg) accumulates W_l(i, k) for k in [8 kg, 8 kg + 8) of every
+  // layer and, for kg = 0, b_l(i): delta_l(s, i) is loaded once per sample and layer, the 8
+  // activations as 4 broadcast double2.
+  const int i = t & 63, kg = t >> 6, sg = kg;  // sg: sample group (samples sg + 8 q) elsewhere
+  double accW[4][8], accB[4];
 #pragma unroll
-  for (int r = 0; r < R; ++r) {
-    const int e = t + THREADS * r;
-    acc[r] = 0.0;
-    map[r] = 0xffffffffu;
-    if (e < N.total) {
-      int l = 3;
-      while (l > 0 && e < S.wr[l]) --l;
-      const int rows = N.out[l];
-      uint32_t dix, pix;
-      if (e < S.br[l]) {
-        const int f = e - S.wr[l];
-        dix = doff(P, l) + f % rows;
-        pix = poff(P, l) + f / rows;
-      } else {
-        dix = doff(P, l) + (e - S.br[l]);
-        pix = one;
-      }
-      map[r] = dix | (pix << 16);
-    }
+  for (int l = 0; l < 4; ++l) {
+    accB[l] = 0.0;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) accW[l][j] = 0.0;
   }
   double lsg0 = 0.0, lsg1 = 0.0, lsum = 0.0;  // log_std gradient (lanes j, j + 32), loss term
   const int c0 = chunk * L.chunk, c1 = min(L.n, c0 + L.chunk);
-  const int i = t & 63, sg = t >> 6;  // neuron / column and sample group of this thread
   __syncthreads();
 
   for (int base = c0; base < c1; base += TILE) {
@@ -141,39 +131,51 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
       if (g < c1) v = L.obs[(size_t)(L.idx ? L.idx[g] : g) * P.obs + k];
       post[s * L.pst + k] = v;
     }
-    if (t < TILE) post[t * L.pst + one] = base + t < c1 ? 1.0 : 0.0;
     __syncthreads();
-    // ---- forward (mlp_forward, policy.cpp:15-31): z = W h + b, ELU on the hidden layers
+    // ---- forward (mlp_forward, policy.cpp:15-31): z = W h + b, ELU on the hidden layers;
+    // thread = neuron i x samples sg + 8 q, input pairs as broadcast double2
     for (int l = 0; l < 4; ++l) {
       const int rows = N.out[l], cols = N.in[l];
       if (i < rows) {
-        const double* Wl = W + S.w[l];
+        const double* Wl = W + S.w[l] + i;
         const int ld = S.ld[l];
-        const double* x0 = post + sg * L.pst + poff(P, l);
-        const double* x1 = x0 + 8 * L.pst;
-        double a0 = 0.0, a1 = 0.0;
-#pragma unroll 4
-        for (int k = 0; k < cols; ++k) {
-          const double wk = Wl[k * ld + i];
-          a0 = fma(wk, x0[k], a0);
-          a1 = fma(wk, x1[k], a1);
+        const double2* x = reinterpret_cast<const double2*>(post + sg * L.pst + poff(P, l));
+        const int xs = 4 * L.pst;  // 8 samples, in double2
+        double a[SPT];
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) a[q] = 0.0;
+#pragma unroll 2
+        for (int k2 = 0; k2 < cols / 2; ++k2) {
+          const double w0 = Wl[2 * k2 * ld], w1 = Wl[(2 * k2 + 1) * ld];
+#pragma unroll
+          for (int q = 0; q < SPT; ++q) {
+            const double2 u = x[q * xs + k2];
+            a[q] = fma(w1, u.y, fma(w0, u.x, a[q]));
+          }
         }
-        const double z0 = a0 + W[S.b[l] + i], z1 = a1 + W[S.b[l] + i];
-        if (l < 3) {
-          post[sg * L.pst + poff(P, l + 1) + i] = z0 > 0.0 ? z0 : expm1(z0);
-          post[(sg + 8) * L.pst + poff(P, l + 1) + i] = z1 > 0.0 ? z1 : expm1(z1);
-          del[sg * L.dst + doff(P, l) + i] = z0 > 0.0 ? 1.0 : exp(z0);  // elu_grad, ppo.cpp:12
-          del[(sg + 8) * L.dst + doff(P, l) + i] = z1 > 0.0 ? 1.0 : exp(z1);
-        } else {
-          out[sg * MAXIO + i] = z0;
-          out[(sg + 8) * MAXIO + i] = z1;
+        if (cols & 1) {
+          const double w0 = Wl[(cols - 1) * ld];
+#pragma unroll
+          for (int q = 0; q < SPT; ++q) a[q] = fma(w0, x[q * xs + cols / 2].x, a[q]);
+        }
+        const double bi = W[S.b[l] + i];
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) {
+          const int s = sg + 8 * q;
+          const double z = a[q] + bi;
+          if (l < 3) {
+            post[s * L.pst + poff(P, l + 1) + i] = z > 0.0 ? z : expm1(z);
+            del[s * L.dst + doff(P, l) + i] = z > 0.0 ? 1.0 : exp(z);  // elu_grad, ppo.cpp:12
+          } else {
+            out[s * L.ost + i] = z;
+          }
         }
       }
       __syncthreads();
     }
     // ---- loss head (ppo.cpp:92-126), warp = sample
-    {
-      const int s = warp, g = base + s;
+    for (int s = warp; s < TILE; s += WARPS) {
+      const int g = base + s;
       const bool valid = g < c1;
       const size_t row = valid ? (size_t)(L.idx ? L.idx[g] : g) : 0;
       double* d3 = del + s * L.dst + doff(P, 3);
@@ -182,12 +184,12 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
         double z0 = 0.0, z1 = 0.0, sd0 = 1.0, sd1 = 1.0, lp = 0.0;
         if (lane < A) {
           sd0 = exp(lstd[lane]);
-          z0 = (L.act[row * A + lane] - out[s * MAXIO + lane]) / sd0;
+          z0 = (L.act[row * A + lane] - out[s * L.ost + lane]) / sd0;
           lp += -0.5 * z0 * z0 - lstd[lane] - kLogSqrt2Pi;
         }
         if (lane + 32 < A) {
           sd1 = exp(lstd[lane + 32]);
-          z1 = (L.act[row * A + lane + 32] - out[s * MAXIO + lane + 32]) / sd1;
+          z1 = (L.act[row * A + lane + 32] - out[s * L.ost + lane + 32]) / sd1;
           lp += -0.5 * z1 * z1 - lstd[lane + 32] - kLogSqrt2Pi;
         }
         lp = warp_sum(lp);
@@ -207,42 +209,59 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
           d3[lane + 32] = on ? g_logp * z1 / sd1 : 0.0;
           if (on) lsg1 += g_logp * (z1 * z1 - 1.0);
         }
+        if (lane == 0 && (A & 1)) d3[A] = 0.0;  // pad of the paired loads
       } else if (lane == 0) {
-        const double verr = valid ? out[s * MAXIO] - L.ret[row] : 0.0;
+        const double verr = valid ? out[s * L.ost] - L.ret[row] : 0.0;
         if (valid) lsum += 0.5 * verr * verr * L.inv_n;
         d3[0] = valid ? L.value_coef * verr * L.inv_n : 0.0;
+        d3[1] = 0.0;  // pad of the paired loads
       }
     }
     __syncthreads();
-    // ---- backward (mlp_backward, ppo.cpp:64-77): delta_{l-1} = (W_l^T delta_l) .* ELU'(z_{l-1})
+    // ---- backward (mlp_backward, ppo.cpp:64-77): delta_{l-1} = (W_l^T delta_l) .* ELU'(z_{l-1});
+    // thread = column i x samples sg + 8 q, delta pairs as broadcast double2
     for (int l = 3; l > 0; --l) {
       const int rows = N.out[l], cols = N.in[l];
       if (i < cols) {
         const double* Wl = W + S.w[l] + i * S.ld[l];
-        const double* e0 = del + sg * L.dst + doff(P, l);
-        const double* e1 = e0 + 8 * L.dst;
-        double b0 = 0.0, b1 = 0.0;
-#pragma unroll 4
-        for (int r = 0; r < rows; ++r) {
-          const double wk = Wl[r];
-          b0 = fma(wk, e0[r], b0);
-          b1 = fma(wk, e1[r], b1);
+        const double2* e = reinterpret_cast<const double2*>(del + sg * L.dst + doff(P, l));
+        const int es = 4 * L.dst;  // 8 samples, in double2
+        double b[SPT];
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) b[q] = 0.0;
+#pragma unroll 2
+        for (int r2 = 0; r2 < (rows + 1) / 2; ++r2) {
+          const double w0 = Wl[2 * r2], w1 = 2 * r2 + 1 < rows ? Wl[2 * r2 + 1] : 0.0;
+#pragma unroll
+          for (int q = 0; q < SPT; ++q) {
+            const double2 u = e[q * es + r2];
+            b[q] = fma(w1, u.y, fma(w0, u.x, b[q]));
+          }
         }
-        del[sg * L.dst + doff(P, l - 1) + i] *= b0;
-        del[(sg + 8) * L.dst + doff(P, l - 1) + i] *= b1;
+#pragma unroll
+        for (int q = 0; q < SPT; ++q) del[(sg + 8 * q) * L.dst + doff(P, l - 1) + i] *= b[q];
       }
       __syncthreads();
     }
     // ---- gradient: W_l += delta_l post_l^T, b_l += delta_l over the tile
+#pragma unroll 1
+    for (int s = 0; s < TILE; ++s) {
 #pragma unroll
-    for (int r = 0; r < R; ++r) {
-      if (map[r] != 0xffffffffu) {
-        const double* dp = del + (map[r] & 0xffffu);
-        const double* pp = post + (map[r] >> 16);
-        double a = acc[r];
+      for (int l = 0; l < 4; ++l) {
+        const int rows = N.out[l], cols = N.in[l];
+        if (i < rows) {
+          const double d = del[s * L.dst + doff(P, l) + i];
+          if (kg == 0) accB[l] += d;
+          if (8 * kg < cols) {
+            const double2* pp = reinterpret_cast<const double2*>(post + s * L.pst + poff(P, l) + 8 * kg);
 #pragma unroll
-        for (int s = 0; s < TILE; ++s) a = fma(dp[s * L.dst], pp[s * L.pst], a);
-        acc[r] = a;
+            for (int j2 = 0; j2 < 4; ++j2) {
+              const double2 u = pp[j2];
+              accW[l][2 * j2] = fma(d, u.x, accW[l][2 * j2]);
+              accW[l][2 * j2 + 1] = fma(d, u.y, accW[l][2 * j2 + 1]);
+            }
+          }
+        }
       }
     }
     __syncthreads();
@@ -250,8 +269,15 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   // ---- per-chunk partials: gradient entries, log_std gradient (pi), loss term
   double* part = L.part + (size_t)(trunk * L.nch + chunk) * L.part_stride;
 #pragma unroll
-  for (int r = 0; r < R; ++r)
-    if (map[r] != 0xffffffffu) part[t + THREADS * r] = acc[r];
+  for (int l = 0; l < 4; ++l) {
+    const int rows = N.out[l], cols = N.in[l];
+    if (i < rows) {
+#pragma unroll
+      for (int j = 0; j < 8; ++j)
+        if (8 * kg + j < cols) part[S.wr[l] + (8 * kg + j) * rows + i] = accW[l][j];
+      if (kg == 0) part[S.br[l] + i] = accB[l];
+    }
+  }
   if (trunk == 0) {
     red[warp * MAXIO + lane] = lsg0;
     red[warp * MAXIO + lane + 32] = lsg1;
@@ -283,8 +309,17 @@ __global__ void reduce_kernel(const PolicyParams P, int nch, int part_stride, co
     } else if (p >= P.total) {
       e = P.pi.total + (p - P.total);
     }
-    double v = 0.0;
-    for (int c = 0; c < nch; ++c) v += part[(size_t)(tr * nch + c) * part_stride + e];
+    const double* q = part + (size_t)tr * nch * part_stride + e;
+    double v0 = 0.0, v1 = 0.0, v2 = 0.0, v3 = 0.0;  // four fixed interleaved chains
+    int c = 0;
+    for (; c + 4 <= nch; c += 4) {
+      v0 += q[(size_t)c * part_stride];
+      v1 += q[(size_t)(c + 1) * part_stride];
+      v2 += q[(size_t)(c + 2) * part_stride];
+      v3 += q[(size_t)(c + 3) * part_stride];
+    }
+    for (; c < nch; ++c) v0 += q[(size_t)c * part_stride];
+    double v = (v0 + v1) + (v2 + v3);
     if (p >= P.total && entropy_coef != 0.0) v -= entropy_coef;
     if (grads) grads[p] = v;
   }
@@ -367,11 +402,6 @@ __global__ void __launch_bounds__(RED_THREADS) adam_kernel(int np, const double*
   }
 }
 
-int rmax_for(int total) {
-  const int need = (total + THREADS - 1) / THREADS;
-  return need <= 8 ? 8 : need <= 16 ? 16 : need <= 24 ? 24 : 33;
-}
-
 TrunkSm trunk_sm(const Net& N) {
   TrunkSm S{};
   int off = 0;
@@ -400,8 +430,10 @@ int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, con
   L.n = n;
   L.nch = std::max(1, std::min(p->sms / 2, (n + TILE - 1) / TILE));
   L.chunk = (n + L.nch - 1) / L.nch;
-  L.pst = P.obs + 3 * P.hidden + 1;
-  L.dst = 3 * P.hidden + MAXIO;
+  const int ob2 = (P.obs + 1) & ~1, h2 = (P.hidden + 1) & ~1;
+  L.pst = ob2 + 3 * h2 + 2;
+  L.dst = 3 * h2 + ((P.act + 1) & ~1);
+  L.ost = (P.act + 1) & ~1;
   L.part_stride = std::max(P.pi.total, P.vf.total) + 2 * MAXIO;
   L.clip_eps = cfg.clip_eps;
   L.value_coef = cfg.value_coef;
@@ -423,16 +455,10 @@ int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, con
   }
   L.part = p->d_part;
   const int wmax = std::max(L.ts[0].wtotal, L.ts[1].wtotal);
-  const int smem = (int)sizeof(double) * (wmax + TILE * L.pst + TILE * L.dst + TILE * MAXIO + WARPS * MAXIO);
-  const int R = rmax_for(std::max(P.pi.total, P.vf.total));
-  auto go = [&](auto kern) {
-    if (cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) return false;
-    kern<<<dim3(L.nch, 2), THREADS, smem, st>>>(L);
-    return true;
-  };
-  const bool ok = R == 8 ? go(loss_kernel<8>) : R == 16 ? go(loss_kernel<16>) : R == 24 ? go(loss_kernel<24>)
-                                                                                : go(loss_kernel<33>);
-  if (!ok) return RMPC_ERR_CUDA;
+  const int smem = (int)sizeof(double) * (wmax + TILE * L.pst + TILE * L.dst + TILE * L.ost);
+  if (cudaFuncSetAttribute(loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
+    return RMPC_ERR_CUDA;
+  loss_kernel<<<dim3(L.nch, 2), THREADS, smem, st>>>(L);
   const int np = P.total + P.act;
   reduce_kernel<<<(np + 255) / 256, 256, 0, st>>>(P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef,
                                                  p->d_w, grads, info);

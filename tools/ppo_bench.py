@@ -1,7 +1,7 @@
 """PPO batch measurement: one ppo_update (ppo.cpp:193-276) at the
 reference Trainer's shape -- n_steps 24 x E envs, 4 epochs x 4 minibatches, hidden 64, obs 23,
-act 6 -- on a device-resident synthetic rollout, plus the ppo_loss kernel alone on one
-minibatch with its FP64 roofline (algorithmic FLOPs / kernel time vs the measured FP64 FMA
+act 6 -- on a device-resident synthetic rollout, plus one ppo_loss call (loss + reduce kernels)
+on one minibatch with its FP64 roofline (algorithmic FLOPs / kernel time vs the measured FP64 FMA
 peak), and the FP64 CPU oracle on a bounded sample of the same loss.
 
 python tools/ppo_bench.py [envs] > profiles/rNN_ppo_bench.json   (on a B200)
@@ -101,8 +101,8 @@ def main():
         "samples_per_s": samples_per_update / t_up,
         "note_update": "host wall time of the synchronous rmpc_ppo_update_device call: GAE, normalisation, host "
                        "Fisher-Yates + one H2D of the permutations, 16 x (loss + reduce + clip/Adam) launches",
-        "loss_kernel": {
-            "minibatch": mb, "ms": t_loss * 1e3, "samples_per_s": mb / t_loss,
+        "ppo_loss": {
+            "launches": "loss_kernel + reduce_kernel", "minibatch": mb, "ms": t_loss * 1e3, "samples_per_s": mb / t_loss,
             "flop_alg_per_sample": fl,
             "roofline": {"bound": "fp64", "achieved": fl * mb / t_loss / 1e12, "peak": peak.value,
                          "unit": "TFLOP/s", "frac": fl * mb / t_loss / 1e12 / peak.value,

@@ -150,7 +150,7 @@ int32_t rmpc_gae_device(int32_t steps, int32_t envs, const double* d_rewards, co
                         const double* d_dones, const double* d_bootstrap, double gamma, double lam,
                         double* d_advantages, double* d_returns, void* stream);
 
-/* AdamOptimizer(num_params, lr) (ppo.cpp:181-191, betas 0.9 / 0.999, eps 1e-8) bound to a
+/* AdamOptimizer(num_params, lr) (ppo.cpp:179-193, betas 0.9 / 0.999, eps 1e-8) bound to a
  * policy: its moment vectors live on the policy's device. */
 typedef struct rmpc_adam rmpc_adam;
 int32_t rmpc_adam_create(rmpc_policy* policy, double lr, rmpc_adam** out);
@@ -159,7 +159,7 @@ void rmpc_adam_destroy(rmpc_adam* adam);
 /* Rng(seed, stream) (rng.hpp:15-25) as its four xoshiro256++ words, for rmpc_ppo_update_device. */
 void rmpc_rng_seed(uint64_t seed, uint64_t stream, uint64_t state[4]);
 
-/* ppo_update (ppo.cpp:193-276) on the policy's device parameters: GAE, advantage
+/* ppo_update (ppo.cpp:195-276) on the policy's device parameters: GAE, advantage
  * normalisation, then epochs x minibatches of {shuffle (Fisher-Yates on rng_state, advanced
  * exactly like the reference's update_rng), ppo_loss + gradient, clip to max_grad_norm, Adam}.
  * The rollout is device-resident, steps x envs (obs steps x envs x obs_dim, actions

@@ -4,11 +4,11 @@
 //
 //   mlp_forward (with cache)   /root/reference/proj/src/policy.cpp:15-31
 //   gaussian_log_prob          policy.cpp:168-176
-//   mlp_backward               ppo.cpp:64-77
+//   mlp_backward               ppo.cpp:63-77
 //   ppo_loss                   ppo.cpp:79-135
 //   gae_advantages             ppo.cpp:28-45
-//   AdamOptimizer::step        ppo.cpp:181-191 (defaults ppo.hpp:93-94)
-//   ppo_update                 ppo.cpp:193-276 (Fisher-Yates with Rng::uniform_int, rng.hpp:43)
+//   AdamOptimizer::step        ppo.cpp:179-193 (defaults ppo.hpp:93-94)
+//   ppo_update                 ppo.cpp:195-276 (Fisher-Yates with Rng::uniform_int, rng.hpp:43)
 //
 // Parameters are the flat vector of flatten_policy (ppo.cpp:144-153): per trunk and layer W
 // (out x in, column-major) then b; pi, then value, then log_std.
@@ -69,7 +69,7 @@ inline std::vector<double> trunk_forward(const double* p, const TrunkShape& t, c
   return h;
 }
 
-// mlp_backward (ppo.cpp:64-77): grads += d(loss)/d(params) of one trunk for output gradient g.
+// mlp_backward (ppo.cpp:63-77): grads += d(loss)/d(params) of one trunk for output gradient g.
 inline void trunk_backward(const double* p, const TrunkShape& t, const TrunkCache& c,
                            std::vector<double> delta, double* g) {
   for (int l = 3; l >= 0; --l) {
@@ -172,7 +172,7 @@ inline void gae(int T, int E, const double* rewards, const double* values, const
   }
 }
 
-struct Adam {  // AdamOptimizer (ppo.cpp:181-191)
+struct Adam {  // AdamOptimizer (ppo.cpp:179-193)
   double lr, beta1 = 0.9, beta2 = 0.999, eps = 1e-8;
   int t = 0;
   std::vector<double> m, v;
@@ -188,7 +188,7 @@ struct Adam {  // AdamOptimizer (ppo.cpp:181-191)
   }
 };
 
-// ppo_update (ppo.cpp:193-276) over a rollout of T steps x E envs (obs T x E x obs_dim,
+// ppo_update (ppo.cpp:195-276) over a rollout of T steps x E envs (obs T x E x obs_dim,
 // actions T x E x act, the rest T x E; bootstrap E).  params are updated in place.
 inline rmpc_ppo_update_stats ppo_update(double* params, int obs_dim, int act, int hidden, int T, int E,
                                         const double* obs, const double* actions, const double* logp,

@@ -4,11 +4,11 @@
 //   rmpc_ppo_loss_device    ppo_loss (ppo.cpp:79-135): policy_forward with the cache
 //                           (policy.cpp:85-102), gaussian_log_prob (policy.cpp:168-176), the
 //                           clipped surrogate / value / entropy terms and mlp_backward
-//                           (ppo.cpp:64-77) summed over the batch
+//                           (ppo.cpp:63-77) summed over the batch
 //   rmpc_gae_device         gae_advantages (ppo.cpp:28-45)
-//   rmpc_ppo_update_device  ppo_update (ppo.cpp:193-276): GAE, advantage normalisation, epochs x
+//   rmpc_ppo_update_device  ppo_update (ppo.cpp:195-276): GAE, advantage normalisation, epochs x
 //                           minibatches of {Fisher-Yates shuffle, ppo_loss, gradient-norm clip,
-//                           AdamOptimizer::step (ppo.cpp:181-191)}
+//                           AdamOptimizer::step (ppo.cpp:179-193)}
 //
 // Loss kernel.  The batch gradient is a sum over samples of outer products delta_l post_l^T,
 // i.e. per layer a (out x n) . (n x in) product with a long reduction dimension: the kernel is
@@ -218,7 +218,7 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
       }
     }
     __syncthreads();
-    // ---- backward (mlp_backward, ppo.cpp:64-77): delta_{l-1} = (W_l^T delta_l) .* ELU'(z_{l-1});
+    // ---- backward (mlp_backward, ppo.cpp:63-77): delta_{l-1} = (W_l^T delta_l) .* ELU'(z_{l-1});
     // thread = column i x samples sg + 8 q, delta pairs as broadcast double2
     for (int l = 3; l > 0; --l) {
       const int rows = N.out[l], cols = N.in[l];
@@ -369,7 +369,7 @@ __device__ double block_sum(double v, double* sh) {
   return r;
 }
 
-// Advantage normalisation of ppo_update (ppo.cpp:199-202), one block.
+// Advantage normalisation of ppo_update (ppo.cpp:201-204), one block.
 __global__ void __launch_bounds__(RED_THREADS) normalize_kernel(int N, double* adv) {
   __shared__ double sh[RED_THREADS];
   double s = 0.0;
@@ -382,7 +382,7 @@ __global__ void __launch_bounds__(RED_THREADS) normalize_kernel(int N, double* a
   for (int k = threadIdx.x; k < N; k += RED_THREADS) adv[k] = (adv[k] - mean) * inv_std;
 }
 
-// Gradient-norm clip (ppo.cpp:255-257) + AdamOptimizer::step (ppo.cpp:181-191), one block.
+// Gradient-norm clip (ppo.cpp:252-256) + AdamOptimizer::step (ppo.cpp:179-193), one block.
 __global__ void __launch_bounds__(RED_THREADS) adam_kernel(int np, const double* __restrict__ g, double* m, double* v,
                                                            double* w, double max_norm, double lr, double b1,
                                                            double b2, double eps, double bc1, double bc2) {

@@ -3,8 +3,8 @@ reference (/root/reference/proj/src/ppo.cpp):
 
   ppo_loss    ppo_loss (ppo.cpp:79-135): loss terms and the gradient of every parameter
   gae         gae_advantages (ppo.cpp:28-45)
-  Adam        AdamOptimizer (ppo.cpp:181-191), moments on the policy's device
-  ppo_update  ppo_update (ppo.cpp:193-276) on a device-resident rollout
+  Adam        AdamOptimizer (ppo.cpp:179-193), moments on the policy's device
+  ppo_update  ppo_update (ppo.cpp:195-276) on a device-resident rollout
 
 Tensors are CUDA float64; rollouts are (steps, envs[, dim]) row-major like RolloutBuffer.
 """

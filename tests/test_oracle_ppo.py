@@ -3,7 +3,7 @@ the reference ships no PPO test (tests/CMakeLists.txt has none), so ppo_loss's g
 (ppo.cpp:79-135) is checked against central finite differences of its own total loss, the
 loss terms against an independent numpy restatement of policy_forward / gaussian_log_prob
 (policy.cpp:15-31, 85-102, 168-176), gae_advantages (ppo.cpp:28-45) against a numpy loop, and
-ppo_update (ppo.cpp:193-276) against the closed form of one Adam step (t = 1) and the Rng
+ppo_update (ppo.cpp:195-276) against the closed form of one Adam step (t = 1) and the Rng
 draws its shuffles consume.  CPU only."""
 import numpy as np
 import pytest
@@ -134,7 +134,7 @@ def test_update_single_step_closed_form(oracle):
     # the shuffle only reorders the sum: the step agrees to rounding
     np.testing.assert_allclose(p - R["params"], -1e-3 * g / (np.abs(g) + 1e-8), rtol=1e-6, atol=1e-12)
     assert adam.t.value == 1
-    # the Rng advanced by exactly N - 1 uniform_int draws (Fisher-Yates, ppo.cpp:222)
+    # the Rng advanced by exactly N - 1 uniform_int draws (Fisher-Yates, ppo.cpp:230)
     x = Xoshiro(0, [0x0272])
     for _ in range(T * E - 1):
         x.next_u64()

@@ -1,4 +1,4 @@
-"""PPO batch measurement: one ppo_update (ppo.cpp:193-276) at the
+"""PPO batch measurement: one ppo_update (ppo.cpp:195-276) at the
 reference Trainer's shape -- n_steps 24 x E envs, 4 epochs x 4 minibatches, hidden 64, obs 23,
 act 6 -- on a device-resident synthetic rollout, plus one ppo_loss call (loss + reduce kernels)
 on one minibatch with its FP64 roofline (algorithmic FLOPs / kernel time vs the measured FP64 FMA

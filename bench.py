@@ -128,12 +128,25 @@ class NvmlClockSampler:
                 pass
             time.sleep(0.001)
 
+    def _sample(self):
+        try:
+            self.samples.append((self.N.nvmlDeviceGetClockInfo(self.h, self.N.NVML_CLOCK_SM),
+                                 self.N.nvmlDeviceGetCurrentClocksEventReasons(self.h)))
+        except Exception:
+            pass
+
     def start(self):
+        # the poller needs the GIL every ~1 ms while the timed loop runs Python between launches
+        self._switch = sys.getswitchinterval()
+        sys.setswitchinterval(2e-4)
+        self._sample()
         self.t.start()
 
     def stop(self):
         self.stop_ev.set()
         self.t.join()
+        self._sample()
+        sys.setswitchinterval(self._switch)
         N = self.N
         if not self.samples:
             return None

@@ -234,8 +234,8 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
 // CTA = P.agents_per_cta warp pairs.  Warp w uses TMEM lanes [32 (w % 4), +32) (the quarter
 // tcgen05.ld/st of warp w can reach) and columns [(w / 4) tmn 32, +tmn 32), tmn = the node
 // blocks its quarter's share holds (tm_nodes); further blocks go to its shared-memory spill.
-template <bool SPILL>
-__global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P) {
+template <bool SPILL, int MAXA>
+__global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   extern __shared__ __align__(16) float smem[];
   __shared__ uint32_t tmem_base;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -273,9 +273,10 @@ __global__ void __launch_bounds__(64 * MAX_AGENTS, 1) rti_kernel(const KParams P
 
 int rmpc_kernel_setup(int) {
   const int bytes = 227 * 1024 - 128;  // static smem: the TMEM base
-  int rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
-  if (rc == 0)
-    rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, bytes);
+  const cudaFuncAttribute a = cudaFuncAttributeMaxDynamicSharedMemorySize;
+  int rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS>, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS>, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS>, a, bytes);
   return rc;
 }
 
@@ -305,9 +306,12 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   P.full_ctas = full_waves * nsm;
   P.tail_agents = tail;
   const int grid = P.full_ctas + tail_ctas;
-  if (c.spill_nodes > 0)
-    rmpc_dev::rti_kernel<true><<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
+  const cudaStream_t st = (cudaStream_t)stream;
+  if (c.dense)
+    rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+  else if (c.spill_nodes > 0)
+    rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
   else
-    rmpc_dev::rti_kernel<false><<<grid, 64 * c.agents, c.smem_bytes, (cudaStream_t)stream>>>(P);
+    rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
   return (int)cudaGetLastError();
 }

@@ -96,7 +96,8 @@ def test_cta_shape_six_agents_per_sm_at_n10():
     assert L.rmpc_agents_per_cta(32) == 2
     for T in range(2, 33):
         A = L.rmpc_agents_per_cta(T)
-        assert 1 <= A <= 6 and A * L.rmpc_smem_bytes(T) <= 227 * 1024 - 128
+        assert 1 <= A <= 8 and A * L.rmpc_smem_bytes(T) <= 227 * 1024 - 128
+        assert (A == 8) == (T <= 8)  # the dense variant: all node blocks in TMEM at 16 warps
     assert L.rmpc_agents_per_cta(0) == -1 and L.rmpc_agents_per_cta(33) == -1
 
 

@@ -16,7 +16,7 @@ import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 LIB = os.environ.get("RMPC_B200_LIB") or os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
-FUNC = os.environ.get("RMPC_NCU_FUNC", "_ZN8rmpc_dev10rti_kernelILb0EEEvNS_7KParamsE")  # the TMEM-only instantiation (T <= 10)
+FUNC = os.environ.get("RMPC_NCU_FUNC", "_ZN8rmpc_dev10rti_kernelILb0ELi6EEEvNS_7KParamsE")  # the wide TMEM-only instantiation (T = 9, 10)
 
 
 def line_table():

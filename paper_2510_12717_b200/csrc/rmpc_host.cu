@@ -26,8 +26,9 @@ thread_local std::string g_create_error;
 struct Shard {
   int device = 0;
   int begin = 0, count = 0;
-  cudaStream_t stream = nullptr;
-  cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+  int sms = 148;
+  cudaStream_t stream = nullptr, stream2 = nullptr;  // stream2: the second chunk of a tick
+  cudaEvent_t ev[8] = {};
   rmpc_state* d_states = nullptr;
   rmpc_command* d_cmds = nullptr;
   rmpc_gait* d_gaits = nullptr;
@@ -164,6 +165,8 @@ bool is_pinned(const void* p) {
 void alloc_shard(rmpc_handle& h, Shard& sh) {
   CK(cudaSetDevice(sh.device));
   CK(cudaStreamCreateWithFlags(&sh.stream, cudaStreamNonBlocking));
+  CK(cudaStreamCreateWithFlags(&sh.stream2, cudaStreamNonBlocking));
+  cudaDeviceGetAttribute(&sh.sms, cudaDevAttrMultiProcessorCount, sh.device);
   for (auto& e : sh.ev) CK(cudaEventCreate(&e));
   const size_t n = std::max(sh.count, 1);
   const size_t zn = n * h.NT * RMPC_NV;
@@ -190,14 +193,20 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
 void free_shard(Shard& sh) {
   cudaSetDevice(sh.device);
   if (sh.stream) cudaStreamSynchronize(sh.stream);
+  if (sh.stream2) cudaStreamSynchronize(sh.stream2);
   cudaFree(sh.d_states); cudaFree(sh.d_cmds); cudaFree(sh.d_gaits); cudaFree(sh.d_prev);
   cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof);
   cudaFreeHost(sh.h_stage_in); cudaFreeHost(sh.h_stage_out);
   for (auto& e : sh.ev) if (e) cudaEventDestroy(e);
   if (sh.stream) cudaStreamDestroy(sh.stream);
+  if (sh.stream2) cudaStreamDestroy(sh.stream2);
 }
 
-// H2D (staging pageable buffers through pinned memory), kernel, D2H, synchronize.
+// H2D (staging pageable buffers through pinned memory), kernel, D2H, synchronize.  A shard of
+// more than two waves runs as two chunks on two streams: the first wave of CTAs, then the
+// rest.  Chunk 1's inputs are small, so its kernel starts early; chunk 2's H2D overlaps chunk
+// 1's kernel, chunk 1's D2H overlaps chunk 2's kernel, and chunk 2's CTAs fill the SMs as
+// chunk 1's finish.  Per-agent results do not depend on the split.
 void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
                const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z,
                rmpc_solution* out, float* z_out) {
@@ -207,70 +216,93 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
   const size_t n = sh.count, b = sh.begin;
   const size_t zrow = (size_t)h.NT * RMPC_NV;
   const bool use_prev = h.settings.warm_start && prev && prev_z;
+  const size_t wave = (size_t)sh.sms * rmpc_dev::cta_shape(h.NT).agents;
+  const size_t n1 = (n > 2 * wave && !h.profile) ? wave : n;
+  const size_t cut[3] = {0, n1, n};
+  const int nchunks = n1 < n ? 2 : 1;
+  const cudaStream_t ss[2] = {sh.stream, sh.stream2};
   struct In {
-    const void* src;
-    void* dst;
-    size_t bytes;
+    const char* src;
+    char* dst;
+    size_t elem;  // bytes per agent
   };
-  std::vector<In> ins = {{states + b, sh.d_states, n * sizeof(rmpc_state)},
-                         {cmds + b, sh.d_cmds, n * sizeof(rmpc_command)},
-                         {gaits + b, sh.d_gaits, n * sizeof(rmpc_gait)}};
+  std::vector<In> ins = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), sizeof(rmpc_state)},
+                         {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), sizeof(rmpc_command)},
+                         {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), sizeof(rmpc_gait)}};
   if (use_prev) {
-    ins.push_back({prev + b, sh.d_prev, n * sizeof(rmpc_solution)});
-    ins.push_back({prev_z + b * zrow, sh.d_prev_z, n * zrow * sizeof(float)});
+    ins.push_back({reinterpret_cast<const char*>(prev + b), reinterpret_cast<char*>(sh.d_prev), sizeof(rmpc_solution)});
+    ins.push_back({reinterpret_cast<const char*>(prev_z + b * zrow), reinterpret_cast<char*>(sh.d_prev_z),
+                   zrow * sizeof(float)});
   }
-  CK(cudaEventRecord(sh.ev[0], sh.stream));
   size_t off = 0;
-  for (const In& c : ins) {
-    const void* src = c.src;
+  for (In& c : ins) {
     if (!is_pinned(c.src)) {
-      std::memcpy(sh.h_stage_in + off, c.src, c.bytes);
-      src = sh.h_stage_in + off;
-      off += (c.bytes + 255) & ~size_t(255);
+      std::memcpy(sh.h_stage_in + off, c.src, n * c.elem);
+      c.src = sh.h_stage_in + off;
+      off += (n * c.elem + 255) & ~size_t(255);
     }
-    CK(cudaMemcpyAsync(c.dst, src, c.bytes, cudaMemcpyHostToDevice, sh.stream));
   }
-  CK(cudaEventRecord(sh.ev[1], sh.stream));
-  rmpc_dev::KParams P = make_params(h);
-  P.n_agents = sh.count;
-  P.states = sh.d_states;
-  P.cmds = sh.d_cmds;
-  P.gaits = sh.d_gaits;
-  P.prev = use_prev ? sh.d_prev : nullptr;
-  P.prev_z = use_prev ? sh.d_prev_z : nullptr;
-  P.out = sh.d_out;
-  P.z_out = z_out ? sh.d_z : nullptr;
-  P.prof = sh.d_prof;
-  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, RMPC_NUM_STAGES * sizeof(unsigned long long), sh.stream));
-  const int rc = rmpc_launch_rti(P, sh.stream);
-  if (rc != 0) {
-    sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
-    sh.msg = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
-    return;
-  }
-  CK(cudaEventRecord(sh.ev[2], sh.stream));
   const bool out_pinned = is_pinned(out), z_pinned = is_pinned(z_out);
-  rmpc_solution* out_dst = out_pinned ? out + b : reinterpret_cast<rmpc_solution*>(sh.h_stage_out);
-  CK(cudaMemcpyAsync(out_dst, sh.d_out, n * sizeof(rmpc_solution), cudaMemcpyDeviceToHost, sh.stream));
-  float* z_dst = nullptr;
-  if (z_out) {
-    z_dst = z_pinned ? z_out + b * zrow
-                     : reinterpret_cast<float*>(sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255)));
-    CK(cudaMemcpyAsync(z_dst, sh.d_z, n * zrow * sizeof(float), cudaMemcpyDeviceToHost, sh.stream));
+  char* out_dst = out_pinned ? reinterpret_cast<char*>(out + b) : sh.h_stage_out;
+  char* z_dst = nullptr;
+  if (z_out)
+    z_dst = z_pinned ? reinterpret_cast<char*>(z_out + b * zrow)
+                     : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
+  CK(cudaEventRecord(sh.ev[0], ss[0]));
+  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
+  if (nchunks == 2) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
+  for (int k = 0; k < nchunks; ++k) {
+    const cudaStream_t st = ss[k];
+    const size_t lo = cut[k], m = cut[k + 1] - cut[k];
+    for (const In& c : ins)
+      CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
+    if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
+    rmpc_dev::KParams P = make_params(h);
+    P.n_agents = (int)m;
+    P.states = sh.d_states + lo;
+    P.cmds = sh.d_cmds + lo;
+    P.gaits = sh.d_gaits + lo;
+    P.prev = use_prev ? sh.d_prev + lo : nullptr;
+    P.prev_z = use_prev ? sh.d_prev_z + lo * zrow : nullptr;
+    P.out = sh.d_out + lo;
+    P.z_out = z_out ? sh.d_z + lo * zrow : nullptr;
+    P.prof = sh.d_prof;
+    const int rc = rmpc_launch_rti(P, st);
+    if (rc != 0) {
+      sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+      sh.msg = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+      cudaStreamSynchronize(ss[0]);
+      cudaStreamSynchronize(ss[1]);
+      return;
+    }
+    CK(cudaEventRecord(sh.ev[2 + k], st));  // kernel k done
+    CK(cudaMemcpyAsync(out_dst + lo * sizeof(rmpc_solution), sh.d_out + lo, m * sizeof(rmpc_solution),
+                       cudaMemcpyDeviceToHost, st));
+    if (z_out)
+      CK(cudaMemcpyAsync(z_dst + lo * zrow * sizeof(float), sh.d_z + lo * zrow, m * zrow * sizeof(float),
+                         cudaMemcpyDeviceToHost, st));
+    CK(cudaEventRecord(sh.ev[4 + k], st));  // results of chunk k on the host
   }
   if (h.profile)
-    CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, sh.stream));
-  CK(cudaEventRecord(sh.ev[3], sh.stream));
-  CK(cudaStreamSynchronize(sh.stream));
+    CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, ss[0]));
+  CK(cudaStreamSynchronize(ss[0]));
+  if (nchunks == 2) CK(cudaStreamSynchronize(ss[1]));
   if (!out_pinned) std::memcpy(out + b, out_dst, n * sizeof(rmpc_solution));
   if (z_out && !z_pinned) std::memcpy(z_out + b * zrow, z_dst, n * zrow * sizeof(float));
-  float t01 = 0, t12 = 0, t23 = 0;
+  // exposed stage times: chunk 1's H2D, first H2D done -> last kernel done, last kernel done ->
+  // last results on the host
+  const int last = nchunks - 1;
+  float t01 = 0, t1k = 0, tkd = 0, tk0 = 0;
   cudaEventElapsedTime(&t01, sh.ev[0], sh.ev[1]);
-  cudaEventElapsedTime(&t12, sh.ev[1], sh.ev[2]);
-  cudaEventElapsedTime(&t23, sh.ev[2], sh.ev[3]);
+  cudaEventElapsedTime(&t1k, sh.ev[1], sh.ev[2 + last]);
+  if (nchunks == 2) {
+    cudaEventElapsedTime(&tk0, sh.ev[1], sh.ev[2]);
+    t1k = std::max(t1k, tk0);
+  }
+  cudaEventElapsedTime(&tkd, sh.ev[2 + last], sh.ev[4 + last]);
   sh.h2d_ms = t01;
-  sh.kernel_ms = t12;
-  sh.d2h_ms = t23;
+  sh.kernel_ms = t1k;
+  sh.d2h_ms = tkd;
 }
 
 void fill_timing(rmpc_handle& h, double total_ms) {

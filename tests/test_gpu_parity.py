@@ -107,10 +107,12 @@ def test_batch_equals_serial_and_order_free():
     assert sh.tobytes() == sol.tobytes() and zh.tobytes() == z.tobytes()
 
 
-def test_device_path_matches_host_path():
+@pytest.mark.parametrize("T,n", [(10, 1000), (10, 2 * 148 * 6 + 37), (5, 2 * 148 * 8 + 5)])
+def test_device_path_matches_host_path(T, n):
+    """The host path splits a shard of more than two waves into two chunks on two streams
+    (rmpc_host.cu run_shard); the device path is one launch.  Bit-identical either way."""
     import torch
-    m, s = default_model(), default_settings(10)
-    n = 1000
+    m, s = default_model(), default_settings(T)
     st, cm, ga = R.synthetic_batch(n, "random", seed=6, model=m, settings=s)
     br = R.BatchRunner(n, m, s)
     sol, z = br.solve(st, cm, ga, want_z=True)
@@ -119,12 +121,36 @@ def test_device_path_matches_host_path():
     with torch.cuda.stream(stream):
         t = [torch.from_numpy(a).to(dev) for a in (st, cm, ga)]
         out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
-        zd = torch.zeros(n * 10 * 26, dtype=torch.float32, device=dev)
+        zd = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
         br.solve_device(*t, out, z_out=zd, stream=stream)
     stream.synchronize()
     got = np.frombuffer(out.cpu().numpy().tobytes(), dtype=SOLUTION_DTYPE)
     assert got.tobytes() == sol.tobytes()
     assert zd.cpu().numpy().tobytes() == z.reshape(-1).tobytes()
+
+
+def test_warm_start_chunked_host_path_matches_device_path():
+    """Warm start through the two-chunk host path (prev and prev z* sliced per chunk) against
+    the one-launch device path: bit-identical over two ticks."""
+    import torch
+    m, s = default_model(), default_settings(10)
+    s.warm_start = 1
+    n = 2 * 148 * 6 + 11
+    st, cm, ga = R.synthetic_batch(n, "random", seed=9, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    sol0, z0 = br.solve(st, cm, ga, want_z=True)
+    ga[:, 0] = (ga[:, 0] + 0.01 / ga[:, 1]) % 1.0
+    sol1, z1 = br.solve(st, cm, ga, prev=(sol0, z0), want_z=True)
+    dev = torch.device("cuda:0")
+    t = [torch.from_numpy(a).to(dev) for a in (st, cm, ga)]
+    pv = torch.from_numpy(np.frombuffer(sol0.tobytes(), dtype=np.uint8).copy()).to(dev)
+    pz = torch.from_numpy(z0.reshape(-1).copy()).to(dev)
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    zd = torch.zeros(n * 10 * 26, dtype=torch.float32, device=dev)
+    br.solve_device(*t, out, z_out=zd, prev=pv, prev_z=pz)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == sol1.tobytes()
+    assert zd.cpu().numpy().tobytes() == z1.reshape(-1).tobytes()
 
 
 def test_full_size_properties_and_sampled_parity(oracle):

@@ -14,16 +14,17 @@
 // i.e. per layer a (out x n) . (n x in) product with a long reduction dimension: the kernel is
 // split-K over the samples.  Grid = (chunks, 2): blockIdx.y picks the trunk (pi / value, which
 // are independent given the batch), blockIdx.x a contiguous chunk of samples.  A block keeps its
-// trunk's weights in shared memory (column stride padded to an odd count, so the transposed
-// product W^T delta of the backward pass reads conflict-free) and walks its chunk in tiles of
-// 32 samples: forward (thread = neuron i x 4 samples, activations and ELU derivatives cached
-// in shared memory), the per-sample loss head (warp = sample), backward layer by layer, then
-// the gradient update.  Thread (i, kg) owns the gradient entries W_l(i, 8 kg .. 8 kg + 7) (and
-// b_l(i) for kg = 0) of every layer in registers for the whole chunk, so the reduction over
-// samples never leaves the SM; the per-chunk partial gradients are summed in a fixed order by a
-// second kernel (deterministic, no atomics).  Every phase is shared-memory bound: activation and
-// delta pairs are read as broadcast double2, weights as per-lane scalars.  TF32/BF16 tensor cores
-// would miss the FP64 reference by orders of magnitude; the FP64 work is ~0.11 MFLOP per sample.
+// trunk's weights in shared memory and walks its chunk in tiles of 32 samples: forward
+// (activations and ELU derivatives cached in shared memory), the per-sample loss head (warp =
+// sample), backward layer by layer, then the gradient update, whose per-thread share stays in
+// registers for the whole chunk; the per-chunk partial gradients are summed in a fixed order by
+// a second kernel (deterministic, no atomics).  Two implementations of the block:
+//   loss_kernel_mma  every product on the FP64 tensor cores (mma.sync.m8n8k4.f64 -- tcgen05 has
+//                    no FP64 kind; TF32/BF16 would miss the FP64 reference by orders of
+//                    magnitude), operands straight from shared memory in 8x8 blocks
+//   loss_kernel<TL>  CUDA-core FMAs for shapes beyond the tensor-core layout (obs > 32 or
+//                    shared memory), thread = neuron x TL/8 samples, paired double2 loads
+// The FP64 work is ~0.11 MFLOP per sample.
 #include <cuda_runtime.h>
 #include <math.h>
 #include <stdint.h>
@@ -84,6 +85,7 @@ __device__ __forceinline__ int poff(const PolicyParams& P, int l) {
 }
 __device__ __forceinline__ int doff(const PolicyParams& P, int l) { return l * even_up(P.hidden); }
 
+template <int TL>
 __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   extern __shared__ __align__(16) double sm[];
   __shared__ double lstd[MAXIO];
@@ -94,8 +96,8 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   const TrunkSm& S = L.ts[trunk];
   double* W = sm;
   double* post = W + S.wtotal;
-  double* del = post + TILE * L.pst;
-  double* out = del + TILE * L.dst;  // TILE x ost trunk outputs
+  double* del = post + TL * L.pst;
+  double* out = del + TL * L.dst;  // TL x ost trunk outputs
   double* red = post;                // WARPS x MAXIO log_std partials (after the last tile)
   const int t = threadIdx.x, lane = t & 31, warp = t >> 5;
 
@@ -106,7 +108,7 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   }
   if (t < P.act) lstd[t] = L.w[P.total + t];
   // pads stay zero (the paired loads read them)
-  for (int e = t; e < TILE * (L.pst + L.dst); e += THREADS) post[e] = 0.0;
+  for (int e = t; e < TL * (L.pst + L.dst); e += THREADS) post[e] = 0.0;
 
   // Gradient ownership: thread (i, kg) accumulates W_l(i, k) for k in [8 kg, 8 kg + 8) of every
   // layer and, for kg = 0, b_l(i): delta_l(s, i) is loaded once per sample and layer, the 8
@@ -123,9 +125,9 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   const int c0 = chunk * L.chunk, c1 = min(L.n, c0 + L.chunk);
   __syncthreads();
 
-  for (int base = c0; base < c1; base += TILE) {
+  for (int base = c0; base < c1; base += TL) {
     // ---- load the tile (rows past the chunk are zero: zero delta, zero contribution)
-    for (int e = t; e < TILE * P.obs; e += THREADS) {
+    for (int e = t; e < TL * P.obs; e += THREADS) {
       const int s = e / P.obs, k = e % P.obs, g = base + s;
       double v = 0.0;
       if (g < c1) v = L.obs[(size_t)(L.idx ? L.idx[g] : g) * P.obs + k];
@@ -141,14 +143,14 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
         const int ld = S.ld[l];
         const double2* x = reinterpret_cast<const double2*>(post + sg * L.pst + poff(P, l));
         const int xs = 4 * L.pst;  // 8 samples, in double2
-        double a[SPT];
+        double a[(TL / 8)];
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) a[q] = 0.0;
+        for (int q = 0; q < (TL / 8); ++q) a[q] = 0.0;
 #pragma unroll 2
         for (int k2 = 0; k2 < cols / 2; ++k2) {
           const double w0 = Wl[2 * k2 * ld], w1 = Wl[(2 * k2 + 1) * ld];
 #pragma unroll
-          for (int q = 0; q < SPT; ++q) {
+          for (int q = 0; q < (TL / 8); ++q) {
             const double2 u = x[q * xs + k2];
             a[q] = fma(w1, u.y, fma(w0, u.x, a[q]));
           }
@@ -156,11 +158,11 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
         if (cols & 1) {
           const double w0 = Wl[(cols - 1) * ld];
 #pragma unroll
-          for (int q = 0; q < SPT; ++q) a[q] = fma(w0, x[q * xs + cols / 2].x, a[q]);
+          for (int q = 0; q < (TL / 8); ++q) a[q] = fma(w0, x[q * xs + cols / 2].x, a[q]);
         }
         const double bi = W[S.b[l] + i];
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) {
+        for (int q = 0; q < (TL / 8); ++q) {
           const int s = sg + 8 * q;
           const double z = a[q] + bi;
           if (l < 3) {
@@ -174,7 +176,7 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
       __syncthreads();
     }
     // ---- loss head (ppo.cpp:92-126), warp = sample
-    for (int s = warp; s < TILE; s += WARPS) {
+    for (int s = warp; s < TL; s += WARPS) {
       const int g = base + s;
       const bool valid = g < c1;
       const size_t row = valid ? (size_t)(L.idx ? L.idx[g] : g) : 0;
@@ -226,26 +228,26 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
         const double* Wl = W + S.w[l] + i * S.ld[l];
         const double2* e = reinterpret_cast<const double2*>(del + sg * L.dst + doff(P, l));
         const int es = 4 * L.dst;  // 8 samples, in double2
-        double b[SPT];
+        double b[(TL / 8)];
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) b[q] = 0.0;
+        for (int q = 0; q < (TL / 8); ++q) b[q] = 0.0;
 #pragma unroll 2
         for (int r2 = 0; r2 < (rows + 1) / 2; ++r2) {
           const double w0 = Wl[2 * r2], w1 = 2 * r2 + 1 < rows ? Wl[2 * r2 + 1] : 0.0;
 #pragma unroll
-          for (int q = 0; q < SPT; ++q) {
+          for (int q = 0; q < (TL / 8); ++q) {
             const double2 u = e[q * es + r2];
             b[q] = fma(w1, u.y, fma(w0, u.x, b[q]));
           }
         }
 #pragma unroll
-        for (int q = 0; q < SPT; ++q) del[(sg + 8 * q) * L.dst + doff(P, l - 1) + i] *= b[q];
+        for (int q = 0; q < (TL / 8); ++q) del[(sg + 8 * q) * L.dst + doff(P, l - 1) + i] *= b[q];
       }
       __syncthreads();
     }
     // ---- gradient: W_l += delta_l post_l^T, b_l += delta_l over the tile
 #pragma unroll 1
-    for (int s = 0; s < TILE; ++s) {
+    for (int s = 0; s < TL; ++s) {
 #pragma unroll
       for (int l = 0; l < 4; ++l) {
         const int rows = N.out[l], cols = N.in[l];
@@ -278,6 +280,271 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
       if (kg == 0) part[S.br[l] + i] = accB[l];
     }
   }
+  if (trunk == 0) {
+    red[warp * MAXIO + lane] = lsg0;
+    red[warp * MAXIO + lane + 32] = lsg1;
+  }
+  if (lane == 0) wred[warp] = lsum;
+  __syncthreads();
+  if (trunk == 0 && t < P.act) {
+    double v = 0.0;
+    for (int w = 0; w < WARPS; ++w) v += red[w * MAXIO + t];
+    part[N.total + t] = v;
+  }
+  if (t == 0) {
+    double v = 0.0;
+    for (int w = 0; w < WARPS; ++w) v += wred[w];
+    part[N.total + MAXIO] = v;
+  }
+}
+
+// ------------------------------------------------------------------------- FP64 tensor-core path
+// The same loss and gradient with every matrix product on the FP64 tensor cores
+// (mma.sync.m8n8k4.f64; tcgen05 has no FP64 kind).  Per tile of 32 samples: forward
+// Z = X W^T + b, backward delta_{l-1} = (delta_l W) .* ELU', gradient G_l += delta_l^T X_l, all
+// as 8x8 output blocks with k-steps of 4, operands straight from shared memory (row strides
+// = 4 mod 16 doubles: conflict-free fragment loads).  A thread's gradient blocks stay in its
+// registers for the whole chunk (C fragments).  Measured peak of the unit on this GPU ~36 TFLOP/s,
+// the same as the FP64 FMA pipe: the gain is 8-16x fewer shared-memory loads per FLOP.
+constexpr int MAXB = 14;  // gradient blocks per warp (obs <= 32, hidden <= 64, act <= 64)
+
+struct MmaTrunk {
+  int K[4], N[4];    // layer in / out
+  int Kp[4], Np[4];  // padded to 8
+  int ldw[4];        // shared row stride of W_l (one row per input k): = 4 mod 16, >= Np
+  int w[4], b[4];    // shared offsets of W_l, b_l
+  int wr[4], br[4];  // parameter offsets relative to the trunk
+  int nblk[4];       // gradient blocks of layer l: (Np / 8) x (Kp / 8)
+  int wtotal;
+};
+
+struct MmaParams {
+  PolicyParams P;
+  MmaTrunk tr[2];
+  int ldx[4], xo[4];  // activation X_l = input of layer l: TILE x ldx_l at xo_l
+  int ldd[4], dd[4];  // delta_l: TILE x ldd_l at dd_l (ELU' first, then the delta)
+  int xtotal, dtotal;
+  int n, chunk, nch, part_stride;
+  double clip_eps, value_coef, inv_n;
+  const double* w;
+  const double* obs;
+  const double* act;
+  const double* old_logp;
+  const double* adv;
+  const double* ret;
+  const int32_t* idx;
+  double* part;
+};
+
+__device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b) {
+  asm("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+      : "+d"(c0), "+d"(c1)
+      : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L) {
+  extern __shared__ __align__(16) double sm[];
+  __shared__ double lstd[MAXIO];
+  __shared__ double wred[WARPS];
+  const int trunk = blockIdx.y, chunk = blockIdx.x;
+  const PolicyParams& P = L.P;
+  const Net& N = trunk == 0 ? P.pi : P.vf;
+  const MmaTrunk& T = L.tr[trunk];
+  double* W = sm;
+  double* X = W + T.wtotal;
+  double* D = X + L.xtotal;
+  double* red = X;  // WARPS x MAXIO log_std partials (after the last tile)
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
+
+  for (int e = t; e < T.wtotal + L.xtotal + L.dtotal; e += THREADS) sm[e] = 0.0;  // pads stay 0
+  __syncthreads();
+  for (int l = 0; l < 4; ++l) {
+    const int rows = N.out[l], cols = N.in[l];
+    for (int e = t; e < rows * cols; e += THREADS) W[T.w[l] + (e / rows) * T.ldw[l] + e % rows] = L.w[N.w[l] + e];
+    for (int i = t; i < rows; i += THREADS) W[T.b[l] + i] = L.w[N.b[l] + i];
+  }
+  if (t < P.act) lstd[t] = L.w[P.total + t];
+
+  double acc[MAXB][2];
+#pragma unroll
+  for (int r = 0; r < MAXB; ++r) acc[r][0] = acc[r][1] = 0.0;
+  // bias gradient entry of this thread: layer bl, row bn (flat over the trunk's biases)
+  int bl = -1, bn = 0;
+  {
+    int e = t;
+    for (int l = 0; l < 4 && bl < 0; ++l) {
+      if (e < N.out[l]) { bl = l; bn = e; }
+      else e -= N.out[l];
+    }
+  }
+  double accB = 0.0;
+  double lsg0 = 0.0, lsg1 = 0.0, lsum = 0.0;
+  const int c0 = chunk * L.chunk, c1 = min(L.n, c0 + L.chunk);
+  __syncthreads();
+
+  for (int base = c0; base < c1; base += TILE) {
+    // ---- load the tile into X_0 (rows past the chunk stay zero)
+    for (int e = t; e < TILE * P.obs; e += THREADS) {
+      const int s = e / P.obs, k = e % P.obs, gi = base + s;
+      X[L.xo[0] + s * L.ldx[0] + k] = gi < c1 ? L.obs[(size_t)(L.idx ? L.idx[gi] : gi) * P.obs + k] : 0.0;
+    }
+    __syncthreads();
+    // ---- forward: Z_l = X_l W_l^T (+ b), unit = (M block mb, N blocks nb0, nb0 + 1)
+    for (int l = 0; l < 4; ++l) {
+      const int nbN = T.Np[l] / 8, units = 4 * ((nbN + 1) / 2);
+      const double* Wl = W + T.w[l];
+      const double* Xl = X + L.xo[l];
+      const int ldw = T.ldw[l], ldx = L.ldx[l];
+      for (int u = warp; u < units; u += WARPS) {
+        const int mb = u & 3, nb0 = 2 * (u >> 2);
+        const bool two = nb0 + 1 < nbN;
+        double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
+        const double* xa = Xl + (8 * mb + g) * ldx + q;
+        const double* wb = Wl + q * ldw + 8 * nb0 + g;
+#pragma unroll 4
+        for (int k4 = 0; k4 < T.Kp[l] / 4; ++k4) {
+          const double a = xa[4 * k4];
+          dmma(z00, z01, a, wb[4 * k4 * ldw]);
+          if (two) dmma(z10, z11, a, wb[4 * k4 * ldw + 8]);
+        }
+        const int s = 8 * mb + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          const int n = 8 * (nb0 + h) + 2 * q;
+          const double za = (h ? z10 : z00) + W[T.b[l] + n], zb = (h ? z11 : z01) + W[T.b[l] + n + 1];
+          if (l < 3) {
+            double* xo = X + L.xo[l + 1] + s * L.ldx[l + 1] + n;
+            double* eo = D + L.dd[l] + s * L.ldd[l] + n;
+            xo[0] = za > 0.0 ? za : expm1(za);
+            xo[1] = zb > 0.0 ? zb : expm1(zb);
+            eo[0] = za > 0.0 ? 1.0 : exp(za);  // elu_grad, ppo.cpp:12
+            eo[1] = zb > 0.0 ? 1.0 : exp(zb);
+          } else {
+            double* zo = D + L.dd[3] + s * L.ldd[3] + n;  // trunk outputs, overwritten by the head
+            zo[0] = za;
+            zo[1] = zb;
+          }
+        }
+      }
+      __syncthreads();
+    }
+    // ---- loss head (ppo.cpp:92-126), warp = sample
+    for (int s = warp; s < TILE; s += WARPS) {
+      const int gi = base + s;
+      const bool valid = gi < c1;
+      const size_t row = valid ? (size_t)(L.idx ? L.idx[gi] : gi) : 0;
+      double* d3 = D + L.dd[3] + s * L.ldd[3];
+      if (trunk == 0) {
+        const int A = P.act;
+        double z0 = 0.0, z1 = 0.0, sd0 = 1.0, sd1 = 1.0, lp = 0.0;
+        if (lane < A) {
+          sd0 = exp(lstd[lane]);
+          z0 = (L.act[row * A + lane] - d3[lane]) / sd0;
+          lp += -0.5 * z0 * z0 - lstd[lane] - kLogSqrt2Pi;
+        }
+        if (lane + 32 < A) {
+          sd1 = exp(lstd[lane + 32]);
+          z1 = (L.act[row * A + lane + 32] - d3[lane + 32]) / sd1;
+          lp += -0.5 * z1 * z1 - lstd[lane + 32] - kLogSqrt2Pi;
+        }
+        lp = warp_sum(lp);
+        const double adv = valid ? L.adv[row] : 0.0;
+        const double ratio = exp(lp - (valid ? L.old_logp[row] : 0.0));
+        const double surr1 = ratio * adv;
+        const double clipped = fmin(fmax(ratio, 1.0 - L.clip_eps), 1.0 + L.clip_eps) * adv;
+        if (lane == 0 && valid) lsum += -fmin(surr1, clipped) * L.inv_n;
+        const double g_r = surr1 <= clipped ? -adv * L.inv_n : 0.0;
+        const bool on = valid && g_r != 0.0;
+        const double g_logp = g_r * ratio;
+        __syncwarp();
+        if (lane < A) {
+          d3[lane] = on ? g_logp * z0 / sd0 : 0.0;
+          if (on) lsg0 += g_logp * (z0 * z0 - 1.0);
+        }
+        if (lane + 32 < A) {
+          d3[lane + 32] = on ? g_logp * z1 / sd1 : 0.0;
+          if (on) lsg1 += g_logp * (z1 * z1 - 1.0);
+        }
+      } else {
+        const double verr = valid ? d3[0] - L.ret[row] : 0.0;
+        __syncwarp();
+        if (lane == 0) {
+          if (valid) lsum += 0.5 * verr * verr * L.inv_n;
+          d3[0] = valid ? L.value_coef * verr * L.inv_n : 0.0;
+        }
+      }
+      // padded output rows carry a zero delta
+      for (int j = N.out[3] + lane; j < T.Np[3]; j += 32) d3[j] = 0.0;
+    }
+    __syncthreads();
+    // ---- backward: delta_{l-1} = (delta_l W_l) .* ELU'(z_{l-1}), unit = (mb, kb0, kb0 + 1)
+    for (int l = 3; l > 0; --l) {
+      const int nbK = T.Kp[l] / 8, units = 4 * ((nbK + 1) / 2);
+      const double* Wl = W + T.w[l];
+      const double* Dl = D + L.dd[l];
+      const int ldw = T.ldw[l], ldd = L.ldd[l];
+      for (int u = warp; u < units; u += WARPS) {
+        const int mb = u & 3, kb0 = 2 * (u >> 2);
+        const bool two = kb0 + 1 < nbK;
+        double b00 = 0.0, b01 = 0.0, b10 = 0.0, b11 = 0.0;
+        const double* da = Dl + (8 * mb + g) * ldd + q;
+        const double* wb = Wl + (8 * kb0 + g) * ldw + q;
+#pragma unroll 4
+        for (int n4 = 0; n4 < T.Np[l] / 4; ++n4) {
+          const double a = da[4 * n4];
+          dmma(b00, b01, a, wb[4 * n4]);
+          if (two) dmma(b10, b11, a, wb[4 * n4 + 8 * ldw]);
+        }
+        const int s = 8 * mb + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          double* eo = D + L.dd[l - 1] + s * L.ldd[l - 1] + 8 * (kb0 + h) + 2 * q;
+          eo[0] *= h ? b10 : b00;
+          eo[1] *= h ? b11 : b01;
+        }
+      }
+      __syncthreads();
+    }
+    // ---- gradient: G_l += delta_l^T X_l over the tile (8 k-steps of 4 samples); biases
+#pragma unroll
+    for (int r = 0; r < MAXB; ++r) {
+      int j = warp + WARPS * r, l = 0;
+      while (l < 4 && j >= T.nblk[l]) j -= T.nblk[l++];
+      if (l < 4) {
+        const int nbk = T.Kp[l] / 8, nb = j / nbk, kb = j % nbk;
+        const double* da = D + L.dd[l] + q * L.ldd[l] + 8 * nb + g;
+        const double* xb = X + L.xo[l] + q * L.ldx[l] + 8 * kb + g;
+#pragma unroll
+        for (int k4 = 0; k4 < TILE / 4; ++k4)
+          dmma(acc[r][0], acc[r][1], da[4 * k4 * L.ldd[l]], xb[4 * k4 * L.ldx[l]]);
+      }
+    }
+    if (bl >= 0) {
+      const double* db = D + L.dd[bl] + bn;
+      double v = 0.0;
+#pragma unroll 8
+      for (int s = 0; s < TILE; ++s) v += db[s * L.ldd[bl]];
+      accB += v;
+    }
+    __syncthreads();
+  }
+  // ---- per-chunk partials
+  double* part = L.part + (size_t)(trunk * L.nch + chunk) * L.part_stride;
+#pragma unroll
+  for (int r = 0; r < MAXB; ++r) {
+    int j = warp + WARPS * r, l = 0;
+    while (l < 4 && j >= T.nblk[l]) j -= T.nblk[l++];
+    if (l < 4) {
+      const int nbk = T.Kp[l] / 8, n = 8 * (j / nbk) + g, k = 8 * (j % nbk) + 2 * q;
+      if (n < T.N[l]) {
+        if (k < T.K[l]) part[T.wr[l] + k * T.N[l] + n] = acc[r][0];
+        if (k + 1 < T.K[l]) part[T.wr[l] + (k + 1) * T.N[l] + n] = acc[r][1];
+      }
+    }
+  }
+  if (bl >= 0) part[T.br[bl] + bn] = accB;
   if (trunk == 0) {
     red[warp * MAXIO + lane] = lsg0;
     red[warp * MAXIO + lane + 32] = lsg1;
@@ -418,6 +685,53 @@ TrunkSm trunk_sm(const Net& N) {
   return S;
 }
 
+int ld4(int n) { return n + ((4 - n % 16) + 16) % 16; }  // >= n, = 4 mod 16
+int up8(int n) { return (n + 7) & ~7; }
+
+// The tensor-core layout; false if the shapes exceed it (then the CUDA-core kernel runs).
+bool mma_layout(const PolicyParams& P, MmaParams& M, int& smem) {
+  M.P = P;
+  int xo = 0, dd = 0;
+  for (int l = 0; l < 4; ++l) {
+    const int kp = l == 0 ? up8(P.obs) : up8(P.hidden), np = l < 3 ? up8(P.hidden) : up8(std::max(P.act, 1));
+    M.ldx[l] = ld4(kp);
+    M.xo[l] = xo;
+    xo += TILE * M.ldx[l];
+    M.ldd[l] = ld4(np);
+    M.dd[l] = dd;
+    dd += TILE * M.ldd[l];
+  }
+  M.xtotal = xo;
+  M.dtotal = dd;
+  int wmax = 0, blocks = 0;
+  for (int tr = 0; tr < 2; ++tr) {
+    const Net& N = tr == 0 ? P.pi : P.vf;
+    MmaTrunk& T = M.tr[tr];
+    int off = 0, nb = 0;
+    for (int l = 0; l < 4; ++l) {
+      T.K[l] = N.in[l];
+      T.N[l] = N.out[l];
+      T.Kp[l] = up8(N.in[l]);
+      T.Np[l] = l < 3 ? up8(N.out[l]) : up8(std::max(P.act, 1));  // both trunks share delta_3's shape
+      T.ldw[l] = ld4(T.Np[l]);
+      T.w[l] = off;
+      off += T.Kp[l] * T.ldw[l];
+      T.b[l] = off;
+      off += T.Np[l];
+      T.wr[l] = N.w[l] - N.w[0];
+      T.br[l] = N.b[l] - N.w[0];
+      T.nblk[l] = (T.Np[l] / 8) * (T.Kp[l] / 8);
+      nb += T.nblk[l];
+    }
+    T.wtotal = (off + 1) & ~1;
+    wmax = std::max(wmax, T.wtotal);
+    blocks = std::max(blocks, nb);
+  }
+  smem = (int)sizeof(double) * (wmax + M.xtotal + M.dtotal);
+  return P.hidden <= MAXH && P.obs <= MAXIO && P.act <= MAXIO && blocks <= WARPS * MAXB &&
+         smem <= 227 * 1024 - 1024;
+}
+
 // One ppo_loss over n samples (optionally gathered through idx) into grads / info.
 int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, const double* old_logp,
                 const double* adv, const double* ret, const int32_t* idx, const rmpc_ppo_config& cfg, double* grads,
@@ -454,11 +768,45 @@ int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, con
     p->part_cap = need;
   }
   L.part = p->d_part;
-  const int wmax = std::max(L.ts[0].wtotal, L.ts[1].wtotal);
-  const int smem = (int)sizeof(double) * (wmax + TILE * L.pst + TILE * L.dst + TILE * L.ost);
-  if (cudaFuncSetAttribute(loss_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess)
-    return RMPC_ERR_CUDA;
-  loss_kernel<<<dim3(L.nch, 2), THREADS, smem, st>>>(L);
+  MmaParams M{};
+  int msmem = 0;
+  if (mma_layout(P, M, msmem)) {  // FP64 tensor cores
+    M.n = L.n;
+    M.chunk = L.chunk;
+    M.nch = L.nch;
+    M.part_stride = L.part_stride;
+    M.clip_eps = L.clip_eps;
+    M.value_coef = L.value_coef;
+    M.inv_n = L.inv_n;
+    M.w = L.w;
+    M.obs = obs;
+    M.act = act;
+    M.old_logp = old_logp;
+    M.adv = adv;
+    M.ret = ret;
+    M.idx = idx;
+    M.part = L.part;
+    if (cudaFuncSetAttribute(loss_kernel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, msmem) != cudaSuccess)
+      return RMPC_ERR_CUDA;
+    loss_kernel_mma<<<dim3(L.nch, 2), THREADS, msmem, st>>>(M);
+  } else {  // CUDA cores (shapes beyond the tensor-core layout): 32- or 16-sample tiles
+    const int wmax = std::max(L.ts[0].wtotal, L.ts[1].wtotal);
+    auto smem_for = [&](int tl) { return (int)sizeof(double) * (wmax + tl * (L.pst + L.dst + L.ost)); };
+    const int limit = 227 * 1024 - 1024;
+    if (smem_for(32) <= limit) {
+      if (cudaFuncSetAttribute(loss_kernel<32>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(32)) !=
+          cudaSuccess)
+        return RMPC_ERR_CUDA;
+      loss_kernel<32><<<dim3(L.nch, 2), THREADS, smem_for(32), st>>>(L);
+    } else if (smem_for(16) <= limit) {
+      if (cudaFuncSetAttribute(loss_kernel<16>, cudaFuncAttributeMaxDynamicSharedMemorySize, smem_for(16)) !=
+          cudaSuccess)
+        return RMPC_ERR_CUDA;
+      loss_kernel<16><<<dim3(L.nch, 2), THREADS, smem_for(16), st>>>(L);
+    } else {
+      return RMPC_ERR_STRUCTURAL;
+    }
+  }
   const int np = P.total + P.act;
   reduce_kernel<<<(np + 255) / 256, 256, 0, st>>>(P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef,
                                                  p->d_w, grads, info);

@@ -53,6 +53,20 @@ def test_loss_and_gradient_parity(oracle, n, hidden):
     close(g[-act:], g_o[-act:])  # log_std
 
 
+def test_loss_parity_cuda_core_fallback(oracle):
+    """obs 64 / act 32 / hidden 64 exceeds the tensor-core layout's shared memory: the CUDA-core
+    kernel runs and must agree just the same."""
+    from paper_2510_12717_b200.env import Policy
+    from paper_2510_12717_b200.ppo import default_ppo_config, ppo_loss
+    obs, act, hidden, n = 64, 32, 64, 300
+    params, o, a, old, adv, ret = make_batch(oracle, 5, n, obs, act, hidden)
+    info_o, g_o = oracle.ppo_loss(params, o, a, old, adv, ret, oracle.ppo_config(), act, hidden)
+    pol = Policy(params, obs, act, hidden)
+    info, g = ppo_loss(pol, *cuda(o, a, old, adv, ret), default_ppo_config())
+    np.testing.assert_allclose(info.total, info_o[0], rtol=1e-9)
+    close(g.cpu().numpy(), g_o)
+
+
 def test_loss_deterministic_and_default_dims(oracle):
     import torch
     from paper_2510_12717_b200.env import Policy

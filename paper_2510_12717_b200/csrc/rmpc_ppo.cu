@@ -972,24 +972,23 @@ int32_t rmpc_ppo_update_device(rmpc_policy* p, rmpc_adam* a, int32_t T, int32_t 
   if (!grow(a->d_info, a->info_cap, (size_t)std::max(epochs * mbc, 1), sizeof(rmpc_ppo_loss_info)))
     return RMPC_ERR_CUDA;
   if (!p->d_grads && cudaMalloc(&p->d_grads, np * sizeof(double)) != cudaSuccess) return RMPC_ERR_CUDA;
-  // every epoch's permutation up front (the Rng advances exactly as the reference's loop)
   cudaStreamSynchronize(st);  // h_order may still feed a previous call's copy
-  std::vector<int32_t> order(N);
-  for (int k = 0; k < N; ++k) order[k] = k;
-  for (int ep = 0; ep < epochs; ++ep) {
-    for (int k = N - 1; k > 0; --k) std::swap(order[k], order[next_u64(rng) % (uint64_t)(k + 1)]);
-    std::copy(order.begin(), order.end(), a->h_order + (size_t)ep * N);
-  }
-  if (epochs > 0 &&
-      cudaMemcpyAsync(a->d_order, a->h_order, (size_t)epochs * N * sizeof(int32_t), cudaMemcpyHostToDevice, st) !=
-          cudaSuccess)
-    return RMPC_ERR_CUDA;
   gae_kernel<<<(E + 127) / 128, 128, 0, st>>>(T, E, rewards, values, dones, boot, cfg->gamma, cfg->lam_gae, a->d_adv,
                                                a->d_ret);
   normalize_kernel<<<1, RED_THREADS, 0, st>>>(N, a->d_adv);
+  // per epoch: the host draws the shuffle (the Rng advances exactly as the reference's loop)
+  // while the device still runs the previous epoch's minibatches
+  std::vector<int32_t> order(N);
+  for (int k = 0; k < N; ++k) order[k] = k;
   const int mb = (N + mbc - 1) / mbc;
   int count = 0;
   for (int ep = 0; ep < epochs; ++ep) {
+    for (int k = N - 1; k > 0; --k) std::swap(order[k], order[next_u64(rng) % (uint64_t)(k + 1)]);
+    int32_t* h = a->h_order + (size_t)ep * N;
+    std::copy(order.begin(), order.end(), h);
+    if (cudaMemcpyAsync(a->d_order + (size_t)ep * N, h, (size_t)N * sizeof(int32_t), cudaMemcpyHostToDevice, st) !=
+        cudaSuccess)
+      return RMPC_ERR_CUDA;
     for (int b = 0; b < mbc; ++b) {
       const int lo = b * mb, hi = std::min(N, lo + mb);
       if (lo >= hi) continue;

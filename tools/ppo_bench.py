@@ -99,8 +99,8 @@ def main():
                     f"minibatches, MLP {obs}-{hidden}-{hidden}-{hidden}-{act} (+ value), FP64, synthetic rollout",
         "ppo_update_ms": t_up * 1e3,
         "samples_per_s": samples_per_update / t_up,
-        "note_update": "host wall time of the synchronous rmpc_ppo_update_device call: GAE, normalisation, host "
-                       "Fisher-Yates + one H2D of the permutations, 16 x (loss + reduce + clip/Adam) launches",
+        "note_update": "host wall time of the synchronous rmpc_ppo_update_device call: GAE, normalisation, per epoch "
+                       "a host Fisher-Yates (overlapping the device) + H2D, 16 x (loss + reduce + clip/Adam) launches",
         "ppo_loss": {
             "launches": "loss_kernel + reduce_kernel", "minibatch": mb, "ms": t_loss * 1e3, "samples_per_s": mb / t_loss,
             "flop_alg_per_sample": fl,

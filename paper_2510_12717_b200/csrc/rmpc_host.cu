@@ -203,10 +203,12 @@ void free_shard(Shard& sh) {
 }
 
 // H2D (staging pageable buffers through pinned memory), kernel, D2H, synchronize.  A shard of
-// more than two waves runs as two chunks on two streams: the first wave of CTAs, then the
-// rest.  Chunk 1's inputs are small, so its kernel starts early; chunk 2's H2D overlaps chunk
-// 1's kernel, chunk 1's D2H overlaps chunk 2's kernel, and chunk 2's CTAs fill the SMs as
-// chunk 1's finish.  Per-agent results do not depend on the split.
+// more than two waves runs as up to three chunks: the first wave of CTAs, the remaining whole
+// waves (second stream), the partial last wave (behind chunk 1 on the first stream).  Chunk 1's
+// inputs are small, so its kernel starts early; the later chunks' H2D overlaps chunk 1's
+// kernel, chunk 1's D2H overlaps the rest, the later kernels' CTAs fill the SMs as earlier
+// ones finish, and only the small tail chunk's D2H is left at the end.  Per-agent results do
+// not depend on the split.
 void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
                const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z,
                rmpc_solution* out, float* z_out) {
@@ -216,11 +218,21 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
   const size_t n = sh.count, b = sh.begin;
   const size_t zrow = (size_t)h.NT * RMPC_NV;
   const bool use_prev = h.settings.warm_start && prev && prev_z;
+  // chunks: the first wave, the remaining whole waves, the partial last wave (its D2H is the
+  // only transfer left exposed at the end)
   const size_t wave = (size_t)sh.sms * rmpc_dev::cta_shape(h.NT).agents;
-  const size_t n1 = (n > 2 * wave && !h.profile) ? wave : n;
-  const size_t cut[3] = {0, n1, n};
-  const int nchunks = n1 < n ? 2 : 1;
-  const cudaStream_t ss[2] = {sh.stream, sh.stream2};
+  size_t cut[4] = {0, n, n, n};
+  int nchunks = 1;
+  if (n > 2 * wave && !h.profile) {
+    const size_t tail = n % wave;
+    cut[1] = wave;
+    nchunks = 2;
+    if (tail > 0 && n - tail > wave) {
+      cut[2] = n - tail;
+      nchunks = 3;
+    }
+  }
+  const cudaStream_t ss[3] = {sh.stream, sh.stream2, sh.stream};  // the tail chunk queues behind chunk 1
   struct In {
     const char* src;
     char* dst;
@@ -250,7 +262,7 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
                      : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
   CK(cudaEventRecord(sh.ev[0], ss[0]));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
-  if (nchunks == 2) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
+  if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
     const size_t lo = cut[k], m = cut[k + 1] - cut[k];
@@ -275,31 +287,31 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
       cudaStreamSynchronize(ss[1]);
       return;
     }
-    CK(cudaEventRecord(sh.ev[2 + k], st));  // kernel k done
+    CK(cudaEventRecord(sh.ev[2 + k], st));  // kernel k done (events 2..4)
     CK(cudaMemcpyAsync(out_dst + lo * sizeof(rmpc_solution), sh.d_out + lo, m * sizeof(rmpc_solution),
                        cudaMemcpyDeviceToHost, st));
     if (z_out)
       CK(cudaMemcpyAsync(z_dst + lo * zrow * sizeof(float), sh.d_z + lo * zrow, m * zrow * sizeof(float),
                          cudaMemcpyDeviceToHost, st));
-    CK(cudaEventRecord(sh.ev[4 + k], st));  // results of chunk k on the host
+    CK(cudaEventRecord(sh.ev[5 + k], st));  // results of chunk k on the host (events 5..7)
   }
   if (h.profile)
     CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, ss[0]));
   CK(cudaStreamSynchronize(ss[0]));
-  if (nchunks == 2) CK(cudaStreamSynchronize(ss[1]));
+  if (nchunks > 1) CK(cudaStreamSynchronize(ss[1]));
   if (!out_pinned) std::memcpy(out + b, out_dst, n * sizeof(rmpc_solution));
   if (z_out && !z_pinned) std::memcpy(z_out + b * zrow, z_dst, n * zrow * sizeof(float));
   // exposed stage times: chunk 1's H2D, first H2D done -> last kernel done, last kernel done ->
   // last results on the host
   const int last = nchunks - 1;
-  float t01 = 0, t1k = 0, tkd = 0, tk0 = 0;
+  float t01 = 0, t1k = 0, tkd = 0;
   cudaEventElapsedTime(&t01, sh.ev[0], sh.ev[1]);
-  cudaEventElapsedTime(&t1k, sh.ev[1], sh.ev[2 + last]);
-  if (nchunks == 2) {
-    cudaEventElapsedTime(&tk0, sh.ev[1], sh.ev[2]);
-    t1k = std::max(t1k, tk0);
+  for (int k = 0; k < nchunks; ++k) {
+    float tk = 0;
+    cudaEventElapsedTime(&tk, sh.ev[1], sh.ev[2 + k]);
+    t1k = std::max(t1k, tk);
   }
-  cudaEventElapsedTime(&tkd, sh.ev[2 + last], sh.ev[4 + last]);
+  cudaEventElapsedTime(&tkd, sh.ev[2 + last], sh.ev[5 + last]);
   sh.h2d_ms = t01;
   sh.kernel_ms = t1k;
   sh.d2h_ms = tkd;

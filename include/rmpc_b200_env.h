@@ -137,7 +137,8 @@ void rmpc_ppo_config_default(rmpc_ppo_config* cfg);
 /* ppo_loss (ppo.cpp:79-135) over n samples (obs n x obs_dim, actions n x act_dim, old_logp /
  * advantages / returns n; device pointers): the loss terms into d_info (device, one struct) and,
  * if d_grads is non-NULL, the gradient of every parameter in flatten_grads order
- * (rmpc_policy_num_params doubles, overwritten).  Deterministic: a fixed-order reduction. */
+ * (rmpc_policy_num_params doubles, overwritten).  Deterministic: a fixed-order reduction.
+ * Calls on one policy share its device workspace: issue them on one stream (or synchronise). */
 int32_t rmpc_ppo_loss_device(rmpc_policy* policy, int32_t n, const double* d_obs,
                              const double* d_actions, const double* d_old_logp,
                              const double* d_advantages, const double* d_returns,

@@ -366,8 +366,20 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
   if (t < P.act) lstd[t] = L.w[P.total + t];
 
   double acc[MAXB][2];
+  // this warp's gradient blocks, decoded once: delta / activation fragment offsets | layer << 30
+  uint32_t gblk[MAXB];
 #pragma unroll
-  for (int r = 0; r < MAXB; ++r) acc[r][0] = acc[r][1] = 0.0;
+  for (int r = 0; r < MAXB; ++r) {
+    acc[r][0] = acc[r][1] = 0.0;
+    int j = warp + WARPS * r, l = 0;
+    while (l < 4 && j >= T.nblk[l]) j -= T.nblk[l++];
+    gblk[r] = 0xffffffffu;
+    if (l < 4) {
+      const int nbk = T.Kp[l] / 8, nb = j / nbk, kb = j % nbk;
+      const uint32_t doff = L.dd[l] + q * L.ldd[l] + 8 * nb + g, xoff = L.xo[l] + q * L.ldx[l] + 8 * kb + g;
+      gblk[r] = doff | (xoff << 15) | ((uint32_t)l << 30);
+    }
+  }
   // bias gradient entry of this thread: layer bl, row bn (flat over the trunk's biases)
   int bl = -1, bn = 0;
   {
@@ -416,10 +428,12 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
           if (l < 3) {
             double* xo = X + L.xo[l + 1] + s * L.ldx[l + 1] + n;
             double* eo = D + L.dd[l] + s * L.ldd[l] + n;
-            xo[0] = za > 0.0 ? za : expm1(za);
-            xo[1] = zb > 0.0 ? zb : expm1(zb);
-            eo[0] = za > 0.0 ? 1.0 : exp(za);  // elu_grad, ppo.cpp:12
-            eo[1] = zb > 0.0 ? 1.0 : exp(zb);
+            // one transcendental per element: ELU = expm1(z), ELU' = exp(z) = expm1(z) + 1 (z <= 0)
+            const double ea = expm1(fmin(za, 0.0)), eb = expm1(fmin(zb, 0.0));
+            xo[0] = za > 0.0 ? za : ea;
+            xo[1] = zb > 0.0 ? zb : eb;
+            eo[0] = za > 0.0 ? 1.0 : ea + 1.0;  // elu_grad, ppo.cpp:12
+            eo[1] = zb > 0.0 ? 1.0 : eb + 1.0;
           } else {
             double* zo = D + L.dd[3] + s * L.ldd[3] + n;  // trunk outputs, overwritten by the head
             zo[0] = za;
@@ -510,15 +524,13 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
     // ---- gradient: G_l += delta_l^T X_l over the tile (8 k-steps of 4 samples); biases
 #pragma unroll
     for (int r = 0; r < MAXB; ++r) {
-      int j = warp + WARPS * r, l = 0;
-      while (l < 4 && j >= T.nblk[l]) j -= T.nblk[l++];
-      if (l < 4) {
-        const int nbk = T.Kp[l] / 8, nb = j / nbk, kb = j % nbk;
-        const double* da = D + L.dd[l] + q * L.ldd[l] + 8 * nb + g;
-        const double* xb = X + L.xo[l] + q * L.ldx[l] + 8 * kb + g;
+      if (gblk[r] != 0xffffffffu) {
+        const int l = gblk[r] >> 30;
+        const double* da = D + (gblk[r] & 0x7fffu);
+        const double* xb = X + ((gblk[r] >> 15) & 0x7fffu);
+        const int sd = 4 * L.ldd[l], sx = 4 * L.ldx[l];
 #pragma unroll
-        for (int k4 = 0; k4 < TILE / 4; ++k4)
-          dmma(acc[r][0], acc[r][1], da[4 * k4 * L.ldd[l]], xb[4 * k4 * L.ldx[l]]);
+        for (int k4 = 0; k4 < TILE / 4; ++k4) dmma(acc[r][0], acc[r][1], da[k4 * sd], xb[k4 * sx]);
       }
     }
     if (bl >= 0) {

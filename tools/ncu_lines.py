@@ -22,7 +22,7 @@ FUNC = os.environ.get("RMPC_NCU_FUNC", "_ZN8rmpc_dev10rti_kernelILb0ELi6EEEvNS_7
 def line_table():
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=d, check=True, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.startswith("rmpc_kernel.") and f.endswith(".cubin")][0]
+        cub = [f for f in os.listdir(d) if f.startswith(os.environ.get("RMPC_NCU_CUBIN", "rmpc_kernel") + ".") and f.endswith(".cubin")][0]
         txt = subprocess.run(["nvdisasm", "--print-line-info", os.path.join(d, cub)],
                              check=True, capture_output=True, text=True).stdout
     cur, out, inside = None, [], False

@@ -166,8 +166,9 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
           const int s = sg + 8 * q;
           const double z = a[q] + bi;
           if (l < 3) {
-            post[s * L.pst + poff(P, l + 1) + i] = z > 0.0 ? z : expm1(z);
-            del[s * L.dst + doff(P, l) + i] = z > 0.0 ? 1.0 : exp(z);  // elu_grad, ppo.cpp:12
+            const double em = expm1(fmin(z, 0.0));  // ELU and ELU' = exp(z) = expm1(z) + 1
+            post[s * L.pst + poff(P, l + 1) + i] = z > 0.0 ? z : em;
+            del[s * L.dst + doff(P, l) + i] = z > 0.0 ? 1.0 : em + 1.0;  // elu_grad, ppo.cpp:12
           } else {
             out[s * L.ost + i] = z;
           }

@@ -182,7 +182,9 @@ int32_t rmpc_fma_peak(int32_t device, double* tflops);
 /* Dynamic shared memory one agent (one warp pair) needs at `horizon` nodes. */
 int32_t rmpc_smem_bytes(int32_t horizon);
 /* Agents per CTA (= per SM: one CTA per SM) at `horizon` nodes, bounded by the 512 TMEM columns
- * that hold the factor, the 227 KB of shared memory and 6 warp pairs (384 threads). */
+ * that hold the factor and the 227 KB of shared memory: 6 warp pairs (384 threads, 168
+ * registers) in general, 8 (512 threads, 128 registers) when every node block fits TMEM
+ * at 4 warps per lane quarter (horizon <= 8). */
 int32_t rmpc_agents_per_cta(int32_t horizon);
 /* sizeof of the ABI structs (0 model, 1 settings, 2 state, 3 command, 4 gait, 5 solution,
  * 6 timing) for binding-side layout checks. */

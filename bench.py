@@ -460,10 +460,11 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            v, cores, walls, v1 = cpu_baseline_run(args, min(args.cpu_sample, n), steps=2)
+            # ~5 ticks of the workload: ~1 s on 16 host threads, ~15 s of CPU work
+            v, cores, walls, v1 = cpu_baseline_run(args, min(args.cpu_sample, n), steps=5)
             cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": "port",
                    "single_thread_value": v1,
-                   "sample": f"2 ticks x {min(args.cpu_sample, n)} agents of the same workload, "
+                   "sample": f"5 ticks x {min(args.cpu_sample, n)} agents of the same workload, "
                              f"{cores} host threads ({cpu_model()}); FP64 oracle restating the "
                              f"reference algorithm incl. per-solve ordering + LDL^T"}
         except Exception as e:  # pragma: no cover

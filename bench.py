@@ -73,6 +73,14 @@ def flop_alg(kind, T):
         return None
 
 
+def hbm_peak_gbs():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f).get("hbm_gbs")
+    except Exception:
+        return None
+
+
 def ncu_traffic():
     path = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     try:
@@ -447,6 +455,10 @@ def main():
         "ncu_executed_fp32_frac": traffic.get("executed_fp32_frac_of_peak") if traffic else None,
         "peak_source": "measured FP32 FMA loop on this GPU (rmpc_fma_peak), of measured",
         "flop_alg_per_solve": fl,
+        # secondary evidence: DRAM bandwidth of the same launch vs HBM peak
+        "dram_gbs": (traffic["dram_bytes_per_launch"] * n / traffic.get("agents", n) / (ms_per_step * 1e-3) / 1e9)
+        if traffic and traffic.get("dram_bytes_per_launch") else None,
+        "hbm_peak_gbs": hbm_peak_gbs(),
         "note": "CUDA-core FP32 kernel (no GEMM, HBM traffic ~0.4 KB/agent): neither the HBM nor "
                 "the tensor roofline applies; FLOP_alg is the reference algorithm's count",
     }

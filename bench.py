@@ -43,6 +43,7 @@ def parse():
     p.add_argument("--horizon", type=int, default=10)
     p.add_argument("--kind", default="random", choices=("random", "mixed", "standing"))
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
+    p.add_argument("--no-ppo", action="store_true", help="skip the PPO batch measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=4096, help="agents in the CPU baseline sample")
     p.add_argument("--cl-agents", type=int, default=8192,
@@ -469,6 +470,16 @@ def main():
     if args.cl_agents > 0:
         closed = closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier)
 
+    # ---- §8(f) row 3: one PPO update at the trainer's shape on this GPU (rank 0 only)
+    ppo = None
+    if rank == 0 and not args.no_ppo:
+        try:
+            sys.path.insert(0, os.path.join(ROOT, "tools"))
+            from ppo_bench import measure as ppo_measure
+            ppo = ppo_measure(4096, cpu_seconds=2.0 if args.no_cpu_baseline else 5.0)
+        except Exception as e:  # pragma: no cover
+            ppo = {"error": str(e)}
+
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
@@ -508,6 +519,7 @@ def main():
             "gpu_launches": args.steps,
             "status_ok": ok, "clocks": clk, "cpu_baseline": cpu,
             "closed_loop": closed,
+            "ppo_update": ppo,
         }
         print(json.dumps(line), flush=True)
     br.close()

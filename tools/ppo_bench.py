@@ -34,13 +34,13 @@ def flop_per_sample(obs, act, hidden):
     return 2 * (fwd + bwd + fwd)
 
 
-def main():
-    E = int(sys.argv[1]) if len(sys.argv) > 1 else 4096
+def measure(E=4096, cpu_seconds=5.0):
     T, obs, act, hidden = 24, 23, 6, 64
     N = T * E
-    from oracle import oracle as O
-    params = O.init_policy(obs, act, hidden, seed=0, zero_final=False)
     rng = np.random.default_rng(0)
+    # synthetic weights, flatten_policy layout: two 4-layer trunks then log_std
+    n_par = sum(i * o + o for out in (act, 1) for i, o in zip((obs, hidden, hidden, hidden), (hidden, hidden, hidden, out)))
+    params = np.concatenate([rng.uniform(-0.2, 0.2, n_par), np.full(act, np.log(0.5))])
     o = rng.normal(size=(T, E, obs))
     a = 0.5 * rng.normal(size=(T, E, act))
     logp = (-0.5 * (a / 0.5) ** 2 - np.log(0.5) - LOG_SQRT_2PI).sum(-1) + 0.2 * rng.normal(size=(T, E))
@@ -82,19 +82,21 @@ def main():
     peak = C.c_double()
     L.rmpc_fma_peak_f64(0, C.byref(peak))
     fl = flop_per_sample(obs, act, hidden)
-    # CPU oracle: ppo_loss + gradient on a bounded sample (the reference's ppo_loss is serial)
+    # CPU baseline: the FP64 oracle's ppo_loss + gradient on a bounded sample (the reference's
+    # ppo_loss is serial); the oracle is only the baseline here, never the measured path
+    from oracle import oracle as O
     ns = 2048
     cb = [roll[0].reshape(N, obs)[:ns], roll[1].reshape(N, act)[:ns], roll[2].reshape(N)[:ns],
           rng.normal(size=ns), rng.normal(size=ns)]
     O.ppo_loss(params, *cb, O.ppo_config(), act, hidden)
     t0 = time.perf_counter()
     reps = 0
-    while time.perf_counter() - t0 < 5.0:
+    while time.perf_counter() - t0 < cpu_seconds:
         O.ppo_loss(params, *cb, O.ppo_config(), act, hidden)
         reps += 1
     cpu_sps = reps * ns / (time.perf_counter() - t0)
     samples_per_update = N * cfg.epochs
-    print(json.dumps({
+    return {
         "workload": f"ppo_update: {T} steps x {E} envs = {N} samples, {cfg.epochs} epochs x {cfg.minibatches} "
                     f"minibatches, MLP {obs}-{hidden}-{hidden}-{hidden}-{act} (+ value), FP64, synthetic rollout",
         "ppo_update_ms": t_up * 1e3,
@@ -109,9 +111,13 @@ def main():
                          "peak_source": "measured FP64 FMA loop on this GPU (rmpc_fma_peak_f64)"},
         },
         "cpu_baseline": {"samples_per_s": cpu_sps, "cores": 1, "kind": "port",
-                         "sample": f"oracle ppo_loss + gradient on {ns} samples, repeated for 5 s "
+                         "sample": f"oracle ppo_loss + gradient on {ns} samples, repeated for {cpu_seconds:g} s "
                                    "(the reference's ppo_loss loop is single-threaded)"},
-    }))
+    }
+
+
+def main():
+    print(json.dumps(measure(int(sys.argv[1]) if len(sys.argv) > 1 else 4096)))
 
 
 if __name__ == "__main__":

@@ -479,6 +479,7 @@ def main():
             ppo = ppo_measure(4096, cpu_seconds=2.0 if args.no_cpu_baseline else 5.0)
         except Exception as e:  # pragma: no cover
             ppo = {"error": str(e)}
+    barrier()  # the other ranks wait for rank 0's PPO measurement
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:

@@ -7,7 +7,7 @@
 // which is block tridiagonal over horizon nodes (26 x 26 blocks) and is solved by block
 // elimination with explicit Schur-complement inverses S_i^-1 kept in tensor memory (TMEM):
 // TMEM lane j holds row j of every block the warp owns, so a row is one tcgen05.ld and the
-// per-agent shared memory drops to the QP data (~27 KB at T = 10, six agents per SM).
+// per-agent shared memory drops to the QP data (~30 KB at T = 10, six agents per SM).
 // See DESIGN.md for the derivation and the HBM / shared-memory budget.
 #pragma once
 

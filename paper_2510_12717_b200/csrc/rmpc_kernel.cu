@@ -21,7 +21,8 @@
 // step is a 12-column update: no warp reductions on either recurrence.  The elimination is
 // two-sided: warp 0 of the agent's pair runs nodes [0, m) top-down and the middle node m, warp 1
 // runs (m, T) bottom-up (mirrored recurrences with T_i = D_i - rho^2 V_i G'_i V_i^T); the pair
-// meets at the middle node only.  Six agents (warp pairs) share a CTA / SM.
+// meets at the middle node only.  Six agents (warp pairs) share a CTA / SM (eight, under a
+// 128-register cap, for horizons <= 8: rti_kernel<SPILL, MAXA>).
 //
 // Precision: gait, guess, linearization, constraint right-hand sides, the objective and the
 // inverse dynamics in FP64; Ruiz, H, S^-1 and the ADMM iterations in FP32.

@@ -608,7 +608,8 @@ constexpr int RED_PARAMS = 32, RED_WARPS = 8;
 __global__ void __launch_bounds__(32 * RED_WARPS) reduce_kernel(const PolicyParams P, int nch, int part_stride,
                                                                  const double* __restrict__ part, double entropy_coef,
                                                                  double value_coef, const double* __restrict__ w,
-                                                                 double* grads, rmpc_ppo_loss_info* info) {
+                                                                 double* grads, rmpc_ppo_loss_info* info,
+                                                                 double* sq) {
   __shared__ double sh[RED_WARPS][RED_PARAMS];
   const int np = P.total + P.act, lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int p = blockIdx.x * RED_PARAMS + lane;
@@ -626,11 +627,19 @@ __global__ void __launch_bounds__(32 * RED_WARPS) reduce_kernel(const PolicyPara
   }
   sh[warp][lane] = v;
   __syncthreads();
-  if (warp == 0 && p < np) {
+  if (warp == 0) {
     double s = 0.0;
-    for (int k = 0; k < RED_WARPS; ++k) s += sh[k][lane];
-    if (p >= P.total && entropy_coef != 0.0) s -= entropy_coef;
-    if (grads) grads[p] = s;
+    if (p < np) {
+      for (int k = 0; k < RED_WARPS; ++k) s += sh[k][lane];
+      if (p >= P.total && entropy_coef != 0.0) s -= entropy_coef;
+      if (grads) grads[p] = s;
+    }
+    if (sq) {  // this block's share of |g|^2 for the clip (fixed butterfly order)
+      double q = p < np ? s * s : 0.0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) q += __shfl_xor_sync(0xffffffffu, q, o);
+      if (lane == 0) sq[blockIdx.x] = q;
+    }
   }
   if (blockIdx.x == 0 && threadIdx.x == 0 && info) {
     double sur = 0.0, vl = 0.0, ent = 0.0;
@@ -691,17 +700,29 @@ __global__ void __launch_bounds__(RED_THREADS) normalize_kernel(int N, double* a
   for (int k = threadIdx.x; k < N; k += RED_THREADS) adv[k] = (adv[k] - mean) * inv_std;
 }
 
-// Gradient-norm clip (ppo.cpp:252-256) + AdamOptimizer::step (ppo.cpp:179-193), one block.
-__global__ void __launch_bounds__(RED_THREADS) adam_kernel(int np, const double* __restrict__ g, double* m, double* v,
-                                                           double* w, double max_norm, double lr, double b1,
-                                                           double b2, double eps, double bc1, double bc2) {
-  __shared__ double sh[RED_THREADS];
+// Gradient-norm clip (ppo.cpp:252-256) + AdamOptimizer::step (ppo.cpp:179-193), one thread per
+// parameter; every block sums the reduce kernel's |g|^2 partials in the same fixed order.
+constexpr int ADAM_THREADS = 256;
+__global__ void __launch_bounds__(ADAM_THREADS) adam_kernel(int np, const double* __restrict__ g,
+                                                            const double* __restrict__ sq, int nsq, double* m,
+                                                            double* v, double* w, double max_norm, double lr,
+                                                            double b1, double b2, double eps, double bc1,
+                                                            double bc2) {
+  __shared__ double sh[ADAM_THREADS];
+  const int t = threadIdx.x;
   double q = 0.0;
-  for (int k = threadIdx.x; k < np; k += RED_THREADS) q += g[k] * g[k];
-  const double norm = sqrt(block_sum(q, sh));
+  for (int k = t; k < nsq; k += ADAM_THREADS) q += sq[k];
+  sh[t] = q;
+  __syncthreads();
+  for (int o = ADAM_THREADS / 2; o > 0; o >>= 1) {
+    if (t < o) sh[t] += sh[t + o];
+    __syncthreads();
+  }
+  const double norm = sqrt(sh[0]);
   const bool clip = max_norm > 0.0 && norm > max_norm;
   const double scale = clip ? max_norm / norm : 1.0;
-  for (int k = threadIdx.x; k < np; k += RED_THREADS) {
+  const int k = blockIdx.x * ADAM_THREADS + t;
+  if (k < np) {
     const double gk = clip ? g[k] * scale : g[k];
     const double mk = b1 * m[k] + (1.0 - b1) * gk;
     const double vk = b2 * v[k] + (1.0 - b2) * (gk * gk);
@@ -777,7 +798,7 @@ bool mma_layout(const PolicyParams& P, MmaParams& M, int& smem) {
 // One ppo_loss over n samples (optionally gathered through idx) into grads / info.
 int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, const double* old_logp,
                 const double* adv, const double* ret, const int32_t* idx, const rmpc_ppo_config& cfg, double* grads,
-                rmpc_ppo_loss_info* info, cudaStream_t st) {
+                rmpc_ppo_loss_info* info, cudaStream_t st, double* sq = nullptr) {
   const PolicyParams& P = p->P;
   LossParams L{};
   L.P = P;
@@ -851,7 +872,7 @@ int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, con
   }
   const int np = P.total + P.act;
   reduce_kernel<<<(np + RED_PARAMS - 1) / RED_PARAMS, 32 * RED_WARPS, 0, st>>>(
-      P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef, p->d_w, grads, info);
+      P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef, p->d_w, grads, info, sq);
   return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
 }
 
@@ -883,6 +904,7 @@ struct rmpc_adam {
   int t = 0;
   double* d_m = nullptr;
   double* d_v = nullptr;
+  double* d_sq = nullptr;  // per reduce block |g|^2 partials
   // ppo_update workspace
   double* d_adv = nullptr;
   double* d_ret = nullptr;
@@ -947,10 +969,13 @@ int32_t rmpc_adam_create(rmpc_policy* p, double lr, rmpc_adam** out) {
   const size_t np = (size_t)(p->P.total + p->P.act);
   if (cudaMalloc(&a->d_m, np * sizeof(double)) != cudaSuccess ||
       cudaMalloc(&a->d_v, np * sizeof(double)) != cudaSuccess ||
+      cudaMalloc(&a->d_sq, ((np + rmpc_ppo_dev::RED_PARAMS - 1) / rmpc_ppo_dev::RED_PARAMS) * sizeof(double)) !=
+          cudaSuccess ||
       cudaMemset(a->d_m, 0, np * sizeof(double)) != cudaSuccess ||
       cudaMemset(a->d_v, 0, np * sizeof(double)) != cudaSuccess) {
     cudaFree(a->d_m);
     cudaFree(a->d_v);
+    cudaFree(a->d_sq);
     delete a;
     return RMPC_ERR_CUDA;
   }
@@ -963,6 +988,7 @@ void rmpc_adam_destroy(rmpc_adam* a) {
   cudaSetDevice(a->policy->device);
   cudaFree(a->d_m);
   cudaFree(a->d_v);
+  cudaFree(a->d_sq);
   cudaFree(a->d_adv);
   cudaFree(a->d_ret);
   cudaFree(a->d_order);
@@ -983,6 +1009,7 @@ int32_t rmpc_ppo_update_device(rmpc_policy* p, rmpc_adam* a, int32_t T, int32_t 
   const int N = T * E;
   const int epochs = std::max(0, cfg->epochs), mbc = std::max(1, cfg->minibatches);
   const int np = p->P.total + p->P.act;
+  const int nsq = (np + RED_PARAMS - 1) / RED_PARAMS;
   auto grow = [](auto*& ptr, size_t& cap, size_t need, size_t elem) {
     if (need <= cap) return true;
     cudaFree(ptr);
@@ -1030,12 +1057,13 @@ int32_t rmpc_ppo_update_device(rmpc_policy* p, rmpc_adam* a, int32_t T, int32_t 
       const int lo = b * mb, hi = std::min(N, lo + mb);
       if (lo >= hi) continue;
       const int rc = launch_loss(p, hi - lo, obs, act, logp, a->d_adv, a->d_ret, a->d_order + (size_t)ep * N + lo, *cfg,
-                                 p->d_grads, a->d_info + count, st);
+                                 p->d_grads, a->d_info + count, st, a->d_sq);
       if (rc != RMPC_OK) return rc;
       ++a->t;
       const double bc1 = 1.0 - std::pow(a->beta1, a->t), bc2 = 1.0 - std::pow(a->beta2, a->t);
-      adam_kernel<<<1, RED_THREADS, 0, st>>>(np, p->d_grads, a->d_m, a->d_v, p->d_w, cfg->max_grad_norm, a->lr,
-                                             a->beta1, a->beta2, a->eps, bc1, bc2);
+      adam_kernel<<<(np + ADAM_THREADS - 1) / ADAM_THREADS, ADAM_THREADS, 0, st>>>(
+          np, p->d_grads, a->d_sq, nsq, a->d_m, a->d_v, p->d_w, cfg->max_grad_norm, a->lr, a->beta1, a->beta2, a->eps,
+          bc1, bc2);
       ++count;
     }
   }

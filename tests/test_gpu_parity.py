@@ -303,3 +303,14 @@ def test_large_batch_host_chunks_equal_device_launch():
     assert int((sol["status"] == 0).sum()) == n
     sol_h, _ = br.solve(st, cm, ga)
     assert sol.tobytes() == sol_h.tobytes()
+
+
+def test_two_chunked_shards_on_one_device_match_one_shard():
+    """Two shards (two host threads, each with its chunked two-stream pipeline) on one GPU give
+    the same bytes as one shard."""
+    m, s = default_model(), default_settings(10)
+    n = 20000
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=4, model=m, settings=s)
+    one, z1 = R.BatchRunner(n, m, s).solve(st, cm, ga, want_z=True)
+    two, z2 = R.BatchRunner(n, m, s, devices=[0, 0]).solve(st, cm, ga, want_z=True)
+    assert one.tobytes() == two.tobytes() and z1.tobytes() == z2.tobytes()

@@ -112,7 +112,7 @@ __device__ __forceinline__ int doff(const PolicyParams& P, int l) { return l * e
 template <int TL>
 __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double lstd[MAXIO];
+  __shared__ double lstd[MAXIO], lsd[MAXIO];  // log_std and exp(log_std), once per block
   __shared__ double wred[WARPS];
   const int trunk = blockIdx.y, chunk = blockIdx.x;
   const PolicyParams& P = L.P;
@@ -130,7 +130,10 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
     for (int e = t; e < rows * cols; e += THREADS) W[S.w[l] + (e / rows) * S.ld[l] + e % rows] = L.w[N.w[l] + e];
     for (int i = t; i < rows; i += THREADS) W[S.b[l] + i] = L.w[N.b[l] + i];
   }
-  if (t < P.act) lstd[t] = L.w[P.total + t];
+  if (t < P.act) {
+    lstd[t] = L.w[P.total + t];
+    lsd[t] = exp(lstd[t]);
+  }
   // pads stay zero (the paired loads read them)
   for (int e = t; e < TL * (L.pst + L.dst); e += THREADS) post[e] = 0.0;
 
@@ -210,12 +213,12 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel(const LossParams L) {
         const int A = P.act;
         double z0 = 0.0, z1 = 0.0, sd0 = 1.0, sd1 = 1.0, lp = 0.0;
         if (lane < A) {
-          sd0 = exp(lstd[lane]);
+          sd0 = lsd[lane];
           z0 = (L.act[row * A + lane] - out[s * L.ost + lane]) / sd0;
           lp += -0.5 * z0 * z0 - lstd[lane] - kLogSqrt2Pi;
         }
         if (lane + 32 < A) {
-          sd1 = exp(lstd[lane + 32]);
+          sd1 = lsd[lane + 32];
           z1 = (L.act[row * A + lane + 32] - out[s * L.ost + lane + 32]) / sd1;
           lp += -0.5 * z1 * z1 - lstd[lane + 32] - kLogSqrt2Pi;
         }
@@ -369,7 +372,7 @@ __device__ __forceinline__ void dmma(double& c0, double& c1, double a, double b)
 
 __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L) {
   extern __shared__ __align__(16) double sm[];
-  __shared__ double lstd[MAXIO];
+  __shared__ double lstd[MAXIO], lsd[MAXIO];  // log_std and exp(log_std), once per block
   __shared__ double wred[WARPS];
   const int trunk = blockIdx.y, chunk = blockIdx.x;
   const PolicyParams& P = L.P;
@@ -388,7 +391,10 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
     for (int e = t; e < rows * cols; e += THREADS) W[T.w[l] + (e / rows) * T.ldw[l] + e % rows] = L.w[N.w[l] + e];
     for (int i = t; i < rows; i += THREADS) W[T.b[l] + i] = L.w[N.b[l] + i];
   }
-  if (t < P.act) lstd[t] = L.w[P.total + t];
+  if (t < P.act) {
+    lstd[t] = L.w[P.total + t];
+    lsd[t] = exp(lstd[t]);
+  }
 
   double acc[MAXB][2];
   // this warp's gradient blocks, decoded once: delta / activation fragment offsets | layer << 30
@@ -478,12 +484,12 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
         const int A = P.act;
         double z0 = 0.0, z1 = 0.0, sd0 = 1.0, sd1 = 1.0, lp = 0.0;
         if (lane < A) {
-          sd0 = exp(lstd[lane]);
+          sd0 = lsd[lane];
           z0 = (L.act[row * A + lane] - d3[lane]) / sd0;
           lp += -0.5 * z0 * z0 - lstd[lane] - kLogSqrt2Pi;
         }
         if (lane + 32 < A) {
-          sd1 = exp(lstd[lane + 32]);
+          sd1 = lsd[lane + 32];
           z1 = (L.act[row * A + lane + 32] - d3[lane + 32]) / sd1;
           lp += -0.5 * z1 * z1 - lstd[lane + 32] - kLogSqrt2Pi;
         }

@@ -2,10 +2,10 @@
 // policy_forward (/root/reference/proj/src/policy.cpp:85-102) = mlp_forward (policy.cpp:15-31)
 // of the pi and value trunks, FP64 like the reference.
 //
-// Why CUDA cores, not tcgen05: per agent the two trunks are 4 layers of at most 64 x 64 (about
-// 40 kFLOP), so 16 k agents are 0.7 GFLOP per tick (~20 us of FP64 CUDA-core time); TF32/BF16
-// tensor-core GEMMs would miss the FP64 reference by 1e-3 and save microseconds.  Layout: one
-// warp per agent, lane j owns output neurons j and j + 32 of every layer, all weights of both
+// The default path is forward_kernel_mma in rmpc_ppo.cu: the PPO loss kernel's forward phase on
+// the FP64 tensor cores (mma.sync m8n8k4 f64; TF32/BF16 would miss the FP64 reference by 1e-3).
+// This file keeps the policy handle and the CUDA-core fallback for shapes beyond that layout:
+// one warp per agent, lane j owns output neurons j and j + 32 of every layer, all weights of both
 // trunks resident in shared memory as Eigen stores them (column-major, so a layer's column is
 // 64 consecutive doubles: conflict-free 8-byte loads across the warp), the layer input staged
 // per warp in shared memory and broadcast.  Persistent CTAs of 8 warps stride over the agents.
@@ -151,6 +151,9 @@ int32_t rmpc_policy_forward_device(rmpc_policy* p, int32_t n, const double* obs,
   if (!p || n < 0 || (n > 0 && !obs)) return RMPC_ERR_INVALID_ARG;
   if (n == 0 || (!mean && !value)) return RMPC_OK;
   if (cudaSetDevice(p->device) != cudaSuccess) return RMPC_ERR_CUDA;
+  int rc = RMPC_OK;
+  if (rmpc_ppo_dev::launch_forward_mma(p, n, obs, mean, value, stream ? (cudaStream_t)stream : cudaStreamLegacy, &rc))
+    return rc;
   const int need = (n + rmpc_policy_dev::WARPS - 1) / rmpc_policy_dev::WARPS;
   rmpc_policy_dev::forward_kernel<<<need < p->grid ? need : p->grid, 32 * rmpc_policy_dev::WARPS, p->smem,
                                     stream ? (cudaStream_t)stream : cudaStreamLegacy>>>(p->P, p->d_w, n, obs,

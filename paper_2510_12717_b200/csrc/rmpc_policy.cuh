@@ -53,6 +53,13 @@ inline PolicyParams policy_shape(int obs, int act, int hidden) {
 
 }  // namespace rmpc_policy_dev
 
+struct rmpc_policy;
+namespace rmpc_ppo_dev {
+// policy_forward on the FP64 tensor cores (rmpc_ppo.cu); false if the shapes exceed its layout.
+bool launch_forward_mma(rmpc_policy* p, int n, const double* obs, double* mean, double* value, cudaStream_t st,
+                        int* rc);
+}  // namespace rmpc_ppo_dev
+
 struct rmpc_policy {
   int device = 0;
   rmpc_policy_dev::PolicyParams P{};

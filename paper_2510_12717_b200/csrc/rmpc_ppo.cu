@@ -606,6 +606,76 @@ __global__ void __launch_bounds__(THREADS, 1) loss_kernel_mma(const MmaParams L)
   }
 }
 
+// policy_forward (policy.cpp:85-102) on the same tensor-core layout: the forward phase of
+// loss_kernel_mma alone, trunk outputs straight to global memory (mean n x act, value n).
+__global__ void __launch_bounds__(THREADS, 1) forward_kernel_mma(const MmaParams L, double* mean, double* value) {
+  extern __shared__ __align__(16) double sm[];
+  const int trunk = blockIdx.y, chunk = blockIdx.x;
+  if ((trunk == 0 && !mean) || (trunk == 1 && !value)) return;
+  const PolicyParams& P = L.P;
+  const Net& N = trunk == 0 ? P.pi : P.vf;
+  const MmaTrunk& T = L.tr[trunk];
+  double* W = sm;
+  double* X = W + T.wtotal;
+  const int t = threadIdx.x, lane = t & 31, warp = t >> 5, g = lane >> 2, q = lane & 3;
+  for (int e = t; e < T.wtotal + L.xtotal; e += THREADS) sm[e] = 0.0;
+  __syncthreads();
+  for (int l = 0; l < 4; ++l) {
+    const int rows = N.out[l], cols = N.in[l];
+    for (int e = t; e < rows * cols; e += THREADS) W[T.w[l] + (e / rows) * T.ldw[l] + e % rows] = L.w[N.w[l] + e];
+    for (int i = t; i < rows; i += THREADS) W[T.b[l] + i] = L.w[N.b[l] + i];
+  }
+  const int c0 = chunk * L.chunk, c1 = min(L.n, c0 + L.chunk);
+  __syncthreads();
+  for (int base = c0; base < c1; base += TILE) {
+    for (int e = t; e < TILE * P.obs; e += THREADS) {
+      const int s = e / P.obs, k = e % P.obs, gi = base + s;
+      X[L.xo[0] + s * L.ldx[0] + k] = gi < c1 ? L.obs[(size_t)gi * P.obs + k] : 0.0;
+    }
+    __syncthreads();
+    for (int l = 0; l < 4; ++l) {
+      const int nbN = T.Np[l] / 8, units = 4 * ((nbN + 1) / 2);
+      const double* Wl = W + T.w[l];
+      const double* Xl = X + L.xo[l];
+      const int ldw = T.ldw[l], ldx = L.ldx[l];
+      for (int u = warp; u < units; u += WARPS) {
+        const int mb = u & 3, nb0 = 2 * (u >> 2);
+        const bool two = nb0 + 1 < nbN;
+        double z00 = 0.0, z01 = 0.0, z10 = 0.0, z11 = 0.0;
+        const double* xa = Xl + (8 * mb + g) * ldx + q;
+        const double* wb = Wl + q * ldw + 8 * nb0 + g;
+#pragma unroll 4
+        for (int k4 = 0; k4 < T.Kp[l] / 4; ++k4) {
+          const double a = xa[4 * k4];
+          dmma(z00, z01, a, wb[4 * k4 * ldw]);
+          if (two) dmma(z10, z11, a, wb[4 * k4 * ldw + 8]);
+        }
+        const int s = 8 * mb + g;
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          if (h == 1 && !two) break;
+          const int n = 8 * (nb0 + h) + 2 * q;
+          const double za = (h ? z10 : z00) + W[T.b[l] + n], zb = (h ? z11 : z01) + W[T.b[l] + n + 1];
+          if (l < 3) {
+            double* xo = X + L.xo[l + 1] + s * L.ldx[l + 1] + n;
+            xo[0] = za > 0.0 ? za : expm1_neg(fmin(za, 0.0));
+            xo[1] = zb > 0.0 ? zb : expm1_neg(fmin(zb, 0.0));
+          } else if (base + s < c1) {
+            const size_t row = (size_t)(base + s);
+            if (trunk == 0) {
+              if (n < P.act) mean[row * P.act + n] = za;
+              if (n + 1 < P.act) mean[row * P.act + n + 1] = zb;
+            } else if (n == 0) {
+              value[row] = za;
+            }
+          }
+        }
+      }
+      __syncthreads();
+    }
+  }
+}
+
 // Fixed-order sum of the chunk partials into the flatten_grads vector and the loss info.
 // Block = 32 parameters (lane) x 8 warps, warp w summing chunks w, w + 8, ...; the eight
 // warp sums are then added in warp order: a fixed order, and ~nch / 8 loads in flight per thread
@@ -880,6 +950,29 @@ int launch_loss(rmpc_policy* p, int n, const double* obs, const double* act, con
   reduce_kernel<<<(np + RED_PARAMS - 1) / RED_PARAMS, 32 * RED_WARPS, 0, st>>>(
       P, L.nch, L.part_stride, L.part, cfg.entropy_coef, cfg.value_coef, p->d_w, grads, info, sq);
   return cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+}
+
+// policy_forward on the tensor cores; false when the shapes exceed the layout (the caller then
+// runs the CUDA-core kernel of rmpc_policy.cu).
+bool launch_forward_mma(rmpc_policy* p, int n, const double* obs, double* mean, double* value, cudaStream_t st,
+                        int* rc) {
+  MmaParams M{};
+  int smem = 0;
+  if (!mma_layout(p->P, M, smem)) return false;
+  const int wmax = std::max(M.tr[0].wtotal, M.tr[1].wtotal);
+  smem = (int)sizeof(double) * (wmax + M.xtotal);
+  M.n = n;
+  M.nch = std::max(1, std::min(p->sms / 2, (n + TILE - 1) / TILE));
+  M.chunk = (n + M.nch - 1) / M.nch;
+  M.w = p->d_w;
+  M.obs = obs;
+  if (cudaFuncSetAttribute(forward_kernel_mma, cudaFuncAttributeMaxDynamicSharedMemorySize, smem) != cudaSuccess) {
+    *rc = RMPC_ERR_CUDA;
+    return true;
+  }
+  forward_kernel_mma<<<dim3(M.nch, 2), THREADS, smem, st>>>(M, mean, value);
+  *rc = cudaGetLastError() == cudaSuccess ? RMPC_OK : RMPC_ERR_CUDA;
+  return true;
 }
 
 // xoshiro256++ (rng.hpp:15-43): seeding and uniform_int for the minibatch shuffles.

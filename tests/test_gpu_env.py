@@ -145,17 +145,23 @@ def test_closed_loop_on_device(oracle):
     assert fin.mean() > 0.5
 
 
-def test_policy_forward_parity(oracle):
+@pytest.mark.parametrize("obs_dim,act,hidden,n", [(23, 6, 64, 4096), (23, 6, 24, 777), (64, 32, 64, 1000)])
+def test_policy_forward_parity(oracle, obs_dim, act, hidden, n):
+    """Default shapes run the FP64 tensor-core kernel (rmpc_ppo.cu forward_kernel_mma); obs 64 /
+    act 32 exceeds its layout and runs the CUDA-core warp-per-agent kernel."""
     from paper_2510_12717_b200.env import Policy
-    params = oracle.init_policy(seed=3, zero_final=False)
-    n = 4096
-    obs = np.random.default_rng(10).uniform(-2, 2, (n, 23))
-    pol = Policy(params)
-    mean = torch.zeros((n, 6), dtype=torch.float64, device=DEV)
+    params = oracle.init_policy(obs_dim, act, hidden, seed=3, zero_final=False)
+    obs = np.random.default_rng(10).uniform(-2, 2, (n, obs_dim))
+    pol = Policy(params, obs_dim, act, hidden)
+    mean = torch.zeros((n, act), dtype=torch.float64, device=DEV)
     value = torch.zeros(n, dtype=torch.float64, device=DEV)
     pol.forward(dev(obs), mean, value)
     torch.cuda.synchronize()
-    rm, rv = oracle.policy_forward(params, obs)
+    rm, rv = oracle.policy_forward(params, obs, act, hidden)
     np.testing.assert_allclose(mean.cpu().numpy(), rm, rtol=1e-12, atol=1e-13)
     np.testing.assert_allclose(value.cpu().numpy(), rv, rtol=1e-12, atol=1e-13)
     np.testing.assert_array_equal(pol.log_std, np.log(0.5))
+    only_value = torch.zeros(n, dtype=torch.float64, device=DEV)
+    pol.forward(dev(obs), None, only_value)
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(only_value.cpu().numpy(), value.cpu().numpy())

@@ -43,7 +43,7 @@ using rmpc_policy_dev::MAXIO;
 using rmpc_policy_dev::Net;
 using rmpc_policy_dev::PolicyParams;
 
-constexpr int THREADS = 512, TILE = 32, WARPS = THREADS / 32, SPT = TILE / (THREADS / 64);
+constexpr int THREADS = 512, TILE = 32, WARPS = THREADS / 32;
 constexpr double kLogSqrt2Pi = 0.91893853320467274178032973640562;
 
 struct TrunkSm {

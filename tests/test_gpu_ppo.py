@@ -53,6 +53,20 @@ def test_loss_and_gradient_parity(oracle, n, hidden):
     close(g[-act:], g_o[-act:])  # log_std
 
 
+@pytest.mark.parametrize("obs,act,hidden", [(17, 3, 20), (31, 7, 40)])
+def test_loss_parity_padded_shapes(oracle, obs, act, hidden):
+    """Shapes that are not multiples of the 8 x 8 tensor-core blocks (zero-padded operands)."""
+    from paper_2510_12717_b200.env import Policy
+    from paper_2510_12717_b200.ppo import default_ppo_config, ppo_loss
+    n = 333
+    params, o, a, old, adv, ret = make_batch(oracle, 6, n, obs, act, hidden)
+    info_o, g_o = oracle.ppo_loss(params, o, a, old, adv, ret, oracle.ppo_config(), act, hidden)
+    pol = Policy(params, obs, act, hidden)
+    info, g = ppo_loss(pol, *cuda(o, a, old, adv, ret), default_ppo_config())
+    np.testing.assert_allclose(info.total, info_o[0], rtol=1e-9)
+    close(g.cpu().numpy(), g_o)
+
+
 def test_loss_parity_cuda_core_fallback(oracle):
     """obs 64 / act 32 / hidden 64 exceeds the tensor-core layout's shared memory: the CUDA-core
     kernel runs and must agree just the same."""

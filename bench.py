@@ -1,17 +1,21 @@
 #!/usr/bin/env python
 """Benchmark of the batched RTI-MPC solve (the Residual-MPC hot path, BASELINE.json).
 
-One step = one control tick: every agent's MpcController::rti_step (N = 10, 25 ADMM
-iterations) for a fresh synthetic batch held in HBM.  Prints ONE JSON line (rank 0).
+One step = one control tick of config C3 (BASELINE.json configs[2]): every
+agent's MpcController::rti_step (N = 10, 25 ADMM iterations) for 16 384 synthetic agents,
+split into contiguous shards over the GPUs (strong scaling: 16 384 / N per GPU).  Prints ONE
+JSON line (rank 0).
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--agents A] [--horizon T]
   python -m torch.distributed.run --nproc-per-node N ... bench.py --gpus N   (one rank per GPU)
-  python bench.py --impl reference   (the reference algorithm on the host cores: the CPU oracle,
-                                      since the Eigen-based reference cannot be built here)
+  python bench.py --impl reference   (the reference's own BatchRunner, built from its sources
+                                      into oracle/_ref, on all host cores, same 16 384 agents)
 
-value   = solves/s over all ranks (agents x steps / max-over-ranks device time), inputs resident
+value   = solves/s over all ranks (agents x steps / max-over-ranks device time), inputs resident,
+          each step returning the solution records AND the planned trajectory z* (the whole
+          MpcSolution)
 e2e     = the same through the C ABI (rmpc_solve) with pinned HOST buffers: H2D of the tick's
-          inputs and D2H of its solution records inside the timed region
+          inputs and D2H of its records + z* inside the timed region
 roofline= FP32 CUDA-core bound: FLOP_alg per agent-solve (instrumented FP64 oracle,
           profiles/flops_per_solve.json) x agents / kernel time vs the measured FMA peak
 """
@@ -39,13 +43,16 @@ def parse():
     p.add_argument("--gpus", type=int, default=1)
     p.add_argument("--steps", type=int, default=20)
     p.add_argument("--warmup", type=int, default=5)
-    p.add_argument("--agents", type=int, default=4096, help="agents per GPU (weak scaling)")
+    p.add_argument("--agents", type=int, default=16384,
+                   help="agents in total, split over the GPUs (strong scaling; C3 = 16 384)")
     p.add_argument("--horizon", type=int, default=10)
     p.add_argument("--kind", default="random", choices=("random", "mixed", "standing"))
     p.add_argument("--impl", default="ours", choices=("ours", "reference"))
     p.add_argument("--no-ppo", action="store_true", help="skip the PPO batch measurement")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--cpu-sample", type=int, default=4096, help="agents in the CPU baseline sample")
+    p.add_argument("--ref-agents", type=int, default=0,
+                   help="agents per reference-arm step (0 = the whole workload, --agents)")
     p.add_argument("--cl-agents", type=int, default=8192,
                    help="C5 closed-loop agents per GPU (65 536 over 8 B200); 0 disables")
     p.add_argument("--cl-ticks", type=int, default=100, help="C5 closed-loop ticks")
@@ -60,8 +67,10 @@ def dist_env():
 
 
 def workload_name(args, world):
-    return (f"C2/C3: {args.agents} agents per GPU x {world} GPU, horizon N={args.horizon}, "
-            f"n_qp=25, {args.kind} synthetic states/commands/gait phases (Rng(0, agent))")
+    cfg = "C3" if (args.agents == 16384 and args.horizon == 10) else "custom"
+    return (f"{cfg}: {args.agents} agents in total, contiguous shards over {world} GPU "
+            f"({args.agents // world} per GPU, strong scaling), horizon N={args.horizon}, n_qp=25, "
+            f"{args.kind} synthetic states/commands/gait phases (Rng(0, agent))")
 
 
 def flop_alg(kind, T):
@@ -234,62 +243,103 @@ def cpu_model():
     return "unknown"
 
 
+def _ref_lib():
+    """The reference's own code (oracle/_ref, built from /root/reference's sources), else None."""
+    try:
+        from oracle import ref as F
+        F.lib()
+        return F
+    except Exception:
+        return None
+
+
 def cpu_baseline_run(args, n_sample, steps=1):
-    """The reference algorithm on the host cores: the FP64 CPU oracle (oracle/) with the
-    reference's atomic-cursor thread pool (batch.cpp:46-62), all hardware threads."""
+    """The reference on the host cores: its own BatchRunner (oracle/_ref; atomic-cursor thread
+    pool over agents, batch.cpp:46-62) with all hardware threads; the restated FP64 oracle
+    (same execution model) when _ref is missing.  Returns (solves/s, cores, walls ms, 1-thread
+    solves/s, kind)."""
     import paper_2510_12717_b200 as R
     from oracle import oracle as O
+    F = _ref_lib()
     m, s = R.default_model(), R.default_settings(args.horizon)
     st, cm, ga = R.synthetic_batch(n_sample, args.kind, seed=0, model=m, settings=s,
                                    nominal=O.nominal_pose(m))
     cores = os.cpu_count() or 1
-    O.solve_batch(m, s, st[:min(64, n_sample)], cm[:min(64, n_sample)], ga[:min(64, n_sample)],
-                  workers=cores, want_z=False)  # warm caches / thread pool
-    walls = []
-    for _ in range(steps):
-        _, _, _, wall = O.solve_batch(m, s, st, cm, ga, workers=cores, want_z=False)
-        walls.append(wall)
-    # and the 1-worker figure (BatchRunner with workers = 1) on a smaller slice
+
+    def run(lo, hi, workers):
+        if F is not None:
+            return F.solve_batch(m, s, st[lo:hi], cm[lo:hi], ga[lo:hi], workers=workers, want_z=False)[4]
+        return O.solve_batch(m, s, st[lo:hi], cm[lo:hi], ga[lo:hi], workers=workers, want_z=False)[3]
+
+    run(0, min(64, n_sample), cores)  # warm caches / thread pool
+    walls = [run(0, n_sample, cores) for _ in range(steps)]
     k = min(256, n_sample)
-    _, _, _, wall1 = O.solve_batch(m, s, st[:k], cm[:k], ga[:k], workers=1, want_z=False)
-    return n_sample * steps / (sum(walls) * 1e-3), cores, walls, k / (wall1 * 1e-3)
+    wall1 = run(0, k, 1)
+    return n_sample * steps / (sum(walls) * 1e-3), cores, walls, k / (wall1 * 1e-3), \
+        ("reference" if F is not None else "port")
 
 
 def run_reference_arm(args):
+    """--impl reference: the reference's own BatchRunner::solve (oracle/_ref: the unmodified
+    /root/reference/proj/src sources compiled against the Eigen-subset shim) over the same
+    workload (all --agents agents per step, same synthetic inputs) with every host thread; the
+    restated oracle if _ref is missing.  Rank 0 only."""
     rank, world, _ = dist_env()
     if rank != 0:
         return
-    n = min(args.cpu_sample, 1024)  # a bounded sample of the workload per step
     import paper_2510_12717_b200 as R
     from oracle import oracle as O
+    F = _ref_lib()
+    n = args.ref_agents or args.agents
     m, s = R.default_model(), R.default_settings(args.horizon)
     st, cm, ga = R.synthetic_batch(n, args.kind, seed=0, model=m, settings=s, nominal=O.nominal_pose(m))
     cores = os.cpu_count() or 1
+
+    def step():
+        if F is not None:  # BatchRunner's own TimingReport::total_ms (batch.cpp:64-66)
+            sol, _, mean, std, wall = F.solve_batch(m, s, st, cm, ga, workers=cores, want_z=True)
+            return wall, sol, mean, std
+        sol, _, stage, wall = O.solve_batch(m, s, st, cm, ga, workers=cores, want_z=True, timed=True)
+        return wall, sol, stage, None
+
     for _ in range(args.warmup):
-        O.solve_batch(m, s, st, cm, ga, workers=cores, want_z=False)
-    walls = []
+        step()
+    walls, last = [], None
     for _ in range(args.steps):
-        _, _, _, wall = O.solve_batch(m, s, st, cm, ga, workers=cores, want_z=False)
+        wall, sol, mean, std = step()
         walls.append(wall)
+        last = (sol, mean, std)
     total = sum(walls)
     value = n * args.steps / (total * 1e-3)
-    sample = f"{n} agents of the workload per step, {cores} host threads ({cpu_model()})"
+    kind = "reference" if F is not None else "port"
+    impl = ("reference BatchRunner::solve built from /root/reference/proj/src (oracle/_ref, "
+            "Eigen-subset shim; AMD ordering substituted)") if F is not None else \
+        "CPU oracle: plain-C++ FP64 restatement of the reference"
+    whole = "the whole tick" if n == args.agents else f"a sample of the {args.agents}-agent tick"
+    sample = f"{n} agents of the workload per step ({whole}), {cores} host threads ({cpu_model()})"
+    stage = None
+    if last[1] is not None:
+        stage = {"mean_ms_per_agent": dict(zip(STAGES, map(float, last[1])))}
+        if last[2] is not None:
+            stage["std_ms"] = dict(zip(STAGES, map(float, last[2])))
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "solves/s",
         "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
-        "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "weak",
+        "ms_per_step": total / args.steps, "higher_is_better": True, "scaling": "strong",
         "vs_baseline": None, "dtype": "f64", "data": "synthetic",
         "p50_tick_ms": statistics.median(walls),
-        "config": {"workload": workload_name(args, world), "agents_per_gpu": args.agents,
-                   "horizon": args.horizon, "sampled_agents_per_step": n,
-                   "implementation": "CPU oracle: plain-C++ FP64 restatement of the reference "
-                                     "(the Eigen-based reference does not build here)",
-                   "parallelism": f"std::thread pool x {cores}"},
-        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": "port",
-                         "sample": sample},
+        "config": {"workload": workload_name(args, world), "agents_total": args.agents,
+                   "horizon": args.horizon, "sampled_agents_per_step": n, "implementation": impl,
+                   "parallelism": f"std::thread pool x {cores}", "same_config": n == args.agents},
+        "cpu_baseline": {"value": value, "unit": "solves/s", "cores": cores, "kind": kind, "sample": sample},
         "e2e": {"value": value, "unit": "solves/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "status_ok": int(np.sum(last[0]["status"] == 0)),
+        "stage_split": stage,
     }
     print(json.dumps(line), flush=True)
+
+
+STAGES = ("init_guess", "param", "kkt_build", "ruiz", "factorize", "admm_iters", "rnea")
 
 
 def closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier):
@@ -368,24 +418,26 @@ def main():
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return t.cpu().numpy()
 
-    n = args.agents
     T = args.horizon
     m, s = R.default_model(), R.default_settings(T)
-    # this rank's contiguous agent range [rank n, (rank+1) n) of the global batch
-    st_all, cm_all, ga_all = R.synthetic_batch(n * world, args.kind, seed=0, model=m, settings=s)
+    # strong scaling: this rank's contiguous range of the args.agents-agent global batch
+    n_total = args.agents
+    st_all, cm_all, ga_all = R.synthetic_batch(n_total, args.kind, seed=0, model=m, settings=s)
     from paper_2510_12717_b200.sharding import shard_range
-    lo, hi = shard_range(rank, world, n * world)
+    lo, hi = shard_range(rank, world, n_total)
+    n = hi - lo
     st, cm, ga = st_all[lo:hi].copy(), cm_all[lo:hi].copy(), ga_all[lo:hi].copy()
     br = R.BatchRunner(n, m, s, devices=[local])
     stream = torch.cuda.Stream(device=dev)
     with torch.cuda.stream(stream):
         d_st, d_cm, d_ga = (torch.from_numpy(a).to(dev) for a in (st, cm, ga))
         d_out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+        d_z = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
         flush = torch.empty(256 * 1024 * 1024, dtype=torch.uint8, device=dev)  # > 126 MB L2
     stream.synchronize()
 
-    def step():
-        br.solve_device(d_st, d_cm, d_ga, d_out, stream=stream)
+    def step():  # the whole MpcSolution: node-0 records and the planned trajectory z*
+        br.solve_device(d_st, d_cm, d_ga, d_out, z_out=d_z, stream=stream)
 
     for _ in range(args.warmup):
         step()
@@ -415,33 +467,39 @@ def main():
     step_ms_local = [a.elapsed_time(b) for a, b in ev]
     step_ms = max_over_ranks(step_ms_local)
     ms_per_step = float(np.mean(step_ms))
-    value = n * world / (ms_per_step * 1e-3)
+    value = n_total / (ms_per_step * 1e-3)
 
-    # ---- end to end through the C ABI with pinned host buffers (rmpc_solve)
+    # ---- end to end through the C ABI with pinned host buffers (rmpc_solve): every step copies
+    #      the tick's inputs H2D and the whole MpcSolution (records + z*) D2H inside the region
     pin = lambda a: torch.from_numpy(a).pin_memory().numpy()  # noqa: E731
     h_st, h_cm, h_ga = pin(st), pin(cm), pin(ga)
     h_out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy().view(SOLUTION_DTYPE)
-    for _ in range(2):
-        br.solve(h_st, h_cm, h_ga, out=h_out)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        br.solve(h_st, h_cm, h_ga, out=h_out)
-    t1 = time.perf_counter()
-    barrier()
-    e2e_ms = float(max_over_ranks([(t1 - t0) * 1e3 / args.steps])[0])
+    h_z = torch.zeros((n, T, 26), dtype=torch.float32).pin_memory().numpy()
+
+    def e2e(with_z):
+        for _ in range(2):
+            br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z if with_z else None)
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z if with_z else None)
+        t1 = time.perf_counter()
+        barrier()
+        return float(max_over_ranks([(t1 - t0) * 1e3 / args.steps])[0])
+
+    e2e_nz_ms = e2e(False)
+    e2e_ms = e2e(True)
     tm = br.last_timing()
     ok = int(np.sum(h_out["status"] == 0))
-    # the full MpcSolution equivalent: the records plus the whole planned trajectory z*
-    h_z = torch.zeros((n, T, 26), dtype=torch.float32).pin_memory().numpy()
-    br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z)
-    barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        br.solve(h_st, h_cm, h_ga, out=h_out, z_out=h_z)
-    t1 = time.perf_counter()
-    barrier()
-    e2e_z_ms = float(max_over_ranks([(t1 - t0) * 1e3 / args.steps])[0])
+    # per-stage split of the kernel (clock64 at the reference's 7 stage boundaries, summed over
+    # agents; the reference's TimingReport / benchmark CSV analogue, batch.cpp:64-77, 81-142)
+    br.set_stage_profiling(True)
+    br.solve(h_st, h_cm, h_ga, out=h_out)
+    stage = br.last_timing()
+    br.set_stage_profiling(False)
+    stage_split = {"kernel_ms": stage["kernel_ms"], "stage_ms": stage["stage_ms"],
+                   "per_agent_mean_ms": stage["stage_mean_ms"], "per_agent_std_ms": stage["stage_std_ms"],
+                   "note": "one profiled tick (clock64 instrumentation on), split of its kernel time"}
 
     # ---- roofline: FP32 CUDA-core bound
     peak = fma_peak_tflops(local)
@@ -484,39 +542,41 @@ def main():
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
-            # ~5 ticks of the workload: ~1 s on 16 host threads, ~15 s of CPU work
-            v, cores, walls, v1 = cpu_baseline_run(args, min(args.cpu_sample, n), steps=5)
-            cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": "port",
+            # 3 ticks x 4096 agents of the workload: ~2 s on 16 host threads, ~30 s of CPU work
+            ns = min(args.cpu_sample, n)
+            v, cores, walls, v1, kind = cpu_baseline_run(args, ns, steps=3)
+            what = ("the reference's own BatchRunner::solve (oracle/_ref, built from its sources)"
+                    if kind == "reference" else "FP64 oracle restating the reference algorithm")
+            cpu = {"value": v, "unit": "solves/s", "cores": cores, "kind": kind,
                    "single_thread_value": v1,
-                   "sample": f"5 ticks x {min(args.cpu_sample, n)} agents of the same workload, "
-                             f"{cores} host threads ({cpu_model()}); FP64 oracle restating the "
-                             f"reference algorithm incl. per-solve ordering + LDL^T"}
+                   "sample": f"3 ticks x {ns} agents of the same workload, {cores} host threads "
+                             f"({cpu_model()}); {what}, incl. per-solve ordering + LDL^T"}
         except Exception as e:  # pragma: no cover
-            cpu = {"value": None, "unit": "solves/s", "cores": 0, "kind": "port", "sample": f"failed: {e}"}
+            cpu = {"value": None, "unit": "solves/s", "cores": 0, "kind": "reference", "sample": f"failed: {e}"}
 
     if rank == 0:
         line = {
             "metric": METRIC, "value": value, "unit": "solves/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f32",
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f32",
             "data": "synthetic",
             "p50_tick_ms": float(np.median(step_ms)), "p99_tick_ms": float(np.percentile(step_ms, 99)),
             "tick_budget_ms": 10.0,
-            "config": {"workload": workload_name(args, world), "agents_per_gpu": n,
-                       "agents_total": n * world, "horizon": T, "n_qp": 25,
-                       "parallelism": f"agent-sharded over {world} GPU, no collectives",
+            "config": {"workload": workload_name(args, world), "agents_total": n_total,
+                       "agents_per_gpu": n, "horizon": T, "n_qp": 25,
+                       "parallelism": f"agent-sharded over {world} GPU (contiguous ranges), no collectives",
                        "l2": "flushed between steps (256 MiB memset outside the per-step events)",
+                       "outputs": "solution records + planned trajectory z* per step",
                        "precision": "FP32 solve, FP64 linearization/objective"},
-            "e2e": {"value": n * world / (e2e_ms * 1e-3), "unit": "solves/s",
-                    "h2d_bytes_per_step": n * (144 + 24 + 56), "d2h_bytes_per_step": n * 140,
-                    "ms_per_step": e2e_ms, "api": "rmpc_solve (C ABI), pinned host buffers",
-                    "with_z_star": {"value": n * world / (e2e_z_ms * 1e-3), "ms_per_step": e2e_z_ms,
-                                    "d2h_bytes_per_step": n * (140 + T * 26 * 4),
-                                    "note": "also returns the planned trajectory z* (T x 26 FP32), "
-                                            "everything the reference's MpcSolution carries"},
+            "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": "solves/s",
+                    "h2d_bytes_per_step": n * (144 + 24 + 56), "d2h_bytes_per_step": n * (140 + T * 26 * 4),
+                    "ms_per_step": e2e_ms, "api": "rmpc_solve (C ABI), pinned host buffers, records + z*",
+                    "without_z_star": {"value": n_total / (e2e_nz_ms * 1e-3), "ms_per_step": e2e_nz_ms,
+                                       "d2h_bytes_per_step": n * 140},
                     "last_timing_ms": {"h2d": tm["h2d_ms"], "kernel": tm["kernel_ms"], "d2h": tm["d2h_ms"],
                                        "total": tm["total_ms"]}},
             "roofline": roofline,
+            "stage_split": stage_split,
             "gpu_launches": args.steps,
             "status_ok": ok, "clocks": clk, "cpu_baseline": cpu,
             "closed_loop": closed,

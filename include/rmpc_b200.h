@@ -103,8 +103,11 @@ typedef struct rmpc_solution {
   int32_t fail_iter;          /* DivergenceError::iteration, -1 otherwise */
 } rmpc_solution;
 
-/* TimingReport (batch.hpp:12-18), measured on the device.  stage_ms splits the fused
- * kernel's time by the reference's 7 stages when stage profiling is enabled, else 0. */
+/* TimingReport (batch.hpp:12-18), measured on the device.  With stage profiling enabled
+ * (rmpc_set_stage_profiling), stage_ms splits the fused kernel's time by the reference's 7
+ * stages, and stage_mean_ms / stage_std_ms are TimingReport::mean_ms / std_ms: the mean and
+ * standard deviation over agents of each agent's time in a stage (clock64 cycles at the
+ * reference's stage boundaries, converted at the device's SM clock); else all 0. */
 typedef struct rmpc_timing {
   int32_t batch_size;
   int32_t devices;
@@ -113,6 +116,8 @@ typedef struct rmpc_timing {
   double kernel_ms;    /* solve kernel (max over devices, CUDA events) */
   double d2h_ms;       /* device->host copies (max over devices, CUDA events) */
   double stage_ms[RMPC_NUM_STAGES];
+  double stage_mean_ms[RMPC_NUM_STAGES];
+  double stage_std_ms[RMPC_NUM_STAGES];
 } rmpc_timing;
 
 typedef struct rmpc_handle rmpc_handle;
@@ -137,11 +142,26 @@ int32_t rmpc_solve(rmpc_handle* handle, const rmpc_state* states, const rmpc_com
                    rmpc_solution* out, float* z_star_out);
 
 /* Same solve with DEVICE arrays already resident on the handle's single device; enqueued on
- * `stream` (a cudaStream_t, NULL = the handle's stream) without host synchronisation. */
+ * `stream` (a cudaStream_t; NULL = the legacy default stream, like every device entry point of
+ * the library) without host synchronisation.  Multi-device handles: rmpc_solve_device_sharded. */
 int32_t rmpc_solve_device(rmpc_handle* handle, const rmpc_state* d_states,
                           const rmpc_command* d_cmds, const rmpc_gait* d_gaits,
                           const rmpc_solution* d_prev, const float* d_prev_z_star,
                           rmpc_solution* d_out, float* d_z_star_out, void* stream);
+
+/* rmpc_solve_device for a handle over several devices: per shard g (rmpc_shard_info: device,
+ * agent range [begin, begin + count) of the batch), its device arrays d_*[g] of `count` agents
+ * on that device and streams[g] (NULL array or entry = the device's legacy default stream).
+ * d_prev / d_prev_z_star / d_z_star_out may be NULL arrays.  Enqueues one launch per device and
+ * returns without host synchronisation; no data crosses devices (agents are independent). */
+int32_t rmpc_solve_device_sharded(rmpc_handle* handle, const rmpc_state* const* d_states,
+                                  const rmpc_command* const* d_cmds, const rmpc_gait* const* d_gaits,
+                                  const rmpc_solution* const* d_prev, const float* const* d_prev_z_star,
+                                  rmpc_solution* const* d_out, float* const* d_z_star_out,
+                                  void* const* streams);
+/* Shard g of the handle: its CUDA device and contiguous agent range. */
+int32_t rmpc_shard_info(const rmpc_handle* handle, int32_t shard, int32_t* device, int32_t* begin,
+                        int32_t* count);
 
 int32_t rmpc_size(const rmpc_handle* handle);        /* BatchRunner::size() */
 int32_t rmpc_workers(const rmpc_handle* handle);     /* BatchRunner::workers(): devices */

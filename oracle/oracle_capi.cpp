@@ -10,17 +10,12 @@
 #include "rmpc_oracle_ppo.hpp"
 #include "rmpc_oracle_rng.hpp"
 #include "oracle_flops.hpp"
+#include "oracle_abi.h"
 
 using namespace oracle;
 
 extern "C" {
 
-typedef struct oracle_solution {
-  double tau_ff[6], q_set[6], qd_set[6], f0[8], base_residual[3];
-  double v_mpc, prim_res, dual_res, delta_inf_norm;
-  double v_quad, v_lin;  // the two terms of V = 1/2 x^T P x + q^T x (cancellation scale)
-  int32_t status, fail_iter, n_vars, n_cons, ldl_nnz, pad;
-} oracle_solution;
 
 void oracle_model_default(rmpc_model* m) { model_default(m); }
 void oracle_settings_default(rmpc_settings* s, int32_t horizon) { settings_default(s, horizon); }

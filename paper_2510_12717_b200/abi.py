@@ -75,7 +75,7 @@ class Timing(C.Structure):
     _fields_ = [
         ("batch_size", _i), ("devices", _i),
         ("total_ms", _d), ("h2d_ms", _d), ("kernel_ms", _d), ("d2h_ms", _d),
-        ("stage_ms", _d * NUM_STAGES),
+        ("stage_ms", _d * NUM_STAGES), ("stage_mean_ms", _d * NUM_STAGES), ("stage_std_ms", _d * NUM_STAGES),
     ]
 
 

@@ -10,8 +10,11 @@
 #include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <condition_variable>
 #include <cstdio>
 #include <cstring>
+#include <functional>
+#include <memory>
 #include <mutex>
 #include <string>
 #include <thread>
@@ -42,9 +45,69 @@ struct Shard {
   char* h_stage_out = nullptr;
   size_t stage_in_bytes = 0, stage_out_bytes = 0;
   double h2d_ms = 0, kernel_ms = 0, d2h_ms = 0;
-  unsigned long long prof[RMPC_NUM_STAGES] = {0};
+  unsigned long long prof[2 * RMPC_NUM_STAGES] = {0};  // per stage: sum, then sum of squares
+  int clock_khz = 0;
   int err = 0;
   std::string msg;
+};
+
+// Persistent host workers for shards 1..G-1 (the calling thread runs shard 0): the reference's
+// BatchRunner spawns min(workers, n) threads per solve (batch.cpp:46-62); a control tick every
+// 10 ms should not pay thread creation, so the workers live as long as the handle.
+class ShardPool {
+ public:
+  explicit ShardPool(int workers) {
+    for (int g = 1; g <= workers; ++g) threads_.emplace_back([this, g]() { loop(g); });
+  }
+  ~ShardPool() {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      stop_ = true;
+    }
+    cv_.notify_all();
+    for (auto& t : threads_) t.join();
+  }
+  // job(g) for g = 0..G-1, g = 0 on the caller; returns when all are done
+  void run(const std::function<void(int)>& job) {
+    {
+      std::lock_guard<std::mutex> lk(mu_);
+      job_ = &job;
+      pending_ = (int)threads_.size();
+      ++epoch_;
+    }
+    cv_.notify_all();
+    job(0);
+    std::unique_lock<std::mutex> lk(mu_);
+    done_.wait(lk, [this]() { return pending_ == 0; });
+    job_ = nullptr;
+  }
+
+ private:
+  void loop(int g) {
+    uint64_t seen = 0;
+    for (;;) {
+      const std::function<void(int)>* job;
+      {
+        std::unique_lock<std::mutex> lk(mu_);
+        cv_.wait(lk, [&]() { return stop_ || epoch_ != seen; });
+        if (stop_) return;
+        seen = epoch_;
+        job = job_;
+      }
+      (*job)(g);
+      {
+        std::lock_guard<std::mutex> lk(mu_);
+        if (--pending_ == 0) done_.notify_one();
+      }
+    }
+  }
+  std::vector<std::thread> threads_;
+  std::mutex mu_;
+  std::condition_variable cv_, done_;
+  const std::function<void(int)>* job_ = nullptr;
+  uint64_t epoch_ = 0;
+  int pending_ = 0;
+  bool stop_ = false;
 };
 
 }  // namespace
@@ -59,6 +122,7 @@ struct rmpc_handle {
   rmpc_timing timing;
   std::string err;
   int profile = 0;
+  std::unique_ptr<ShardPool> pool;  // shards >= 2 only
 };
 
 namespace {
@@ -177,7 +241,8 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
   CK(cudaMalloc(&sh.d_prev_z, zn * sizeof(float)));
   CK(cudaMalloc(&sh.d_out, n * sizeof(rmpc_solution)));
   CK(cudaMalloc(&sh.d_z, zn * sizeof(float)));
-  CK(cudaMalloc(&sh.d_prof, RMPC_NUM_STAGES * sizeof(unsigned long long)));
+  CK(cudaMalloc(&sh.d_prof, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long)));
+  cudaDeviceGetAttribute(&sh.clock_khz, cudaDevAttrClockRate, sh.device);
   sh.stage_in_bytes = n * (sizeof(rmpc_state) + sizeof(rmpc_command) + sizeof(rmpc_gait) + sizeof(rmpc_solution)) +
                       zn * sizeof(float) + 8 * 256;  // 256-byte aligned sub-buffers
   sh.stage_out_bytes = n * sizeof(rmpc_solution) + zn * sizeof(float) + 2 * 256;
@@ -261,7 +326,7 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
     z_dst = z_pinned ? reinterpret_cast<char*>(z_out + b * zrow)
                      : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
   CK(cudaEventRecord(sh.ev[0], ss[0]));
-  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
+  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
   if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
@@ -323,19 +388,63 @@ void fill_timing(rmpc_handle& h, double total_ms) {
   t.batch_size = h.n;
   t.devices = (int)h.shards.size();
   t.total_ms = total_ms;
-  unsigned long long prof[RMPC_NUM_STAGES] = {0};
+  double sum[RMPC_NUM_STAGES] = {0}, sq[RMPC_NUM_STAGES] = {0};
+  int clock_khz = 0;
   for (const Shard& sh : h.shards) {
     t.h2d_ms = std::max(t.h2d_ms, sh.h2d_ms);
     t.kernel_ms = std::max(t.kernel_ms, sh.kernel_ms);
     t.d2h_ms = std::max(t.d2h_ms, sh.d2h_ms);
-    for (int s = 0; s < RMPC_NUM_STAGES; ++s) prof[s] += sh.prof[s];
+    for (int s = 0; s < RMPC_NUM_STAGES; ++s) {
+      sum[s] += (double)sh.prof[s];
+      sq[s] += (double)sh.prof[RMPC_NUM_STAGES + s];
+    }
+    clock_khz = std::max(clock_khz, sh.clock_khz);
   }
   if (h.profile) {
+    // split of the kernel time by stage (cycles summed over agents), and the per-agent stage
+    // time statistics of TimingReport::mean_ms / std_ms (batch.cpp:67-77) from the SM clock
     double tot = 0;
-    for (int s = 0; s < RMPC_NUM_STAGES; ++s) tot += (double)prof[s];
-    if (tot > 0)
-      for (int s = 0; s < RMPC_NUM_STAGES; ++s) t.stage_ms[s] = t.kernel_ms * (double)prof[s] / tot;
+    for (int s = 0; s < RMPC_NUM_STAGES; ++s) tot += sum[s];
+    const double n = (double)h.n, cyc_ms = clock_khz > 0 ? 1.0 / clock_khz : 0.0;
+    for (int s = 0; s < RMPC_NUM_STAGES; ++s) {
+      if (tot > 0) t.stage_ms[s] = t.kernel_ms * sum[s] / tot;
+      const double mean = sum[s] / n;
+      t.stage_mean_ms[s] = mean * cyc_ms;
+      t.stage_std_ms[s] = std::sqrt(std::max(0.0, sq[s] / n - mean * mean)) * cyc_ms;
+    }
   }
+}
+
+// One launch of the fused kernel for `n` device-resident agents of shard `sh` on `stream`
+// (NULL = the legacy default stream, as every other device entry point of the library).
+int32_t launch_device(rmpc_handle& h, Shard& sh, int n, const rmpc_state* d_states, const rmpc_command* d_cmds,
+                      const rmpc_gait* d_gaits, const rmpc_solution* d_prev, const float* d_prev_z,
+                      rmpc_solution* d_out, float* d_z, uint8_t* d_active, void* stream) {
+  if (cudaSetDevice(sh.device) != cudaSuccess) {
+    cudaGetLastError();
+    h.err = "cudaSetDevice failed";
+    return RMPC_ERR_CUDA;
+  }
+  rmpc_dev::KParams P = make_params(h);
+  P.n_agents = n;
+  P.states = d_states;
+  P.cmds = d_cmds;
+  P.gaits = d_gaits;
+  const bool use_prev = h.settings.warm_start && d_prev && d_prev_z && !d_active;
+  P.prev = use_prev ? d_prev : nullptr;
+  P.prev_z = use_prev ? d_prev_z : nullptr;
+  P.out = d_out;
+  P.z_out = d_z;
+  P.act_out = d_active;
+  P.prof = sh.d_prof;
+  P.profile = 0;
+  if (d_active) P.warm_start = 0;
+  const int rc = rmpc_launch_rti(P, stream);
+  if (rc != 0) {
+    h.err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+  }
+  return RMPC_OK;
 }
 
 }  // namespace
@@ -468,12 +577,14 @@ int32_t rmpc_create(const rmpc_model* model, const rmpc_settings* settings, int3
       return RMPC_ERR_CUDA;
     }
   }
+  if (G > 1) h->pool.reset(new ShardPool(G - 1));
   *out = h;
   return RMPC_OK;
 }
 
 void rmpc_destroy(rmpc_handle* h) {
   if (!h) return;
+  h->pool.reset();
   for (Shard& sh : h->shards) free_shard(sh);
   delete h;
 }
@@ -489,10 +600,10 @@ int32_t rmpc_solve(rmpc_handle* h, const rmpc_state* states, const rmpc_command*
   if (h->shards.size() == 1) {
     run_shard(*h, h->shards[0], states, cmds, gaits, prev, prev_z_star, out, z_star_out);
   } else {
-    std::vector<std::thread> pool;
-    for (Shard& sh : h->shards)
-      pool.emplace_back([&, ptr = &sh]() { run_shard(*h, *ptr, states, cmds, gaits, prev, prev_z_star, out, z_star_out); });
-    for (auto& t : pool) t.join();
+    const std::function<void(int)> job = [&](int g) {
+      run_shard(*h, h->shards[g], states, cmds, gaits, prev, prev_z_star, out, z_star_out);
+    };
+    h->pool->run(job);
   }
   const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
   for (const Shard& sh : h->shards)
@@ -505,27 +616,42 @@ int32_t rmpc_solve_device(rmpc_handle* h, const rmpc_state* d_states, const rmpc
                           const rmpc_gait* d_gaits, const rmpc_solution* d_prev, const float* d_prev_z_star,
                           rmpc_solution* d_out, float* d_z_star_out, void* stream) {
   if (!h) return RMPC_ERR_INVALID_ARG;
-  if (h->shards.size() != 1) { h->err = "rmpc_solve_device: single-device handles only"; return RMPC_ERR_INVALID_ARG; }
-  if (!d_states || !d_cmds || !d_gaits || !d_out) { h->err = "rmpc_solve_device: NULL array"; return RMPC_ERR_STRUCTURAL; }
-  Shard& sh = h->shards[0];
-  cudaSetDevice(sh.device);
-  rmpc_dev::KParams P = make_params(*h);
-  P.n_agents = h->n;
-  P.states = d_states;
-  P.cmds = d_cmds;
-  P.gaits = d_gaits;
-  const bool use_prev = h->settings.warm_start && d_prev && d_prev_z_star;
-  P.prev = use_prev ? d_prev : nullptr;
-  P.prev_z = use_prev ? d_prev_z_star : nullptr;
-  P.out = d_out;
-  P.z_out = d_z_star_out;
-  P.prof = sh.d_prof;
-  P.profile = 0;
-  const int rc = rmpc_launch_rti(P, stream ? stream : (void*)sh.stream);
-  if (rc != 0) {
-    h->err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
-    return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+  if (h->shards.size() != 1) {
+    h->err = "rmpc_solve_device: multi-device handle, use rmpc_solve_device_sharded";
+    return RMPC_ERR_INVALID_ARG;
   }
+  if (!d_states || !d_cmds || !d_gaits || !d_out) { h->err = "rmpc_solve_device: NULL array"; return RMPC_ERR_STRUCTURAL; }
+  return launch_device(*h, h->shards[0], h->n, d_states, d_cmds, d_gaits, d_prev, d_prev_z_star, d_out, d_z_star_out,
+                       nullptr, stream);
+}
+
+int32_t rmpc_solve_device_sharded(rmpc_handle* h, const rmpc_state* const* d_states, const rmpc_command* const* d_cmds,
+                                  const rmpc_gait* const* d_gaits, const rmpc_solution* const* d_prev,
+                                  const float* const* d_prev_z_star, rmpc_solution* const* d_out,
+                                  float* const* d_z_star_out, void* const* streams) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (!d_states || !d_cmds || !d_gaits || !d_out) { h->err = "rmpc_solve_device_sharded: NULL array"; return RMPC_ERR_STRUCTURAL; }
+  for (size_t g = 0; g < h->shards.size(); ++g) {
+    Shard& sh = h->shards[g];
+    if (sh.count == 0) continue;
+    if (!d_states[g] || !d_cmds[g] || !d_gaits[g] || !d_out[g]) {
+      h->err = "rmpc_solve_device_sharded: NULL array for shard " + std::to_string(g);
+      return RMPC_ERR_STRUCTURAL;
+    }
+    const int rc = launch_device(*h, sh, sh.count, d_states[g], d_cmds[g], d_gaits[g], d_prev ? d_prev[g] : nullptr,
+                                 d_prev_z_star ? d_prev_z_star[g] : nullptr, d_out[g],
+                                 d_z_star_out ? d_z_star_out[g] : nullptr, nullptr, streams ? streams[g] : nullptr);
+    if (rc != RMPC_OK) return rc;
+  }
+  return RMPC_OK;
+}
+
+int32_t rmpc_shard_info(const rmpc_handle* h, int32_t shard, int32_t* device, int32_t* begin, int32_t* count) {
+  if (!h || shard < 0 || shard >= (int32_t)h->shards.size()) return RMPC_ERR_INVALID_ARG;
+  const Shard& sh = h->shards[shard];
+  if (device) *device = sh.device;
+  if (begin) *begin = sh.begin;
+  if (count) *count = sh.count;
   return RMPC_OK;
 }
 
@@ -535,23 +661,8 @@ int32_t rmpc_solve_device_active_set(rmpc_handle* h, const rmpc_state* d_states,
   if (!h) return RMPC_ERR_INVALID_ARG;
   if (h->shards.size() != 1) { h->err = "rmpc_solve_device_active_set: single-device handles only"; return RMPC_ERR_INVALID_ARG; }
   if (!d_states || !d_cmds || !d_gaits || !d_out || !d_active) { h->err = "rmpc_solve_device_active_set: NULL array"; return RMPC_ERR_STRUCTURAL; }
-  Shard& sh = h->shards[0];
-  cudaSetDevice(sh.device);
-  rmpc_dev::KParams P = make_params(*h);
-  P.n_agents = h->n;
-  P.states = d_states;
-  P.cmds = d_cmds;
-  P.gaits = d_gaits;
-  P.out = d_out;
-  P.act_out = d_active;
-  P.prof = sh.d_prof;
-  P.warm_start = 0;
-  const int rc = rmpc_launch_rti(P, stream ? stream : (void*)sh.stream);
-  if (rc != 0) {
-    h->err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
-    return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
-  }
-  return RMPC_OK;
+  return launch_device(*h, h->shards[0], h->n, d_states, d_cmds, d_gaits, nullptr, nullptr, d_out, nullptr, d_active,
+                       stream);
 }
 
 int32_t rmpc_size(const rmpc_handle* h) { return h ? h->n : 0; }

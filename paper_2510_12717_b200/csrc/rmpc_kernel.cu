@@ -30,6 +30,8 @@
 #include <math.h>
 #include <stdint.h>
 
+#include <atomic>
+
 #include "rmpc_device.cuh"
 #include "rmpc_kin.cuh"
 
@@ -47,7 +49,11 @@ namespace rmpc_dev {
 __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage, long long& t0) {
   if (P.profile) {
     const long long t1 = clock64();
-    if (lane == 0) atomicAdd(P.prof + stage, (unsigned long long)(t1 - t0));
+    if (lane == 0) {
+      const unsigned long long d = (unsigned long long)(t1 - t0);
+      atomicAdd(P.prof + stage, d);
+      atomicAdd(P.prof + RMPC_NUM_STAGES + stage, d * d);
+    }
     t0 = t1;
   }
 }
@@ -291,11 +297,16 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   // Whole waves of full CTAs (one CTA per SM), then the remainder spread over the SMs at
   // ceil(R / SMs) agents per CTA: a partial wave of fewer agents per SM runs faster than a
   // partial wave of full CTAs on a subset of the SMs.
-  static int sms[64] = {0};
+  // SM count per device, cached; several host threads (one per shard) may launch at once
+  static std::atomic<int> sms[64];
   int dev = 0;
   cudaGetDevice(&dev);
-  if (dev < 64 && sms[dev] == 0) cudaDeviceGetAttribute(&sms[dev], cudaDevAttrMultiProcessorCount, dev);
-  const int nsm = dev < 64 && sms[dev] > 0 ? sms[dev] : 148;
+  int nsm = dev < 64 ? sms[dev].load(std::memory_order_relaxed) : 0;
+  if (nsm == 0) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    if (dev < 64) sms[dev].store(nsm, std::memory_order_relaxed);
+  }
   const int wave = nsm * c.agents;
   const int full_waves = P.n_agents / wave;
   const int rem = P.n_agents - full_waves * wave;

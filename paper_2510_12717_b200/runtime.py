@@ -29,7 +29,8 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_solve", "rmpc_solve_device", "rmpc_solve_device_active_set", "rmpc_size", "rmpc_workers", "rmpc_horizon",
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
-           "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak")
+           "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak",
+           "rmpc_solve_device_sharded", "rmpc_shard_info")
 
 
 class RmpcError(RuntimeError):
@@ -57,6 +58,10 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_solve_device.restype = _I
     L.rmpc_solve_device_active_set.argtypes = [_VP] * 7
     L.rmpc_solve_device_active_set.restype = _I
+    L.rmpc_solve_device_sharded.argtypes = [_VP] * 9
+    L.rmpc_solve_device_sharded.restype = _I
+    L.rmpc_shard_info.argtypes = [_VP, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]
+    L.rmpc_shard_info.restype = _I
     for f in ("rmpc_size", "rmpc_workers", "rmpc_horizon"):
         getattr(L, f).argtypes = [_VP]
         getattr(L, f).restype = _I
@@ -157,25 +162,35 @@ class BatchRunner:
     def solve(self, states, cmds, gaits, prev=None, order=None, *, want_z: bool = False,
               out: np.ndarray | None = None, z_out: np.ndarray | None = None):
         """BatchRunner::solve.  states (n,18), cmds (n,3), gaits (n,7) float64; prev =
-        (solutions, z_star) of the previous tick (read only when settings.warm_start).  `order`
-        is accepted for API parity: results never depend on processing order.  Returns
-        (solutions, z_star or None)."""
+        (solutions, z_star) of the previous tick (read only when settings.warm_start; z_star
+        (n, T, 26) float32 -- without it no agent is warm-started, the reference's fallback for
+        a prev without a valid plan, mpc.cpp:258).  `order` is accepted for API parity: results
+        never depend on processing order.  Returns (solutions, z_star or None)."""
         del order
         states, cmds, gaits = _arr(states, 18), _arr(cmds, 3), _arr(gaits, 7)
-        n = self._n
+        n, T = self._n, self.horizon
         if states.shape[0] != n or cmds.shape[0] != n or gaits.shape[0] != n:
             raise RmpcError(RMPC_ERR_STRUCTURAL, "BatchRunner::solve: input lengths != n_envs")
         if out is None:
             out = np.zeros(n, dtype=SOLUTION_DTYPE)
+        elif out.dtype != SOLUTION_DTYPE or out.shape != (n,) or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a contiguous SOLUTION_DTYPE array of length {n}")
         if want_z and z_out is None:
-            z_out = np.zeros((n, self.horizon, NV), dtype=np.float32)
+            z_out = np.zeros((n, T, NV), dtype=np.float32)
+        if z_out is not None and (z_out.dtype != np.float32 or z_out.shape != (n, T, NV)
+                                  or not z_out.flags["C_CONTIGUOUS"]):
+            raise ValueError(f"z_out must be a contiguous float32 array of shape ({n}, {T}, {NV})")
         pv = pz = None
         if prev is not None:
             psol, pzs = prev
             if len(psol) != n:
                 raise RmpcError(RMPC_ERR_STRUCTURAL, "BatchRunner::solve: prev length != n_envs")
-            pv = np.ascontiguousarray(psol, dtype=SOLUTION_DTYPE)
-            pz = np.ascontiguousarray(pzs, dtype=np.float32)
+            if pzs is not None:
+                pz = np.asarray(pzs)
+                if pz.dtype != np.float32 or pz.shape != (n, T, NV):
+                    raise ValueError(f"prev z_star must be float32 of shape ({n}, {T}, {NV})")
+                pz = np.ascontiguousarray(pz)
+                pv = np.ascontiguousarray(psol, dtype=SOLUTION_DTYPE)
         rc = self._lib.rmpc_solve(self._h, states.ctypes.data, cmds.ctypes.data, gaits.ctypes.data,
                                   pv.ctypes.data if pv is not None else None,
                                   pz.ctypes.data if pz is not None else None, out.ctypes.data,
@@ -184,21 +199,65 @@ class BatchRunner:
             self._err(rc)
         return out, z_out
 
+    @staticmethod
+    def _stream(stream, tensors):
+        """cudaStream_t for a launch: an explicit torch.cuda.Stream / int, else torch's current
+        stream of the tensors' device (so the launch is ordered after the torch ops that
+        produced them), else 0 = the legacy default stream."""
+        if stream is not None:
+            return stream if isinstance(stream, int) else stream.cuda_stream
+        for t in tensors:
+            if t is not None and not isinstance(t, int) and hasattr(t, "device"):
+                import torch
+                return torch.cuda.current_stream(t.device).cuda_stream
+        return 0
+
+    def _check_device(self, name, t, nbytes):
+        if t is None or isinstance(t, int):
+            return
+        if not t.is_cuda or not t.is_contiguous():
+            raise ValueError(f"{name} must be a contiguous CUDA tensor")
+        if t.numel() * t.element_size() < nbytes:
+            raise ValueError(f"{name} holds {t.numel() * t.element_size()} bytes, needs {nbytes}")
+
     def solve_device(self, states, cmds, gaits, out, z_out=None, prev=None, prev_z=None,
                      stream=None):
         """Device-resident solve: arguments are CUDA tensors (or raw device pointers) on this
-        runner's device; enqueued on `stream` (torch.cuda.Stream / cudaStream_t int), no sync."""
+        runner's device; enqueued on `stream` (default: torch's current stream), no sync."""
         def p(t):
             if t is None:
                 return None
             return t if isinstance(t, int) else t.data_ptr()
-        s = None
-        if stream is not None:
-            s = stream if isinstance(stream, int) else stream.cuda_stream
-            if s == 0:
-                s = 1  # cudaStreamLegacy: NULL would select the runner's own stream
+        n, T = self._n, self.horizon
+        for name, t, nb in (("states", states, n * 144), ("cmds", cmds, n * 24), ("gaits", gaits, n * 56),
+                            ("out", out, n * SOLUTION_DTYPE.itemsize), ("z_out", z_out, n * T * NV * 4),
+                            ("prev", prev, n * SOLUTION_DTYPE.itemsize), ("prev_z", prev_z, n * T * NV * 4)):
+            self._check_device(name, t, nb)
+        s = self._stream(stream, (states, out))
         rc = self._lib.rmpc_solve_device(self._h, p(states), p(cmds), p(gaits), p(prev), p(prev_z),
                                          p(out), p(z_out), s)
+        if rc != 0:
+            self._err(rc)
+
+    def shard_info(self, g: int):
+        """(device, begin, count) of shard g (rmpc_shard_info)."""
+        d, b, c = _I(), _I(), _I()
+        rc = self._lib.rmpc_shard_info(self._h, g, C.byref(d), C.byref(b), C.byref(c))
+        if rc != 0:
+            self._err(rc)
+        return d.value, b.value, c.value
+
+    def solve_device_sharded(self, states, cmds, gaits, out, z_out=None, streams=None):
+        """Multi-device handle: per shard g lists of CUDA tensors on shard g's device holding its
+        `count` agents (rmpc_solve_device_sharded); streams[g] default: torch's current stream."""
+        G = self.workers()
+        P = C.c_void_p * G
+
+        def arr(ts):
+            return None if ts is None else P(*[None if t is None else t.data_ptr() for t in ts])
+        ss = P(*[self._stream(None if streams is None else streams[g], (states[g],)) for g in range(G)])
+        rc = self._lib.rmpc_solve_device_sharded(self._h, arr(states), arr(cmds), arr(gaits), None, None,
+                                                 arr(out), arr(z_out), ss)
         if rc != 0:
             self._err(rc)
 
@@ -207,11 +266,7 @@ class BatchRunner:
         tensor of n x (T+1) x 40 codes (0 inactive, 1 at lo, 2 at hi, 3 equality / no row)."""
         def p(t):
             return t if isinstance(t, int) else t.data_ptr()
-        s = None
-        if stream is not None:
-            s = stream if isinstance(stream, int) else stream.cuda_stream
-            if s == 0:
-                s = 1
+        s = self._stream(stream, (states, out))
         rc = self._lib.rmpc_solve_device_active_set(self._h, p(states), p(cmds), p(gaits), p(out), p(active), s)
         if rc != 0:
             self._err(rc)
@@ -224,7 +279,9 @@ class BatchRunner:
         self._lib.rmpc_last_timing(self._h, C.byref(t))
         return dict(batch_size=t.batch_size, devices=t.devices, total_ms=t.total_ms,
                     h2d_ms=t.h2d_ms, kernel_ms=t.kernel_ms, d2h_ms=t.d2h_ms,
-                    stage_ms=dict(zip(STAGE_NAMES, list(t.stage_ms))))
+                    stage_ms=dict(zip(STAGE_NAMES, list(t.stage_ms))),
+                    stage_mean_ms=dict(zip(STAGE_NAMES, list(t.stage_mean_ms))),
+                    stage_std_ms=dict(zip(STAGE_NAMES, list(t.stage_std_ms))))
 
     def mpc_torque(self, solution, state) -> np.ndarray:
         """mpc_torque (mpc.cpp:340-344): PD + feed-forward, clamped; raises on a failed solve."""

@@ -1,26 +1,40 @@
-"""Parity metrics between the CUDA solver (FP32 records) and the FP64 CPU oracle.
+"""Parity metrics between the CUDA solver (FP32 records) and the FP64 CPU checkers (the
+restated oracle, oracle/, or the reference built from its own sources, oracle/_ref).
 
-Tolerances (north star, BASELINE.json): relative error <= 1e-4 in FP32 for
-  * tau_ff and F*[0]: max |gpu - ref| / max(max|ref|, floor), floors 1 N m and 1 N (a near-zero
-    torque vector has no meaningful relative error);
-  * V_MPC: |gpu - ref| / (|1/2 x^T P x| + |q^T x|): the objective is a difference of two terms
-    that can cancel to 1e-5 of their size (tools/precision_study.py), so its error is measured
-    against the size of the terms it is computed from.
+North star (BASELINE.json): relative error <= 1e-4 in FP32 of torques, forces and the QP
+objective.  Every metric is a per-agent relative error with an explicit absolute floor (a
+quantity near zero has no meaningful relative error); the floors are physical scales:
+  * tau_ff, F*[0], base_residual: max_k |gpu - ref| / max(max_k |ref|, 1)   (1 N m, 1 N)
+  * V_MPC ("v"):  |gpu - ref| / max(|ref|, 1)  -- the plain relative error of the objective
+    with a 1-unit floor (V is O(1..30) on the walking batches; standing gives V = 0 exactly)
+  * V_MPC ("v_terms", reported only): |gpu - ref| / (|1/2 x^T P x| + |q^T x|), the error
+    against the size of the two terms V is the difference of (oracle records only)
+  * prim_res, dual_res (unscaled ||Ax - z||_inf, ||Px + q + A^T y||_inf after the fixed 25
+    iterations, qp.cpp:192-200): |gpu - ref| / max(|ref|, RES_FLOOR).  25 ADMM iterations
+    stop far from convergence (prim_res 1..20), and both are max-norms over hundreds of rows
+    computed from FP32 iterates, so their bar is RES_TOL (stated, looser than 1e-4).
+  * delta_inf_norm (||dz||_inf): relative, floor 1e-3.
 """
 from __future__ import annotations
 
 import numpy as np
 
-TOL = 1e-4
+TOL = 1e-4          # tau_ff, F*[0], V_MPC, base_residual
+RES_TOL = 1e-3      # prim_res, dual_res
+RES_FLOOR = 1e-2
+V_FLOOR = 1.0
 
 
 def rel_vec(gpu, ref, floor):
     gpu = np.asarray(gpu, dtype=np.float64)
     ref = np.asarray(ref, dtype=np.float64)
+    if gpu.ndim == 1:
+        gpu, ref = gpu[:, None], ref[:, None]
     return np.max(np.abs(gpu - ref), axis=-1) / np.maximum(np.max(np.abs(ref), axis=-1), floor)
 
 
 def v_err(gpu_sol, ref_sol):
+    """Term-scaled objective error (oracle records carry v_quad / v_lin)."""
     scale = np.abs(ref_sol["v_quad"]) + np.abs(ref_sol["v_lin"])
     return np.abs(gpu_sol["v_mpc"].astype(np.float64) - ref_sol["v_mpc"]) / np.maximum(scale, 1e-12)
 
@@ -30,21 +44,38 @@ def compare(gpu_sol, ref_sol, gpu_z=None, ref_z=None):
     ok = (gpu_sol["status"] == 0) & (ref_sol["status"] == 0)
     out = dict(
         status_equal=bool(np.all(gpu_sol["status"] == ref_sol["status"])),
+        fail_iter_equal=bool(np.all(gpu_sol["fail_iter"] == ref_sol["fail_iter"])),
         n_ok=int(ok.sum()),
         tau=rel_vec(gpu_sol["tau_ff"], ref_sol["tau_ff"], 1.0)[ok],
         f0=rel_vec(gpu_sol["f0"], ref_sol["f0"], 1.0)[ok],
-        v=v_err(gpu_sol, ref_sol)[ok],
+        v=rel_vec(gpu_sol["v_mpc"], ref_sol["v_mpc"], V_FLOOR)[ok],
+        base=rel_vec(gpu_sol["base_residual"], ref_sol["base_residual"], 1.0)[ok],
+        prim=rel_vec(gpu_sol["prim_res"], ref_sol["prim_res"], RES_FLOOR)[ok],
+        dual=rel_vec(gpu_sol["dual_res"], ref_sol["dual_res"], RES_FLOOR)[ok],
         q_set=np.max(np.abs(gpu_sol["q_set"] - ref_sol["q_set"]), axis=-1)[ok],
-        delta=rel_vec(gpu_sol["delta_inf_norm"][:, None], ref_sol["delta_inf_norm"][:, None], 1e-3)[ok],
+        qd_set=np.max(np.abs(gpu_sol["qd_set"] - ref_sol["qd_set"]), axis=-1)[ok],
+        delta=rel_vec(gpu_sol["delta_inf_norm"], ref_sol["delta_inf_norm"], 1e-3)[ok],
     )
+    if "v_quad" in ref_sol.dtype.names and np.all(np.isfinite(ref_sol["v_quad"][ok])):
+        out["v_terms"] = v_err(gpu_sol, ref_sol)[ok]
     if gpu_z is not None and ref_z is not None:
         out["z"] = np.max(np.abs(gpu_z.astype(np.float64) - ref_z), axis=(1, 2))[ok]
     return out
 
 
+GATES = (("tau", TOL), ("f0", TOL), ("v", TOL), ("base", TOL), ("prim", RES_TOL), ("dual", RES_TOL))
+
+
+def check(c, what=""):
+    """Assert every gated metric of compare() meets its tolerance."""
+    assert c["status_equal"], f"{what}: statuses differ"
+    for k, tol in GATES:
+        mx = float(c[k].max()) if c[k].size else 0.0
+        assert mx <= tol, f"{what}: {k} max rel err {mx:.3e} > {tol:g}"
+
+
 def summary(c) -> str:
     def mx(a):
         return float(a.max()) if a.size else 0.0
-    return (f"ok={c['n_ok']} tau={mx(c['tau']):.2e} f0={mx(c['f0']):.2e} v={mx(c['v']):.2e} "
-            f"q_set={mx(c['q_set']):.2e} delta={mx(c['delta']):.2e}" +
-            (f" z={mx(c['z']):.2e}" if "z" in c else ""))
+    keys = ("tau", "f0", "v", "base", "prim", "dual", "q_set", "delta") + tuple(k for k in ("v_terms", "z") if k in c)
+    return f"ok={c['n_ok']} " + " ".join(f"{k}={mx(c[k]):.2e}" for k in keys)

@@ -40,7 +40,8 @@ CASES = [
 def save(name, m, s, st, cm, ga, prev_z=None, prev_ok=None, extra=None):
     sol, z, _, _, _ = F.solve_batch(m, s, st, cm, ga, prev_z=prev_z, prev_ok=prev_ok, workers=1)
     arrays = dict(states=st, cmds=cm, gaits=ga, horizon=np.int32(s.horizon),
-                  warm_start=np.int32(s.warm_start), z=z, **{k: sol[k] for k in FIELDS})
+                  warm_start=np.int32(s.warm_start), mu=np.float64(s.mu), sigma=np.float64(s.sigma),
+                  w_f=np.array(s.w_f[:8]), z=z, **{k: sol[k] for k in FIELDS})
     if prev_z is not None:
         arrays.update(prev_z=prev_z, prev_ok=np.asarray(prev_ok, np.int32))
     if extra:
@@ -76,6 +77,16 @@ def main():
     st[1, 4] = np.nan
     cm[2, 1] = np.nan
     save("failures_T10", m, s, st, cm, ga)
+
+    # SingularityError (ldl.cpp:159-164): mu = 0 leaves the stance F_z of the last node touched
+    # only by explicit-zero friction entries; with sigma = 0 and w_f = 0 its KKT column is zero,
+    # so the factorization meets an exact zero pivot (the device: a singular 2x2 pivot block)
+    s = R.default_settings(10)
+    s.mu, s.sigma = 0.0, 0.0
+    for k in range(8):
+        s.w_f[k] = 0.0
+    st, cm, ga = R.synthetic_batch(4, "mixed", seed=18, model=m, settings=s, nominal=nominal)
+    save("singular_T10", m, s, st, cm, ga)
 
     # warm start: tick 2 from tick 1's z* (mpc.cpp:258-265), one agent with a failed prev
     s = R.default_settings(10)

@@ -4,7 +4,8 @@ restated oracle, oracle/, or the reference built from its own sources, oracle/_r
 North star (BASELINE.json): relative error <= 1e-4 in FP32 of torques, forces and the QP
 objective.  Every metric is a per-agent relative error with an explicit absolute floor (a
 quantity near zero has no meaningful relative error); the floors are physical scales:
-  * tau_ff, F*[0], base_residual: max_k |gpu - ref| / max(max_k |ref|, 1)   (1 N m, 1 N)
+  * tau_ff, F*[0], base_residual: max_k |gpu - ref| / max(max_k |ref|, 1)   (1 N m, 1 N);
+    base_residual is gated at RES_TOL (see GATES)
   * V_MPC ("v"):  |gpu - ref| / max(|ref|, 1)  -- the plain relative error of the objective
     with a 1-unit floor (V is O(1..30) on the walking batches; standing gives V = 0 exactly)
   * V_MPC ("v_terms", reported only): |gpu - ref| / (|1/2 x^T P x| + |q^T x|), the error
@@ -19,8 +20,8 @@ from __future__ import annotations
 
 import numpy as np
 
-TOL = 1e-4          # tau_ff, F*[0], V_MPC, base_residual
-RES_TOL = 1e-3      # prim_res, dual_res
+TOL = 1e-4          # tau_ff, F*[0], V_MPC
+RES_TOL = 1e-3      # prim_res, dual_res, base_residual
 RES_FLOOR = 1e-2
 V_FLOOR = 1.0
 
@@ -56,14 +57,30 @@ def compare(gpu_sol, ref_sol, gpu_z=None, ref_z=None):
         qd_set=np.max(np.abs(gpu_sol["qd_set"] - ref_sol["qd_set"]), axis=-1)[ok],
         delta=rel_vec(gpu_sol["delta_inf_norm"], ref_sol["delta_inf_norm"], 1e-3)[ok],
     )
-    if "v_quad" in ref_sol.dtype.names and np.all(np.isfinite(ref_sol["v_quad"][ok])):
+    names = ref_sol.dtype.names if hasattr(ref_sol, "dtype") else tuple(ref_sol.keys())
+    if "v_quad" in names and np.all(np.isfinite(ref_sol["v_quad"][ok])):
         out["v_terms"] = v_err(gpu_sol, ref_sol)[ok]
     if gpu_z is not None and ref_z is not None:
         out["z"] = np.max(np.abs(gpu_z.astype(np.float64) - ref_z), axis=(1, 2))[ok]
     return out
 
 
-GATES = (("tau", TOL), ("f0", TOL), ("v", TOL), ("base", TOL), ("prim", RES_TOL), ("dual", RES_TOL))
+# base_residual (rows 0..2 of M qdd + h - J^T F at node 0, robot.cpp:211-233) is a residual of
+# the unconverged 25-iteration plan (10..25 N), computed from qdd = (qd*_1 - qd*_0) / dt: FP32
+# plan differences amplified by 1/dt = 20, so it is gated with the residuals.
+GATES = (("tau", TOL), ("f0", TOL), ("v", TOL), ("base", RES_TOL), ("prim", RES_TOL), ("dual", RES_TOL))
+
+
+def fixture_settings(g):
+    """MpcSettings of a tests/golden/ref_*.npz fixture."""
+    from paper_2510_12717_b200.abi import default_settings
+    s = default_settings(int(g["horizon"]))
+    s.warm_start = int(g["warm_start"])
+    if "mu" in g.files:
+        s.mu, s.sigma = float(g["mu"]), float(g["sigma"])
+        for k in range(8):
+            s.w_f[k] = float(g["w_f"][k])
+    return s
 
 
 def check(c, what=""):

@@ -10,7 +10,7 @@ import numpy as np
 import pytest
 
 import paper_2510_12717_b200 as R
-from parity import check, compare, summary
+from parity import check, compare, fixture_settings, summary
 
 pytestmark = pytest.mark.gpu
 HERE = os.path.dirname(os.path.abspath(__file__))
@@ -21,8 +21,7 @@ FILES = sorted(glob.glob(os.path.join(HERE, "golden", "ref_*.npz")))
 def test_device_matches_reference_outputs(path):
     g = np.load(path)
     m = R.default_model()
-    s = R.default_settings(int(g["horizon"]))
-    s.warm_start = int(g["warm_start"])
+    s = fixture_settings(g)
     n = g["states"].shape[0]
     prev = None
     if "prev_z" in g.files:

@@ -16,7 +16,7 @@ ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 sys.path.insert(0, ROOT)
 sys.path.insert(0, os.path.join(ROOT, "tests"))
 import paper_2510_12717_b200 as R  # noqa: E402
-from parity import compare  # noqa: E402
+from parity import compare, fixture_settings  # noqa: E402
 
 
 def stats(c):
@@ -33,8 +33,7 @@ def main():
     m = R.default_model()
     for f in sorted(glob.glob(os.path.join(ROOT, "tests", "golden", "ref_*.npz"))):
         g = np.load(f)
-        s = R.default_settings(int(g["horizon"]))
-        s.warm_start = int(g["warm_start"])
+        s = fixture_settings(g)
         n = g["states"].shape[0]
         br = R.BatchRunner(n, m, s)
         prev = None

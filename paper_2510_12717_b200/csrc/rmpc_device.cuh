@@ -94,8 +94,40 @@ struct KParams {
   rmpc_solution* out;
   float* z_out;
   uint8_t* act_out;  // optional: final active set, (T+1) x NSLOT codes per agent
-  unsigned long long* prof;  // [RMPC_NUM_STAGES] cycle accumulators (profile only)
+  unsigned long long* prof;  // [2 RMPC_NUM_STAGES] cycle sums and sums of squares (profile only)
+  // Schedule-shared factorization (cold start).  With warm_start off, the QP
+  // matrices, the Ruiz scaling and the factor depend only on the contact schedule (the stance
+  // flags of every node), so they are computed once per distinct schedule (mode 1, one warp
+  // pair per schedule) into `store` and loaded by every agent of that schedule (mode 0).
+  int32_t mode;              // 0 solve, 1 build the schedule store (no ADMM, no outputs)
+  int32_t store_cap;         // schedules the store holds; ids >= cap solve unshared
+  int32_t store_stride;      // floats per schedule (store_layout)
+  int32_t pad2_;
+  const int32_t* slot_of;    // mode 0: hash slot of each agent's schedule, -1 = unshared
+  const int32_t* slot_id;    // hash slot -> schedule id (-1 = over capacity)
+  const int32_t* rep_list;   // mode 1: the agent that represents schedule id
+  const int32_t* n_sched;    // mode 1: number of schedule ids
+  float* store;
 };
+
+// One schedule's entry in the store (floats, 16-byte aligned regions): the Ruiz-scaled
+// coefficient blocks (incl. the G_dd entries of the factorization), the column scales e, the
+// row scales d, the stance flags + factorization status, and the factor's node blocks as
+// TMEM rows (32 lanes x 32 columns per node).
+struct StoreLayout {
+  int coef, e, d, flags, blocks, total;
+};
+__host__ __device__ inline StoreLayout store_layout(int NT) {
+  StoreLayout L;
+  int o = 0;
+  L.coef = o;   o += ((NT + 1) * C_SIZE + 3) & ~3;
+  L.e = o;      o += (NT * NV + 3) & ~3;
+  L.d = o;      o += ((NT + 1) * NSLOT + 3) & ~3;
+  L.flags = o;  o += (NT + 1 + 3) & ~3;  // NT flag words, then the status word (1 = factor ok)
+  L.blocks = o; o += NT * 32 * TCOLS;
+  L.total = o;
+  return L;
+}
 
 // Shared-memory footprint of one agent (warp pair) in floats, every region 16-byte aligned.
 struct Layout {
@@ -178,4 +210,20 @@ inline CtaShape cta_shape(int NT) {
 // Launch the fused kernel for params.n_agents agents on `stream` (implemented in
 // rmpc_kernel.cu).  Returns a cudaError_t value.
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream);
+
+// Device buffers of the schedule-shared path, per shard (rmpc_host.cu allocates them).
+struct RmpcSchedBuffers {
+  unsigned long long* table;  // open-addressing hash of schedule keys, `slots` entries
+  int32_t* slot_id;           // per slot: schedule id
+  int32_t* slot_of;           // per agent: slot, -1 = unshared
+  int32_t* rep_list;          // per schedule id: representative agent
+  int32_t* n_sched;           // schedule count
+  float* store;               // cap x store_layout(T).total floats
+  int32_t slots, cap, agents;
+};
+// Schedule pass for params.n_agents agents (cold start only): clear the table, hash every
+// agent's stance schedule, then build the store (mode 1) -- three launches on `stream`.
+// On return params_out is params with the lookup fields set for the solve launch.
+int rmpc_launch_sched(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream,
+                      rmpc_dev::KParams* params_out);
 int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory

@@ -25,6 +25,7 @@
 namespace {
 
 thread_local std::string g_create_error;
+constexpr size_t kSchedCap = 1024;  // distinct schedules stored per shard and tick
 
 struct Shard {
   int device = 0;
@@ -40,6 +41,8 @@ struct Shard {
   rmpc_solution* d_out = nullptr;
   float* d_z = nullptr;
   unsigned long long* d_prof = nullptr;
+  RmpcSchedBuffers sched = {};  // schedule-shared factorization workspace
+  cudaEvent_t ev_sched = nullptr;
   // pinned staging for pageable caller buffers
   char* h_stage_in = nullptr;
   char* h_stage_out = nullptr;
@@ -122,6 +125,7 @@ struct rmpc_handle {
   rmpc_timing timing;
   std::string err;
   int profile = 0;
+  int share = 1;  // schedule-shared factorization for cold-start solves
   std::unique_ptr<ShardPool> pool;  // shards >= 2 only
 };
 
@@ -248,6 +252,19 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
   sh.stage_out_bytes = n * sizeof(rmpc_solution) + zn * sizeof(float) + 2 * 256;
   CK(cudaMallocHost(&sh.h_stage_in, sh.stage_in_bytes));
   CK(cudaMallocHost(&sh.h_stage_out, sh.stage_out_bytes));
+  // schedule pass: a hash table of >= 2n slots, up to kSchedCap distinct schedules stored
+  RmpcSchedBuffers& sb = sh.sched;
+  sb.agents = (int)n;
+  sb.slots = 64;
+  while (sb.slots < 2 * (int)n) sb.slots *= 2;
+  sb.cap = (int)std::min<size_t>(n, kSchedCap);
+  CK(cudaMalloc(&sb.table, (size_t)sb.slots * sizeof(unsigned long long)));
+  CK(cudaMalloc(&sb.slot_id, (size_t)sb.slots * sizeof(int32_t)));
+  CK(cudaMalloc(&sb.slot_of, n * sizeof(int32_t)));
+  CK(cudaMalloc(&sb.rep_list, (size_t)sb.cap * sizeof(int32_t)));
+  CK(cudaMalloc(&sb.n_sched, sizeof(int32_t)));
+  CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
+  CK(cudaEventCreateWithFlags(&sh.ev_sched, cudaEventDisableTiming));
   const int rc = rmpc_kernel_setup(rmpc_dev::MAXT);
   if (rc != 0) {
     sh.err = RMPC_ERR_CUDA;
@@ -262,6 +279,9 @@ void free_shard(Shard& sh) {
   cudaFree(sh.d_states); cudaFree(sh.d_cmds); cudaFree(sh.d_gaits); cudaFree(sh.d_prev);
   cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof);
   cudaFreeHost(sh.h_stage_in); cudaFreeHost(sh.h_stage_out);
+  cudaFree(sh.sched.table); cudaFree(sh.sched.slot_id); cudaFree(sh.sched.slot_of);
+  cudaFree(sh.sched.rep_list); cudaFree(sh.sched.n_sched); cudaFree(sh.sched.store);
+  if (sh.ev_sched) cudaEventDestroy(sh.ev_sched);
   for (auto& e : sh.ev) if (e) cudaEventDestroy(e);
   if (sh.stream) cudaStreamDestroy(sh.stream);
   if (sh.stream2) cudaStreamDestroy(sh.stream2);
@@ -327,14 +347,40 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
                      : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
   CK(cudaEventRecord(sh.ev[0], ss[0]));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
-  if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
+  // cold start with schedule sharing: every input first, then the schedule pass over the whole
+  // shard (it needs every agent's gait), then the chunks' solve kernels read its store
+  const bool share = h.share && !h.settings.warm_start;
+  rmpc_dev::KParams PS;
+  if (share) {
+    for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, n * c.elem, cudaMemcpyHostToDevice, ss[0]));
+    CK(cudaEventRecord(sh.ev[1], ss[0]));
+    rmpc_dev::KParams P0 = make_params(h);
+    P0.n_agents = (int)n;
+    P0.states = sh.d_states;
+    P0.cmds = sh.d_cmds;
+    P0.gaits = sh.d_gaits;
+    const int rc = rmpc_launch_sched(P0, sh.sched, ss[0], &PS);
+    if (rc != 0) {
+      sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+      sh.msg = std::string("schedule pass: ") + cudaGetErrorString((cudaError_t)rc);
+      cudaStreamSynchronize(ss[0]);
+      return;
+    }
+    CK(cudaEventRecord(sh.ev_sched, ss[0]));
+    if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev_sched, 0));
+  } else if (nchunks > 1) {
+    CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
+  }
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
     const size_t lo = cut[k], m = cut[k + 1] - cut[k];
-    for (const In& c : ins)
-      CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
-    if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
-    rmpc_dev::KParams P = make_params(h);
+    if (!share) {
+      for (const In& c : ins)
+        CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
+      if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
+    }
+    rmpc_dev::KParams P = share ? PS : make_params(h);
+    if (share) P.slot_of = PS.slot_of + lo;
     P.n_agents = (int)m;
     P.states = sh.d_states + lo;
     P.cmds = sh.d_cmds + lo;
@@ -439,6 +485,13 @@ int32_t launch_device(rmpc_handle& h, Shard& sh, int n, const rmpc_state* d_stat
   P.prof = sh.d_prof;
   P.profile = 0;
   if (d_active) P.warm_start = 0;
+  if (h.share && !P.warm_start) {  // cold start: the schedule pass, then the solve reads its store
+    const int rs = rmpc_launch_sched(P, sh.sched, stream, &P);
+    if (rs != 0) {
+      h.err = std::string("schedule pass: ") + cudaGetErrorString((cudaError_t)rs);
+      return rs == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+    }
+  }
   const int rc = rmpc_launch_rti(P, stream);
   if (rc != 0) {
     h.err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -702,6 +755,12 @@ int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol, const
                      model->kd[j] * ((double)sol->qd_set[j] - state->qd[3 + j]) + (double)sol->tau_ff[j];
     tau_out[j] = std::min(std::max(t, -model->tau_limit[j]), model->tau_limit[j]);
   }
+  return RMPC_OK;
+}
+
+int32_t rmpc_set_schedule_sharing(rmpc_handle* h, int32_t enabled) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  h->share = enabled ? 1 : 0;
   return RMPC_OK;
 }
 

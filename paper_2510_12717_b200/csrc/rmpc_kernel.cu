@@ -58,11 +58,77 @@ __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage,
   }
 }
 
+// ------------------------------------------------------------------------- schedule store
+// Mode 1: after the factorization of a schedule's representative agent, copy everything the
+// rest of the solve reads from the schedule-dependent part -- the scaled coefficient blocks
+// (with the G_dd entries factorize left in them), e, d, the stance flags and the factor's
+// node blocks (each warp its own, as TMEM rows) -- into the store entry `st`.
+__device__ void dump_schedule(const KParams& P, const Sm& sm, float* st, int lane, int warp, int status) {
+  const int NT = P.NT, tid = warp * 32 + lane;
+  const StoreLayout SL = store_layout(NT);
+  const float4* c4 = reinterpret_cast<const float4*>(sm.coef);
+  float4* o4 = reinterpret_cast<float4*>(st + SL.coef);
+  for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += 64) o4[k] = c4[k];
+  const float4* d4 = reinterpret_cast<const float4*>(sm.dsc);
+  float4* od = reinterpret_cast<float4*>(st + SL.d);
+  for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) od[k] = d4[k];
+  for (int k = tid; k < NT * NV; k += 64) st[SL.e + k] = sm.V(k / NV, V_E)[k % NV];
+  int32_t* fl = reinterpret_cast<int32_t*>(st + SL.flags);
+  for (int i = tid; i < NT; i += 64) fl[i] = (int32_t)sm.flags[i];
+  if (tid == 0) fl[NT] = status;
+  const int m = sm.mid;
+  for (int i = warp == 0 ? 0 : m + 1; i <= (warp == 0 ? m : NT - 1); ++i) {
+    float v[TCOLS];
+    blk_load(sm, i, lane, v);
+    float4* r = reinterpret_cast<float4*>(st + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
+#pragma unroll
+    for (int q = 0; q < TCOLS / 4; ++q) r[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+// Mode 0, shared schedule: load the entry instead of Ruiz + scaling + factorize, and scale this
+// agent's bounds and q by d / e exactly as apply_scaling does.  Returns the factorization
+// status (1 ok, 0 singular).  The results are bit-identical to the agent's own factorization.
+__device__ int load_schedule(const KParams& P, const Sm& sm, const float* st, int lane, int warp) {
+  const int NT = P.NT, tid = warp * 32 + lane;
+  const StoreLayout SL = store_layout(NT);
+  const float4* c4 = reinterpret_cast<const float4*>(st + SL.coef);
+  float4* s4 = reinterpret_cast<float4*>(sm.coef);
+  for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += 64) s4[k] = c4[k];
+  const float4* d4 = reinterpret_cast<const float4*>(st + SL.d);
+  float4* sd = reinterpret_cast<float4*>(sm.dsc);
+  for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) sd[k] = d4[k];
+  for (int k = tid; k < NT * NV; k += 64) sm.V(k / NV, V_E)[k % NV] = st[SL.e + k];
+  const int m = sm.mid;
+  for (int i = warp == 0 ? 0 : m + 1; i <= (warp == 0 ? m : NT - 1); ++i) {
+    const float4* r = reinterpret_cast<const float4*>(st + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
+    float v[TCOLS];
+#pragma unroll
+    for (int q = 0; q < TCOLS / 4; ++q) {
+      const float4 w = r[q];
+      v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
+    }
+    blk_store(sm, i, lane, v);
+  }
+  pair_sync(sm);
+  for (int i = warp; i < NT; i += 2)
+    if (lane < NV) sm.V(i, V_QH)[lane] *= sm.V(i, V_E)[lane];
+  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
+    float4 rd = sm.row[r];
+    const float dr = sm.dsc[r];
+    rd.x *= dr;
+    rd.y *= dr;
+    sm.row[r] = rd;
+  }
+  pair_sync(sm);
+  return reinterpret_cast<const int32_t*>(st + SL.flags)[NT];
+}
+
 // One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
-// blocks at `tm`, named barrier `bar`.
+// blocks at `tm`, named barrier `bar`.  `sched` is the schedule id the pair builds in mode 1.
 template <bool SPILL>
 __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int tmn, int bar,
-                                            int agent, int lane, int warp) {
+                                            int agent, int sched, int lane, int warp) {
   const int NT = P.NT;
   const Layout L = make_layout(NT, P.spill_nodes);
   Sm sm;
@@ -122,13 +188,41 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
                   : setup_dynamics(P, sm, lane, st, cmd, gait, warm, pz)) && st_ok;
   ok = pair_and(sm, ok);
   prof_mark(P, tid, 2, t0);
+  if (P.mode == 1 && !ok) {  // cannot happen for a representative (finite inputs); unshared
+    if (tid == 0) reinterpret_cast<int32_t*>(P.store + (size_t)sched * P.store_stride + store_layout(NT).flags)[NT] = -1;
+    return;
+  }
   if (!ok) {
     out.status = RMPC_STATUS_NONFINITE_INPUT;
   } else {
-    if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
-    apply_scaling(P, sm, lane, warp);
-    prof_mark(P, tid, 3, t0);
-    const int good = factorize(P, sm, lane, warp);
+    // the schedule's precomputed entry, if any (mode 0); a flag mismatch (hash collision) or an
+    // invalid entry falls back to the agent's own factorization
+    const float* entry = nullptr;
+    if (P.mode == 0 && P.slot_of != nullptr) {
+      const int sl = P.slot_of[agent];
+      const int sid = sl >= 0 ? P.slot_id[sl] : -1;
+      if (sid >= 0 && sid < P.store_cap) {
+        entry = P.store + (size_t)sid * P.store_stride;
+        const int32_t* fl = reinterpret_cast<const int32_t*>(entry + store_layout(NT).flags);
+        bool same = fl[NT] >= 0;
+        for (int i = tid; i < NT; i += 64) same = same && (uint32_t)fl[i] == sm.flags[i];
+        if (!pair_and(sm, same)) entry = nullptr;
+      }
+    }
+    int good;
+    if (entry != nullptr) {
+      good = load_schedule(P, sm, entry, lane, warp);
+      prof_mark(P, tid, 3, t0);
+    } else {
+      if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
+      apply_scaling(P, sm, lane, warp);
+      prof_mark(P, tid, 3, t0);
+      good = factorize(P, sm, lane, warp);
+      if (P.mode == 1) {
+        dump_schedule(P, sm, P.store + (size_t)sched * P.store_stride, lane, warp, good ? 1 : 0);
+        return;
+      }
+    }
     if (!good) {
       out.status = RMPC_STATUS_SINGULAR;
     } else {
@@ -259,15 +353,22 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   const uint32_t tb = tmem_base;
   const int pair = w >> 1;
   const int b = blockIdx.x;
-  const int agent = b < P.full_ctas ? b * P.agents_per_cta + pair
-                                    : (pair < P.tail_agents ? P.full_ctas * P.agents_per_cta +
-                                                                   (b - P.full_ctas) * P.tail_agents + pair
-                                                             : P.n_agents);
+  int agent, sched = -1;
+  if (P.mode == 1) {  // schedule store: pair -> schedule id -> its representative agent
+    sched = b * P.agents_per_cta + pair;
+    const int ns = min(*P.n_sched, P.store_cap);
+    agent = sched < ns ? P.rep_list[sched] : P.n_agents;
+  } else {
+    agent = b < P.full_ctas ? b * P.agents_per_cta + pair
+                            : (pair < P.tail_agents ? P.full_ctas * P.agents_per_cta +
+                                                           (b - P.full_ctas) * P.tail_agents + pair
+                                                     : P.n_agents);
+  }
   if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
-    solve_agent<SPILL>(P, smem + pair * make_layout(P.NT, P.spill_nodes).total, tm, tmn, 1 + pair, agent, lane,
-                       w & 1);
+    solve_agent<SPILL>(P, smem + pair * make_layout(P.NT, P.spill_nodes).total, tm, tmn, 1 + pair, agent, sched,
+                       lane, w & 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -285,6 +386,17 @@ int rmpc_kernel_setup(int) {
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS>, a, bytes);
   return rc;
+}
+
+static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st) {
+  if (grid <= 0) return 0;
+  if (c.dense)
+    rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+  else if (c.spill_nodes > 0)
+    rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+  else
+    rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+  return (int)cudaGetLastError();
 }
 
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
@@ -317,13 +429,102 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   }
   P.full_ctas = full_waves * nsm;
   P.tail_agents = tail;
-  const int grid = P.full_ctas + tail_ctas;
+  return launch_variant(P, c, P.full_ctas + tail_ctas, (cudaStream_t)stream);
+}
+
+namespace rmpc_dev {
+
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {  // splitmix64 finalizer
+  x ^= x >> 30;
+  x *= 0xbf58476d1ce4e5b9ull;
+  x ^= x >> 27;
+  x *= 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+
+// One thread per agent: the stance schedule (node_schedule, the same FP64 code the solve's setup
+// runs) as the hash key; the first agent to claim a key's slot becomes its representative and
+// draws the schedule id.  Agents with a non-finite input are left unshared (their own setup
+// reports the failure, as the reference's build_qp does).
+__global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= P.n_agents) return;
+  const rmpc_state st = P.states[a];
+  const rmpc_command cmd = P.cmds[a];
+  const rmpc_gait g = P.gaits[a];
+  bool fin = isfinite(cmd.height) && isfinite(cmd.vx) && isfinite(cmd.wpitch) && isfinite(g.phase) &&
+             isfinite(g.period) && isfinite(g.phase_switch);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) fin = fin && isfinite(st.q[k]) && isfinite(st.qd[k]);
+#pragma unroll
+  for (int c = 0; c < 4; ++c) fin = fin && isfinite(g.offsets[c]);
+  if (!fin) {
+    b.slot_of[a] = -1;
+    return;
+  }
+  unsigned long long k0 = 0, k1 = 0;  // 4 bits per node, nodes 0..15 and 16..31
+  for (int i = 0; i < P.NT; ++i) {
+    double sw[4];
+    const unsigned long long bits = node_schedule(P, g, i, sw);
+    if (i < 16) k0 |= bits << (4 * i); else k1 |= bits << (4 * (i - 16));
+  }
+  unsigned long long h = mix64(k0 ^ mix64(k1 + 0x9e3779b97f4a7c15ull));
+  if (h == ~0ull) h = ~0ull - 1;
+  unsigned int slot = (unsigned int)h & (unsigned int)(b.slots - 1);
+  for (;;) {
+    const unsigned long long prev = atomicCAS(b.table + slot, ~0ull, h);
+    if (prev == ~0ull) {
+      const int id = atomicAdd(b.n_sched, 1);
+      b.slot_id[slot] = id < b.cap ? id : -1;
+      if (id < b.cap) b.rep_list[id] = a;
+      break;
+    }
+    if (prev == h) break;
+    slot = (slot + 1) & (unsigned int)(b.slots - 1);
+  }
+  b.slot_of[a] = (int)slot;
+}
+
+}  // namespace rmpc_dev
+
+int rmpc_launch_sched(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream,
+                      rmpc_dev::KParams* params_out) {
+  *params_out = params;
+  if (params.n_agents <= 0 || params.n_agents > b.agents) return 0;
   const cudaStream_t st = (cudaStream_t)stream;
-  if (c.dense)
-    rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
-  else if (c.spill_nodes > 0)
-    rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
-  else
-    rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
-  return (int)cudaGetLastError();
+  int rc = (int)cudaMemsetAsync(b.table, 0xFF, (size_t)b.slots * sizeof(unsigned long long), st);
+  if (rc == 0) rc = (int)cudaMemsetAsync(b.n_sched, 0, sizeof(int32_t), st);
+  if (rc != 0) return rc;
+  rmpc_dev::sched_key_kernel<<<(params.n_agents + 255) / 256, 256, 0, st>>>(params, b);
+  rc = (int)cudaGetLastError();
+  if (rc != 0) return rc;
+  const rmpc_dev::CtaShape c = rmpc_dev::cta_shape(params.NT);
+  rmpc_dev::KParams F = params;
+  F.mode = 1;
+  F.rep_list = b.rep_list;
+  F.n_sched = b.n_sched;
+  F.store = b.store;
+  F.store_cap = b.cap;
+  F.store_stride = rmpc_dev::store_layout(params.NT).total;
+  F.slot_of = nullptr;
+  F.out = nullptr;
+  F.z_out = nullptr;
+  F.act_out = nullptr;
+  F.profile = 0;
+  F.agents_per_cta = c.agents;
+  F.spill_nodes = c.spill_nodes;
+  F.tmem_cols = c.tmem_cols;
+  const int grid = (b.cap + c.agents - 1) / c.agents;
+  F.full_ctas = grid;
+  F.tail_agents = 0;
+  rc = launch_variant(F, c, grid, st);
+  if (rc != 0) return rc;
+  rmpc_dev::KParams& P = *params_out;
+  P.mode = 0;
+  P.slot_of = b.slot_of;
+  P.slot_id = b.slot_id;
+  P.store = b.store;
+  P.store_cap = b.cap;
+  P.store_stride = F.store_stride;
+  return 0;
 }

@@ -30,7 +30,7 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
            "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak",
-           "rmpc_solve_device_sharded", "rmpc_shard_info")
+           "rmpc_solve_device_sharded", "rmpc_shard_info", "rmpc_set_schedule_sharing")
 
 
 class RmpcError(RuntimeError):
@@ -78,6 +78,8 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_mpc_torque.restype = _I
     L.rmpc_set_stage_profiling.argtypes = [_VP, _I]
     L.rmpc_set_stage_profiling.restype = _I
+    L.rmpc_set_schedule_sharing.argtypes = [_VP, _I]
+    L.rmpc_set_schedule_sharing.restype = _I
     L.rmpc_build_info.restype = C.c_char_p
     L.rmpc_smem_bytes.argtypes = [_I]
     L.rmpc_smem_bytes.restype = _I
@@ -273,6 +275,11 @@ class BatchRunner:
 
     def set_stage_profiling(self, enabled: bool = True):
         self._lib.rmpc_set_stage_profiling(self._h, int(enabled))
+
+    def set_schedule_sharing(self, enabled: bool = True):
+        """Cold-start solves factorize each distinct contact schedule once (default on);
+        results are bit-identical either way (rmpc_set_schedule_sharing)."""
+        self._lib.rmpc_set_schedule_sharing(self._h, int(enabled))
 
     def last_timing(self) -> dict:
         t = Timing()

@@ -321,3 +321,31 @@ def test_two_chunked_shards_on_one_device_match_one_shard():
     one, z1 = R.BatchRunner(n, m, s).solve(st, cm, ga, want_z=True)
     two, z2 = R.BatchRunner(n, m, s, devices=[0, 0]).solve(st, cm, ga, want_z=True)
     assert one.tobytes() == two.tobytes() and z1.tobytes() == z2.tobytes()
+
+
+@pytest.mark.parametrize("T,kind,n", [(10, "random", 4096), (10, "mixed", 2048), (5, "random", 2048),
+                                      (20, "mixed", 1024), (3, "mixed", 512), (12, "random", 999),
+                                      (32, "mixed", 64)])
+def test_schedule_sharing_is_bit_identical(T, kind, n):
+    """Cold start: the schedule-shared factorization (rmpc_set_schedule_sharing, default on)
+    gives exactly the per-agent result -- the matrices, Ruiz scales and factor depend only on
+    the stance schedule (mpc.cpp:266-276) -- including next to a failing agent, and on the
+    host (chunked) and device paths."""
+    import torch
+    m, s = default_model(), default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, kind, seed=T, model=m, settings=s)
+    st = st.copy()
+    st[5, 3] = np.nan
+    br = R.BatchRunner(n, m, s)
+    a, za = br.solve(st, cm, ga, want_z=True)
+    br.set_schedule_sharing(False)
+    b, zb = br.solve(st, cm, ga, want_z=True)
+    assert a.tobytes() == b.tobytes() and za.tobytes() == zb.tobytes()
+    assert a["status"][5] == STATUS_NONFINITE_INPUT
+    br.set_schedule_sharing(True)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    br.solve_device(*d, out)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == a.tobytes()

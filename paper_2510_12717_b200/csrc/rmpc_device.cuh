@@ -12,6 +12,7 @@
 #pragma once
 
 #include <stdint.h>
+#include <stdlib.h>
 
 #include "../../include/rmpc_b200.h"
 
@@ -103,11 +104,20 @@ struct KParams {
   int32_t store_cap;         // schedules the store holds; ids >= cap solve unshared
   int32_t store_stride;      // floats per schedule (store_layout)
   int32_t pad2_;
-  const int32_t* slot_of;    // mode 0: hash slot of each agent's schedule, -1 = unshared
+  const int32_t* slot_of;    // hash slot of each agent's schedule, -1 = unshared
   const int32_t* slot_id;    // hash slot -> schedule id (-1 = over capacity)
   const int32_t* rep_list;   // mode 1: the agent that represents schedule id
-  const int32_t* n_sched;    // mode 1: number of schedule ids
+  const int32_t* n_sched;    // number of schedule ids
   float* store;
+  // shared-schedule solve (rti_shared_kernel): agents grouped by schedule, each CTA serves up to
+  // agents_per_cta agents of one group; the rest run rti_kernel over an agent list
+  const int32_t* order;      // agent indices grouped by schedule
+  const int32_t* grp_cta;    // per schedule id: first CTA (prefix sum), [n_groups] = total
+  const int32_t* grp_first;  // per schedule id: first position in `order`
+  const int32_t* grp_count;  // per schedule id: agents
+  const int32_t* agent_list; // rti_kernel: solve these agents (NULL = 0..n_agents-1)
+  int32_t* n_list;           // its length (device); rti_shared_kernel appends fallbacks
+  int32_t* list_out;         // = agent_list, writable (fallbacks of rti_shared_kernel)
 };
 
 // One schedule's entry in the store (floats, 16-byte aligned regions): the Ruiz-scaled
@@ -115,7 +125,7 @@ struct KParams {
 // row scales d, the stance flags + factorization status, and the factor's node blocks as
 // TMEM rows (32 lanes x 32 columns per node).
 struct StoreLayout {
-  int coef, e, d, flags, blocks, total;
+  int coef, e, d, rows, flags, blocks, total;
 };
 __host__ __device__ inline StoreLayout store_layout(int NT) {
   StoreLayout L;
@@ -123,6 +133,7 @@ __host__ __device__ inline StoreLayout store_layout(int NT) {
   L.coef = o;   o += ((NT + 1) * C_SIZE + 3) & ~3;
   L.e = o;      o += (NT * NV + 3) & ~3;
   L.d = o;      o += ((NT + 1) * NSLOT + 3) & ~3;
+  L.rows = o;   o += (NT + 1) * NSLOT * 2;       // scaled {lo, hi} of the representative
   L.flags = o;  o += (NT + 1 + 3) & ~3;  // NT flag words, then the status word (1 = factor ok)
   L.blocks = o; o += NT * 32 * TCOLS;
   L.total = o;
@@ -205,25 +216,85 @@ inline CtaShape cta_shape(int NT) {
   return c;
 }
 
+// Shared-schedule CTA (rti_shared_kernel): one schedule's coefficients, d and flags once per
+// CTA, the factor once in TMEM (top-half node blocks in lane quarters 0 / 2, bottom half in
+// 1 / 3, read by every warp pair of the CTA); per agent only its vectors, rows and scratch.
+struct LayoutShared {
+  int coef, d, flags, cta_total;   // CTA region
+  int scr, vec, row, tt, bc, total;  // per agent
+};
+__host__ __device__ inline LayoutShared make_layout_shared(int NT) {
+  LayoutShared L;
+  int o = 0;
+  L.coef = o;  o += (NT + 1) * C_SIZE;
+  L.d = o;     o += (NT + 1) * NSLOT;
+  L.flags = o; o += align4(NT);
+  L.cta_total = o;
+  o = 0;
+  L.scr = o;   o += 256;                       // z* rows of nodes 0, 1 (FP64)
+  L.vec = o;   o += NT * V_NUM * V_STRIDE;
+  L.row = o;   o += 4 * (NT + 1) * NSLOT;
+  L.tt = o;    o += (NT + 1) * NSLOT;
+  L.bc = o;    o += 128;
+  L.total = o;
+  return L;
+}
+constexpr int SHARED_AGENTS = 8;  // rti_shared_kernel: up to 8 warp pairs (512 threads, 128 registers)
+struct CtaShapeShared {
+  int agents, tmem_cols, smem_bytes;
+};
+// Agents per shared-schedule CTA: 6 warp pairs under 168 registers (rti_shared_kernel<6>, no
+// spills) or 8 under a 128-register cap (<8>, spills in the ADMM loop).  Measured at 16 384
+// agents (tools/time_solve.py): 6 is faster for every horizon but T = 3 (within 2%), e.g.
+// T = 10: 3.67 vs 3.93 ms, T = 20: 6.75 vs 8.17 ms.  RMPC_SHARED_AGENTS=8 selects the other
+// variant (tuning experiments).
+inline int shared_agents_cap(int NT) {
+  (void)NT;
+  static const int env = [] {
+    const char* e = getenv("RMPC_SHARED_AGENTS");
+    return e ? atoi(e) : 0;
+  }();
+  return env == SHARED_AGENTS ? SHARED_AGENTS : MAX_AGENTS;
+}
+inline CtaShapeShared cta_shape_shared(int NT, int cap = SHARED_AGENTS) {
+  CtaShapeShared c;
+  const LayoutShared L = make_layout_shared(NT);
+  int A = cap;
+  while (A > 1 && (L.cta_total + A * L.total) * 4 > 227 * 1024 - 256) --A;
+  c.agents = A;
+  int cols = 32;
+  while (cols < nodes_per_warp(NT) * TCOLS) cols *= 2;
+  c.tmem_cols = cols;
+  c.smem_bytes = (L.cta_total + A * L.total) * 4;
+  return c;
+}
+
 }  // namespace rmpc_dev
 
 // Launch the fused kernel for params.n_agents agents on `stream` (implemented in
 // rmpc_kernel.cu).  Returns a cudaError_t value.
 int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream);
 
-// Device buffers of the schedule-shared path, per shard (rmpc_host.cu allocates them).
+// Device buffers of the schedule-shared path, one set per chunk of a shard (rmpc_host.cu).
 struct RmpcSchedBuffers {
   unsigned long long* table;  // open-addressing hash of schedule keys, `slots` entries
   int32_t* slot_id;           // per slot: schedule id
   int32_t* slot_of;           // per agent: slot, -1 = unshared
   int32_t* rep_list;          // per schedule id: representative agent
   int32_t* n_sched;           // schedule count
+  int32_t* cnt;               // per schedule id: agents (cap)
+  int32_t* pos;               // per agent: position within its group, -1 = unshared
+  int32_t* grp_cta;           // cap + 1
+  int32_t* grp_first;         // cap
+  int32_t* order;             // agents grouped by schedule
+  int32_t* ulist;             // unshared agents (and fallbacks)
+  int32_t* n_unshared;
   float* store;               // cap x store_layout(T).total floats
   int32_t slots, cap, agents;
 };
-// Schedule pass for params.n_agents agents (cold start only): clear the table, hash every
-// agent's stance schedule, then build the store (mode 1) -- three launches on `stream`.
-// On return params_out is params with the lookup fields set for the solve launch.
-int rmpc_launch_sched(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream,
-                      rmpc_dev::KParams* params_out);
+// The whole cold-start solve with schedule sharing for params.n_agents agents on `stream`:
+// hash every agent's stance schedule, build the store (one factorization per schedule), group
+// the agents by schedule, solve the groups (rti_shared_kernel: one schedule per CTA) and the
+// rest (rti_kernel over an agent list).  Seven launches plus memsets, no host synchronisation.
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream);
 int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory

@@ -41,8 +41,7 @@ struct Shard {
   rmpc_solution* d_out = nullptr;
   float* d_z = nullptr;
   unsigned long long* d_prof = nullptr;
-  RmpcSchedBuffers sched = {};  // schedule-shared factorization workspace
-  cudaEvent_t ev_sched = nullptr;
+  RmpcSchedBuffers sched[3] = {};  // schedule-shared workspace, one per chunk of a tick
   // pinned staging for pageable caller buffers
   char* h_stage_in = nullptr;
   char* h_stage_out = nullptr;
@@ -252,19 +251,27 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
   sh.stage_out_bytes = n * sizeof(rmpc_solution) + zn * sizeof(float) + 2 * 256;
   CK(cudaMallocHost(&sh.h_stage_in, sh.stage_in_bytes));
   CK(cudaMallocHost(&sh.h_stage_out, sh.stage_out_bytes));
-  // schedule pass: a hash table of >= 2n slots, up to kSchedCap distinct schedules stored
-  RmpcSchedBuffers& sb = sh.sched;
-  sb.agents = (int)n;
-  sb.slots = 64;
-  while (sb.slots < 2 * (int)n) sb.slots *= 2;
-  sb.cap = (int)std::min<size_t>(n, kSchedCap);
-  CK(cudaMalloc(&sb.table, (size_t)sb.slots * sizeof(unsigned long long)));
-  CK(cudaMalloc(&sb.slot_id, (size_t)sb.slots * sizeof(int32_t)));
-  CK(cudaMalloc(&sb.slot_of, n * sizeof(int32_t)));
-  CK(cudaMalloc(&sb.rep_list, (size_t)sb.cap * sizeof(int32_t)));
-  CK(cudaMalloc(&sb.n_sched, sizeof(int32_t)));
-  CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
-  CK(cudaEventCreateWithFlags(&sh.ev_sched, cudaEventDisableTiming));
+  // schedule-shared solves: per chunk a hash table of >= 2n slots and up to kSchedCap
+  // distinct schedules in the store
+  for (RmpcSchedBuffers& sb : sh.sched) {
+    sb.agents = (int)n;
+    sb.slots = 64;
+    while (sb.slots < 2 * (int)n) sb.slots *= 2;
+    sb.cap = (int)std::min<size_t>(n, kSchedCap);
+    CK(cudaMalloc(&sb.table, (size_t)sb.slots * sizeof(unsigned long long)));
+    CK(cudaMalloc(&sb.slot_id, (size_t)sb.slots * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.slot_of, n * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.pos, n * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.order, n * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.ulist, n * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.rep_list, (size_t)sb.cap * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.cnt, (size_t)sb.cap * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.grp_first, (size_t)sb.cap * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.grp_cta, ((size_t)sb.cap + 1) * sizeof(int32_t)));
+    CK(cudaMalloc(&sb.n_sched, sizeof(int32_t)));
+    CK(cudaMalloc(&sb.n_unshared, sizeof(int32_t)));
+    CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
+  }
   const int rc = rmpc_kernel_setup(rmpc_dev::MAXT);
   if (rc != 0) {
     sh.err = RMPC_ERR_CUDA;
@@ -279,9 +286,12 @@ void free_shard(Shard& sh) {
   cudaFree(sh.d_states); cudaFree(sh.d_cmds); cudaFree(sh.d_gaits); cudaFree(sh.d_prev);
   cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof);
   cudaFreeHost(sh.h_stage_in); cudaFreeHost(sh.h_stage_out);
-  cudaFree(sh.sched.table); cudaFree(sh.sched.slot_id); cudaFree(sh.sched.slot_of);
-  cudaFree(sh.sched.rep_list); cudaFree(sh.sched.n_sched); cudaFree(sh.sched.store);
-  if (sh.ev_sched) cudaEventDestroy(sh.ev_sched);
+  for (RmpcSchedBuffers& sb : sh.sched) {
+    for (void* p : {(void*)sb.table, (void*)sb.slot_id, (void*)sb.slot_of, (void*)sb.pos, (void*)sb.order,
+                    (void*)sb.ulist, (void*)sb.rep_list, (void*)sb.cnt, (void*)sb.grp_first, (void*)sb.grp_cta,
+                    (void*)sb.n_sched, (void*)sb.n_unshared, (void*)sb.store})
+      cudaFree(p);
+  }
   for (auto& e : sh.ev) if (e) cudaEventDestroy(e);
   if (sh.stream) cudaStreamDestroy(sh.stream);
   if (sh.stream2) cudaStreamDestroy(sh.stream2);
@@ -305,7 +315,9 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
   const bool use_prev = h.settings.warm_start && prev && prev_z;
   // chunks: the first wave, the remaining whole waves, the partial last wave (its D2H is the
   // only transfer left exposed at the end)
-  const size_t wave = (size_t)sh.sms * rmpc_dev::cta_shape(h.NT).agents;
+  const bool share_tick = h.share && !h.settings.warm_start;
+  const size_t wave = (size_t)sh.sms * (share_tick ? rmpc_dev::cta_shape_shared(h.NT, rmpc_dev::shared_agents_cap(h.NT)).agents
+                                                   : rmpc_dev::cta_shape(h.NT).agents);
   size_t cut[4] = {0, n, n, n};
   int nchunks = 1;
   if (n > 2 * wave && !h.profile) {
@@ -347,40 +359,17 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
                      : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
   CK(cudaEventRecord(sh.ev[0], ss[0]));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
-  // cold start with schedule sharing: every input first, then the schedule pass over the whole
-  // shard (it needs every agent's gait), then the chunks' solve kernels read its store
+  // cold start with schedule sharing: each chunk runs the whole shared solve (schedule pass,
+  // grouped solve, the rest) on its own workspace
   const bool share = h.share && !h.settings.warm_start;
-  rmpc_dev::KParams PS;
-  if (share) {
-    for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, n * c.elem, cudaMemcpyHostToDevice, ss[0]));
-    CK(cudaEventRecord(sh.ev[1], ss[0]));
-    rmpc_dev::KParams P0 = make_params(h);
-    P0.n_agents = (int)n;
-    P0.states = sh.d_states;
-    P0.cmds = sh.d_cmds;
-    P0.gaits = sh.d_gaits;
-    const int rc = rmpc_launch_sched(P0, sh.sched, ss[0], &PS);
-    if (rc != 0) {
-      sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
-      sh.msg = std::string("schedule pass: ") + cudaGetErrorString((cudaError_t)rc);
-      cudaStreamSynchronize(ss[0]);
-      return;
-    }
-    CK(cudaEventRecord(sh.ev_sched, ss[0]));
-    if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev_sched, 0));
-  } else if (nchunks > 1) {
-    CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
-  }
+  if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
     const size_t lo = cut[k], m = cut[k + 1] - cut[k];
-    if (!share) {
-      for (const In& c : ins)
-        CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
-      if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
-    }
-    rmpc_dev::KParams P = share ? PS : make_params(h);
-    if (share) P.slot_of = PS.slot_of + lo;
+    for (const In& c : ins)
+      CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
+    if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
+    rmpc_dev::KParams P = make_params(h);
     P.n_agents = (int)m;
     P.states = sh.d_states + lo;
     P.cmds = sh.d_cmds + lo;
@@ -390,7 +379,7 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
     P.out = sh.d_out + lo;
     P.z_out = z_out ? sh.d_z + lo * zrow : nullptr;
     P.prof = sh.d_prof;
-    const int rc = rmpc_launch_rti(P, st);
+    const int rc = share ? rmpc_launch_shared(P, sh.sched[k], st) : rmpc_launch_rti(P, st);
     if (rc != 0) {
       sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
       sh.msg = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -485,14 +474,8 @@ int32_t launch_device(rmpc_handle& h, Shard& sh, int n, const rmpc_state* d_stat
   P.prof = sh.d_prof;
   P.profile = 0;
   if (d_active) P.warm_start = 0;
-  if (h.share && !P.warm_start) {  // cold start: the schedule pass, then the solve reads its store
-    const int rs = rmpc_launch_sched(P, sh.sched, stream, &P);
-    if (rs != 0) {
-      h.err = std::string("schedule pass: ") + cudaGetErrorString((cudaError_t)rs);
-      return rs == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
-    }
-  }
-  const int rc = rmpc_launch_rti(P, stream);
+  const int rc = (h.share && !P.warm_start) ? rmpc_launch_shared(P, sh.sched[0], stream)  // cold start
+                                            : rmpc_launch_rti(P, stream);
   if (rc != 0) {
     h.err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
     return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;

@@ -58,183 +58,12 @@ __device__ __forceinline__ void prof_mark(const KParams& P, int lane, int stage,
   }
 }
 
-// ------------------------------------------------------------------------- schedule store
-// Mode 1: after the factorization of a schedule's representative agent, copy everything the
-// rest of the solve reads from the schedule-dependent part -- the scaled coefficient blocks
-// (with the G_dd entries factorize left in them), e, d, the stance flags and the factor's
-// node blocks (each warp its own, as TMEM rows) -- into the store entry `st`.
-__device__ void dump_schedule(const KParams& P, const Sm& sm, float* st, int lane, int warp, int status) {
-  const int NT = P.NT, tid = warp * 32 + lane;
-  const StoreLayout SL = store_layout(NT);
-  const float4* c4 = reinterpret_cast<const float4*>(sm.coef);
-  float4* o4 = reinterpret_cast<float4*>(st + SL.coef);
-  for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += 64) o4[k] = c4[k];
-  const float4* d4 = reinterpret_cast<const float4*>(sm.dsc);
-  float4* od = reinterpret_cast<float4*>(st + SL.d);
-  for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) od[k] = d4[k];
-  for (int k = tid; k < NT * NV; k += 64) st[SL.e + k] = sm.V(k / NV, V_E)[k % NV];
-  int32_t* fl = reinterpret_cast<int32_t*>(st + SL.flags);
-  for (int i = tid; i < NT; i += 64) fl[i] = (int32_t)sm.flags[i];
-  if (tid == 0) fl[NT] = status;
-  const int m = sm.mid;
-  for (int i = warp == 0 ? 0 : m + 1; i <= (warp == 0 ? m : NT - 1); ++i) {
-    float v[TCOLS];
-    blk_load(sm, i, lane, v);
-    float4* r = reinterpret_cast<float4*>(st + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
-#pragma unroll
-    for (int q = 0; q < TCOLS / 4; ++q) r[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
-  }
-}
-
-// Mode 0, shared schedule: load the entry instead of Ruiz + scaling + factorize, and scale this
-// agent's bounds and q by d / e exactly as apply_scaling does.  Returns the factorization
-// status (1 ok, 0 singular).  The results are bit-identical to the agent's own factorization.
-__device__ int load_schedule(const KParams& P, const Sm& sm, const float* st, int lane, int warp) {
-  const int NT = P.NT, tid = warp * 32 + lane;
-  const StoreLayout SL = store_layout(NT);
-  const float4* c4 = reinterpret_cast<const float4*>(st + SL.coef);
-  float4* s4 = reinterpret_cast<float4*>(sm.coef);
-  for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += 64) s4[k] = c4[k];
-  const float4* d4 = reinterpret_cast<const float4*>(st + SL.d);
-  float4* sd = reinterpret_cast<float4*>(sm.dsc);
-  for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) sd[k] = d4[k];
-  for (int k = tid; k < NT * NV; k += 64) sm.V(k / NV, V_E)[k % NV] = st[SL.e + k];
-  const int m = sm.mid;
-  for (int i = warp == 0 ? 0 : m + 1; i <= (warp == 0 ? m : NT - 1); ++i) {
-    const float4* r = reinterpret_cast<const float4*>(st + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
-    float v[TCOLS];
-#pragma unroll
-    for (int q = 0; q < TCOLS / 4; ++q) {
-      const float4 w = r[q];
-      v[4 * q] = w.x; v[4 * q + 1] = w.y; v[4 * q + 2] = w.z; v[4 * q + 3] = w.w;
-    }
-    blk_store(sm, i, lane, v);
-  }
-  pair_sync(sm);
-  for (int i = warp; i < NT; i += 2)
-    if (lane < NV) sm.V(i, V_QH)[lane] *= sm.V(i, V_E)[lane];
-  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
-    float4 rd = sm.row[r];
-    const float dr = sm.dsc[r];
-    rd.x *= dr;
-    rd.y *= dr;
-    sm.row[r] = rd;
-  }
-  pair_sync(sm);
-  return reinterpret_cast<const int32_t*>(st + SL.flags)[NT];
-}
-
-// One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
-// blocks at `tm`, named barrier `bar`.  `sched` is the schedule id the pair builds in mode 1.
-template <bool SPILL>
-__device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int tmn, int bar,
-                                            int agent, int sched, int lane, int warp) {
+// Residuals and objective on the unscaled problem (qp.cpp:192-200), z* = guess + dz and the
+// inverse dynamics at node 0 (mpc.cpp:305-330), the active set (optional), the record.
+__device__ __forceinline__ void finish_agent(const KParams& P, const Sm& sm, int agent, int lane, int warp,
+                                             rmpc_solution& out, const rmpc_state& st, const rmpc_command& cmd,
+                                             bool warm, const float* pz, long long& t0) {
   const int NT = P.NT;
-  const Layout L = make_layout(NT, P.spill_nodes);
-  Sm sm;
-  sm.scr = base + L.scr;
-  sm.coef = base + L.coef;
-  sm.vec = base + L.vec;
-  sm.row = reinterpret_cast<float4*>(base + L.row);
-  sm.tt = base + L.tt;
-  sm.dsc = base + L.dsc;
-  sm.bc = base + L.bc;
-  sm.flags = reinterpret_cast<uint32_t*>(base + L.flags);
-  sm.NT = NT;
-  sm.mid = mid_node(NT);
-  sm.tm = tm;
-  sm.tmn = tmn;
-  sm.spills = SPILL;
-  sm.spill = base + L.spill + warp * P.spill_nodes * SPILL_BLK;
-  sm.bar = bar;
-  const int tid = warp * 32 + lane;
-  long long t0 = P.profile ? clock64() : 0;
-
-  // zero coefficients (incl. block -1), rows, vectors; d = e = 1
-  for (int k = tid; k < (NT + 1) * C_SIZE; k += 64) sm.coef[k] = 0.f;
-  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
-    sm.row[r] = make_float4(0.f, 0.f, 0.f, 0.f);
-    sm.tt[r] = 0.f;
-    sm.dsc[r] = 1.f;
-  }
-  for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;
-  pair_sync(sm);
-  for (int i = warp; i < NT; i += 2)
-    if (lane < NV) sm.V(i, V_E)[lane] = 1.f;
-  sm.bc[tid] = 0.f;
-
-  const rmpc_state st = P.states[agent];
-  const rmpc_command cmd = P.cmds[agent];
-  const rmpc_gait gait = P.gaits[agent];
-  const bool warm = P.warm_start && P.prev != nullptr && P.prev_z != nullptr &&
-                    P.prev[agent].status == RMPC_STATUS_OK;
-  const float* pz = warm ? P.prev_z + (size_t)agent * NT * NV : nullptr;
-
-  rmpc_solution out;
-  {
-    float* o = reinterpret_cast<float*>(&out);
-    for (int k = 0; k < 33; ++k) o[k] = 0.f;
-    out.status = RMPC_STATUS_OK;
-    out.fail_iter = -1;
-  }
-  bool st_ok = true;
-#pragma unroll
-  for (int k = 0; k < 9; ++k) st_ok = st_ok && isfinite(st.q[k]) && isfinite(st.qd[k]);
-  prof_mark(P, tid, 0, t0);
-  pair_sync(sm);
-
-  int ok = 1;
-  ok = (warp == 0 ? setup_nodes(P, sm, lane, st, cmd, gait, warm, pz)
-                  : setup_dynamics(P, sm, lane, st, cmd, gait, warm, pz)) && st_ok;
-  ok = pair_and(sm, ok);
-  prof_mark(P, tid, 2, t0);
-  if (P.mode == 1 && !ok) {  // cannot happen for a representative (finite inputs); unshared
-    if (tid == 0) reinterpret_cast<int32_t*>(P.store + (size_t)sched * P.store_stride + store_layout(NT).flags)[NT] = -1;
-    return;
-  }
-  if (!ok) {
-    out.status = RMPC_STATUS_NONFINITE_INPUT;
-  } else {
-    // the schedule's precomputed entry, if any (mode 0); a flag mismatch (hash collision) or an
-    // invalid entry falls back to the agent's own factorization
-    const float* entry = nullptr;
-    if (P.mode == 0 && P.slot_of != nullptr) {
-      const int sl = P.slot_of[agent];
-      const int sid = sl >= 0 ? P.slot_id[sl] : -1;
-      if (sid >= 0 && sid < P.store_cap) {
-        entry = P.store + (size_t)sid * P.store_stride;
-        const int32_t* fl = reinterpret_cast<const int32_t*>(entry + store_layout(NT).flags);
-        bool same = fl[NT] >= 0;
-        for (int i = tid; i < NT; i += 64) same = same && (uint32_t)fl[i] == sm.flags[i];
-        if (!pair_and(sm, same)) entry = nullptr;
-      }
-    }
-    int good;
-    if (entry != nullptr) {
-      good = load_schedule(P, sm, entry, lane, warp);
-      prof_mark(P, tid, 3, t0);
-    } else {
-      if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
-      apply_scaling(P, sm, lane, warp);
-      prof_mark(P, tid, 3, t0);
-      good = factorize(P, sm, lane, warp);
-      if (P.mode == 1) {
-        dump_schedule(P, sm, P.store + (size_t)sched * P.store_stride, lane, warp, good ? 1 : 0);
-        return;
-      }
-    }
-    if (!good) {
-      out.status = RMPC_STATUS_SINGULAR;
-    } else {
-      prof_mark(P, tid, 4, t0);
-      const int bad_it = admm(P, sm, lane, warp);
-      prof_mark(P, tid, 5, t0);
-      if (bad_it >= 0) {
-        out.status = RMPC_STATUS_DIVERGED;
-        out.fail_iter = bad_it;
-      }
-    }
-  }
   if (out.status == RMPC_STATUS_OK) {  // (pair-uniform) residuals, objective, z*: nodes split
                                        // between the warps; inverse dynamics on warp 0
     // unscaled residuals (qp.cpp:192-200): prim = |A^x - z| / d, dual = |P^x + q^ + A^T y| / e
@@ -332,6 +161,130 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   if (lane == 0) P.out[agent] = out;
 }
 
+// ------------------------------------------------------------------------- schedule store
+// Mode 1: after the factorization of a schedule's representative agent, copy everything the
+// rest of the solve reads from the schedule-dependent part -- the scaled coefficient blocks
+// (with the G_dd entries factorize left in them), e, d, the stance flags and the factor's
+// node blocks (each warp its own, as TMEM rows) -- into the store entry `st`.
+__device__ void dump_schedule(const KParams& P, const Sm& sm, float* st, int lane, int warp, int status) {
+  const int NT = P.NT, tid = warp * 32 + lane;
+  const StoreLayout SL = store_layout(NT);
+  const float4* c4 = reinterpret_cast<const float4*>(sm.coef);
+  float4* o4 = reinterpret_cast<float4*>(st + SL.coef);
+  for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += 64) o4[k] = c4[k];
+  const float4* d4 = reinterpret_cast<const float4*>(sm.dsc);
+  float4* od = reinterpret_cast<float4*>(st + SL.d);
+  for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) od[k] = d4[k];
+  for (int k = tid; k < NT * NV; k += 64) st[SL.e + k] = sm.V(k / NV, V_E)[k % NV];
+  float2* rw = reinterpret_cast<float2*>(st + SL.rows);
+  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) rw[r] = make_float2(sm.row[r].x, sm.row[r].y);
+  int32_t* fl = reinterpret_cast<int32_t*>(st + SL.flags);
+  for (int i = tid; i < NT; i += 64) fl[i] = (int32_t)sm.flags[i];
+  if (tid == 0) fl[NT] = status;
+  const int m = sm.mid;
+  for (int i = warp == 0 ? 0 : m + 1; i <= (warp == 0 ? m : NT - 1); ++i) {
+    float v[TCOLS];
+    blk_load(sm, i, lane, v);
+    float4* r = reinterpret_cast<float4*>(st + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
+#pragma unroll
+    for (int q = 0; q < TCOLS / 4; ++q) r[q] = make_float4(v[4 * q], v[4 * q + 1], v[4 * q + 2], v[4 * q + 3]);
+  }
+}
+
+// One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
+// blocks at `tm`, named barrier `bar`.  `sched` is the schedule id the pair builds in mode 1.
+template <bool SPILL>
+__device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int tmn, int bar,
+                                            int agent, int sched, int lane, int warp) {
+  const int NT = P.NT;
+  const Layout L = make_layout(NT, P.spill_nodes);
+  Sm sm;
+  sm.scr = base + L.scr;
+  sm.coef = base + L.coef;
+  sm.vec = base + L.vec;
+  sm.row = reinterpret_cast<float4*>(base + L.row);
+  sm.tt = base + L.tt;
+  sm.dsc = base + L.dsc;
+  sm.bc = base + L.bc;
+  sm.flags = reinterpret_cast<uint32_t*>(base + L.flags);
+  sm.NT = NT;
+  sm.mid = mid_node(NT);
+  sm.tm = tm;
+  sm.tmn = tmn;
+  sm.spills = SPILL;
+  sm.spill = base + L.spill + warp * P.spill_nodes * SPILL_BLK;
+  sm.bar = bar;
+  const int tid = warp * 32 + lane;
+  long long t0 = P.profile ? clock64() : 0;
+
+  // zero coefficients (incl. block -1), rows, vectors; d = e = 1
+  for (int k = tid; k < (NT + 1) * C_SIZE; k += 64) sm.coef[k] = 0.f;
+  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
+    sm.row[r] = make_float4(0.f, 0.f, 0.f, 0.f);
+    sm.tt[r] = 0.f;
+    sm.dsc[r] = 1.f;
+  }
+  for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;
+  pair_sync(sm);
+  for (int i = warp; i < NT; i += 2)
+    if (lane < NV) sm.V(i, V_E)[lane] = 1.f;
+  sm.bc[tid] = 0.f;
+
+  const rmpc_state st = P.states[agent];
+  const rmpc_command cmd = P.cmds[agent];
+  const rmpc_gait gait = P.gaits[agent];
+  const bool warm = P.warm_start && P.prev != nullptr && P.prev_z != nullptr &&
+                    P.prev[agent].status == RMPC_STATUS_OK;
+  const float* pz = warm ? P.prev_z + (size_t)agent * NT * NV : nullptr;
+
+  rmpc_solution out;
+  {
+    float* o = reinterpret_cast<float*>(&out);
+    for (int k = 0; k < 33; ++k) o[k] = 0.f;
+    out.status = RMPC_STATUS_OK;
+    out.fail_iter = -1;
+  }
+  bool st_ok = true;
+#pragma unroll
+  for (int k = 0; k < 9; ++k) st_ok = st_ok && isfinite(st.q[k]) && isfinite(st.qd[k]);
+  prof_mark(P, tid, 0, t0);
+  pair_sync(sm);
+
+  int ok = 1;
+  ok = (warp == 0 ? setup_nodes(P, sm, lane, st, cmd, gait, warm, pz)
+                  : setup_dynamics(P, sm, lane, st, cmd, gait, warm, pz)) && st_ok;
+  ok = pair_and(sm, ok);
+  prof_mark(P, tid, 2, t0);
+  if (P.mode == 1 && !ok) {  // cannot happen for a representative (finite inputs); unshared
+    if (tid == 0) reinterpret_cast<int32_t*>(P.store + (size_t)sched * P.store_stride + store_layout(NT).flags)[NT] = -1;
+    return;
+  }
+  if (!ok) {
+    out.status = RMPC_STATUS_NONFINITE_INPUT;
+  } else {
+    if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
+    apply_scaling(P, sm, lane, warp);
+    prof_mark(P, tid, 3, t0);
+    const int good = factorize(P, sm, lane, warp);
+    if (P.mode == 1) {
+      dump_schedule(P, sm, P.store + (size_t)sched * P.store_stride, lane, warp, good ? 1 : 0);
+      return;
+    }
+    if (!good) {
+      out.status = RMPC_STATUS_SINGULAR;
+    } else {
+      prof_mark(P, tid, 4, t0);
+      const int bad_it = admm(P, sm, lane, warp);
+      prof_mark(P, tid, 5, t0);
+      if (bad_it >= 0) {
+        out.status = RMPC_STATUS_DIVERGED;
+        out.fail_iter = bad_it;
+      }
+    }
+  }
+  finish_agent(P, sm, agent, lane, warp, out, st, cmd, warm, pz, t0);
+}
+
 // CTA = P.agents_per_cta warp pairs.  Warp w uses TMEM lanes [32 (w % 4), +32) (the quarter
 // tcgen05.ld/st of warp w can reach) and columns [(w / 4) tmn 32, +tmn 32), tmn = the node
 // blocks its quarter's share holds (tm_nodes); further blocks go to its shared-memory spill.
@@ -340,6 +293,25 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   extern __shared__ __align__(16) float smem[];
   __shared__ uint32_t tmem_base;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int pair = w >> 1;
+  const int b = blockIdx.x;
+  int agent, sched = -1;
+  if (P.mode == 1) {  // schedule store: pair -> schedule id -> its representative agent
+    const int ns = min(*P.n_sched, P.store_cap);
+    if (b * P.agents_per_cta >= ns) return;  // whole CTA idle
+    sched = b * P.agents_per_cta + pair;
+    agent = sched < ns ? P.rep_list[sched] : P.n_agents;
+  } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve)
+    const int nl = *P.n_list;
+    if (b * P.agents_per_cta >= nl) return;
+    const int idx = b * P.agents_per_cta + pair;
+    agent = idx < nl ? P.agent_list[idx] : P.n_agents;
+  } else {
+    agent = b < P.full_ctas ? b * P.agents_per_cta + pair
+                            : (pair < P.tail_agents ? P.full_ctas * P.agents_per_cta +
+                                                           (b - P.full_ctas) * P.tail_agents + pair
+                                                     : P.n_agents);
+  }
   if (w == 0) {
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
                      (uint32_t)__cvta_generic_to_shared(&tmem_base)),
@@ -351,24 +323,233 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
-  const int pair = w >> 1;
-  const int b = blockIdx.x;
-  int agent, sched = -1;
-  if (P.mode == 1) {  // schedule store: pair -> schedule id -> its representative agent
-    sched = b * P.agents_per_cta + pair;
-    const int ns = min(*P.n_sched, P.store_cap);
-    agent = sched < ns ? P.rep_list[sched] : P.n_agents;
-  } else {
-    agent = b < P.full_ctas ? b * P.agents_per_cta + pair
-                            : (pair < P.tail_agents ? P.full_ctas * P.agents_per_cta +
-                                                           (b - P.full_ctas) * P.tail_agents + pair
-                                                     : P.n_agents);
-  }
   if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
     solve_agent<SPILL>(P, smem + pair * make_layout(P.NT, P.spill_nodes).total, tm, tmn, 1 + pair, agent, sched,
                        lane, w & 1);
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  if (w == 0)
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tb), "r"(P.tmem_cols) : "memory");
+}
+
+// ------------------------------------------------------------------------- shared schedule
+// One agent of a shared-schedule CTA: the coefficient blocks, d, the flags and the factor are
+// the CTA's (one copy for every pair); this agent brings its own bounds -- the schedule's
+// scaled rows with its initial-state and swing-height rows replaced -- and q^, computed in
+// FP64 by exactly the operations setup_nodes / setup_dynamics / apply_scaling use, so the
+// solve is bit-identical to the agent's own factorization.  An agent whose stance flags differ
+// from the group's (a 64-bit hash collision) is handed to rti_kernel's list instead.
+__device__ __forceinline__ void solve_agent_shared(const KParams& P, float* cta, float* base, const float* entry,
+                                                const double* con_pz, uint32_t tm, int bar, int agent, int lane,
+                                                int warp) {
+  const int NT = P.NT;
+  const LayoutShared L = make_layout_shared(NT);
+  const StoreLayout SL = store_layout(NT);
+  Sm sm;
+  sm.scr = base + L.scr;
+  sm.coef = cta + L.coef;
+  sm.vec = base + L.vec;
+  sm.row = reinterpret_cast<float4*>(base + L.row);
+  sm.tt = base + L.tt;
+  sm.dsc = cta + L.d;
+  sm.bc = base + L.bc;
+  sm.flags = reinterpret_cast<uint32_t*>(cta + L.flags);
+  sm.NT = NT;
+  sm.mid = mid_node(NT);
+  sm.tm = tm;
+  sm.tmn = nodes_per_warp(NT);
+  sm.spills = false;
+  sm.spill = nullptr;
+  sm.bar = bar;
+  const int tid = warp * 32 + lane;
+  long long t0 = P.profile ? clock64() : 0;
+
+  // the schedule's scaled bounds, zero z / t / vectors, e
+  const float2* er = reinterpret_cast<const float2*>(entry + SL.rows);
+  for (int r = tid; r < (NT + 1) * NSLOT; r += 64) {
+    const float2 lh = er[r];
+    sm.row[r] = make_float4(lh.x, lh.y, 0.f, 0.f);
+    sm.tt[r] = 0.f;
+  }
+  for (int k = tid; k < NT * V_NUM * V_STRIDE; k += 64) sm.vec[k] = 0.f;
+  pair_sync(sm);
+  for (int k = tid; k < NT * NV; k += 64) sm.V(k / NV, V_E)[k % NV] = entry[SL.e + k];
+  sm.bc[tid] = 0.f;
+  const rmpc_state st = P.states[agent];
+  const rmpc_command cmd = P.cmds[agent];
+  const rmpc_gait gait = P.gaits[agent];
+  rmpc_solution out;
+  {
+    float* o = reinterpret_cast<float*>(&out);
+    for (int k = 0; k < 33; ++k) o[k] = 0.f;
+    out.status = RMPC_STATUS_OK;
+    out.fail_iter = -1;
+  }
+  prof_mark(P, tid, 0, t0);
+  pair_sync(sm);
+  bool same = true;
+  if (warp == 0) {
+    // initial-state rows (setup_nodes, mpc.cpp:126-136): guess = nominal at the measured x
+    if (lane < NQ) {
+      const int k = lane;
+      const double gq = k == 0 ? st.q[0] : P.nominal[k];
+      const double rq = st.q[k] - gq, rqd = st.qd[k] - 0.0;
+      float4* ri = sm.R(-1) + INIT0;
+      const float* di = sm.D(-1) + INIT0;
+      const float a = bound_f(rq) * di[k], c = bound_f(rqd) * di[9 + k];
+      ri[k] = make_float4(a, a, 0.f, 0.f);
+      ri[9 + k] = make_float4(c, c, 0.f, 0.f);
+    }
+    // swing-height rows (mpc.cpp:210-216) of nodes >= 1
+#pragma unroll 1
+    for (int i = lane; i < NT; i += 32) {
+      double swt[4];
+      const uint32_t bits = node_schedule(P, gait, i, swt);
+      same = same && bits == sm.flags[i];
+      if (i > 0) {
+#pragma unroll
+        for (int c = 0; c < 4; ++c) {
+          if ((bits >> c) & 1u) continue;
+          const double h = bezier_height(swt[c], P.z_swing, P.v_to, P.v_td);
+          const double r = h - con_pz[c];
+          const float v = bound_f(r) * sm.D(i)[14 + 4 * c];
+          sm.R(i)[14 + 4 * c] = make_float4(v, v, 0.f, 0.f);
+        }
+      }
+    }
+  } else {
+    // q^ = e w dt (guess - desired) (setup_dynamics, mpc.cpp:81-103, then apply_scaling)
+#pragma unroll 1
+    for (int i = lane; i < NT; i += 32) {
+      double swt[4];
+      const uint32_t bits = node_schedule(P, gait, i, swt);
+      float* qh = sm.V(i, V_QH);
+      const float* ei = sm.V(i, V_E);
+#pragma unroll 1
+      for (int j = 0; j < NV; ++j) {
+        double g, des;
+        guess_and_target(P, i, j, false, nullptr, st, cmd, bits, g, des);
+        qh[j] = to_f(wcost(P, j) * P.dt[i] * (g - des)) * ei[j];
+      }
+    }
+  }
+  same = __all_sync(FULL, same);
+  if (!pair_and(sm, same)) {  // not this CTA's schedule: solve it in rti_kernel's list
+    if (tid == 0) P.list_out[atomicAdd(P.n_list, 1)] = agent;
+    return;
+  }
+  prof_mark(P, tid, 2, t0);  // (Ruiz and the factorization ran once per schedule, unprofiled)
+  const int status = reinterpret_cast<const int32_t*>(entry + SL.flags)[NT];
+  if (status != 1) {
+    out.status = RMPC_STATUS_SINGULAR;
+  } else {
+    prof_mark(P, tid, 4, t0);
+    const int bad_it = admm(P, sm, lane, warp);
+    prof_mark(P, tid, 5, t0);
+    if (bad_it >= 0) {
+      out.status = RMPC_STATUS_DIVERGED;
+      out.fail_iter = bad_it;
+    }
+  }
+  finish_agent(P, sm, agent, lane, warp, out, st, cmd, false, nullptr, t0);
+}
+
+// CTA = up to agents_per_cta agents of one schedule group (grp_cta / grp_first / order).  The
+// CTA loads the group's store entry once: coefficients, d and flags into shared memory, the
+// factor's node blocks into TMEM -- top half (nodes 0..m) in lane quarters 0 and 2, bottom half
+// in 1 and 3, the quarters of the pairs' even and odd warps -- then every pair solves its agent.
+template <int MAXA>
+__global__ void __launch_bounds__(64 * MAXA, 1) rti_shared_kernel(const KParams P) {
+  extern __shared__ __align__(16) float smem[];
+  __shared__ uint32_t tmem_base;
+  __shared__ int s_g, s_first, s_cnt;
+  __shared__ double s_con[4];
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31, tid = threadIdx.x;
+  const int NT = P.NT;
+  if (tid == 0) {
+    const int ng = min(*P.n_sched, P.store_cap);
+    int g = -1, first = 0, cnt = 0;
+    if (ng > 0 && (int)blockIdx.x < P.grp_cta[ng]) {
+      int lo = 0, hi = ng - 1;  // last group whose first CTA is <= blockIdx.x
+      while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (P.grp_cta[mid] <= (int)blockIdx.x) lo = mid; else hi = mid - 1;
+      }
+      g = lo;
+      const int k = (int)blockIdx.x - P.grp_cta[g];
+      first = P.grp_first[g] + k * P.agents_per_cta;
+      cnt = min(P.agents_per_cta, P.grp_count[g] - k * P.agents_per_cta);
+    }
+    s_g = g;
+    s_first = first;
+    s_cnt = cnt;
+  }
+  __syncthreads();
+  if (s_cnt <= 0) return;  // whole CTA idle
+  if (w == 0) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(&tmem_base)),
+                 "r"(P.tmem_cols)
+                 : "memory");
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
+  }
+  const LayoutShared L = make_layout_shared(NT);
+  const StoreLayout SL = store_layout(NT);
+  const float* entry = P.store + (size_t)s_g * P.store_stride;
+  {  // the CTA region: coefficients, d, flags
+    const float4* c4 = reinterpret_cast<const float4*>(entry + SL.coef);
+    float4* s4 = reinterpret_cast<float4*>(smem + L.coef);
+    for (int k = tid; k < (NT + 1) * C_SIZE / 4; k += blockDim.x) s4[k] = c4[k];
+    const float4* d4 = reinterpret_cast<const float4*>(entry + SL.d);
+    float4* sd = reinterpret_cast<float4*>(smem + L.d);
+    for (int k = tid; k < (NT + 1) * NSLOT / 4; k += blockDim.x) sd[k] = d4[k];
+    const int32_t* fl = reinterpret_cast<const int32_t*>(entry + SL.flags);
+    for (int k = tid; k < NT; k += blockDim.x) reinterpret_cast<int32_t*>(smem + L.flags)[k] = fl[k];
+  }
+  if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)
+    double gq[9], gqd[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      gq[k] = P.nominal[k];
+      gqd[k] = 0.0;
+    }
+    Frames F;
+    fk_frames(P, gq, gqd, F);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) s_con[c] = F.con[c].pz;
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tb = tmem_base;
+  if (w < 4) {  // warp w fills lane quarter w with its half of the factor
+    const uint32_t tq = tb + ((uint32_t)(32 * w) << 16);
+    const int m = mid_node(NT);
+    const bool top = (w & 1) == 0;
+    for (int i = top ? 0 : m + 1; i <= (top ? m : NT - 1); ++i) {
+      const int blk = top ? i : i - m - 1;
+      const float4* r = reinterpret_cast<const float4*>(entry + SL.blocks + (size_t)(i * 32 + lane) * TCOLS);
+      float v[TCOLS];
+#pragma unroll
+      for (int q = 0; q < TCOLS / 4; ++q) {
+        const float4 x = r[q];
+        v[4 * q] = x.x; v[4 * q + 1] = x.y; v[4 * q + 2] = x.z; v[4 * q + 3] = x.w;
+      }
+      tm_store(tq + (uint32_t)(TCOLS * blk), v);
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const int pair = w >> 1;
+  if (pair < s_cnt) {
+    const int agent = P.order[s_first + pair];
+    const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16);
+    solve_agent_shared(P, smem, smem + L.cta_total + pair * L.total, entry, s_con, tm, 1 + pair, agent, lane, w & 1);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -385,6 +566,8 @@ int rmpc_kernel_setup(int) {
   int rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS>, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::SHARED_AGENTS>, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::MAX_AGENTS>, a, bytes);
   return rc;
 }
 
@@ -485,28 +668,88 @@ __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
   b.slot_of[a] = (int)slot;
 }
 
+// One thread per agent: its group position (atomic per schedule id; the order inside a group
+// does not matter, every agent's result is independent of it) or the unshared list.
+__global__ void sched_count_kernel(const KParams P, RmpcSchedBuffers b) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= P.n_agents) return;
+  const int sl = b.slot_of[a];
+  const int id = sl >= 0 ? b.slot_id[sl] : -1;
+  if (id >= 0) {
+    b.pos[a] = atomicAdd(b.cnt + id, 1);
+  } else {
+    b.pos[a] = -1;
+    b.ulist[atomicAdd(b.n_unshared, 1)] = a;
+  }
+}
+
+// One CTA of 1024 threads (cap <= 1024 groups): exclusive prefix sums of the group sizes and of
+// their CTA counts (ceil(count / A)).
+__global__ void sched_scan_kernel(RmpcSchedBuffers b, int A) {
+  __shared__ int wsum[2][32];
+  const int t = threadIdx.x, lane = t & 31, wid = t >> 5;
+  const int ng = min(*b.n_sched, b.cap);
+  const int c = t < ng ? b.cnt[t] : 0;
+  int v0 = c, v1 = (c + A - 1) / A;  // agents, CTAs
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y0 = __shfl_up_sync(FULL, v0, o), y1 = __shfl_up_sync(FULL, v1, o);
+    if (lane >= o) { v0 += y0; v1 += y1; }
+  }
+  if (lane == 31) { wsum[0][wid] = v0; wsum[1][wid] = v1; }
+  __syncthreads();
+  if (wid == 0) {
+    int s0 = wsum[0][lane], s1 = wsum[1][lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y0 = __shfl_up_sync(FULL, s0, o), y1 = __shfl_up_sync(FULL, s1, o);
+      if (lane >= o) { s0 += y0; s1 += y1; }
+    }
+    wsum[0][lane] = s0;
+    wsum[1][lane] = s1;
+  }
+  __syncthreads();
+  const int base0 = wid > 0 ? wsum[0][wid - 1] : 0, base1 = wid > 0 ? wsum[1][wid - 1] : 0;
+  const int incl0 = v0 + base0, incl1 = v1 + base1;
+  if (t < ng) {
+    b.grp_first[t] = incl0 - c;
+    b.grp_cta[t] = incl1 - (c + A - 1) / A;
+  }
+  if (t == (ng > 0 ? ng - 1 : 0)) b.grp_cta[ng] = ng > 0 ? incl1 : 0;
+}
+
+__global__ void sched_scatter_kernel(const KParams P, RmpcSchedBuffers b) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= P.n_agents) return;
+  const int p = b.pos[a];
+  if (p >= 0) b.order[b.grp_first[b.slot_id[b.slot_of[a]]] + p] = a;
+}
+
 }  // namespace rmpc_dev
 
-int rmpc_launch_sched(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream,
-                      rmpc_dev::KParams* params_out) {
-  *params_out = params;
-  if (params.n_agents <= 0 || params.n_agents > b.agents) return 0;
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream) {
+  using namespace rmpc_dev;
+  if (params.n_agents <= 0) return 0;
+  if (params.n_agents > b.agents) return (int)cudaErrorInvalidValue;
   const cudaStream_t st = (cudaStream_t)stream;
+  const int n = params.n_agents, NT = params.NT;
+  const int blocks = (n + 255) / 256;
   int rc = (int)cudaMemsetAsync(b.table, 0xFF, (size_t)b.slots * sizeof(unsigned long long), st);
   if (rc == 0) rc = (int)cudaMemsetAsync(b.n_sched, 0, sizeof(int32_t), st);
+  if (rc == 0) rc = (int)cudaMemsetAsync(b.n_unshared, 0, sizeof(int32_t), st);
+  if (rc == 0) rc = (int)cudaMemsetAsync(b.cnt, 0, (size_t)b.cap * sizeof(int32_t), st);
   if (rc != 0) return rc;
-  rmpc_dev::sched_key_kernel<<<(params.n_agents + 255) / 256, 256, 0, st>>>(params, b);
-  rc = (int)cudaGetLastError();
-  if (rc != 0) return rc;
-  const rmpc_dev::CtaShape c = rmpc_dev::cta_shape(params.NT);
-  rmpc_dev::KParams F = params;
+  sched_key_kernel<<<blocks, 256, 0, st>>>(params, b);
+  sched_count_kernel<<<blocks, 256, 0, st>>>(params, b);
+  // the store: one warp pair per schedule runs setup + Ruiz + factorization (mode 1)
+  const CtaShape c = cta_shape(NT);
+  KParams F = params;
   F.mode = 1;
   F.rep_list = b.rep_list;
   F.n_sched = b.n_sched;
   F.store = b.store;
   F.store_cap = b.cap;
-  F.store_stride = rmpc_dev::store_layout(params.NT).total;
-  F.slot_of = nullptr;
+  F.store_stride = store_layout(NT).total;
   F.out = nullptr;
   F.z_out = nullptr;
   F.act_out = nullptr;
@@ -514,17 +757,44 @@ int rmpc_launch_sched(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b
   F.agents_per_cta = c.agents;
   F.spill_nodes = c.spill_nodes;
   F.tmem_cols = c.tmem_cols;
-  const int grid = (b.cap + c.agents - 1) / c.agents;
-  F.full_ctas = grid;
+  F.full_ctas = (b.cap + c.agents - 1) / c.agents;
   F.tail_agents = 0;
-  rc = launch_variant(F, c, grid, st);
+  rc = launch_variant(F, c, F.full_ctas, st);
   if (rc != 0) return rc;
-  rmpc_dev::KParams& P = *params_out;
-  P.mode = 0;
-  P.slot_of = b.slot_of;
-  P.slot_id = b.slot_id;
-  P.store = b.store;
-  P.store_cap = b.cap;
-  P.store_stride = F.store_stride;
-  return 0;
+  const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
+  sched_scan_kernel<<<1, 1024, 0, st>>>(b, cs.agents);
+  sched_scatter_kernel<<<blocks, 256, 0, st>>>(params, b);
+  // the groups: one schedule per CTA (grid: an upper bound of sum ceil(count / A))
+  KParams S = params;
+  S.mode = 0;
+  S.n_sched = b.n_sched;
+  S.store = b.store;
+  S.store_cap = b.cap;
+  S.store_stride = F.store_stride;
+  S.order = b.order;
+  S.grp_cta = b.grp_cta;
+  S.grp_first = b.grp_first;
+  S.grp_count = b.cnt;
+  S.n_list = b.n_unshared;
+  S.list_out = b.ulist;
+  S.agents_per_cta = cs.agents;
+  S.tmem_cols = cs.tmem_cols;
+  const int grid_s = (n + cs.agents - 1) / cs.agents + std::min(b.cap, n);
+  if (cs.agents > MAX_AGENTS)
+    rti_shared_kernel<SHARED_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);
+  else
+    rti_shared_kernel<MAX_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);
+  rc = (int)cudaGetLastError();
+  if (rc != 0) return rc;
+  // the rest (over-capacity schedules, non-finite inputs, hash collisions): per-agent solves
+  KParams U = params;
+  U.mode = 0;
+  U.agent_list = b.ulist;
+  U.n_list = b.n_unshared;
+  U.agents_per_cta = c.agents;
+  U.spill_nodes = c.spill_nodes;
+  U.tmem_cols = c.tmem_cols;
+  U.full_ctas = (n + c.agents - 1) / c.agents;
+  U.tail_agents = 0;
+  return launch_variant(U, c, U.full_ctas, st);
 }

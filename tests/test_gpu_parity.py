@@ -6,7 +6,7 @@ import pytest
 import paper_2510_12717_b200 as R
 from paper_2510_12717_b200.abi import (SOLUTION_DTYPE, STATUS_DIVERGED, STATUS_NONFINITE_INPUT,
                                        STATUS_OK, default_model, default_settings)
-from parity import TOL, compare, summary
+from parity import TOL, check, compare, summary
 
 pytestmark = pytest.mark.gpu
 
@@ -192,10 +192,15 @@ def test_timing_report_and_stage_profile():
     assert t["batch_size"] == n and t["devices"] == 1
     assert t["kernel_ms"] > 0 and t["total_ms"] >= t["kernel_ms"]
     br.set_stage_profiling(True)
-    br.solve(st, cm, ga)
-    t = br.last_timing()
-    assert abs(sum(t["stage_ms"].values()) - t["kernel_ms"]) <= 1e-6 * t["kernel_ms"] + 1e-9
-    assert t["stage_ms"]["admm_iters"] > 0 and t["stage_ms"]["ruiz"] > 0
+    for share in (True, False):  # shared schedules: Ruiz + factorization run once per schedule
+        br.set_schedule_sharing(share)
+        br.solve(st, cm, ga)
+        t = br.last_timing()
+        assert abs(sum(t["stage_ms"].values()) - t["kernel_ms"]) <= 1e-6 * t["kernel_ms"] + 1e-9
+        assert t["stage_ms"]["admm_iters"] > 0 and (share or t["stage_ms"]["ruiz"] > 0)
+        # TimingReport::mean_ms / std_ms over agents (batch.cpp:67-77)
+        assert t["stage_mean_ms"]["admm_iters"] > 0 and t["stage_std_ms"]["admm_iters"] >= 0
+        assert t["stage_mean_ms"]["admm_iters"] < t["kernel_ms"]
 
 
 def test_mpc_torque_from_gpu_solution(oracle):

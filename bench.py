@@ -570,7 +570,9 @@ def main():
                        "precision": "FP32 solve, FP64 linearization/objective"},
             "e2e": {"value": n_total / (e2e_ms * 1e-3), "unit": "solves/s",
                     "h2d_bytes_per_step": n * (144 + 24 + 56), "d2h_bytes_per_step": n * (140 + T * 26 * 4),
-                    "ms_per_step": e2e_ms, "api": "rmpc_solve (C ABI), pinned host buffers, records + z*",
+                    "ms_per_step": e2e_ms,
+                    "api": "rmpc_solve (C ABI), pinned host buffers: inputs copied H2D, records + z* "
+                           "written by the solve into the mapped pinned output buffers over PCIe",
                     "without_z_star": {"value": n_total / (e2e_nz_ms * 1e-3), "ms_per_step": e2e_nz_ms,
                                        "d2h_bytes_per_step": n * 140},
                     "last_timing_ms": {"h2d": tm["h2d_ms"], "kernel": tm["kernel_ms"], "d2h": tm["d2h_ms"],

@@ -217,3 +217,24 @@ def ppo_update_seq(params, obs, actions, logp, values, rewards, dones, bootstrap
                              ptr(_f64(values)), ptr(_f64(rewards)), ptr(_f64(dones)), ptr(_f64(bootstrap)),
                              C.byref(cfg), C.c_uint64(seed), C.c_uint64(stream), C.c_int32(n_updates), st)
     return p, [tuple(st[4 * k:4 * k + 4]) for k in range(n_updates)]
+
+
+REASONS = ("survived", "non_finite", "height", "orientation", "velocity", "self_collision",
+           "controller_failed")
+
+
+def closed_loop(model: Model, settings: Settings, cfg, phase_switch=1.0, ticks=500):
+    """The reference's own closed loop (rti_step -> mpc_torque -> Env::step) from the nominal
+    standing pose at zero command: (ticks survived, reason, trace (ticks, 18) of the states)."""
+    trace = np.full((ticks, 18), np.nan)
+    reason = C.c_int32(0)
+    lib().ref_closed_loop.restype = C.c_int32
+    alive = lib().ref_closed_loop(C.byref(model), C.byref(settings), C.byref(cfg), C.c_double(phase_switch),
+                                  C.c_int32(ticks), ptr(trace), C.byref(reason))
+    return alive, REASONS[reason.value], trace
+
+
+def check_termination(model: Model, cfg, state) -> str:
+    """The reference's check_termination on one state (n/a reasons: 'survived' = not terminated)."""
+    lib().ref_check_termination.restype = C.c_int32
+    return REASONS[lib().ref_check_termination(C.byref(model), C.byref(cfg), ptr(_f64(state, (18,))))]

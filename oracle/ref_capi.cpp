@@ -474,4 +474,67 @@ void ref_ppo_update_seq(double* params, int32_t obs, int32_t act, int32_t hidden
   std::copy(f.data(), f.data() + f.size(), params);
 }
 
+// check_termination (env.cpp:111-140) on a state with the base model: the reason code of
+// ref_closed_loop (0 = none).
+int32_t ref_check_termination(const rmpc_model* model, const rmpc_env_config* cfg, const rmpc_state* state) {
+  EnvState es;
+  es.robot = to_state(*state);
+  const TerminationCheck t = check_termination(es, to_env(*cfg), to_model(*model));
+  if (!t.terminated) return 0;
+  const std::string& w = t.reason;
+  return w == "height" ? 2 : w == "orientation" ? 3 : w == "velocity" ? 4 : w == "self_collision" ? 5 : 1;
+}
+
+// The reference's own closed loop (run_episode without a policy, analysis.cpp:75-149): every
+// control tick rti_step on the env state -> mpc_torque (zero torque for a failed solve) ->
+// Env::step (physics_step, termination).  The env is the reference's Env with randomisation
+// pinned (friction = model mu, mass scale 1, no initial velocity, zero command) and the gait
+// of `settings`.  SPEC.md acceptance #4: standing, zero command, 5 s survival.  Writes
+// trace[t] = {q[0..8], qd[0..8]} after tick t (ticks x 18) and returns the ticks survived;
+// *reason: 0 survived, 1 non_finite / sim_blowup, 2 height, 3 orientation, 4 velocity,
+// 5 self_collision, 6 controller_failed.
+int32_t ref_closed_loop(const rmpc_model* model, const rmpc_settings* st, const rmpc_env_config* cfg,
+                        double phase_switch, int32_t ticks, double* trace, int32_t* reason) {
+  const ModelParams mp = to_model(*model);
+  MpcSettings ms = to_settings(*st);
+  EnvConfig ec = to_env(*cfg);
+  ec.friction_lo = ec.friction_hi = mp.mu;
+  ec.mass_scale_lo = ec.mass_scale_hi = 1.0;
+  ec.init_vx = 0.0;
+  ec.init_pitch_rate = 0.0;
+  ec.cmd_vx_lo = ec.cmd_vx_hi = 0.0;
+  ec.cmd_height_lo = ec.cmd_height_hi = mp.nominal_height();
+  ec.gait_period = ms.gait_period;
+  ec.phase_switch = phase_switch;
+  ec.phase_offsets = ms.phase_offsets;
+  ec.episode_length = 1e9;
+  Env env(mp, ec, 0, 0);
+  MpcController ctrl(mp, ms);
+  MpcSolution prev;
+  bool have_prev = false;
+  *reason = 0;
+  for (int t = 0; t < ticks; ++t) {
+    const EnvState s = env.state();
+    const MpcSolution sol = ctrl.rti_step(s.robot, s.cmd, s.gait, have_prev ? &prev : nullptr);
+    const bool failed = sol.status != MpcStatus::kOk;
+    const Vec6 tau = failed ? Vec6::Zero() : mpc_torque(sol, s.robot, env.model());
+    const EnvState before = env.state();
+    const Env::StepResult res = env.step(tau, Vec6::Zero(), failed);
+    const RobotState& r = res.done ? before.robot : env.state().robot;  // reset() replaced it
+    for (int k = 0; k < kNq; ++k) {
+      trace[(size_t)t * 18 + k] = res.done ? std::nan("") : r.q[k];
+      trace[(size_t)t * 18 + 9 + k] = res.done ? std::nan("") : r.qd[k];
+    }
+    if (res.done) {
+      const std::string& w = res.reason;
+      *reason = w == "height" ? 2 : w == "orientation" ? 3 : w == "velocity" ? 4 : w == "self_collision" ? 5
+              : w == "controller_failed" ? 6 : 1;
+      return t;
+    }
+    prev = sol;
+    have_prev = true;
+  }
+  return ticks;
+}
+
 }  // extern "C"

@@ -41,7 +41,7 @@ struct Shard {
   rmpc_solution* d_out = nullptr;
   float* d_z = nullptr;
   unsigned long long* d_prof = nullptr;
-  RmpcSchedBuffers sched[3] = {};  // schedule-shared workspace, one per chunk of a tick
+  RmpcSchedBuffers sched[1] = {};  // schedule-shared workspace
   // pinned staging for pageable caller buffers
   char* h_stage_in = nullptr;
   char* h_stage_out = nullptr;
@@ -251,8 +251,8 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
   sh.stage_out_bytes = n * sizeof(rmpc_solution) + zn * sizeof(float) + 2 * 256;
   CK(cudaMallocHost(&sh.h_stage_in, sh.stage_in_bytes));
   CK(cudaMallocHost(&sh.h_stage_out, sh.stage_out_bytes));
-  // schedule-shared solves: per chunk a hash table of >= 2n slots and up to kSchedCap
-  // distinct schedules in the store
+  // schedule-shared solves: a hash table of >= 2n slots and up to kSchedCap distinct
+  // schedules in the store
   for (RmpcSchedBuffers& sb : sh.sched) {
     sb.agents = (int)n;
     sb.slots = 64;
@@ -304,20 +304,102 @@ void free_shard(Shard& sh) {
 // kernel, chunk 1's D2H overlaps the rest, the later kernels' CTAs fill the SMs as earlier
 // ones finish, and only the small tail chunk's D2H is left at the end.  Per-agent results do
 // not depend on the split.
+// Device address of host memory the kernel can write directly (pinned, hence mapped under UVA).
+template <class T>
+T* mapped(T* p) {
+  void* d = nullptr;
+  if (cudaHostGetDevicePointer(&d, (void*)p, 0) != cudaSuccess) {
+    cudaGetLastError();
+    return nullptr;
+  }
+  return static_cast<T*>(d);
+}
+
+// Cold start with schedule sharing: the inputs in one H2D copy each, then the whole shared
+// solve (schedule pass, grouped solve) writing its records and z* straight into the pinned
+// host buffers (the caller's, or the handle's staging copy for pageable ones) over PCIe while
+// it runs -- the grouped solve finishes every agent at once at the end, so there is no later
+// chunk whose kernel a D2H could overlap.
+void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
+                      const rmpc_gait* gaits, rmpc_solution* out, float* z_out) {
+  const size_t n = sh.count, b = sh.begin;
+  const size_t zrow = (size_t)h.NT * RMPC_NV;
+  const cudaStream_t st = sh.stream;
+  struct In {
+    const char* src;
+    char* dst;
+    size_t bytes;
+  };
+  In ins[3] = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), n * sizeof(rmpc_state)},
+               {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), n * sizeof(rmpc_command)},
+               {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), n * sizeof(rmpc_gait)}};
+  size_t off = 0;
+  for (In& c : ins) {
+    if (!is_pinned(c.src)) {
+      std::memcpy(sh.h_stage_in + off, c.src, c.bytes);
+      c.src = sh.h_stage_in + off;
+      off += (c.bytes + 255) & ~size_t(255);
+    }
+  }
+  const bool out_pinned = is_pinned(out), z_pinned = is_pinned(z_out);
+  rmpc_solution* h_out = out_pinned ? out + b : reinterpret_cast<rmpc_solution*>(sh.h_stage_out);
+  float* h_z = z_out ? (z_pinned ? z_out + b * zrow
+                                 : reinterpret_cast<float*>(sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255))))
+                     : nullptr;
+  rmpc_solution* d_out = mapped(h_out);
+  float* d_z = h_z ? mapped(h_z) : nullptr;
+  CK(cudaEventRecord(sh.ev[0], st));
+  if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), st));
+  for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, st));
+  CK(cudaEventRecord(sh.ev[1], st));
+  rmpc_dev::KParams P = make_params(h);
+  P.n_agents = (int)n;
+  P.states = sh.d_states;
+  P.cmds = sh.d_cmds;
+  P.gaits = sh.d_gaits;
+  P.out = d_out ? d_out : sh.d_out;
+  P.z_out = z_out ? (d_z ? d_z : sh.d_z) : nullptr;
+  P.prof = sh.d_prof;
+  const int rc = rmpc_launch_shared(P, sh.sched[0], st);
+  if (rc != 0) {
+    sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
+    sh.msg = std::string("rti_shared_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    cudaStreamSynchronize(st);
+    return;
+  }
+  CK(cudaEventRecord(sh.ev[2], st));
+  if (!d_out) CK(cudaMemcpyAsync(h_out, sh.d_out, n * sizeof(rmpc_solution), cudaMemcpyDeviceToHost, st));
+  if (z_out && !d_z) CK(cudaMemcpyAsync(h_z, sh.d_z, n * zrow * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (h.profile) CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, st));
+  CK(cudaEventRecord(sh.ev[5], st));
+  CK(cudaStreamSynchronize(st));
+  if (!out_pinned) std::memcpy(out + b, h_out, n * sizeof(rmpc_solution));
+  if (z_out && !z_pinned) std::memcpy(z_out + b * zrow, h_z, n * zrow * sizeof(float));
+  float t01 = 0, t12 = 0, t25 = 0;
+  cudaEventElapsedTime(&t01, sh.ev[0], sh.ev[1]);
+  cudaEventElapsedTime(&t12, sh.ev[1], sh.ev[2]);  // the solve, incl. the mapped output writes
+  cudaEventElapsedTime(&t25, sh.ev[2], sh.ev[5]);
+  sh.h2d_ms = t01;
+  sh.kernel_ms = t12;
+  sh.d2h_ms = t25;
+}
+
 void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
                const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z,
                rmpc_solution* out, float* z_out) {
   sh.err = 0;
   if (sh.count == 0) return;
   CK(cudaSetDevice(sh.device));
+  if (h.share && !h.settings.warm_start) {
+    run_shard_shared(h, sh, states, cmds, gaits, out, z_out);
+    return;
+  }
   const size_t n = sh.count, b = sh.begin;
   const size_t zrow = (size_t)h.NT * RMPC_NV;
   const bool use_prev = h.settings.warm_start && prev && prev_z;
   // chunks: the first wave, the remaining whole waves, the partial last wave (its D2H is the
   // only transfer left exposed at the end)
-  const bool share_tick = h.share && !h.settings.warm_start;
-  const size_t wave = (size_t)sh.sms * (share_tick ? rmpc_dev::cta_shape_shared(h.NT, rmpc_dev::shared_agents_cap(h.NT)).agents
-                                                   : rmpc_dev::cta_shape(h.NT).agents);
+  const size_t wave = (size_t)sh.sms * rmpc_dev::cta_shape(h.NT).agents;
   size_t cut[4] = {0, n, n, n};
   int nchunks = 1;
   if (n > 2 * wave && !h.profile) {
@@ -359,9 +441,6 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
                      : sh.h_stage_out + ((n * sizeof(rmpc_solution) + 255) & ~size_t(255));
   CK(cudaEventRecord(sh.ev[0], ss[0]));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), ss[0]));
-  // cold start with schedule sharing: each chunk runs the whole shared solve (schedule pass,
-  // grouped solve, the rest) on its own workspace
-  const bool share = h.share && !h.settings.warm_start;
   if (nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[0], 0));
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
@@ -379,7 +458,7 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
     P.out = sh.d_out + lo;
     P.z_out = z_out ? sh.d_z + lo * zrow : nullptr;
     P.prof = sh.d_prof;
-    const int rc = share ? rmpc_launch_shared(P, sh.sched[k], st) : rmpc_launch_rti(P, st);
+    const int rc = rmpc_launch_rti(P, st);
     if (rc != 0) {
       sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
       sh.msg = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);

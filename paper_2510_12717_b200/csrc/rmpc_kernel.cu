@@ -646,10 +646,14 @@ __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
     return;
   }
   unsigned long long k0 = 0, k1 = 0;  // 4 bits per node, nodes 0..15 and 16..31
+  double shift = 0.0;  // node_schedule's cumulative shift, the same additions in the same order
   for (int i = 0; i < P.NT; ++i) {
-    double sw[4];
-    const unsigned long long bits = node_schedule(P, g, i, sw);
+    unsigned long long bits = 0;
+#pragma unroll
+    for (int c = 0; c < 4; ++c)
+      if (wrap01(g.phase + shift + g.offsets[c]) < g.phase_switch) bits |= 1ull << c;
     if (i < 16) k0 |= bits << (4 * i); else k1 |= bits << (4 * (i - 16));
+    shift += P.dt[i] / g.period;
   }
   unsigned long long h = mix64(k0 ^ mix64(k1 + 0x9e3779b97f4a7c15ull));
   if (h == ~0ull) h = ~0ull - 1;
@@ -741,8 +745,16 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   if (rc != 0) return rc;
   sched_key_kernel<<<blocks, 256, 0, st>>>(params, b);
   sched_count_kernel<<<blocks, 256, 0, st>>>(params, b);
-  // the store: one warp pair per schedule runs setup + Ruiz + factorization (mode 1)
+  // the store: setup + Ruiz + factorization of each schedule's representative (mode 1), one
+  // warp pair per CTA (the few schedules' latency chains run alone on their SMs)
   const CtaShape c = cta_shape(NT);
+  CtaShape c1 = c;
+  c1.agents = 1;
+  c1.spill_nodes = 0;
+  c1.dense = false;
+  c1.tmem_cols = 32;
+  while (c1.tmem_cols < nodes_per_warp(NT) * TCOLS) c1.tmem_cols *= 2;
+  c1.smem_bytes = smem_bytes(NT, 0);
   KParams F = params;
   F.mode = 1;
   F.rep_list = b.rep_list;
@@ -754,12 +766,12 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   F.z_out = nullptr;
   F.act_out = nullptr;
   F.profile = 0;
-  F.agents_per_cta = c.agents;
-  F.spill_nodes = c.spill_nodes;
-  F.tmem_cols = c.tmem_cols;
-  F.full_ctas = (b.cap + c.agents - 1) / c.agents;
+  F.agents_per_cta = 1;
+  F.spill_nodes = 0;
+  F.tmem_cols = c1.tmem_cols;
+  F.full_ctas = b.cap;
   F.tail_agents = 0;
-  rc = launch_variant(F, c, F.full_ctas, st);
+  rc = launch_variant(F, c1, F.full_ctas, st);
   if (rc != 0) return rc;
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
   sched_scan_kernel<<<1, 1024, 0, st>>>(b, cs.agents);

@@ -16,7 +16,7 @@ SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rmpc_kernel.cu", "rmpc_host.
                                                        "rmpc_ppo.cu")]
 HEADERS = [os.path.join(HERE, "csrc", h) for h in ("rmpc_device.cuh", "rmpc_kin.cuh", "rmpc_sm.cuh",
                                                    "rmpc_views.cuh", "rmpc_model.cuh", "rmpc_setup.cuh",
-                                                   "rmpc_ruiz.cuh", "rmpc_factor.cuh", "rmpc_admm.cuh",
+                                                   "rmpc_ruiz.cuh", "rmpc_factor.cuh", "rmpc_admm.cuh", "rmpc_squad.cuh",
                                                    "rmpc_policy.cuh")] + \
     [os.path.join(ROOT, "include", h) for h in ("rmpc_b200.h", "rmpc_b200_env.h")]
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",

@@ -122,10 +122,11 @@ struct KParams {
 
 // One schedule's entry in the store (floats, 16-byte aligned regions): the Ruiz-scaled
 // coefficient blocks (incl. the G_dd entries of the factorization), the column scales e, the
-// row scales d, the stance flags + factorization status, and the factor's node blocks as
-// TMEM rows (32 lanes x 32 columns per node).
+// row scales d, the stance flags + factorization status, the factor's node blocks as TMEM
+// rows (32 lanes x 32 columns per node) and the representative's scaled q^ (the squad solve
+// replaces its four agent-dependent components).
 struct StoreLayout {
-  int coef, e, d, rows, flags, blocks, total;
+  int coef, e, d, rows, flags, blocks, qh, total;
 };
 __host__ __device__ inline StoreLayout store_layout(int NT) {
   StoreLayout L;
@@ -136,6 +137,7 @@ __host__ __device__ inline StoreLayout store_layout(int NT) {
   L.rows = o;   o += (NT + 1) * NSLOT * 2;       // scaled {lo, hi} of the representative
   L.flags = o;  o += (NT + 1 + 3) & ~3;  // NT flag words, then the status word (1 = factor ok)
   L.blocks = o; o += NT * 32 * TCOLS;
+  L.qh = o;     o += (NT * NV + 3) & ~3;
   L.total = o;
   return L;
 }
@@ -296,5 +298,7 @@ struct RmpcSchedBuffers {
 // hash every agent's stance schedule, build the store (one factorization per schedule), group
 // the agents by schedule, solve the groups (rti_shared_kernel: one schedule per CTA) and the
 // rest (rti_kernel over an agent list).  Seven launches plus memsets, no host synchronisation.
-int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream);
+// variant 1: warp-pair-per-agent CTAs of one schedule (rti_shared_kernel, bit-identical to the
+// per-agent solve); 2: lane-per-agent squads (rti_squad_kernel) where the horizon fits them.
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant);
 int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory

@@ -124,7 +124,7 @@ struct rmpc_handle {
   rmpc_timing timing;
   std::string err;
   int profile = 0;
-  int share = 1;  // schedule-shared factorization for cold-start solves
+  int share = 2;  // cold-start schedule sharing: 0 off, 1 warp-pair CTAs, 2 squads
   std::unique_ptr<ShardPool> pool;  // shards >= 2 only
 };
 
@@ -360,7 +360,7 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   P.out = d_out ? d_out : sh.d_out;
   P.z_out = z_out ? (d_z ? d_z : sh.d_z) : nullptr;
   P.prof = sh.d_prof;
-  const int rc = rmpc_launch_shared(P, sh.sched[0], st);
+  const int rc = rmpc_launch_shared(P, sh.sched[0], st, h.share);
   if (rc != 0) {
     sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
     sh.msg = std::string("rti_shared_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -553,7 +553,7 @@ int32_t launch_device(rmpc_handle& h, Shard& sh, int n, const rmpc_state* d_stat
   P.prof = sh.d_prof;
   P.profile = 0;
   if (d_active) P.warm_start = 0;
-  const int rc = (h.share && !P.warm_start) ? rmpc_launch_shared(P, sh.sched[0], stream)  // cold start
+  const int rc = (h.share && !P.warm_start) ? rmpc_launch_shared(P, sh.sched[0], stream, h.share)  // cold start
                                             : rmpc_launch_rti(P, stream);
   if (rc != 0) {
     h.err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -822,7 +822,7 @@ int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol, const
 
 int32_t rmpc_set_schedule_sharing(rmpc_handle* h, int32_t enabled) {
   if (!h) return RMPC_ERR_INVALID_ARG;
-  h->share = enabled ? 1 : 0;
+  h->share = enabled < 0 ? 0 : (enabled > 2 ? 2 : enabled);
   return RMPC_OK;
 }
 

@@ -42,6 +42,7 @@
 #include "rmpc_ruiz.cuh"
 #include "rmpc_factor.cuh"
 #include "rmpc_admm.cuh"
+#include "rmpc_squad.cuh"
 
 namespace rmpc_dev {
 
@@ -175,7 +176,10 @@ __device__ void dump_schedule(const KParams& P, const Sm& sm, float* st, int lan
   const float4* d4 = reinterpret_cast<const float4*>(sm.dsc);
   float4* od = reinterpret_cast<float4*>(st + SL.d);
   for (int k = tid; k < (NT + 1) * NSLOT / 4; k += 64) od[k] = d4[k];
-  for (int k = tid; k < NT * NV; k += 64) st[SL.e + k] = sm.V(k / NV, V_E)[k % NV];
+  for (int k = tid; k < NT * NV; k += 64) {
+    st[SL.e + k] = sm.V(k / NV, V_E)[k % NV];
+    st[SL.qh + k] = sm.V(k / NV, V_QH)[k % NV];
+  }
   float2* rw = reinterpret_cast<float2*>(st + SL.rows);
   for (int r = tid; r < (NT + 1) * NSLOT; r += 64) rw[r] = make_float2(sm.row[r].x, sm.row[r].y);
   int32_t* fl = reinterpret_cast<int32_t*>(st + SL.flags);
@@ -568,6 +572,7 @@ int rmpc_kernel_setup(int) {
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::SHARED_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::MAX_AGENTS>, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_squad_kernel, a, bytes);
   return rc;
 }
 
@@ -731,7 +736,7 @@ __global__ void sched_scatter_kernel(const KParams P, RmpcSchedBuffers b) {
 
 }  // namespace rmpc_dev
 
-int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream) {
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant) {
   using namespace rmpc_dev;
   if (params.n_agents <= 0) return 0;
   if (params.n_agents > b.agents) return (int)cudaErrorInvalidValue;
@@ -773,8 +778,9 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   F.tail_agents = 0;
   rc = launch_variant(F, c1, F.full_ctas, st);
   if (rc != 0) return rc;
+  const bool squads = variant == 2 && sq_supported(NT);
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
-  sched_scan_kernel<<<1, 1024, 0, st>>>(b, cs.agents);
+  sched_scan_kernel<<<1, 1024, 0, st>>>(b, squads ? 32 : cs.agents);
   sched_scatter_kernel<<<blocks, 256, 0, st>>>(params, b);
   // the groups: one schedule per CTA (grid: an upper bound of sum ceil(count / A))
   KParams S = params;
@@ -792,7 +798,16 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   S.agents_per_cta = cs.agents;
   S.tmem_cols = cs.tmem_cols;
   const int grid_s = (n + cs.agents - 1) / cs.agents + std::min(b.cap, n);
-  if (cs.agents > MAX_AGENTS)
+  if (squads) {  // lane-per-agent squads, two per CTA (grid: an upper bound of sum ceil(count / 32) / 2)
+    S.agents_per_cta = 32;
+    const int nsq = (n + 31) / 32 + std::min(b.cap, n);
+    static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
+      const char* e = getenv("RMPC_SQUAD_SOLO");
+      return e ? atoi(e) : 0;
+    }();
+    S.pad2_ = solo;
+    rti_squad_kernel<<<solo ? nsq : (nsq + 1) / 2, 128, sq_smem_bytes(NT), st>>>(S);
+  } else if (cs.agents > MAX_AGENTS)
     rti_shared_kernel<SHARED_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);
   else
     rti_shared_kernel<MAX_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);

@@ -276,10 +276,13 @@ class BatchRunner:
     def set_stage_profiling(self, enabled: bool = True):
         self._lib.rmpc_set_stage_profiling(self._h, int(enabled))
 
-    def set_schedule_sharing(self, enabled: bool = True):
-        """Cold-start solves factorize each distinct contact schedule once (default on);
-        results are bit-identical either way (rmpc_set_schedule_sharing)."""
-        self._lib.rmpc_set_schedule_sharing(self._h, int(enabled))
+    def set_schedule_sharing(self, level=True):
+        """Cold-start schedule sharing (rmpc_set_schedule_sharing): each distinct contact
+        schedule is factorized once.  True / 2 (default): lane-per-agent squads where the
+        horizon fits them (T <= 10); 1: warp-pair CTAs per schedule, bit-identical to the
+        per-agent solve; False / 0: per-agent factorization."""
+        level = 2 if level is True else int(level)
+        self._lib.rmpc_set_schedule_sharing(self._h, level)
 
     def last_timing(self) -> dict:
         t = Timing()

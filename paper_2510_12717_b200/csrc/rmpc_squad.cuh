@@ -25,13 +25,15 @@ namespace rmpc_dev {
 #endif
 
 constexpr int SQ_MAXT = 10;   // horizons served by squads (5 node slabs of 96 TMEM columns per thread)
-constexpr int SQ_SLAB = 96;   // TMEM columns per own node
+constexpr int SQ_SLAB = 98;   // TMEM columns per own node
 constexpr int SQ_X = 0;       // x (26)
-constexpr int SQ_S = 26;      // s / x~ (26), then gamma (3)
-constexpr int SQ_TI = 55;     // t of the node's interval rows, slots 0..11
-constexpr int SQ_TO = 67;     // t of the node's own rows, slots 12..39
-constexpr int SQ_TINIT = 480; // top thread: t of the 18 initial-state rows (block -1)
-constexpr int SQ_MF = 756;    // packed node matrix: 29 rows x 26 (S^-1 rows, then W_b^T), padded
+constexpr int SQ_S = 26;      // s / x~ (26), then gamma (3) and 3 spare (the matvec writes 32 rows)
+constexpr int SQ_TI = 58;     // t of the node's interval rows, slots 0..11
+constexpr int SQ_TO = 70;     // t of the node's own rows, slots 12..39
+constexpr int SQ_TINIT = 490; // top thread: t of the 18 initial-state rows (block -1)
+constexpr int SQ_MROW = 28;   // floats per packed matrix row (26 + 2 zero: 16-byte aligned rows)
+constexpr int SQ_MF = 32 * SQ_MROW;  // packed node matrix: S^-1 rows 0..25, W_b^T rows 26..28, zero rows 29..31
+constexpr int SQ_NXI = 21;    // private scratch: the backward step's xi (12 top, 21 bottom)
 constexpr int SQ_NZ = 20;     // z of a node's inequality rows: t0/t1 of the 4 contacts, 12 boxes
 constexpr int SQ_PRIV = 28;   // private shared elements per own node: 20 z, 4 swing lo, 4 q^ parts
 constexpr int SQ_FIN = 26 * 32 + 2 * 2 * NV * 32 + 5 * 32;  // finish scratch (reuses the matrices)
@@ -52,7 +54,7 @@ __host__ __device__ inline SqLayout sq_layout(int NT) {
   L.e = o;     o += align4(NT * NV);    // Ruiz column scales
   L.qh = o;    o += align4(NT * NV);    // the schedule's scaled q^
   L.flags = o; o += align4(NT + 1);     // stance bits per node, then the factorization status
-  L.priv_warp = 32 * (nb * SQ_PRIV + NINIT);
+  L.priv_warp = 32 * (nb * SQ_PRIV + NINIT + SQ_NXI);
   L.priv = o;  o += 2 * L.priv_warp;
   L.cross = o; o += 32 * 56;
   L.total = o;
@@ -191,6 +193,7 @@ struct Sq {
   __device__ __forceinline__ int AL(int b, int c) const { return nb * SQ_NZ + 4 * b + c; }
   __device__ __forceinline__ int QA(int b, int q) const { return nb * 24 + 4 * b + q; }
   __device__ __forceinline__ int IL(int l) const { return nb * SQ_PRIV + l; }
+  __device__ __forceinline__ int XS(int r) const { return nb * SQ_PRIV + NINIT + r; }
 };
 
 // foot-contact Jacobian columns (chain_col): does column k belong to contact c's chain?
@@ -252,38 +255,54 @@ __device__ __forceinline__ void sq_colview(const float* cf, const float* cp, con
   }
 }
 
-// s (rows) = M u for the packed node matrix (26 columns per row, rows contiguous)
-template <int ROWS>
-__device__ __forceinline__ void sq_matvec(const float* M, const float u[NV], float s[ROWS]) {
-  const float4* M4 = reinterpret_cast<const float4*>(M);
-  float acc[ROWS][2];
+// Rows [0, 4 nch) of the packed node matrix times u, 4 rows per step (8 independent FMA chains),
+// each step's 4 results stored to TMEM columns dst + 4 c.  A runtime loop: the matvec is the
+// bulk of every node step, and a fully unrolled copy per call site overflows the instruction
+// cache at one warp per scheduler.
+__device__ __forceinline__ void sq_matvec_tm(const float* M, const float u[NV], uint32_t dst, int nch) {
+#pragma unroll 1
+  for (int c = 0; c < nch; ++c) {
+    const float4* R = reinterpret_cast<const float4*>(M + 4 * SQ_MROW * c);
+    float a[4][2];
 #pragma unroll
-  for (int j = 0; j < ROWS; ++j) acc[j][0] = acc[j][1] = 0.f;
+    for (int r = 0; r < 4; ++r) a[r][0] = a[r][1] = 0.f;
 #pragma unroll
-  for (int p = 0; p < (ROWS * NV + 3) / 4; ++p) {
-    const float4 w = M4[p];
-    const float wv[4] = {w.x, w.y, w.z, w.w};
+    for (int qq = 0; qq < SQ_MROW / 4; ++qq) {
 #pragma unroll
-    for (int r = 0; r < 4; ++r) {
-      const int n = 4 * p + r;
-      if (n < ROWS * NV) {
-        const int j = n / NV, k = n % NV;
-        acc[j][k & 1] = fmaf(wv[r], u[k], acc[j][k & 1]);
+      for (int r = 0; r < 4; ++r) {
+        const float4 w = R[(SQ_MROW / 4) * r + qq];
+        a[r][0] = fmaf(w.x, u[4 * qq], a[r][0]);
+        a[r][1] = fmaf(w.y, u[4 * qq + 1], a[r][1]);
+        if (4 * qq + 2 < NV) {
+          a[r][0] = fmaf(w.z, u[4 * qq + 2], a[r][0]);
+          a[r][1] = fmaf(w.w, u[4 * qq + 3], a[r][1]);
+        }
       }
     }
-  }
+    float o[4];
 #pragma unroll
-  for (int j = 0; j < ROWS; ++j) s[j] = acc[j][0] + acc[j][1];
+    for (int r = 0; r < 4; ++r) o[r] = a[r][0] + a[r][1];
+    tq_st4(dst + 4 * c, o);
+  }
 }
 
-// acc[0..25] += sum over the given rows r of M of c[r] * M[r][:]  (rows contiguous, 26 each)
-template <int R0, int NR>
-__device__ __forceinline__ void sq_axpy_rows(const float* M, const float* c, float acc[NV]) {
+// acc[0..25] += sum_r xs[r] M[row(r)][:], row(r) = r < NQR ? r : 26 + r - NQR, for r < NR; the
+// coefficients come from the lane's private scratch (shared memory), the rows as broadcasts.
+__device__ __forceinline__ void sq_axpy_tm(const Sq& q, const float* M, int nqr, int nr, float acc[NV]) {
+#pragma unroll 1
+  for (int r = 0; r < nr; ++r) {
+    const float c = q.pv(q.XS(r));
+    const float4* R = reinterpret_cast<const float4*>(M + SQ_MROW * (r < nqr ? r : 26 + r - nqr));
 #pragma unroll
-  for (int r = 0; r < NR; ++r) {
-    const float* row = M + (R0 + r) * NV;
-#pragma unroll
-    for (int j = 0; j < NV; ++j) acc[j] = fmaf(c[r], row[j], acc[j]);
+    for (int qq = 0; qq < SQ_MROW / 4; ++qq) {
+      const float4 w = R[qq];
+      acc[4 * qq] = fmaf(c, w.x, acc[4 * qq]);
+      acc[4 * qq + 1] = fmaf(c, w.y, acc[4 * qq + 1]);
+      if (4 * qq + 2 < NV) {
+        acc[4 * qq + 2] = fmaf(c, w.z, acc[4 * qq + 2]);
+        acc[4 * qq + 3] = fmaf(c, w.w, acc[4 * qq + 3]);
+      }
+    }
   }
 }
 
@@ -391,11 +410,32 @@ __device__ __forceinline__ void sq_rhs(const KParams& P, const Sq& q, int i, int
 }
 
 // ------------------------------------------------------------------------- the two halves
+// - rho U_{i-1} g_{i-1} (top_corr): cp = C(i-1)
+__device__ __forceinline__ void sq_top_corr(const float* cp, const float gint[9], const float g[3], float rho,
+                                            float u[NV]) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) {
+    u[k] -= rho * (cp[C_A1 + k] * gint[k]);
+    u[9 + k] -= rho * (cp[C_A3 + k] * gint[k] +
+                       (cp[C_DYNU + k] * g[0] + cp[C_DYNU + 12 + k] * g[1] + cp[C_DYNU + 24 + k] * g[2]));
+  }
+}
+// - rho V_i g'_{i+1} (bot_corr): cf = C(i)
+__device__ __forceinline__ void sq_bot_corr(const float* cf, const float gint[9], const float g[3], float rho,
+                                            float u[NV]) {
+#pragma unroll
+  for (int k = 0; k < 9; ++k) u[k] -= rho * (cf[C_A2 + k] * gint[k]);
+#pragma unroll
+  for (int jv = 0; jv < 17; ++jv)
+    u[9 + jv] -= rho * (cf[C_DYNV + jv] * g[0] + cf[C_DYNV + 20 + jv] * g[1] + cf[C_DYNV + 40 + jv] * g[2]);
+}
+
 // AdmmSolver::run (qp.cpp:156-190) for the agent of this lane, top half (nodes 0..m): forward
-// sweep, the middle node, backward sweep, exactly as admm() (rmpc_admm.cuh) but with the agent
-// in the lane and the node-vector index in registers.  Returns the first iteration with a
-// non-finite iterate (or INT_MAX).
-__device__ int sq_admm_top(const KParams& P, const Sq& q, const AdmmConst& K) {
+// sweep with the middle node as its last step, backward sweep with node 0's own rows as its
+// last step -- admm() (rmpc_admm.cuh) with the agent in the lane and the node-vector index in
+// registers, one copy of each step in the code.  Returns the first iteration with a non-finite
+// iterate (or INT_MAX).
+__device__ __forceinline__ int sq_admm_top(const KParams& P, const Sq& q, const AdmmConst& K) {
   const int NT = q.NT, m = q.m;
   const float rho = K.rho;
   int first_bad = 0x7fffffff;
@@ -403,147 +443,140 @@ __device__ int sq_admm_top(const KParams& P, const Sq& q, const AdmmConst& K) {
   for (int it = 0; it < P.n_qp; ++it) {
     const bool first = it == 0;
     bool bad = false;
-    float gint[9], g[3], tp[12];
+    float gint[9], g[3], tp[12], xn[NV];
 #pragma unroll
     for (int k = 0; k < 9; ++k) gint[k] = 0.f;
 #pragma unroll
     for (int k = 0; k < 12; ++k) tp[k] = 0.f;
     g[0] = g[1] = g[2] = 0.f;
-    // ---------------------------------------------------------------- forward i = 0..m-1
+    // ------------------------------------------------ forward i = 0..m-1, then the middle i = m
 #pragma unroll 1
-    for (int i = 0; i < m; ++i) {
+    for (int i = 0; i <= m; ++i) {
+      const bool mid = i == m;
       float ti[12];
-      tq_ld<12>(q.slab(i) + SQ_TI, ti);  // (waited for inside sq_rhs)
+      if (mid) {
+        tq_wait_st();
+        sq_bar(q.bar);  // the bottom half's forward sweep is done (g'_{m+1}, interval m rows)
+#pragma unroll
+        for (int k = 0; k < 12; ++k) ti[k] = q.cx(SQX_TM + k);
+      } else {
+        tq_ld<12>(q.slab(i) + SQ_TI, ti);  // (waited for inside sq_rhs)
+      }
       float u[NV];
       sq_rhs(P, q, i, i, ti, tp, u);
-      {  // - rho U_{i-1} g_{i-1} (top_corr)
-        const float* cp = q.C(i - 1);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) {
-          u[k] -= rho * (cp[C_A1 + k] * gint[k]);
-          u[9 + k] -= rho * (cp[C_A3 + k] * gint[k] +
-                             (cp[C_DYNU + k] * g[0] + cp[C_DYNU + 12 + k] * g[1] + cp[C_DYNU + 24 + k] * g[2]));
-        }
-      }
-      float s[SROWS];
-      sq_matvec<SROWS>(q.MF(i), u, s);
-      tq_st<SROWS>(q.slab(i) + SQ_S, s);
-      const float* cf = q.C(i);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) gint[k] = cf[C_A2 + k] * s[k];
-      g[0] = s[26];
-      g[1] = s[27];
-      g[2] = s[28];
-#pragma unroll
-      for (int k = 0; k < 12; ++k) tp[k] = ti[k];
-    }
-    tq_wait_st();
-    sq_bar(q.bar);  // the bottom half's forward sweep is done (g'_{m+1}, interval m rows)
-    // ---------------------------------------------------------------- middle
-    float xn[NV];
-    {
-      float ti[12];
-#pragma unroll
-      for (int k = 0; k < 12; ++k) ti[k] = q.cx(SQX_TM + k);
-      float u[NV];
-      sq_rhs(P, q, m, m, ti, tp, u);
-      const float* cp = q.C(m - 1);
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        u[k] -= rho * (cp[C_A1 + k] * gint[k]);
-        u[9 + k] -= rho * (cp[C_A3 + k] * gint[k] +
-                           (cp[C_DYNU + k] * g[0] + cp[C_DYNU + 12 + k] * g[1] + cp[C_DYNU + 24 + k] * g[2]));
-      }
-      if (m + 1 < NT) {  // - rho V_m g'_{m+1} (bot_corr)
-        const float* cf = q.C(m);
+      sq_top_corr(q.C(i - 1), gint, g, rho, u);
+      if (mid && m + 1 < NT) {
         float gb[12];
 #pragma unroll
         for (int k = 0; k < 12; ++k) gb[k] = q.cx(SQX_GB + k);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) u[k] -= rho * (cf[C_A2 + k] * gb[k]);
-#pragma unroll
-        for (int jv = 0; jv < 17; ++jv)
-          u[9 + jv] -= rho * (cf[C_DYNV + jv] * gb[9] + cf[C_DYNV + 20 + jv] * gb[10] + cf[C_DYNV + 40 + jv] * gb[11]);
+        sq_bot_corr(q.C(m), gb, gb + 9, rho, u);
       }
-      sq_matvec<NV>(q.MF(m), u, xn);
+      sq_matvec_tm(q.MF(i), u, q.slab(i) + SQ_S, mid ? 7 : 8);
+      tq_wait_st();
+      if (!mid) {
+        float s9[9], s3[3];
+        tq_ld<9>(q.slab(i) + SQ_S, s9);
+        tq_ld<3>(q.slab(i) + SQ_S + 26, s3);
+        tq_wait_ld();
+        tq_fence<9>(s9);
+        tq_fence<3>(s3);
+        const float* cf = q.C(i);
 #pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        bad = bad || !isfinite(xn[j]);
-        q.cx(SQX_XM + j) = xn[j];
+        for (int k = 0; k < 9; ++k) gint[k] = cf[C_A2 + k] * s9[k];
+        g[0] = s3[0];
+        g[1] = s3[1];
+        g[2] = s3[2];
+#pragma unroll
+        for (int k = 0; k < 12; ++k) tp[k] = ti[k];
+      } else {
+        tq_ld<NV>(q.slab(m) + SQ_S, xn);
+        tq_wait_ld();
+        tq_fence<NV>(xn);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          bad = bad || !isfinite(xn[j]);
+          q.cx(SQX_XM + j) = xn[j];
+        }
       }
     }
-    sq_bar(q.bar);
-    // ---------------------------------------------------------------- backward i = m-1..0
+    sq_bar(q.bar);  // x~_m published
+    // ------------------------------------------------ backward i = m-1..0, then node 0's rows
 #pragma unroll 1
-    for (int i = m - 1; i >= 0; --i) {
-      const float* cf = q.C(i);
-      float s[SROWS], ti[12];
-      tq_ld<SROWS>(q.slab(i) + SQ_S, s);
-      tq_ld<12>(q.slab(i) + SQ_TI, ti);
-      // xi_k = a2_k (a1_k x[q_k] + a3_k x[qd_k]) = a2_k dl_k; xi_{9+b} = u_b . x_{i+1}[qd]
-      float dl[9], xi[12];
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        dl[k] = cf[C_A1 + k] * xn[k] + cf[C_A3 + k] * xn[NQ + k];
-        xi[k] = cf[C_A2 + k] * dl[k];
-      }
-#pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        float a0 = 0.f, a1 = 0.f;
+    for (int i = m - 1; i >= -1; --i) {
+      float xc[NV];
+      if (i >= 0) {
+        const float* cf = q.C(i);
+        float s[SROWS], ti[12];
+        tq_ld<SROWS>(q.slab(i) + SQ_S, s);
+        tq_ld<12>(q.slab(i) + SQ_TI, ti);
+        // xi_k = a2_k (a1_k x[q_k] + a3_k x[qd_k]) = a2_k dl_k; xi_{9+b} = u_b . x_{i+1}[qd]
+        float dl[9], xi[12];
 #pragma unroll
         for (int k = 0; k < 9; ++k) {
-          if (k & 1) a1 = fmaf(cf[C_DYNU + 12 * bb + k], xn[NQ + k], a1);
-          else a0 = fmaf(cf[C_DYNU + 12 * bb + k], xn[NQ + k], a0);
+          dl[k] = cf[C_A1 + k] * xn[k] + cf[C_A3 + k] * xn[NQ + k];
+          xi[k] = cf[C_A2 + k] * dl[k];
         }
-        xi[9 + bb] = a0 + a1;
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          float a0 = 0.f, a1 = 0.f;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) {
+            if (k & 1) a1 = fmaf(cf[C_DYNU + 12 * bb + k], xn[NQ + k], a1);
+            else a0 = fmaf(cf[C_DYNU + 12 * bb + k], xn[NQ + k], a0);
+          }
+          xi[9 + bb] = a0 + a1;
+        }
+#pragma unroll
+        for (int r = 0; r < 12; ++r) q.pv(q.XS(r)) = xi[r];
+        // x~_i = s_i - rho (S_i^-1[:, 0..8] xi_int + W_i xi_dyn): by symmetry rows 0..8 and 26..28
+        const float* M = q.MF(i);
+        float acc[NV];
+#pragma unroll
+        for (int j = 0; j < NV; ++j) acc[j] = 0.f;
+        sq_axpy_tm(q, M, 9, 12, acc);
+        tq_wait_ld();
+        tq_fence<SROWS>(s);
+        tq_fence<12>(ti);
+#pragma unroll
+        for (int j = 0; j < NV; ++j) {
+          xc[j] = s[j] - rho * acc[j];
+          bad = bad || !isfinite(xc[j]);
+        }
+        // z~: integration row k = a2 x~_i[q_k] + dl_k; dynamics row b = g_b - rho (W_b^T xi_int + G_b xi_dyn) + xi_b
+#pragma unroll
+        for (int k = 0; k < 9; ++k) {
+          const float zt = fmaf(cf[C_A2 + k], xc[k], dl[k]);
+          sq_rupd_eq(ti[k], q.LO(i, k), first, zt, K);
+          bad = bad || !isfinite(zt);
+        }
+#pragma unroll
+        for (int bb = 0; bb < 3; ++bb) {
+          float a = 0.f;
+#pragma unroll
+          for (int k = 0; k < 9; ++k) a = fmaf(M[(26 + bb) * SQ_MROW + k], xi[k], a);
+#pragma unroll
+          for (int b2 = 0; b2 < 3; ++b2) a = fmaf(cf[C_G + 3 * bb + b2], xi[9 + b2], a);
+          const float zt = s[26 + bb] - rho * a + xi[9 + bb];
+          sq_rupd_eq(ti[9 + bb], q.LO(i, 9 + bb), first, zt, K);
+          bad = bad || !isfinite(zt);
+        }
+        tq_st<NV>(q.slab(i) + SQ_S, xc);
+        tq_st<12>(q.slab(i) + SQ_TI, ti);
       }
       bad = sq_finish_node(q, i + 1, i + 1, xn, first, K) || bad;  // node i+1's own rows, x
-      tq_wait_ld();
-      tq_fence<SROWS>(s);
-      tq_fence<12>(ti);
-      // x~_i = s_i - rho (S_i^-1 [:, 0..8] xi_int + W_i xi_dyn), by symmetry from rows 0..8 / 26..28
-      const float* M = q.MF(i);
-      float acc[NV];
-#pragma unroll
-      for (int j = 0; j < NV; ++j) acc[j] = 0.f;
-      sq_axpy_rows<0, 9>(M, xi, acc);
-      sq_axpy_rows<26, 3>(M, xi + 9, acc);
-#pragma unroll
-      for (int j = 0; j < NV; ++j) {
-        xn[j] = s[j] - rho * acc[j];
-        bad = bad || !isfinite(xn[j]);
-      }
-      // z~: integration row k = a2 x~_i[q_k] + dl_k; dynamics row b = g_b - rho (W_b^T xi_int + G_b xi_dyn) + xi_b
-#pragma unroll
-      for (int k = 0; k < 9; ++k) {
-        const float zt = fmaf(cf[C_A2 + k], xn[k], dl[k]);
-        sq_rupd_eq(ti[k], q.LO(i, k), first, zt, K);
-        bad = bad || !isfinite(zt);
-      }
-#pragma unroll
-      for (int bb = 0; bb < 3; ++bb) {
-        float a = 0.f;
-#pragma unroll
-        for (int k = 0; k < 9; ++k) a = fmaf(M[(26 + bb) * NV + k], xi[k], a);
-#pragma unroll
-        for (int b2 = 0; b2 < 3; ++b2) a = fmaf(cf[C_G + 3 * bb + b2], xi[9 + b2], a);
-        const float zt = s[26 + bb] - rho * a + xi[9 + bb];
-        sq_rupd_eq(ti[9 + bb], q.LO(i, 9 + bb), first, zt, K);
-        bad = bad || !isfinite(zt);
-      }
-      tq_st<NV>(q.slab(i) + SQ_S, xn);
-      tq_st<12>(q.slab(i) + SQ_TI, ti);
       tq_wait_st();
+      if (i >= 0) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) xn[j] = xc[j];
+      }
     }
-    bad = sq_finish_node(q, 0, 0, xn, first, K) || bad;
-    tq_wait_st();
     if (bad && first_bad > it) first_bad = it;
   }
   return first_bad;
 }
 
 // Bottom half (nodes m+1..T-1), mirrored recurrences (T_i = D_i - rho^2 V_i G'_i V_i^T).
-__device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
+__device__ __forceinline__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
   const int NT = q.NT, m = q.m;
   const float rho = K.rho;
   int first_bad = 0x7fffffff;
@@ -571,23 +604,21 @@ __device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
       }
       float u[NV];
       sq_rhs(P, q, i, b, ti, tp, u);
-      {  // - rho V_i g'_{i+1} (bot_corr)
-        const float* cf = q.C(i);
-#pragma unroll
-        for (int k = 0; k < 9; ++k) u[k] -= rho * (cf[C_A2 + k] * gint[k]);
-#pragma unroll
-        for (int jv = 0; jv < 17; ++jv)
-          u[9 + jv] -= rho * (cf[C_DYNV + jv] * g[0] + cf[C_DYNV + 20 + jv] * g[1] + cf[C_DYNV + 40 + jv] * g[2]);
-      }
-      float s[SROWS];
-      sq_matvec<SROWS>(q.MF(i), u, s);
-      tq_st<SROWS>(q.slab(b) + SQ_S, s);
+      sq_bot_corr(q.C(i), gint, g, rho, u);
+      sq_matvec_tm(q.MF(i), u, q.slab(b) + SQ_S, 8);
+      tq_wait_st();
+      float s18[18], s3[3];
+      tq_ld<18>(q.slab(b) + SQ_S, s18);
+      tq_ld<3>(q.slab(b) + SQ_S + 26, s3);
+      tq_wait_ld();
+      tq_fence<18>(s18);
+      tq_fence<3>(s3);
       const float* cp = q.C(i - 1);  // g'_int_k = a1_k s[q_k] + a3_k s[qd_k]
 #pragma unroll
-      for (int k = 0; k < 9; ++k) gint[k] = cp[C_A1 + k] * s[k] + cp[C_A3 + k] * s[NQ + k];
-      g[0] = s[26];
-      g[1] = s[27];
-      g[2] = s[28];
+      for (int k = 0; k < 9; ++k) gint[k] = cp[C_A1 + k] * s18[k] + cp[C_A3 + k] * s18[NQ + k];
+      g[0] = s3[0];
+      g[1] = s3[1];
+      g[2] = s3[2];
 #pragma unroll
       for (int k = 0; k < 12; ++k) ti[k] = tp[k];
     }
@@ -596,7 +627,6 @@ __device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
     q.cx(SQX_GB + 9) = g[0];
     q.cx(SQX_GB + 10) = g[1];
     q.cx(SQX_GB + 11) = g[2];
-    tq_wait_st();
     sq_bar(q.bar);
     sq_bar(q.bar);  // the middle node's x~_m is published
     // ---------------------------------------------------------------- backward i = m+1..T-1
@@ -633,15 +663,16 @@ __device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
         }
         xib[18 + bb] = a0 + a1 + a2;
       }
-      tq_wait_ld();
-      tq_fence<SROWS>(s);
-      if (i - 1 > m) tq_fence<12>(tr);
+#pragma unroll
+      for (int r = 0; r < 21; ++r) q.pv(q.XS(r)) = xib[r];
       const float* M = q.MF(i);
       float acc[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) acc[j] = 0.f;
-      sq_axpy_rows<0, 18>(M, xib, acc);
-      sq_axpy_rows<26, 3>(M, xib + 18, acc);
+      sq_axpy_tm(q, M, 18, 21, acc);
+      tq_wait_ld();
+      tq_fence<SROWS>(s);
+      if (i - 1 > m) tq_fence<12>(tr);
       float xt[NV];
 #pragma unroll
       for (int j = 0; j < NV; ++j) {
@@ -659,7 +690,7 @@ __device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
       for (int bb = 0; bb < 3; ++bb) {
         float a = 0.f;
 #pragma unroll
-        for (int k = 0; k < 18; ++k) a = fmaf(M[(26 + bb) * NV + k], xib[k], a);
+        for (int k = 0; k < 18; ++k) a = fmaf(M[(26 + bb) * SQ_MROW + k], xib[k], a);
 #pragma unroll
         for (int b2 = 0; b2 < 3; ++b2) a = fmaf(cp[C_G + 3 * bb + b2], xib[18 + b2], a);
         const float zt = xib[18 + bb] + s[26 + bb] - rho * a;
@@ -689,7 +720,7 @@ __device__ int sq_admm_bot(const KParams& P, const Sq& q, const AdmmConst& K) {
 // swing contacts (mpc.cpp:210-216); the initial-state bounds (top, mpc.cpp:126-136), all in
 // FP64 by the operations of setup_nodes / setup_dynamics / apply_scaling.  Returns whether the
 // agent's stance flags equal the squad's (a 64-bit schedule-hash collision otherwise).
-__device__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const rmpc_state& st,
+__device__ __noinline__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const rmpc_state& st,
                          const rmpc_command& cmd, const rmpc_gait& gait, const double* con_pz) {
   float zero[32];
 #pragma unroll
@@ -699,6 +730,7 @@ __device__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const
     tq_st<32>(q.slab(b), zero);
     tq_st<32>(q.slab(b) + 32, zero);
     tq_st<32>(q.slab(b) + 64, zero);
+    tq_st<SQ_SLAB - 96>(q.slab(b) + 96, zero);
   }
   if (top) tq_st<NINIT>(q.tm + SQ_TINIT, zero);
   for (int k = 0; k < q.nb * SQ_NZ; ++k) q.pv(k) = 0.f;
@@ -746,7 +778,7 @@ __device__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const
 // inverse dynamics at node 0 (mpc.cpp:305-330), the active set (optional) and the record
 // (finish_agent), lane-parallel.  fin: the squad's finish scratch (the matrices are dead).
 // Every lane runs it (the pair barriers); `write` lanes store.
-__device__ void sq_finish(const KParams& P, const Sq& q, bool top, int own, int agent, bool write, int status,
+__device__ __noinline__ void sq_finish(const KParams& P, const Sq& q, bool top, int own, int agent, bool write, int status,
                           int fail_iter, const rmpc_state& st, const rmpc_command& cmd, float* fin) {
   const int NT = q.NT, m = q.m, lane = q.lane;
   float* fx = fin;                                      // x_m, [26][32]
@@ -1095,9 +1127,9 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
       reg[L.qh + k] = entry[SL.qh + k];
     }
     for (int k = t; k <= NT; k += 64) reg[L.flags + k] = entry[SL.flags + k];
-    for (int k = t; k < NT * SROWS * NV; k += 64) {
-      const int i = k / (SROWS * NV), r = k % (SROWS * NV);
-      reg[L.mf + i * SQ_MF + r] = entry[SL.blocks + (size_t)(i * 32 + r / NV) * TCOLS + r % NV];
+    for (int k = t; k < NT * SQ_MF; k += 64) {  // rows of 28: block row r, columns 0..25; rows >= 29 zero
+      const int i = k / SQ_MF, r = (k % SQ_MF) / SQ_MROW, c = k % SQ_MROW;
+      reg[L.mf + k] = r < SROWS && c < NV ? entry[SL.blocks + (size_t)(i * 32 + r) * TCOLS + c] : 0.f;
     }
   }
   if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)

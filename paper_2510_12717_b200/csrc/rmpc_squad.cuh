@@ -36,7 +36,10 @@ constexpr int SQ_MF = 32 * SQ_MROW;  // packed node matrix: S^-1 rows 0..25, W_b
 constexpr int SQ_NXI = 21;    // private scratch: the backward step's xi (12 top, 21 bottom)
 constexpr int SQ_NZ = 20;     // z of a node's inequality rows: t0/t1 of the 4 contacts, 12 boxes
 constexpr int SQ_PRIV = 28;   // private shared elements per own node: 20 z, 4 swing lo, 4 q^ parts
-constexpr int SQ_FIN = 26 * 32 + 2 * 2 * NV * 32 + 5 * 32;  // finish scratch (reuses the matrices)
+// finish scratch (reuses the matrices): x_m, z* rows 0/1 (FP64), the bottom's partials, and per
+// warp a 32 x 27 transpose buffer that turns lane-per-agent results into contiguous records
+constexpr int SQ_FIN_XP = 26 * 32 + 2 * 2 * NV * 32 + 5 * 32;
+constexpr int SQ_FIN = SQ_FIN_XP + 2 * 32 * 27;
 
 // Shared-memory layout of one squad (floats, 16-byte aligned regions).
 struct SqLayout {
@@ -784,6 +787,7 @@ __device__ __noinline__ void sq_finish(const KParams& P, const Sq& q, bool top, 
   float* fx = fin;                                      // x_m, [26][32]
   double* fz = reinterpret_cast<double*>(fin + 26 * 32);  // z* rows of nodes 0, 1 (FP64), [2][26][32]
   float* fc = fin + 26 * 32 + 2 * 2 * NV * 32;          // bottom's prim, dual, dinf, obj (FP64)
+  float* xp = fin + SQ_FIN_XP + (top ? 0 : 32 * 27);     // this warp's transpose buffer [lane][27]
   const bool ok = status == RMPC_STATUS_OK;
   const float rho = (float)P.rho;
   const bool eqz = P.n_qp > 0;  // equality rows: z = lo after the first update
@@ -924,8 +928,18 @@ __device__ __noinline__ void sq_finish(const KParams& P, const Sq& q, bool top, 
       obj += 0.5 * w * dz * dz + w * (g - des) * dz;
       dinf = fmaxf(dinf, fabsf(e * x[j]));
       const double zv = g + dz;  // z* = guess + dz (mpc.cpp:308-314)
-      if (write && ok && P.z_out) P.z_out[((size_t)agent * NT + i) * NV + j] = (float)zv;
+      xp[lane * 27 + j] = ok ? (float)zv : 0.f;  // (a failed agent's z* is zero)
       if (i < 2) fz[(i * NV + j) * 32 + lane] = zv;
+    }
+    if (P.z_out) {  // node i of the warp's agents: one contiguous 26-float row per agent
+      __syncwarp();
+      const unsigned wm = __ballot_sync(FULL, write);
+#pragma unroll 1
+      for (int l = 0; l < 32; ++l) {
+        const int al = __shfl_sync(FULL, agent, l);
+        if (((wm >> l) & 1u) && lane < NV) P.z_out[((size_t)al * NT + i) * NV + lane] = xp[l * 27 + lane];
+      }
+      __syncwarp();
     }
     if (P.act_out && write) {  // final active set (scaled space)
       uint8_t* ao = P.act_out + (size_t)agent * (NT + 1) * NSLOT + (size_t)(i + 1) * NSLOT;
@@ -987,10 +1001,23 @@ __device__ __noinline__ void sq_finish(const KParams& P, const Sq& q, bool top, 
     }
     for (int k = 0; k < 8; ++k) out.f0[k] = (float)F[k];
   }
-  if (write) {
-    if (!ok && P.z_out)
-      for (int k = 0; k < NT * NV; ++k) P.z_out[(size_t)agent * NT * NV + k] = 0.f;
-    P.out[agent] = out;
+  // the records through shared memory (both transpose buffers; the bottom's z* rows are out):
+  // one contiguous 140-byte record per agent
+  constexpr int RW = (int)(sizeof(rmpc_solution) / 4);  // 35 words, odd stride: no bank conflicts
+  float* rs = fin + SQ_FIN_XP;
+  const float* o = reinterpret_cast<const float*>(&out);
+#pragma unroll
+  for (int k = 0; k < RW; ++k) rs[lane * RW + k] = o[k];
+  __syncwarp();
+  const unsigned wm = __ballot_sync(FULL, write);
+#pragma unroll 1
+  for (int l = 0; l < 32; ++l) {
+    const int al = __shfl_sync(FULL, agent, l);
+    if ((wm >> l) & 1u) {
+      float* dst = reinterpret_cast<float*>(P.out + al);
+      dst[lane] = rs[l * RW + lane];
+      if (lane < RW - 32) dst[32 + lane] = rs[l * RW + 32 + lane];
+    }
   }
 }
 
@@ -1127,9 +1154,15 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
       reg[L.qh + k] = entry[SL.qh + k];
     }
     for (int k = t; k <= NT; k += 64) reg[L.flags + k] = entry[SL.flags + k];
-    for (int k = t; k < NT * SQ_MF; k += 64) {  // rows of 28: block row r, columns 0..25; rows >= 29 zero
+    // rows of 28: block row r, columns 0..25 (the inverse symmetrized: the backward sweep reads
+    // its columns as rows); rows >= 29 zero
+    for (int k = t; k < NT * SQ_MF; k += 64) {
       const int i = k / SQ_MF, r = (k % SQ_MF) / SQ_MROW, c = k % SQ_MROW;
-      reg[L.mf + k] = r < SROWS && c < NV ? entry[SL.blocks + (size_t)(i * 32 + r) * TCOLS + c] : 0.f;
+      const float* blk = entry + SL.blocks + (size_t)i * 32 * TCOLS;
+      float v = 0.f;
+      if (r < NV && c < NV) v = 0.5f * (blk[r * TCOLS + c] + blk[c * TCOLS + r]);
+      else if (r < SROWS && c < NV) v = blk[r * TCOLS + c];
+      reg[L.mf + k] = v;
     }
   }
   if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)

@@ -330,24 +330,33 @@ def test_two_chunked_shards_on_one_device_match_one_shard():
 
 @pytest.mark.parametrize("T,kind,n", [(10, "random", 4096), (10, "mixed", 2048), (5, "random", 2048),
                                       (20, "mixed", 1024), (3, "mixed", 512), (12, "random", 999),
-                                      (32, "mixed", 64)])
-def test_schedule_sharing_is_bit_identical(T, kind, n):
-    """Cold start: the schedule-shared factorization (rmpc_set_schedule_sharing, default on)
-    gives exactly the per-agent result -- the matrices, Ruiz scales and factor depend only on
-    the stance schedule (mpc.cpp:266-276) -- including next to a failing agent, and on the
-    host (chunked) and device paths."""
+                                      (32, "mixed", 64), (2, "mixed", 300), (7, "random", 777)])
+def test_schedule_sharing(T, kind, n):
+    """Cold start: the matrices, Ruiz scales and factor depend only on the stance schedule
+    (mpc.cpp:266-276), so each distinct schedule is factorized once (rmpc_set_schedule_sharing).
+    Level 1 (warp-pair CTAs of one schedule) gives exactly the per-agent bytes; level 2 (the
+    default: lane-per-agent squads for T <= 10, level 1 beyond) runs the same iterates with the
+    agent in the lane -- equal to the per-agent solve within the parity gates, identical statuses
+    (a failing agent next to working ones included), and identical bytes on the host (chunked)
+    and device paths."""
     import torch
     m, s = default_model(), default_settings(T)
     st, cm, ga = R.synthetic_batch(n, kind, seed=T, model=m, settings=s)
     st = st.copy()
     st[5, 3] = np.nan
     br = R.BatchRunner(n, m, s)
-    a, za = br.solve(st, cm, ga, want_z=True)
-    br.set_schedule_sharing(False)
-    b, zb = br.solve(st, cm, ga, want_z=True)
-    assert a.tobytes() == b.tobytes() and za.tobytes() == zb.tobytes()
+    sols = {}
+    for level in (2, 1, 0):
+        br.set_schedule_sharing(level)
+        sols[level] = br.solve(st, cm, ga, want_z=True)
+    (a, za), (p, zp), (b, zb) = sols[2], sols[1], sols[0]
+    assert p.tobytes() == b.tobytes() and zp.tobytes() == zb.tobytes()
     assert a["status"][5] == STATUS_NONFINITE_INPUT
-    br.set_schedule_sharing(True)
+    c = compare(a, b, za, zb)
+    print(f"T={T} {kind}: squads vs per-agent", summary(c))
+    check(c, f"squads vs per-agent T={T} {kind}")
+    assert c["z"].max() <= 1e-3
+    br.set_schedule_sharing(2)
     dev = torch.device("cuda:0")
     d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
     out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)

@@ -118,6 +118,7 @@ struct KParams {
   const int32_t* agent_list; // rti_kernel: solve these agents (NULL = 0..n_agents-1)
   int32_t* n_list;           // its length (device); rti_shared_kernel appends fallbacks
   int32_t* list_out;         // = agent_list, writable (fallbacks of rti_shared_kernel)
+  float* sqpack;             // per schedule id: the squad image (rti_squad_kernel, sq_pack_kernel)
 };
 
 // One schedule's entry in the store (floats, 16-byte aligned regions): the Ruiz-scaled
@@ -271,6 +272,50 @@ inline CtaShapeShared cta_shape_shared(int NT, int cap = SHARED_AGENTS) {
   return c;
 }
 
+// ------------------------------------------------------------------------- squads
+// Lane-per-agent schedule-shared solve (rmpc_squad.cuh).
+constexpr int SQ_MAXT = 10;   // horizons served by squads (5 node slabs of 96 TMEM columns per thread)
+constexpr int SQ_SLAB = 98;   // TMEM columns per own node
+constexpr int SQ_X = 0;       // x (26)
+constexpr int SQ_S = 26;      // s / x~ (26), then gamma (3) and 3 spare (the matvec writes 32 rows)
+constexpr int SQ_TI = 58;     // t of the node's interval rows, slots 0..11
+constexpr int SQ_TO = 70;     // t of the node's own rows, slots 12..39
+constexpr int SQ_TINIT = 490; // top thread: t of the 18 initial-state rows (block -1)
+constexpr int SQ_MROW = 28;   // floats per packed matrix row (26 + 2 zero: 16-byte aligned rows)
+constexpr int SQ_MF = 32 * SQ_MROW;  // packed node matrix: S^-1 rows 0..25, W_b^T rows 26..28, zero rows 29..31
+constexpr int SQ_NXI = 21;    // private scratch: the backward step's xi (12 top, 21 bottom)
+constexpr int SQ_NZ = 20;     // z of a node's inequality rows: t0/t1 of the 4 contacts, 12 boxes
+constexpr int SQ_PRIV = 28;   // private shared elements per own node: 20 z, 4 swing lo, 4 q^ parts
+// finish scratch (reuses the matrices): x_m, z* rows 0/1 (FP64), the bottom's partials, and per
+// warp a 32 x 27 transpose buffer that turns lane-per-agent results into contiguous records
+constexpr int SQ_FIN_XP = 26 * 32 + 2 * 2 * NV * 32 + 5 * 32;
+constexpr int SQ_FIN = SQ_FIN_XP + 2 * 32 * 27;
+
+// Shared-memory layout of one squad (floats, 16-byte aligned regions).
+struct SqLayout {
+  int coef, mf, lo, hi, d, e, qh, flags, priv, cross, total, priv_warp;
+};
+__host__ __device__ inline SqLayout sq_layout(int NT) {
+  SqLayout L;
+  int o = 0;
+  const int nb = nodes_per_warp(NT);
+  L.coef = o;  o += (NT + 1) * C_SIZE;  // block -1 first
+  L.mf = o;    o += NT * SQ_MF > SQ_FIN ? NT * SQ_MF : SQ_FIN;
+  L.lo = o;    o += (NT + 1) * NSLOT;   // the schedule's scaled bounds (block -1 first)
+  L.hi = o;    o += (NT + 1) * NSLOT;
+  L.d = o;     o += (NT + 1) * NSLOT;   // Ruiz row scales
+  L.e = o;     o += align4(NT * NV);    // Ruiz column scales
+  L.qh = o;    o += align4(NT * NV);    // the schedule's scaled q^
+  L.flags = o; o += align4(NT + 1);     // stance bits per node, then the factorization status
+  L.priv_warp = 32 * (nb * SQ_PRIV + NINIT + SQ_NXI);
+  L.priv = o;  o += 2 * L.priv_warp;
+  L.cross = o; o += 32 * 56;
+  L.total = o;
+  return L;
+}
+inline int sq_smem_bytes(int NT) { return 2 * sq_layout(NT).total * 4; }
+inline bool sq_supported(int NT) { return NT >= 2 && NT <= SQ_MAXT && sq_smem_bytes(NT) <= 227 * 1024 - 256; }
+
 }  // namespace rmpc_dev
 
 // Launch the fused kernel for params.n_agents agents on `stream` (implemented in
@@ -292,6 +337,7 @@ struct RmpcSchedBuffers {
   int32_t* ulist;             // unshared agents (and fallbacks)
   int32_t* n_unshared;
   float* store;               // cap x store_layout(T).total floats
+  float* sqpack;              // cap x sq_layout(T).priv floats (squads), or NULL
   int32_t slots, cap, agents;
 };
 // The whole cold-start solve with schedule sharing for params.n_agents agents on `stream`:

@@ -778,7 +778,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   F.tail_agents = 0;
   rc = launch_variant(F, c1, F.full_ctas, st);
   if (rc != 0) return rc;
-  const bool squads = variant == 2 && sq_supported(NT);
+  const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
   sched_scan_kernel<<<1, 1024, 0, st>>>(b, squads ? 32 : cs.agents);
   sched_scatter_kernel<<<blocks, 256, 0, st>>>(params, b);
@@ -800,6 +800,8 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   const int grid_s = (n + cs.agents - 1) / cs.agents + std::min(b.cap, n);
   if (squads) {  // lane-per-agent squads, two per CTA (grid: an upper bound of sum ceil(count / 32) / 2)
     S.agents_per_cta = 32;
+    S.sqpack = b.sqpack;
+    sq_pack_kernel<<<b.cap, 256, 0, st>>>(S);
     const int nsq = (n + 31) / 32 + std::min(b.cap, n);
     static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
       const char* e = getenv("RMPC_SQUAD_SOLO");

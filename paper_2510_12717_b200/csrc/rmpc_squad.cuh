@@ -24,47 +24,7 @@ namespace rmpc_dev {
 #define FULL 0xffffffffu
 #endif
 
-constexpr int SQ_MAXT = 10;   // horizons served by squads (5 node slabs of 96 TMEM columns per thread)
-constexpr int SQ_SLAB = 98;   // TMEM columns per own node
-constexpr int SQ_X = 0;       // x (26)
-constexpr int SQ_S = 26;      // s / x~ (26), then gamma (3) and 3 spare (the matvec writes 32 rows)
-constexpr int SQ_TI = 58;     // t of the node's interval rows, slots 0..11
-constexpr int SQ_TO = 70;     // t of the node's own rows, slots 12..39
-constexpr int SQ_TINIT = 490; // top thread: t of the 18 initial-state rows (block -1)
-constexpr int SQ_MROW = 28;   // floats per packed matrix row (26 + 2 zero: 16-byte aligned rows)
-constexpr int SQ_MF = 32 * SQ_MROW;  // packed node matrix: S^-1 rows 0..25, W_b^T rows 26..28, zero rows 29..31
-constexpr int SQ_NXI = 21;    // private scratch: the backward step's xi (12 top, 21 bottom)
-constexpr int SQ_NZ = 20;     // z of a node's inequality rows: t0/t1 of the 4 contacts, 12 boxes
-constexpr int SQ_PRIV = 28;   // private shared elements per own node: 20 z, 4 swing lo, 4 q^ parts
-// finish scratch (reuses the matrices): x_m, z* rows 0/1 (FP64), the bottom's partials, and per
-// warp a 32 x 27 transpose buffer that turns lane-per-agent results into contiguous records
-constexpr int SQ_FIN_XP = 26 * 32 + 2 * 2 * NV * 32 + 5 * 32;
-constexpr int SQ_FIN = SQ_FIN_XP + 2 * 32 * 27;
-
-// Shared-memory layout of one squad (floats, 16-byte aligned regions).
-struct SqLayout {
-  int coef, mf, lo, hi, d, e, qh, flags, priv, cross, total, priv_warp;
-};
-__host__ __device__ inline SqLayout sq_layout(int NT) {
-  SqLayout L;
-  int o = 0;
-  const int nb = nodes_per_warp(NT);
-  L.coef = o;  o += (NT + 1) * C_SIZE;  // block -1 first
-  L.mf = o;    o += NT * SQ_MF > SQ_FIN ? NT * SQ_MF : SQ_FIN;
-  L.lo = o;    o += (NT + 1) * NSLOT;   // the schedule's scaled bounds (block -1 first)
-  L.hi = o;    o += (NT + 1) * NSLOT;
-  L.d = o;     o += (NT + 1) * NSLOT;   // Ruiz row scales
-  L.e = o;     o += align4(NT * NV);    // Ruiz column scales
-  L.qh = o;    o += align4(NT * NV);    // the schedule's scaled q^
-  L.flags = o; o += align4(NT + 1);     // stance bits per node, then the factorization status
-  L.priv_warp = 32 * (nb * SQ_PRIV + NINIT + SQ_NXI);
-  L.priv = o;  o += 2 * L.priv_warp;
-  L.cross = o; o += 32 * 56;
-  L.total = o;
-  return L;
-}
-inline int sq_smem_bytes(int NT) { return 2 * sq_layout(NT).total * 4; }
-inline bool sq_supported(int NT) { return NT >= 2 && NT <= SQ_MAXT && sq_smem_bytes(NT) <= 227 * 1024 - 256; }
+// Layout constants and sq_layout: rmpc_device.cuh.
 
 // Cross-thread elements of an agent (shared by its two threads), [element][lane].
 constexpr int SQX_XM = 0;     // x~_m of the middle node (top -> bottom)
@@ -263,7 +223,7 @@ __device__ __forceinline__ void sq_colview(const float* cf, const float* cp, con
 // bulk of every node step, and a fully unrolled copy per call site overflows the instruction
 // cache at one warp per scheduler.
 __device__ __forceinline__ void sq_matvec_tm(const float* M, const float u[NV], uint32_t dst, int nch) {
-#pragma unroll 1
+#pragma unroll 2
   for (int c = 0; c < nch; ++c) {
     const float4* R = reinterpret_cast<const float4*>(M + 4 * SQ_MROW * c);
     float a[4][2];
@@ -292,7 +252,7 @@ __device__ __forceinline__ void sq_matvec_tm(const float* M, const float u[NV], 
 // acc[0..25] += sum_r xs[r] M[row(r)][:], row(r) = r < NQR ? r : 26 + r - NQR, for r < NR; the
 // coefficients come from the lane's private scratch (shared memory), the rows as broadcasts.
 __device__ __forceinline__ void sq_axpy_tm(const Sq& q, const float* M, int nqr, int nr, float acc[NV]) {
-#pragma unroll 1
+#pragma unroll 3
   for (int r = 0; r < nr; ++r) {
     const float c = q.pv(q.XS(r));
     const float4* R = reinterpret_cast<const float4*>(M + SQ_MROW * (r < nqr ? r : 26 + r - nqr));
@@ -1136,34 +1096,12 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
   const StoreLayout SL = store_layout(NT);
   const int sqi = w >> 1;
   float* reg = smem + sqi * L.total;
-  if (s_cnt[sqi] > 0) {  // this squad's schedule entry into its region (64 threads)
+  if (s_cnt[sqi] > 0) {  // this squad's schedule image (sq_pack_kernel) into its region (64 threads)
+    const float4* src = reinterpret_cast<const float4*>(P.sqpack + (size_t)s_g[sqi] * L.priv);
+    float4* dst = reinterpret_cast<float4*>(reg);
     const int t = tid & 63;
-    const float* entry = P.store + (size_t)s_g[sqi] * P.store_stride;
-    const float4* c4 = reinterpret_cast<const float4*>(entry + SL.coef);
-    float4* r4 = reinterpret_cast<float4*>(reg + L.coef);
-    for (int k = t; k < (NT + 1) * C_SIZE / 4; k += 64) r4[k] = c4[k];
-    const float2* rw = reinterpret_cast<const float2*>(entry + SL.rows);
-    for (int k = t; k < (NT + 1) * NSLOT; k += 64) {
-      const float2 lh = rw[k];
-      reg[L.lo + k] = lh.x;
-      reg[L.hi + k] = lh.y;
-      reg[L.d + k] = entry[SL.d + k];
-    }
-    for (int k = t; k < NT * NV; k += 64) {
-      reg[L.e + k] = entry[SL.e + k];
-      reg[L.qh + k] = entry[SL.qh + k];
-    }
-    for (int k = t; k <= NT; k += 64) reg[L.flags + k] = entry[SL.flags + k];
-    // rows of 28: block row r, columns 0..25 (the inverse symmetrized: the backward sweep reads
-    // its columns as rows); rows >= 29 zero
-    for (int k = t; k < NT * SQ_MF; k += 64) {
-      const int i = k / SQ_MF, r = (k % SQ_MF) / SQ_MROW, c = k % SQ_MROW;
-      const float* blk = entry + SL.blocks + (size_t)i * 32 * TCOLS;
-      float v = 0.f;
-      if (r < NV && c < NV) v = 0.5f * (blk[r * TCOLS + c] + blk[c * TCOLS + r]);
-      else if (r < SROWS && c < NV) v = blk[r * TCOLS + c];
-      reg[L.mf + k] = v;
-    }
+#pragma unroll 4
+    for (int k = t; k < L.priv / 4; k += 64) dst[k] = src[k];
   }
   if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)
     double gq[9], gqd[9];
@@ -1187,6 +1125,38 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   if (w == 0) asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tb) : "memory");
+}
+
+// The squad image of every stored schedule (the region [0, L.priv) of sq_layout): coefficients,
+// the factor's node blocks packed as 28-float rows (inverse symmetrized: the backward sweep reads
+// its columns as rows; rows >= 29 zero), bounds, scales, q^, flags.  One CTA per schedule id.
+__global__ void sq_pack_kernel(const KParams P) {
+  const int g = blockIdx.x;
+  if (g >= min(*P.n_sched, P.store_cap)) return;
+  const int NT = P.NT;
+  const SqLayout L = sq_layout(NT);
+  const StoreLayout SL = store_layout(NT);
+  const float* entry = P.store + (size_t)g * P.store_stride;
+  float* reg = P.sqpack + (size_t)g * L.priv;
+  for (int k = threadIdx.x; k < (NT + 1) * C_SIZE; k += blockDim.x) reg[L.coef + k] = entry[SL.coef + k];
+  for (int k = threadIdx.x; k < (NT + 1) * NSLOT; k += blockDim.x) {
+    reg[L.lo + k] = entry[SL.rows + 2 * k];
+    reg[L.hi + k] = entry[SL.rows + 2 * k + 1];
+    reg[L.d + k] = entry[SL.d + k];
+  }
+  for (int k = threadIdx.x; k < NT * NV; k += blockDim.x) {
+    reg[L.e + k] = entry[SL.e + k];
+    reg[L.qh + k] = entry[SL.qh + k];
+  }
+  for (int k = threadIdx.x; k <= NT; k += blockDim.x) reg[L.flags + k] = entry[SL.flags + k];
+  for (int k = threadIdx.x; k < NT * SQ_MF; k += blockDim.x) {
+    const int i = k / SQ_MF, r = (k % SQ_MF) / SQ_MROW, c = k % SQ_MROW;
+    const float* blk = entry + SL.blocks + (size_t)i * 32 * TCOLS;
+    float v = 0.f;
+    if (r < NV && c < NV) v = 0.5f * (blk[r * TCOLS + c] + blk[c * TCOLS + r]);
+    else if (r < SROWS && c < NV) v = blk[r * TCOLS + c];
+    reg[L.mf + k] = v;
+  }
 }
 
 }  // namespace rmpc_dev

@@ -683,7 +683,7 @@ __device__ __forceinline__ int sq_admm_bot(const KParams& P, const Sq& q, const 
 // swing contacts (mpc.cpp:210-216); the initial-state bounds (top, mpc.cpp:126-136), all in
 // FP64 by the operations of setup_nodes / setup_dynamics / apply_scaling.  Returns whether the
 // agent's stance flags equal the squad's (a 64-bit schedule-hash collision otherwise).
-__device__ __noinline__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const rmpc_state& st,
+__device__ __forceinline__ bool sq_setup(const KParams& P, const Sq& q, bool top, int own, const rmpc_state& st,
                          const rmpc_command& cmd, const rmpc_gait& gait, const double* con_pz) {
   float zero[32];
 #pragma unroll
@@ -741,7 +741,7 @@ __device__ __noinline__ bool sq_setup(const KParams& P, const Sq& q, bool top, i
 // inverse dynamics at node 0 (mpc.cpp:305-330), the active set (optional) and the record
 // (finish_agent), lane-parallel.  fin: the squad's finish scratch (the matrices are dead).
 // Every lane runs it (the pair barriers); `write` lanes store.
-__device__ __noinline__ void sq_finish(const KParams& P, const Sq& q, bool top, int own, int agent, bool write, int status,
+__device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool top, int own, int agent, bool write, int status,
                           int fail_iter, const rmpc_state& st, const rmpc_command& cmd, float* fin) {
   const int NT = q.NT, m = q.m, lane = q.lane;
   float* fx = fin;                                      // x_m, [26][32]
@@ -1039,9 +1039,9 @@ __device__ void sq_solve(const KParams& P, float* reg, uint32_t tm, int sqi, int
     const AdmmConst K{(float)P.rho, (float)P.sigma, (float)P.alpha, 1.f - (float)P.alpha, (float)(1.0 / P.rho)};
     const int fb = top ? sq_admm_top(P, q, K) : sq_admm_bot(P, q, K);
     q.cx(SQX_BAD + (top ? 0 : 1)) = __int_as_float(fb);
-    sq_prof(P, mine && top, 5, t0);
   }
   sq_bar(q.bar);  // both halves done: the matrices are dead, their space is the finish scratch
+  if (fstat == 1) sq_prof(P, mine && top, 5, t0);
   if (fstat == 1) {
     const int f0 = __float_as_int(q.cx(SQX_BAD)), f1 = __float_as_int(q.cx(SQX_BAD + 1));
     const int f = f0 < f1 ? f0 : f1;

@@ -398,7 +398,7 @@ def main():
     import torch
     import paper_2510_12717_b200 as R
     from paper_2510_12717_b200.abi import SOLUTION_DTYPE
-    from paper_2510_12717_b200.runtime import fma_peak_tflops
+    from paper_2510_12717_b200.runtime import fma_peak_tflops, kernel_launches
 
     rank, world, local = dist_env()
     torch.cuda.set_device(local)
@@ -454,6 +454,7 @@ def main():
     barrier()
     torch.cuda.synchronize()
     clocks.start()
+    launches0 = kernel_launches()
     with torch.cuda.stream(stream):
         for k in range(args.steps):
             flush.zero_()
@@ -464,6 +465,7 @@ def main():
     torch.cuda.synchronize()
     barrier()
     clk = clocks.stop()
+    launches = kernel_launches() - launches0
     step_ms_local = [a.elapsed_time(b) for a, b in ev]
     step_ms = max_over_ranks(step_ms_local)
     ms_per_step = float(np.mean(step_ms))
@@ -490,6 +492,17 @@ def main():
     e2e_nz_ms = e2e(False)
     e2e_ms = e2e(True)
     tm = br.last_timing()
+    # the same through the structure-of-arrays boundary (rmpc_solve_soa): one pinned FP32 block
+    # of 28 component rows, 112 B per agent H2D instead of 224
+    h_soa = pin(R.to_soa(st, cm, ga))
+    for _ in range(2):
+        br.solve_soa(h_soa, out=h_out, z_out=h_z)
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        br.solve_soa(h_soa, out=h_out, z_out=h_z)
+    soa_ms = float(max_over_ranks([(time.perf_counter() - t0) * 1e3 / args.steps])[0])
+    tm_soa = br.last_timing()
     ok = int(np.sum(h_out["status"] == 0))
     # per-stage split of the kernel (clock64 at the reference's 7 stage boundaries, summed over
     # agents; the reference's TimingReport / benchmark CSV analogue, batch.cpp:64-77, 81-142)
@@ -576,10 +589,20 @@ def main():
                     "without_z_star": {"value": n_total / (e2e_nz_ms * 1e-3), "ms_per_step": e2e_nz_ms,
                                        "d2h_bytes_per_step": n * 140},
                     "last_timing_ms": {"h2d": tm["h2d_ms"], "kernel": tm["kernel_ms"], "d2h": tm["d2h_ms"],
-                                       "total": tm["total_ms"]}},
+                                       "total": tm["total_ms"]},
+                    "soa": {"value": n_total / (soa_ms * 1e-3), "ms_per_step": soa_ms,
+                            "h2d_bytes_per_step": n * 28 * 4, "d2h_bytes_per_step": n * (140 + T * 26 * 4),
+                            "api": "rmpc_solve_soa (C ABI): one pinned FP32 block of 28 component rows in, "
+                                   "unpacked on the device; records + z* out as above",
+                            "last_timing_ms": {"h2d": tm_soa["h2d_ms"], "kernel": tm_soa["kernel_ms"],
+                                               "d2h": tm_soa["d2h_ms"], "total": tm_soa["total_ms"]}}},
             "roofline": roofline,
             "stage_split": stage_split,
-            "gpu_launches": args.steps,
+            "gpu_launches": launches,
+            "gpu_launches_note": "solve-path kernels the library launched in the timed region "
+                                 "(rmpc_kernel_launches): per step the schedule pass (key, count, scan, "
+                                 "scatter), one factorization per schedule, the schedule images, the "
+                                 "squad solve and the per-agent list solve",
             "status_ok": ok, "clocks": clk, "cpu_baseline": cpu,
             "closed_loop": closed,
             "ppo_update": ppo,

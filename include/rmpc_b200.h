@@ -159,6 +159,34 @@ int32_t rmpc_solve_device_sharded(rmpc_handle* handle, const rmpc_state* const* 
                                   const rmpc_solution* const* d_prev, const float* const* d_prev_z_star,
                                   rmpc_solution* const* d_out, float* const* d_z_star_out,
                                   void* const* streams);
+/* ---- structure-of-arrays boundary (north star: agents laid out SoA for coalesced HBM access) ----
+ * The same solve with the per-agent inputs as one FP32 block of RMPC_SOA_FIELDS component rows,
+ * row r holding component r of every agent: soa[r * ld + agent], ld >= n_agents.  112 bytes per
+ * agent instead of the 224 of the FP64 records.  Row order (the fields of RobotState, MpcCommand
+ * and GaitState, robot.hpp:52-55, mpc.hpp:59-63, gait.hpp:16-29): */
+#define RMPC_SOA_Q 0              /* q[0..8]       rows 0..8   */
+#define RMPC_SOA_QD 9             /* qd[0..8]      rows 9..17  */
+#define RMPC_SOA_HEIGHT 18        /* cmd.height */
+#define RMPC_SOA_VX 19            /* cmd.vx */
+#define RMPC_SOA_WPITCH 20        /* cmd.wpitch */
+#define RMPC_SOA_PHASE 21         /* gait.phase */
+#define RMPC_SOA_PERIOD 22        /* gait.period */
+#define RMPC_SOA_PHASE_SWITCH 23  /* gait.phase_switch */
+#define RMPC_SOA_OFFSETS 24       /* gait.offsets[0..3] rows 24..27 */
+#define RMPC_SOA_FIELDS 28
+/* Each value is widened to FP64 exactly (float -> double), so the result equals rmpc_solve on
+ * the FP64 records holding those widened values, bit for bit.  A device kernel unpacks the block
+ * with coalesced loads (one thread per agent, consecutive agents on consecutive lanes) into the
+ * handle's per-agent records.  Host version: soa may be pageable or pinned, any number of
+ * devices (shard g reads columns [begin, begin + count) of every row). */
+int32_t rmpc_solve_soa(rmpc_handle* handle, const float* soa, int64_t ld, const rmpc_solution* prev,
+                       const float* prev_z_star, rmpc_solution* out, float* z_star_out);
+/* Device version (single-device handles): d_soa resident on the handle's device, enqueued on
+ * `stream` (NULL = legacy default stream).  Unpacks into the handle's own record buffers, so
+ * device solves of one handle must be issued on one stream (as for schedule sharing). */
+int32_t rmpc_solve_soa_device(rmpc_handle* handle, const float* d_soa, int64_t ld, const rmpc_solution* d_prev,
+                              const float* d_prev_z_star, rmpc_solution* d_out, float* d_z_star_out, void* stream);
+
 /* Shard g of the handle: its CUDA device and contiguous agent range. */
 int32_t rmpc_shard_info(const rmpc_handle* handle, int32_t shard, int32_t* device, int32_t* begin,
                         int32_t* count);
@@ -201,6 +229,10 @@ int32_t rmpc_set_schedule_sharing(rmpc_handle* handle, int32_t enabled);
 /* Stage-profiling switch: when on, the kernel samples the SM clock at the reference's stage
  * boundaries and rmpc_last_timing() reports the per-stage split of kernel_ms. */
 int32_t rmpc_set_stage_profiling(rmpc_handle* handle, int32_t enabled);
+
+/* Solve-path kernels this process has launched so far (every entry point, every handle):
+ * benchmarks difference it over a timed region to count the library's launches. */
+int64_t rmpc_kernel_launches(void);
 
 /* Build provenance: "sm_100a" and the kernel variant compiled in. */
 const char* rmpc_build_info(void);

@@ -11,10 +11,11 @@ from __future__ import annotations
 from .abi import (NC, NF, NJ, NQ, NV, SOLUTION_DTYPE, STAGE_NAMES, STATUS_DIVERGED,  # noqa: F401
                   STATUS_NONFINITE_INPUT, STATUS_OK, STATUS_SINGULAR, Model, Settings, Timing,
                   default_model, default_settings, gait_row, standing_gait_row)
-from .runtime import BatchRunner, RmpcError, library, load_library  # noqa: F401
+from .runtime import SOA_FIELDS, BatchRunner, RmpcError, from_soa, library, load_library, to_soa  # noqa: F401
 from .synthetic import synthetic_batch  # noqa: F401
 from .env import Env, EnvConfig, Policy, default_env_config  # noqa: F401
 
 __all__ = ["BatchRunner", "RmpcError", "Model", "Settings", "Timing", "default_model",
            "default_settings", "gait_row", "standing_gait_row", "synthetic_batch",
-           "SOLUTION_DTYPE", "load_library", "library", "Env", "EnvConfig", "Policy", "default_env_config"]
+           "SOLUTION_DTYPE", "load_library", "library", "Env", "EnvConfig", "Policy", "default_env_config",
+           "to_soa", "from_soa", "SOA_FIELDS"]

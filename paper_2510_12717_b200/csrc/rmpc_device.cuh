@@ -74,7 +74,8 @@ constexpr int G_SCR = 160;    // 12 x 13 G block (+ pad) of the factorization
 struct KParams {
   int32_t NT, n_qp, ruiz_iters, warm_start;
   int32_t n_agents, profile;
-  int32_t agents_per_cta, spill_nodes, tmem_cols, pad_;
+  int32_t agents_per_cta, spill_nodes, tmem_cols;
+  int32_t sq_cta_base;  // rti_squad_kernel: CTA index of this launch's first CTA (split launches)
   // launch shape: full_ctas CTAs of agents_per_cta agents, then CTAs of tail_agents (the
   // last, partial wave spread over every SM at fewer agents per CTA)
   int32_t full_ctas, tail_agents;
@@ -346,5 +347,24 @@ struct RmpcSchedBuffers {
 // rest (rti_kernel over an agent list).  Seven launches plus memsets, no host synchronisation.
 // variant 1: warp-pair-per-agent CTAs of one schedule (rti_shared_kernel, bit-identical to the
 // per-agent solve); 2: lane-per-agent squads (rti_squad_kernel) where the horizon fits them.
-int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant);
+// End-to-end outputs of a squad solve (host solve with outputs in pinned, mapped host memory):
+// the solve writes params.out / params.z_out (device buffers), its squads run as two launches
+// (the first wave of CTAs, then the rest), and sq_copyout_kernel moves the first wave's records
+// and z* rows to h_out / h_z on stream2 while the second launch runs; the rest follows on
+// `stream`.  Events ev_a / ev_b order the two copies.  Only the squad path splits; elsewhere the
+// solve writes h_out / h_z directly.
+struct RmpcCopyOut {
+  void* stream2;
+  void* ev_a;
+  void* ev_b;
+  rmpc_solution* h_out;  // device address of the mapped host records
+  float* h_z;            // device address of the mapped host z* (NULL: no z*)
+  int sms;
+};
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant,
+                       const RmpcCopyOut* co = nullptr);
 int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory
+// SoA FP32 inputs (rmpc_solve_soa, RMPC_SOA_* rows of `ld` floats) -> the per-agent FP64
+// records the solve kernels read; one thread per agent, coalesced row loads.
+int rmpc_launch_soa_unpack(const float* soa, long long ld, int n, rmpc_state* states, rmpc_command* cmds,
+                           rmpc_gait* gaits, void* stream);

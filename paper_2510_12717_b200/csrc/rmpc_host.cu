@@ -40,6 +40,7 @@ struct Shard {
   float* d_prev_z = nullptr;
   rmpc_solution* d_out = nullptr;
   float* d_z = nullptr;
+  float* d_soa = nullptr;  // rmpc_solve_soa: the shard's FP32 component rows
   unsigned long long* d_prof = nullptr;
   RmpcSchedBuffers sched[1] = {};  // schedule-shared workspace
   // pinned staging for pageable caller buffers
@@ -244,6 +245,7 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
   CK(cudaMalloc(&sh.d_prev_z, zn * sizeof(float)));
   CK(cudaMalloc(&sh.d_out, n * sizeof(rmpc_solution)));
   CK(cudaMalloc(&sh.d_z, zn * sizeof(float)));
+  CK(cudaMalloc(&sh.d_soa, n * RMPC_SOA_FIELDS * sizeof(float)));
   CK(cudaMalloc(&sh.d_prof, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long)));
   cudaDeviceGetAttribute(&sh.clock_khz, cudaDevAttrClockRate, sh.device);
   sh.stage_in_bytes = n * (sizeof(rmpc_state) + sizeof(rmpc_command) + sizeof(rmpc_gait) + sizeof(rmpc_solution)) +
@@ -287,7 +289,7 @@ void free_shard(Shard& sh) {
   if (sh.stream) cudaStreamSynchronize(sh.stream);
   if (sh.stream2) cudaStreamSynchronize(sh.stream2);
   cudaFree(sh.d_states); cudaFree(sh.d_cmds); cudaFree(sh.d_gaits); cudaFree(sh.d_prev);
-  cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof);
+  cudaFree(sh.d_prev_z); cudaFree(sh.d_out); cudaFree(sh.d_z); cudaFree(sh.d_prof); cudaFree(sh.d_soa);
   cudaFreeHost(sh.h_stage_in); cudaFreeHost(sh.h_stage_out);
   for (RmpcSchedBuffers& sb : sh.sched) {
     for (void* p : {(void*)sb.table, (void*)sb.slot_id, (void*)sb.slot_of, (void*)sb.pos, (void*)sb.order,
@@ -318,13 +320,44 @@ T* mapped(T* p) {
   return static_cast<T*>(d);
 }
 
+// SoA inputs of rmpc_solve_soa: the caller's block and its row stride (floats).
+struct SoaIn {
+  const float* soa;
+  int64_t ld;
+};
+
+// The shard's columns [begin, begin + count) of the SoA block: one 2D H2D copy (28 rows; a
+// pageable block is first gathered into the pinned staging buffer), then the unpack kernel into
+// the shard's FP64 records -- on `st`, in place of the three record copies.
+void stage_soa(Shard& sh, const SoaIn& in, cudaStream_t st) {
+  const size_t n = sh.count, b = sh.begin;
+  const float* src = in.soa + b;
+  size_t pitch = (size_t)in.ld * sizeof(float);
+  if (!is_pinned(in.soa)) {
+    float* stg = reinterpret_cast<float*>(sh.h_stage_in);
+    for (int r = 0; r < RMPC_SOA_FIELDS; ++r) std::memcpy(stg + r * n, in.soa + r * in.ld + b, n * sizeof(float));
+    src = stg;
+    pitch = n * sizeof(float);
+  }
+  if (pitch == n * sizeof(float))  // one contiguous block
+    CK(cudaMemcpyAsync(sh.d_soa, src, RMPC_SOA_FIELDS * n * sizeof(float), cudaMemcpyHostToDevice, st));
+  else
+    CK(cudaMemcpy2DAsync(sh.d_soa, n * sizeof(float), src, pitch, n * sizeof(float), RMPC_SOA_FIELDS,
+                         cudaMemcpyHostToDevice, st));
+  const int rc = rmpc_launch_soa_unpack(sh.d_soa, (long long)n, (int)n, sh.d_states, sh.d_cmds, sh.d_gaits, st);
+  if (rc != 0) {
+    sh.err = RMPC_ERR_CUDA;
+    sh.msg = std::string("soa_unpack_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+  }
+}
+
 // Cold start with schedule sharing: the inputs in one H2D copy each, then the whole shared
 // solve (schedule pass, grouped solve) writing its records and z* straight into the pinned
 // host buffers (the caller's, or the handle's staging copy for pageable ones) over PCIe while
 // it runs -- the grouped solve finishes every agent at once at the end, so there is no later
 // chunk whose kernel a D2H could overlap.
 void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
-                      const rmpc_gait* gaits, rmpc_solution* out, float* z_out) {
+                      const rmpc_gait* gaits, rmpc_solution* out, float* z_out, const SoaIn* soa) {
   const size_t n = sh.count, b = sh.begin;
   const size_t zrow = (size_t)h.NT * RMPC_NV;
   const cudaStream_t st = sh.stream;
@@ -333,9 +366,11 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
     char* dst;
     size_t bytes;
   };
-  In ins[3] = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), n * sizeof(rmpc_state)},
-               {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), n * sizeof(rmpc_command)},
-               {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), n * sizeof(rmpc_gait)}};
+  std::vector<In> ins;
+  if (!soa)
+    ins = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), n * sizeof(rmpc_state)},
+           {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), n * sizeof(rmpc_command)},
+           {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), n * sizeof(rmpc_gait)}};
   size_t off = 0;
   for (In& c : ins) {
     if (!is_pinned(c.src)) {
@@ -353,6 +388,10 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   float* d_z = h_z ? mapped(h_z) : nullptr;
   CK(cudaEventRecord(sh.ev[0], st));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), st));
+  if (soa) {
+    stage_soa(sh, *soa, st);
+    if (sh.err) return;
+  }
   for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, st));
   CK(cudaEventRecord(sh.ev[1], st));
   rmpc_dev::KParams P = make_params(h);
@@ -360,10 +399,14 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   P.states = sh.d_states;
   P.cmds = sh.d_cmds;
   P.gaits = sh.d_gaits;
-  P.out = d_out ? d_out : sh.d_out;
-  P.z_out = z_out ? (d_z ? d_z : sh.d_z) : nullptr;
   P.prof = sh.d_prof;
-  const int rc = rmpc_launch_shared(P, sh.sched[0], st, h.share);
+  // mapped host outputs: the solve writes the device buffers and copy-out kernels move the
+  // results over PCIe, the first wave's beside the second wave's solve (RmpcCopyOut)
+  RmpcCopyOut co{sh.stream2, sh.ev[3], sh.ev[4], d_out, d_z, sh.sms};
+  const bool copyout = d_out != nullptr && d_z != nullptr;  // (records alone: written in the solve)
+  P.out = copyout ? sh.d_out : (d_out ? d_out : sh.d_out);
+  P.z_out = z_out ? (copyout ? sh.d_z : (d_z ? d_z : sh.d_z)) : nullptr;
+  const int rc = rmpc_launch_shared(P, sh.sched[0], st, h.share, copyout ? &co : nullptr);
   if (rc != 0) {
     sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
     sh.msg = std::string("rti_shared_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -371,8 +414,10 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
     return;
   }
   CK(cudaEventRecord(sh.ev[2], st));
-  if (!d_out) CK(cudaMemcpyAsync(h_out, sh.d_out, n * sizeof(rmpc_solution), cudaMemcpyDeviceToHost, st));
-  if (z_out && !d_z) CK(cudaMemcpyAsync(h_z, sh.d_z, n * zrow * sizeof(float), cudaMemcpyDeviceToHost, st));
+  if (!copyout) {
+    if (!d_out) CK(cudaMemcpyAsync(h_out, sh.d_out, n * sizeof(rmpc_solution), cudaMemcpyDeviceToHost, st));
+    if (z_out && !d_z) CK(cudaMemcpyAsync(h_z, sh.d_z, n * zrow * sizeof(float), cudaMemcpyDeviceToHost, st));
+  }
   if (h.profile) CK(cudaMemcpyAsync(sh.prof, sh.d_prof, sizeof(sh.prof), cudaMemcpyDeviceToHost, st));
   CK(cudaEventRecord(sh.ev[5], st));
   CK(cudaStreamSynchronize(st));
@@ -389,12 +434,12 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
 
 void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_command* cmds,
                const rmpc_gait* gaits, const rmpc_solution* prev, const float* prev_z,
-               rmpc_solution* out, float* z_out) {
+               rmpc_solution* out, float* z_out, const SoaIn* soa = nullptr) {
   sh.err = 0;
   if (sh.count == 0) return;
   CK(cudaSetDevice(sh.device));
   if (h.share && !h.settings.warm_start) {
-    run_shard_shared(h, sh, states, cmds, gaits, out, z_out);
+    run_shard_shared(h, sh, states, cmds, gaits, out, z_out, soa);
     return;
   }
   const size_t n = sh.count, b = sh.begin;
@@ -420,9 +465,11 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
     char* dst;
     size_t elem;  // bytes per agent
   };
-  std::vector<In> ins = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), sizeof(rmpc_state)},
-                         {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), sizeof(rmpc_command)},
-                         {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), sizeof(rmpc_gait)}};
+  std::vector<In> ins;
+  if (!soa)  // (SoA: the whole shard's records are unpacked on the device ahead of chunk 0)
+    ins = {{reinterpret_cast<const char*>(states + b), reinterpret_cast<char*>(sh.d_states), sizeof(rmpc_state)},
+           {reinterpret_cast<const char*>(cmds + b), reinterpret_cast<char*>(sh.d_cmds), sizeof(rmpc_command)},
+           {reinterpret_cast<const char*>(gaits + b), reinterpret_cast<char*>(sh.d_gaits), sizeof(rmpc_gait)}};
   if (use_prev) {
     ins.push_back({reinterpret_cast<const char*>(prev + b), reinterpret_cast<char*>(sh.d_prev), sizeof(rmpc_solution)});
     ins.push_back({reinterpret_cast<const char*>(prev_z + b * zrow), reinterpret_cast<char*>(sh.d_prev_z),
@@ -448,9 +495,14 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
   for (int k = 0; k < nchunks; ++k) {
     const cudaStream_t st = ss[k];
     const size_t lo = cut[k], m = cut[k + 1] - cut[k];
+    if (soa && k == 0) {
+      stage_soa(sh, *soa, st);
+      if (sh.err) return;
+    }
     for (const In& c : ins)
       CK(cudaMemcpyAsync(c.dst + lo * c.elem, c.src + lo * c.elem, m * c.elem, cudaMemcpyHostToDevice, st));
     if (k == 0) CK(cudaEventRecord(sh.ev[1], st));
+    if (soa && k == 0 && nchunks > 1) CK(cudaStreamWaitEvent(ss[1], sh.ev[1], 0));  // the unpacked records
     rmpc_dev::KParams P = make_params(h);
     P.n_agents = (int)m;
     P.states = sh.d_states + lo;
@@ -728,6 +780,58 @@ int32_t rmpc_solve(rmpc_handle* h, const rmpc_state* states, const rmpc_command*
     if (sh.err) { h->err = sh.msg; return sh.err; }
   fill_timing(*h, ms);
   return RMPC_OK;
+}
+
+int32_t rmpc_solve_soa(rmpc_handle* h, const float* soa, int64_t ld, const rmpc_solution* prev,
+                       const float* prev_z_star, rmpc_solution* out, float* z_star_out) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (!soa || !out) {
+    h->err = "rmpc_solve_soa: NULL array";
+    return RMPC_ERR_STRUCTURAL;
+  }
+  if (ld < h->n) {
+    h->err = "rmpc_solve_soa: row stride ld < n_envs";
+    return RMPC_ERR_STRUCTURAL;
+  }
+  const SoaIn in{soa, ld};
+  const auto t0 = std::chrono::steady_clock::now();
+  if (h->shards.size() == 1) {
+    run_shard(*h, h->shards[0], nullptr, nullptr, nullptr, prev, prev_z_star, out, z_star_out, &in);
+  } else {
+    const std::function<void(int)> job = [&](int g) {
+      run_shard(*h, h->shards[g], nullptr, nullptr, nullptr, prev, prev_z_star, out, z_star_out, &in);
+    };
+    h->pool->run(job);
+  }
+  const double ms = std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0).count();
+  for (const Shard& sh : h->shards)
+    if (sh.err) { h->err = sh.msg; return sh.err; }
+  fill_timing(*h, ms);
+  return RMPC_OK;
+}
+
+int32_t rmpc_solve_soa_device(rmpc_handle* h, const float* d_soa, int64_t ld, const rmpc_solution* d_prev,
+                              const float* d_prev_z_star, rmpc_solution* d_out, float* d_z_star_out, void* stream) {
+  if (!h) return RMPC_ERR_INVALID_ARG;
+  if (h->shards.size() != 1) {
+    h->err = "rmpc_solve_soa_device: single-device handles only (rmpc_solve_soa shards host blocks)";
+    return RMPC_ERR_INVALID_ARG;
+  }
+  if (!d_soa || !d_out) { h->err = "rmpc_solve_soa_device: NULL array"; return RMPC_ERR_STRUCTURAL; }
+  if (ld < h->n) { h->err = "rmpc_solve_soa_device: row stride ld < n_envs"; return RMPC_ERR_STRUCTURAL; }
+  Shard& sh = h->shards[0];
+  if (cudaSetDevice(sh.device) != cudaSuccess) {
+    cudaGetLastError();
+    h->err = "cudaSetDevice failed";
+    return RMPC_ERR_CUDA;
+  }
+  const int rc = rmpc_launch_soa_unpack(d_soa, (long long)ld, h->n, sh.d_states, sh.d_cmds, sh.d_gaits, stream);
+  if (rc != 0) {
+    h->err = std::string("soa_unpack_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
+    return RMPC_ERR_CUDA;
+  }
+  return launch_device(*h, sh, h->n, sh.d_states, sh.d_cmds, sh.d_gaits, d_prev, d_prev_z_star, d_out, d_z_star_out,
+                       nullptr, stream);
 }
 
 int32_t rmpc_solve_device(rmpc_handle* h, const rmpc_state* d_states, const rmpc_command* d_cmds,

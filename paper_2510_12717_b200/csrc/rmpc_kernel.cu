@@ -576,8 +576,13 @@ int rmpc_kernel_setup(int) {
   return rc;
 }
 
+// Kernels of the solve path launched by this process (rmpc_kernel_launches): the bench's
+// gpu_launches is the difference over its timed region.
+static std::atomic<long long> g_launches{0};
+
 static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st) {
   if (grid <= 0) return 0;
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   if (c.dense)
     rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
   else if (c.spill_nodes > 0)
@@ -736,7 +741,8 @@ __global__ void sched_scatter_kernel(const KParams P, RmpcSchedBuffers b) {
 
 }  // namespace rmpc_dev
 
-int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant) {
+int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant,
+                       const RmpcCopyOut* co) {
   using namespace rmpc_dev;
   if (params.n_agents <= 0) return 0;
   if (params.n_agents > b.agents) return (int)cudaErrorInvalidValue;
@@ -750,6 +756,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   if (rc != 0) return rc;
   sched_key_kernel<<<blocks, 256, 0, st>>>(params, b);
   sched_count_kernel<<<blocks, 256, 0, st>>>(params, b);
+  g_launches.fetch_add(2, std::memory_order_relaxed);
   // the store: setup + Ruiz + factorization of each schedule's representative (mode 1), one
   // warp pair per CTA (the few schedules' latency chains run alone on their SMs)
   const CtaShape c = cta_shape(NT);
@@ -779,9 +786,21 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   rc = launch_variant(F, c1, F.full_ctas, st);
   if (rc != 0) return rc;
   const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
+  static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
+    const char* e = getenv("RMPC_SQUAD_SOLO");
+    return e ? atoi(e) : 0;
+  }();
+  // a split pays only where a second wave of squad CTAs follows the first
+  if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > 2 * co->sms)) {  // the solve writes the mapped host buffers
+    KParams Q = params;
+    Q.out = co->h_out;
+    Q.z_out = co->h_z;
+    return rmpc_launch_shared(Q, b, stream, variant, nullptr);
+  }
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
   sched_scan_kernel<<<1, 1024, 0, st>>>(b, squads ? 32 : cs.agents);
   sched_scatter_kernel<<<blocks, 256, 0, st>>>(params, b);
+  g_launches.fetch_add(3, std::memory_order_relaxed);  // + the group kernel below
   // the groups: one schedule per CTA (grid: an upper bound of sum ceil(count / A))
   KParams S = params;
   S.mode = 0;
@@ -802,13 +821,25 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
     S.agents_per_cta = 32;
     S.sqpack = b.sqpack;
     sq_pack_kernel<<<b.cap, 256, 0, st>>>(S);
+    g_launches.fetch_add(1, std::memory_order_relaxed);
     const int nsq = (n + 31) / 32 + std::min(b.cap, n);
-    static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
-      const char* e = getenv("RMPC_SQUAD_SOLO");
-      return e ? atoi(e) : 0;
-    }();
     S.pad2_ = solo;
-    rti_squad_kernel<<<solo ? nsq : (nsq + 1) / 2, 128, sq_smem_bytes(NT), st>>>(S);
+    const int grid = solo ? nsq : (nsq + 1) / 2;
+    if (co) {  // (grid > co->sms here)  // split: first wave, its copy-out beside the second launch
+      S.sq_cta_base = 0;
+      rti_squad_kernel<<<co->sms, 128, sq_smem_bytes(NT), st>>>(S);
+      cudaEventRecord((cudaEvent_t)co->ev_a, st);
+      cudaStreamWaitEvent((cudaStream_t)co->stream2, (cudaEvent_t)co->ev_a, 0);
+      sq_copyout_kernel<<<64, 256, 0, (cudaStream_t)co->stream2>>>(S, 0, co->sms, 0, co->h_out, co->h_z);
+      cudaEventRecord((cudaEvent_t)co->ev_b, (cudaStream_t)co->stream2);
+      S.sq_cta_base = co->sms;  // the second launch writes the mapped host buffers itself: its
+      S.out = co->h_out;        // CTAs are the last ones, nothing waits for their SMs
+      S.z_out = co->h_z;
+      rti_squad_kernel<<<grid - co->sms, 128, sq_smem_bytes(NT), st>>>(S);
+      g_launches.fetch_add(2, std::memory_order_relaxed);
+    } else {
+      rti_squad_kernel<<<grid, 128, sq_smem_bytes(NT), st>>>(S);
+    }
   } else if (cs.agents > MAX_AGENTS)
     rti_shared_kernel<SHARED_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);
   else
@@ -825,5 +856,55 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   U.tmem_cols = c.tmem_cols;
   U.full_ctas = (n + c.agents - 1) / c.agents;
   U.tail_agents = 0;
+  if (co) {
+    // the per-agent list writes the mapped host buffers too, after the first wave's copy-out: a
+    // fallback agent of the first wave is in both, and its list record must land last
+    cudaStreamWaitEvent(st, (cudaEvent_t)co->ev_b, 0);
+    U.out = co->h_out;
+    U.z_out = co->h_z;
+  }
   return launch_variant(U, c, U.full_ctas, st);
 }
+
+namespace rmpc_dev {
+
+// rmpc_solve_soa's unpack: thread a reads column a of the 28 component rows (each warp-wide row
+// read is one coalesced 128-byte transaction) and writes agent a's FP64 records.  float -> double
+// is exact, so the solve sees exactly the values the caller's FP32 block holds.
+__global__ void __launch_bounds__(256) soa_unpack_kernel(const float* __restrict__ soa, long long ld, int n,
+                                                         rmpc_state* states, rmpc_command* cmds, rmpc_gait* gaits) {
+  const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a >= n) return;
+  const float* c = soa + a;
+  rmpc_state st;
+#pragma unroll
+  for (int k = 0; k < RMPC_NQ; ++k) {
+    st.q[k] = (double)__ldg(c + (RMPC_SOA_Q + k) * ld);
+    st.qd[k] = (double)__ldg(c + (RMPC_SOA_QD + k) * ld);
+  }
+  rmpc_command cm;
+  cm.height = (double)__ldg(c + RMPC_SOA_HEIGHT * ld);
+  cm.vx = (double)__ldg(c + RMPC_SOA_VX * ld);
+  cm.wpitch = (double)__ldg(c + RMPC_SOA_WPITCH * ld);
+  rmpc_gait g;
+  g.phase = (double)__ldg(c + RMPC_SOA_PHASE * ld);
+  g.period = (double)__ldg(c + RMPC_SOA_PERIOD * ld);
+  g.phase_switch = (double)__ldg(c + RMPC_SOA_PHASE_SWITCH * ld);
+#pragma unroll
+  for (int k = 0; k < RMPC_NC; ++k) g.offsets[k] = (double)__ldg(c + (RMPC_SOA_OFFSETS + k) * ld);
+  states[a] = st;
+  cmds[a] = cm;
+  gaits[a] = g;
+}
+
+}  // namespace rmpc_dev
+
+int rmpc_launch_soa_unpack(const float* soa, long long ld, int n, rmpc_state* states, rmpc_command* cmds,
+                           rmpc_gait* gaits, void* stream) {
+  if (n <= 0) return 0;
+  rmpc_dev::soa_unpack_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(soa, ld, n, states, cmds, gaits);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
+}
+
+extern "C" int64_t rmpc_kernel_launches(void) { return (int64_t)g_launches.load(std::memory_order_relaxed); }

@@ -1067,7 +1067,8 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
   const int NT = P.NT;
   if (tid < 2) {
     const int ng = min(*P.n_sched, P.store_cap);
-    const int sq = P.pad2_ ? (tid == P.pad2_ - 1 ? (int)blockIdx.x : 1 << 30) : 2 * (int)blockIdx.x + tid;
+    const int cta = (int)blockIdx.x + P.sq_cta_base;
+    const int sq = P.pad2_ ? (tid == P.pad2_ - 1 ? cta : 1 << 30) : 2 * cta + tid;
     int g = -1, first = 0, cnt = 0;
     if (ng > 0 && sq < P.grp_cta[ng]) {
       int lo = 0, hi = ng - 1;  // last group whose first squad is <= sq
@@ -1156,6 +1157,47 @@ __global__ void sq_pack_kernel(const KParams P) {
     if (r < NV && c < NV) v = 0.5f * (blk[r * TCOLS + c] + blk[c * TCOLS + r]);
     else if (r < SROWS && c < NV) v = blk[r * TCOLS + c];
     reg[L.mf + k] = v;
+  }
+}
+
+// Position in `order` of squad sq's first agent (squads are laid out group by group, so the
+// agents of squads [0, sq) are the prefix order[0, sq_pos(sq))); sq past the last squad: the
+// number of grouped agents.
+__device__ __forceinline__ int sq_pos(const KParams& P, int sq) {
+  const int ng = min(*P.n_sched, P.store_cap);
+  if (ng <= 0) return 0;
+  if (sq >= P.grp_cta[ng]) return P.grp_first[ng - 1] + P.grp_count[ng - 1];
+  int lo = 0, hi = ng - 1;
+  while (lo < hi) {
+    const int mid = (lo + hi + 1) >> 1;
+    if (P.grp_cta[mid] <= sq) lo = mid; else hi = mid - 1;
+  }
+  return P.grp_first[lo] + 32 * (sq - P.grp_cta[lo]);
+}
+
+// End-to-end output path of a split squad solve (rmpc_launch_shared with host outputs): copy the
+// records and z* rows of the agents of squad CTAs [cta_lo, cta_hi) -- and, with `list`, of the
+// per-agent list -- from the device buffers P.out / P.z_out to the mapped host buffers, one warp
+// per agent, consecutive lanes on consecutive 8-byte words.  Runs beside the squad launch of the
+// next CTA range, so the PCIe transfer of one wave overlaps the solve of the next.
+__global__ void __launch_bounds__(256) sq_copyout_kernel(const KParams P, int cta_lo, int cta_hi, int list,
+                                                         rmpc_solution* h_out, float* h_z) {
+  const int p0 = sq_pos(P, 2 * cta_lo), p1 = cta_hi >= (1 << 29) ? sq_pos(P, 1 << 30) : sq_pos(P, 2 * cta_hi);
+  const int nl = list ? *P.n_list : 0;
+  const int lane = threadIdx.x & 31;
+  const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;
+  const int zw = P.NT * NV / 2;  // float2 words of one agent's z*
+  for (int k = wg; k < (p1 - p0) + nl; k += nw) {
+    const int a = k < p1 - p0 ? P.order[p0 + k] : P.agent_list[k - (p1 - p0)];
+    const float* rs = reinterpret_cast<const float*>(P.out + a);
+    float* rd = reinterpret_cast<float*>(h_out + a);
+    constexpr int RW = (int)(sizeof(rmpc_solution) / 4);
+    for (int w = lane; w < RW; w += 32) rd[w] = rs[w];
+    if (h_z) {
+      const float2* zs = reinterpret_cast<const float2*>(P.z_out + (size_t)a * P.NT * NV);
+      float2* zd = reinterpret_cast<float2*>(h_z + (size_t)a * P.NT * NV);
+      for (int w = lane; w < zw; w += 32) zd[w] = zs[w];
+    }
   }
 }
 

@@ -30,7 +30,10 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_last_timing", "rmpc_last_error", "rmpc_status_message", "rmpc_stage_name",
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
            "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak",
-           "rmpc_solve_device_sharded", "rmpc_shard_info", "rmpc_set_schedule_sharing")
+           "rmpc_solve_device_sharded", "rmpc_shard_info", "rmpc_set_schedule_sharing",
+           "rmpc_solve_soa", "rmpc_solve_soa_device", "rmpc_kernel_launches")
+
+SOA_FIELDS = 28  # RMPC_SOA_FIELDS: q 0..8, qd 9..17, height, vx, wpitch, phase, period, phase_switch, offsets 24..27
 
 
 class RmpcError(RuntimeError):
@@ -56,6 +59,10 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_solve.restype = _I
     L.rmpc_solve_device.argtypes = [_VP] * 9
     L.rmpc_solve_device.restype = _I
+    L.rmpc_solve_soa.argtypes = [_VP, _VP, C.c_int64, _VP, _VP, _VP, _VP]
+    L.rmpc_solve_soa.restype = _I
+    L.rmpc_solve_soa_device.argtypes = [_VP, _VP, C.c_int64, _VP, _VP, _VP, _VP, _VP]
+    L.rmpc_solve_soa_device.restype = _I
     L.rmpc_solve_device_active_set.argtypes = [_VP] * 7
     L.rmpc_solve_device_active_set.restype = _I
     L.rmpc_solve_device_sharded.argtypes = [_VP] * 9
@@ -85,9 +92,16 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_smem_bytes.restype = _I
     L.rmpc_sizeof.argtypes = [_I]
     L.rmpc_sizeof.restype = _I
+    L.rmpc_kernel_launches.argtypes = []
+    L.rmpc_kernel_launches.restype = C.c_int64
     L.rmpc_fma_peak.argtypes = [_I, _VP]
     L.rmpc_fma_peak.restype = _I
     return L
+
+
+def kernel_launches() -> int:
+    """Solve-path kernels launched by this process so far (rmpc_kernel_launches)."""
+    return int(library().rmpc_kernel_launches())
 
 
 def fma_peak_tflops(device: int = 0) -> float:
@@ -113,6 +127,23 @@ def _arr(a, cols, dtype=np.float64):
     if a.shape[1] != cols:
         raise ValueError(f"expected rows of {cols} values, got shape {a.shape}")
     return a
+
+
+def to_soa(states, cmds, gaits, ld: int | None = None) -> np.ndarray:
+    """The FP32 structure-of-arrays block of rmpc_solve_soa: row r = component r of every agent
+    (RMPC_SOA_* order: the 18 state values, the 3 command values, the 7 gait values)."""
+    states, cmds, gaits = _arr(states, 18), _arr(cmds, 3), _arr(gaits, 7)
+    n = states.shape[0]
+    out = np.zeros((SOA_FIELDS, ld or n), dtype=np.float32)
+    out[:, :n] = np.hstack([states, cmds, gaits]).T
+    return out
+
+
+def from_soa(soa, n: int):
+    """FP64 records (states, cmds, gaits) holding the block's values widened exactly to FP64:
+    rmpc_solve on them equals rmpc_solve_soa on the block."""
+    a = np.asarray(soa, dtype=np.float32)[:, :n].T.astype(np.float64)
+    return np.ascontiguousarray(a[:, :18]), np.ascontiguousarray(a[:, 18:21]), np.ascontiguousarray(a[:, 21:28])
 
 
 def nominal_pose(model: Model | None = None) -> np.ndarray:
@@ -200,6 +231,64 @@ class BatchRunner:
         if rc != 0:
             self._err(rc)
         return out, z_out
+
+    def solve_soa(self, soa, prev=None, *, want_z: bool = False, out: np.ndarray | None = None,
+                  z_out: np.ndarray | None = None):
+        """rmpc_solve_soa: the inputs as one float32 (28, ld >= n) block (to_soa).  Same results
+        as solve() on from_soa(soa); prev as in solve().  Returns (solutions, z_star or None)."""
+        soa = np.asarray(soa)
+        n, T = self._n, self.horizon
+        if soa.dtype != np.float32 or soa.ndim != 2 or soa.shape[0] != SOA_FIELDS or soa.shape[1] < n \
+                or not soa.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"soa must be a contiguous float32 array of shape ({SOA_FIELDS}, >= {n})")
+        if out is None:
+            out = np.zeros(n, dtype=SOLUTION_DTYPE)
+        elif out.dtype != SOLUTION_DTYPE or out.shape != (n,) or not out.flags["C_CONTIGUOUS"]:
+            raise ValueError(f"out must be a contiguous SOLUTION_DTYPE array of length {n}")
+        if want_z and z_out is None:
+            z_out = np.zeros((n, T, NV), dtype=np.float32)
+        if z_out is not None and (z_out.dtype != np.float32 or z_out.shape != (n, T, NV)
+                                  or not z_out.flags["C_CONTIGUOUS"]):
+            raise ValueError(f"z_out must be a contiguous float32 array of shape ({n}, {T}, {NV})")
+        pv = pz = None
+        if prev is not None and prev[1] is not None:
+            pz = np.asarray(prev[1])
+            if pz.dtype != np.float32 or pz.shape != (n, T, NV):
+                raise ValueError(f"prev z_star must be float32 of shape ({n}, {T}, {NV})")
+            pz = np.ascontiguousarray(pz)
+            pv = np.ascontiguousarray(prev[0], dtype=SOLUTION_DTYPE)
+            if pv.shape != (n,):
+                raise RmpcError(RMPC_ERR_STRUCTURAL, "BatchRunner::solve: prev length != n_envs")
+        rc = self._lib.rmpc_solve_soa(self._h, soa.ctypes.data, soa.shape[1],
+                                      pv.ctypes.data if pv is not None else None,
+                                      pz.ctypes.data if pz is not None else None, out.ctypes.data,
+                                      z_out.ctypes.data if z_out is not None else None)
+        if rc != 0:
+            self._err(rc)
+        return out, z_out
+
+    def solve_soa_device(self, soa, out, z_out=None, prev=None, prev_z=None, stream=None):
+        """rmpc_solve_soa_device: `soa` a contiguous float32 CUDA tensor (28, ld >= n); other
+        arguments as solve_device."""
+        def p(t):
+            if t is None:
+                return None
+            return t if isinstance(t, int) else t.data_ptr()
+        n, T = self._n, self.horizon
+        if not isinstance(soa, int):
+            if soa.dim() != 2 or soa.shape[0] != SOA_FIELDS or soa.shape[1] < n or str(soa.dtype) != "torch.float32":
+                raise ValueError(f"soa must be a float32 CUDA tensor of shape ({SOA_FIELDS}, >= {n})")
+            self._check_device("soa", soa, SOA_FIELDS * n * 4)
+            ld = soa.shape[1]
+        else:
+            ld = n
+        for name, t, nb in (("out", out, n * SOLUTION_DTYPE.itemsize), ("z_out", z_out, n * T * NV * 4),
+                            ("prev", prev, n * SOLUTION_DTYPE.itemsize), ("prev_z", prev_z, n * T * NV * 4)):
+            self._check_device(name, t, nb)
+        s = self._stream(stream, (soa, out))
+        rc = self._lib.rmpc_solve_soa_device(self._h, p(soa), ld, p(prev), p(prev_z), p(out), p(z_out), s)
+        if rc != 0:
+            self._err(rc)
 
     @staticmethod
     def _stream(stream, tensors):

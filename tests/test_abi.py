@@ -162,3 +162,25 @@ def test_synthetic_batch_ranges():
     assert set(np.unique(gm[:, 2])) == {0.4, 0.5, 0.65, 1.0}
     st1, cm1, ga1 = R.synthetic_batch(3, "standing", model=m, settings=s)
     assert np.all(ga1[:, 2] == 1.0) and np.all(st1[:, 9:] == 0)
+
+
+def test_soa_layout_matches_header():
+    """RMPC_SOA_* rows (include/rmpc_b200.h) = the to_soa layout: the 18 state values, the 3
+    command values, the 7 gait values, each row one component of every agent."""
+    import re
+    hdr = open(os.path.join(INCLUDE, "rmpc_b200.h")).read()
+    d = {k: int(v) for k, v in re.findall(r"#define RMPC_SOA_(\w+) (\d+)", hdr)}
+    assert d == {"Q": 0, "QD": 9, "HEIGHT": 18, "VX": 19, "WPITCH": 20, "PHASE": 21, "PERIOD": 22,
+                 "PHASE_SWITCH": 23, "OFFSETS": 24, "FIELDS": 28}
+    assert R.SOA_FIELDS == d["FIELDS"]
+    st, cm, ga = R.synthetic_batch(7, "mixed", seed=1)
+    soa = R.to_soa(st, cm, ga, ld=9)
+    assert soa.shape == (28, 9) and soa.dtype == np.float32 and not soa[:, 7:].any()
+    np.testing.assert_array_equal(soa[d["Q"] + 1, :7], st[:, 1].astype(np.float32))
+    np.testing.assert_array_equal(soa[d["QD"] + 4, :7], st[:, 9 + 4].astype(np.float32))
+    np.testing.assert_array_equal(soa[d["VX"], :7], cm[:, 1].astype(np.float32))
+    np.testing.assert_array_equal(soa[d["OFFSETS"] + 3, :7], ga[:, 6].astype(np.float32))
+    s2, c2, g2 = R.from_soa(soa, 7)
+    np.testing.assert_array_equal(s2, st.astype(np.float32).astype(np.float64))
+    np.testing.assert_array_equal(g2, ga.astype(np.float32).astype(np.float64))
+    assert s2.flags["C_CONTIGUOUS"] and c2.shape == (7, 3)

@@ -30,6 +30,13 @@ def main():
         print("T", T, "ok", int((sol["status"] == 0).sum()), int((sol3["status"] == 0).sum()),
               "shared == per-agent", sol.tobytes() == sol2.tobytes() and z.tobytes() == z2.tobytes(),
               float(np.abs(z).max()), flush=True)
+    # full squads: 70 agents of the random batch share few schedules (lanes 0..31 of a squad busy)
+    s = R.default_settings(10)
+    st, cm, ga = R.synthetic_batch(70, "random", seed=5, model=m, settings=s)
+    br = R.BatchRunner(70, m, s)
+    sol, z = br.solve(st, cm, ga, want_z=True)
+    br.close()
+    print("T 10 random squads ok", int((sol["status"] == 0).sum()), flush=True)
 
 
 if __name__ == "__main__":

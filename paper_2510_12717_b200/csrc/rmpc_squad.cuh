@@ -876,7 +876,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
     float qh[NV];
     sq_qhat(q, i, b, qh);
     const float* ei = q.e + i * NV;
-#pragma unroll 1
+#pragma unroll
     for (int j = 0; j < NV; ++j) {
       const float e = ei[j];
       const float ph = (float)(wcost(P, j) * P.dt[i]) * e * e;

@@ -12,7 +12,7 @@ import subprocess
 import sys
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-LIB = os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
+LIB = os.environ.get("RMPC_SASS_FILE") or os.path.join(ROOT, "paper_2510_12717_b200", "lib", "librmpc_b200.so")
 KEEP = ("FFMA", "FMUL", "FADD", "DFMA", "DMUL", "DADD", "DMMA", "HMMA", "UTCMMA", "UTCHMMA", "LDTM", "STTM",
         "LDS", "STS", "LDG", "STG", "LDL", "STL", "SHFL", "BAR", "MUFU", "UBLKCP", "UTMALDG")
 

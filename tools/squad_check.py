@@ -63,5 +63,6 @@ for T, n in ((10, 16384),) if quick else ((10, 16384), (10, 4096), (5, 8192), (3
         tm = br.last_timing()
         br.set_stage_profiling(False)
         print(f"T={T} n={n} level={lvl}: {ms:.3f} ms/tick -> {n / ms / 1e3:.2f} M solves/s | stages",
-              {k: round(v, 3) for k, v in tm["stage_ms"].items()}, flush=True)
+              {k: round(v, 3) for k, v in tm["stage_ms"].items()}, "| per-agent means (us)",
+              {k: round(v * 1e3, 1) for k, v in tm["stage_mean_ms"].items() if v > 0}, flush=True)
     br.close()

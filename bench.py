@@ -370,12 +370,15 @@ def closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier):
           for _ in range(args.cl_ticks)]
     barrier()
     torch.cuda.synchronize()
+    from paper_2510_12717_b200.runtime import kernel_launches
+    l0 = kernel_launches()
     with torch.cuda.stream(stream):
         for k in range(args.cl_ticks):
             ev[k][0].record(stream)
             tick()
             ev[k][1].record(stream)
     stream.synchronize()
+    launches = (kernel_launches() - l0) / args.cl_ticks + 1  # + plan_feedback (env library)
     barrier()
     tick_ms = max_over_ranks([a.elapsed_time(b) for a, b in ev])
     sol = d_out.cpu().numpy().view(SOLUTION_DTYPE)
@@ -387,7 +390,7 @@ def closed_loop_run(args, R, m, dev, rank, world, max_over_ranks, barrier):
             "p50_tick_ms": float(np.median(tick_ms)), "p99_tick_ms": float(np.percentile(tick_ms, 99)),
             "solves_per_s": n * world / (float(np.mean(tick_ms)) * 1e-3),
             "tick_budget_ms": 10.0, "failed_solves_last_tick_max_rank": ok,
-            "gpu_launches_per_tick": 2}
+            "gpu_launches_per_tick": launches}
 
 
 def main():

@@ -217,13 +217,16 @@ int32_t rmpc_solve_device_active_set(rmpc_handle* handle, const rmpc_state* d_st
                                      const rmpc_command* d_cmds, const rmpc_gait* d_gaits,
                                      rmpc_solution* d_out, uint8_t* d_active, void* stream);
 
-/* Schedule-shared factorization (default on).  With warm_start off the QP matrices, the Ruiz
- * scaling and the KKT factor of an agent depend only on its contact schedule (the stance flags
- * of every horizon node; mpc.cpp:266-276 linearizes about the nominal pose), so each solve
+/* Schedule-shared factorization (default: level 2).  With warm_start off the QP matrices, the
+ * Ruiz scaling and the KKT factor of an agent depend only on its contact schedule (the stance
+ * flags of every horizon node; mpc.cpp:266-276 linearizes about the nominal pose), so each solve
  * first hashes every agent's schedule, factorizes each distinct schedule once, and lets every
- * agent of that schedule load the result: bit-identical to the per-agent factorization, which
- * warm-started solves (and this switch off) use.  Calls on one handle share the schedule
- * workspace: issue device solves of one handle on one stream. */
+ * agent of that schedule load the result.  Levels: 0 off (per-agent factorization, also every
+ * warm-started solve); 1 one warp pair per agent on the shared factor (bit-identical to 0);
+ * 3 squads -- 32 agents of a schedule per warp pair, lane = agent (horizon <= 10, else level 1);
+ * 2 (default) squads where the shard is larger than two waves of the per-agent kernel, else 0
+ * (a squad's latency exceeds a small batch's per-agent solve).  Calls on one handle share the
+ * schedule workspace: issue device solves of one handle on one stream. */
 int32_t rmpc_set_schedule_sharing(rmpc_handle* handle, int32_t enabled);
 
 /* Stage-profiling switch: when on, the kernel samples the SM clock at the reference's stage

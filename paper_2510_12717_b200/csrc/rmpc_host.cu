@@ -125,7 +125,7 @@ struct rmpc_handle {
   rmpc_timing timing;
   std::string err;
   int profile = 0;
-  int share = 2;  // cold-start schedule sharing: 0 off, 1 warp-pair CTAs, 2 squads
+  int share = 2;  // cold-start schedule sharing: 0 off, 1 warp-pair CTAs, 2 auto, 3 squads
   std::unique_ptr<ShardPool> pool;  // shards >= 2 only
 };
 
@@ -208,6 +208,19 @@ rmpc_dev::KParams make_params(const rmpc_handle& h) {
   P.weight = tm * m.gravity;
   P.profile = h.profile;
   return P;
+}
+
+// The solve path of the handle (rmpc_set_schedule_sharing): 0 per-agent, 1 shared warp pairs,
+// 2 squads.  Level 2 ("auto") picks the per-agent kernel when the batch fits two of its waves on
+// one device: a squad's latency (~0.6 ms at N = 10) is ~2.5 per-agent waves, so below that the
+// per-agent kernel finishes first (C1: 0.21 vs 0.75 ms).  Decided on the whole batch, so every
+// shard of a multi-device handle runs the same path (results never depend on the sharding).
+// Level 3 forces squads.
+int solve_path(const rmpc_handle& h, int sms, bool cold = false) {
+  if ((h.settings.warm_start && !cold) || h.share == 0) return 0;
+  if (h.share == 1) return 1;
+  if (h.share == 2 && h.n <= 2 * sms * rmpc_dev::cta_shape(h.NT).agents) return 0;
+  return 2;
 }
 
 #define CK(expr)                                                   \
@@ -406,7 +419,7 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   const bool copyout = d_out != nullptr && d_z != nullptr;  // (records alone: written in the solve)
   P.out = copyout ? sh.d_out : (d_out ? d_out : sh.d_out);
   P.z_out = z_out ? (copyout ? sh.d_z : (d_z ? d_z : sh.d_z)) : nullptr;
-  const int rc = rmpc_launch_shared(P, sh.sched[0], st, h.share, copyout ? &co : nullptr);
+  const int rc = rmpc_launch_shared(P, sh.sched[0], st, solve_path(h, sh.sms), copyout ? &co : nullptr);
   if (rc != 0) {
     sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
     sh.msg = std::string("rti_shared_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -438,7 +451,7 @@ void run_shard(rmpc_handle& h, Shard& sh, const rmpc_state* states, const rmpc_c
   sh.err = 0;
   if (sh.count == 0) return;
   CK(cudaSetDevice(sh.device));
-  if (h.share && !h.settings.warm_start) {
+  if (solve_path(h, sh.sms) != 0) {
     run_shard_shared(h, sh, states, cmds, gaits, out, z_out, soa);
     return;
   }
@@ -608,8 +621,9 @@ int32_t launch_device(rmpc_handle& h, Shard& sh, int n, const rmpc_state* d_stat
   P.prof = sh.d_prof;
   P.profile = 0;
   if (d_active) P.warm_start = 0;
-  const int rc = (h.share && !P.warm_start) ? rmpc_launch_shared(P, sh.sched[0], stream, h.share)  // cold start
-                                            : rmpc_launch_rti(P, stream);
+  const int path = solve_path(h, sh.sms, d_active != nullptr);  // (the active-set solve is cold)
+  const int rc = path != 0 ? rmpc_launch_shared(P, sh.sched[0], stream, path)  // cold start, shared
+                           : rmpc_launch_rti(P, stream);
   if (rc != 0) {
     h.err = std::string("rti_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
     return rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
@@ -929,7 +943,7 @@ int32_t rmpc_mpc_torque(const rmpc_model* model, const rmpc_solution* sol, const
 
 int32_t rmpc_set_schedule_sharing(rmpc_handle* h, int32_t enabled) {
   if (!h) return RMPC_ERR_INVALID_ARG;
-  h->share = enabled < 0 ? 0 : (enabled > 2 ? 2 : enabled);
+  h->share = enabled < 0 ? 0 : (enabled > 3 ? 3 : enabled);
   return RMPC_OK;
 }
 

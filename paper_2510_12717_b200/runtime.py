@@ -368,8 +368,9 @@ class BatchRunner:
     def set_schedule_sharing(self, level=True):
         """Cold-start schedule sharing (rmpc_set_schedule_sharing): each distinct contact
         schedule is factorized once.  True / 2 (default): lane-per-agent squads where the
-        horizon fits them (T <= 10); 1: warp-pair CTAs per schedule, bit-identical to the
-        per-agent solve; False / 0: per-agent factorization."""
+        horizon fits them (T <= 10) and the batch exceeds two waves of the per-agent kernel,
+        else the per-agent kernel; 3: squads always; 1: warp-pair CTAs per schedule,
+        bit-identical to the per-agent solve; False / 0: per-agent factorization."""
         level = 2 if level is True else int(level)
         self._lib.rmpc_set_schedule_sharing(self._h, level)
 

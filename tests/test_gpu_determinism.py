@@ -1,0 +1,70 @@
+"""Race evidence without compute-sanitizer (closed on this GPU pool): the squad
+solve's bytes do not depend on which squad slot of a CTA serves a squad, nor on whether the
+CTA's other slot is busy (RMPC_SQUAD_SOLO=1 / 2 run one squad per CTA in slot 0 / slot 1), nor on
+the output path (device buffers, mapped host buffers, split launch with copy-out).  Needs a B200."""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import paper_2510_12717_b200 as R
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, %r)
+import paper_2510_12717_b200 as R
+m, s = R.default_model(), R.default_settings(%d)
+st, cm, ga = R.synthetic_batch(%d, "mixed", seed=9, model=m, settings=s)
+sol, z = R.BatchRunner(len(st), m, s).solve(st, cm, ga, want_z=True)
+sys.stdout.buffer.write(sol.tobytes() + z.tobytes())
+"""
+
+
+def run(T, n, solo):
+    env = dict(os.environ)
+    env.pop("RMPC_SQUAD_SOLO", None)
+    if solo:
+        env["RMPC_SQUAD_SOLO"] = str(solo)
+    r = subprocess.run([sys.executable, "-c", SCRIPT % (ROOT, T, n)], env=env, capture_output=True, timeout=600)
+    assert r.returncode == 0, r.stderr.decode()[-2000:]
+    return r.stdout
+
+
+@pytest.mark.parametrize("T,n", [(10, 5000), (3, 1500), (7, 700)])
+def test_squad_slot_independence(T, n):
+    base = run(T, n, 0)
+    assert len(base) > 0
+    assert run(T, n, 1) == base
+    assert run(T, n, 2) == base
+
+
+def test_output_paths_agree():
+    """Host solve (split launch: first wave copied out beside the second, which writes the mapped
+    buffers) == device solve, at C3 where the squads span two waves."""
+    import torch
+    from paper_2510_12717_b200.abi import SOLUTION_DTYPE
+    n, T = 16384, 10
+    m, s = R.default_model(), R.default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, "random", seed=21, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    host, zh = br.solve(st, cm, ga, want_z=True)
+    rec_only, _ = br.solve(st, cm, ga)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    z = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
+    br.solve_device(*d, out, z_out=z)
+    torch.cuda.synchronize()
+    assert (host["status"] == 0).all()
+    assert out.cpu().numpy().tobytes() == host.tobytes() == rec_only.tobytes()
+    assert z.cpu().numpy().tobytes() == zh.tobytes()
+    pinned = torch.zeros((n, T, 26), dtype=torch.float32).pin_memory().numpy()
+    po = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8).pin_memory().numpy().view(SOLUTION_DTYPE)
+    br.solve(st, cm, ga, out=po, z_out=pinned)
+    assert po.tobytes() == host.tobytes() and pinned.tobytes() == zh.tobytes()
+    assert np.isfinite(zh).all()

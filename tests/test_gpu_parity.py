@@ -334,8 +334,8 @@ def test_two_chunked_shards_on_one_device_match_one_shard():
 def test_schedule_sharing(T, kind, n):
     """Cold start: the matrices, Ruiz scales and factor depend only on the stance schedule
     (mpc.cpp:266-276), so each distinct schedule is factorized once (rmpc_set_schedule_sharing).
-    Level 1 (warp-pair CTAs of one schedule) gives exactly the per-agent bytes; level 2 (the
-    default: lane-per-agent squads for T <= 10, level 1 beyond) runs the same iterates with the
+    Level 1 (warp-pair CTAs of one schedule) gives exactly the per-agent bytes; level 3 (squads
+    forced: lane-per-agent squads for T <= 10, level 1 beyond) runs the same iterates with the
     agent in the lane -- equal to the per-agent solve within the parity gates, identical statuses
     (a failing agent next to working ones included), and identical bytes on the host (chunked)
     and device paths."""
@@ -346,20 +346,34 @@ def test_schedule_sharing(T, kind, n):
     st[5, 3] = np.nan
     br = R.BatchRunner(n, m, s)
     sols = {}
-    for level in (2, 1, 0):
+    for level in (3, 1, 0):
         br.set_schedule_sharing(level)
         sols[level] = br.solve(st, cm, ga, want_z=True)
-    (a, za), (p, zp), (b, zb) = sols[2], sols[1], sols[0]
+    (a, za), (p, zp), (b, zb) = sols[3], sols[1], sols[0]
     assert p.tobytes() == b.tobytes() and zp.tobytes() == zb.tobytes()
     assert a["status"][5] == STATUS_NONFINITE_INPUT
     c = compare(a, b, za, zb)
     print(f"T={T} {kind}: squads vs per-agent", summary(c))
     check(c, f"squads vs per-agent T={T} {kind}")
     assert c["z"].max() <= 1e-3
-    br.set_schedule_sharing(2)
+    br.set_schedule_sharing(3)
     dev = torch.device("cuda:0")
     d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
     out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     br.solve_device(*d, out)
     torch.cuda.synchronize()
     assert out.cpu().numpy().tobytes() == a.tobytes()
+
+
+@pytest.mark.parametrize("n", [1, 600, 1776, 1777, 4096])
+def test_auto_path_selection(n):
+    """Level 2 (default) = the per-agent kernel up to two of its waves (148 SMs x 6 agents x 2 =
+    1776 agents at N = 10: a squad's latency exceeds that), squads beyond: bytes equal to the
+    forced levels."""
+    m, s = default_model(), default_settings(10)
+    st, cm, ga = R.synthetic_batch(n, "random", seed=3, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    auto = br.solve(st, cm, ga, want_z=True)
+    br.set_schedule_sharing(0 if n <= 1776 else 3)
+    forced = br.solve(st, cm, ga, want_z=True)
+    assert auto[0].tobytes() == forced[0].tobytes() and auto[1].tobytes() == forced[1].tobytes()

@@ -17,8 +17,9 @@ def batch(n, kind, T, seed=2):
     return m, s, R.to_soa(st, cm, ga, ld=n + 5)
 
 
-@pytest.mark.parametrize("T,kind,n,share", [(10, "random", 4096, 2), (10, "mixed", 1000, 2), (10, "mixed", 300, 1),
-                                            (10, "random", 300, 0), (5, "random", 2000, 2), (20, "mixed", 256, 2)])
+@pytest.mark.parametrize("T,kind,n,share", [(10, "random", 4096, 2), (10, "mixed", 1000, 3), (10, "mixed", 300, 1),
+                                            (10, "random", 300, 0), (5, "random", 2000, 3), (20, "mixed", 256, 3),
+                                            (10, "random", 700, 2)])
 def test_soa_equals_aos_records(T, kind, n, share):
     m, s, soa = batch(n, kind, T)
     br = R.BatchRunner(n, m, s)

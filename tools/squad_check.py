@@ -26,11 +26,11 @@ for T, kind, n in cases[:3] if quick else cases:
         st[5, 3] = np.nan
     br = R.BatchRunner(n, m, s)
     res = {}
-    for lvl in (2, 1, 0):
+    for lvl in (3, 1, 0):
         br.set_schedule_sharing(lvl)
         res[lvl] = br.solve(st, cm, ga, want_z=True)
     ref, zr, _, _ = O.solve_batch(m, s, st, cm, ga, workers=16)
-    a, za = res[2]
+    a, za = res[3]
     print(f"T={T} {kind} n={n} status counts {np.bincount(a['status'], minlength=4)}", flush=True)
     print("  squad vs per-agent:", summary(compare(a, res[0][0], za, res[0][1])), flush=True)
     print("  squad vs oracle:   ", summary(compare(a, ref, za, zr)), flush=True)
@@ -46,7 +46,7 @@ for T, n in ((10, 16384),) if quick else ((10, 16384), (10, 4096), (5, 8192), (3
     d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
     out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
     z = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
-    for lvl in (2, 1):
+    for lvl in (3, 1):
         br.set_schedule_sharing(lvl)
         for _ in range(3):
             br.solve_device(*d, out, z_out=z)

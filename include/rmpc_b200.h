@@ -187,6 +187,9 @@ int32_t rmpc_solve_soa(rmpc_handle* handle, const float* soa, int64_t ld, const 
 int32_t rmpc_solve_soa_device(rmpc_handle* handle, const float* d_soa, int64_t ld, const rmpc_solution* d_prev,
                               const float* d_prev_z_star, rmpc_solution* d_out, float* d_z_star_out, void* stream);
 
+/* The agent split of rmpc_create and of one-rank-per-GPU deployments: shard g of G owns
+ * [floor(g n / G), floor((g + 1) n / G)).  Host only (no device needed). */
+int32_t rmpc_shard_range(int32_t n_agents, int32_t n_shards, int32_t shard, int32_t* begin, int32_t* count);
 /* Shard g of the handle: its CUDA device and contiguous agent range. */
 int32_t rmpc_shard_info(const rmpc_handle* handle, int32_t shard, int32_t* device, int32_t* begin,
                         int32_t* count);

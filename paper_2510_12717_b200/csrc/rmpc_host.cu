@@ -751,8 +751,7 @@ int32_t rmpc_create(const rmpc_model* model, const rmpc_settings* settings, int3
   for (int g = 0; g < G; ++g) {  // contiguous ranges [g n / G, (g+1) n / G)
     Shard& sh = h->shards[g];
     sh.device = devs[g];
-    sh.begin = (int)((long long)g * n_agents / G);
-    sh.count = (int)((long long)(g + 1) * n_agents / G) - sh.begin;
+    rmpc_shard_range(n_agents, G, g, &sh.begin, &sh.count);
     alloc_shard(*h, sh);
     if (sh.err) {
       g_create_error = sh.msg;
@@ -879,6 +878,15 @@ int32_t rmpc_solve_device_sharded(rmpc_handle* h, const rmpc_state* const* d_sta
                                  d_z_star_out ? d_z_star_out[g] : nullptr, nullptr, streams ? streams[g] : nullptr);
     if (rc != RMPC_OK) return rc;
   }
+  return RMPC_OK;
+}
+
+int32_t rmpc_shard_range(int32_t n_agents, int32_t n_shards, int32_t shard, int32_t* begin, int32_t* count) {
+  if (n_agents < 0 || n_shards < 1 || shard < 0 || shard >= n_shards) return RMPC_ERR_INVALID_ARG;
+  const int32_t b = (int32_t)((long long)shard * n_agents / n_shards);
+  const int32_t e = (int32_t)((long long)(shard + 1) * n_agents / n_shards);
+  if (begin) *begin = b;
+  if (count) *count = e - b;
   return RMPC_OK;
 }
 

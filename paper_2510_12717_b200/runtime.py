@@ -31,7 +31,7 @@ EXPORTS = ("rmpc_model_default", "rmpc_settings_default", "rmpc_create", "rmpc_d
            "rmpc_nominal_pose", "rmpc_mpc_torque", "rmpc_set_stage_profiling", "rmpc_build_info",
            "rmpc_smem_bytes", "rmpc_agents_per_cta", "rmpc_sizeof", "rmpc_fma_peak",
            "rmpc_solve_device_sharded", "rmpc_shard_info", "rmpc_set_schedule_sharing",
-           "rmpc_solve_soa", "rmpc_solve_soa_device", "rmpc_kernel_launches")
+           "rmpc_solve_soa", "rmpc_solve_soa_device", "rmpc_kernel_launches", "rmpc_shard_range")
 
 SOA_FIELDS = 28  # RMPC_SOA_FIELDS: q 0..8, qd 9..17, height, vx, wpitch, phase, period, phase_switch, offsets 24..27
 
@@ -69,6 +69,8 @@ def load_library(path: str | None = None, build_if_missing: bool = True):
     L.rmpc_solve_device_sharded.restype = _I
     L.rmpc_shard_info.argtypes = [_VP, _I, C.POINTER(_I), C.POINTER(_I), C.POINTER(_I)]
     L.rmpc_shard_info.restype = _I
+    L.rmpc_shard_range.argtypes = [_I, _I, _I, C.POINTER(_I), C.POINTER(_I)]
+    L.rmpc_shard_range.restype = _I
     for f in ("rmpc_size", "rmpc_workers", "rmpc_horizon"):
         getattr(L, f).argtypes = [_VP]
         getattr(L, f).restype = _I

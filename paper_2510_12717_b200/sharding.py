@@ -5,11 +5,17 @@ from __future__ import annotations
 
 
 def shard_range(rank: int, world: int, n_total: int) -> tuple[int, int]:
-    """Contiguous range [lo, hi) of rank `rank`: floor(r n / W) .. floor((r+1) n / W), the same
-    split rmpc_create uses across devices (rmpc_host.cu)."""
+    """Contiguous range [lo, hi) of rank `rank`: floor(r n / W) .. floor((r+1) n / W) -- the
+    library's own split (rmpc_shard_range, the one rmpc_create uses across devices)."""
+    import ctypes as C
+    from .runtime import library
     if world < 1 or not 0 <= rank < world:
         raise ValueError("bad rank/world")
-    return rank * n_total // world, (rank + 1) * n_total // world
+    b, c = C.c_int32(), C.c_int32()
+    rc = library().rmpc_shard_range(int(n_total), int(world), int(rank), C.byref(b), C.byref(c))
+    if rc != 0:
+        raise ValueError(f"rmpc_shard_range({n_total}, {world}, {rank}) failed: {rc}")
+    return b.value, b.value + c.value
 
 
 def max_over_ranks(values, dist=None, device=None):

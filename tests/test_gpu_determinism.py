@@ -68,3 +68,20 @@ def test_output_paths_agree():
     br.solve(st, cm, ga, out=po, z_out=pinned)
     assert po.tobytes() == host.tobytes() and pinned.tobytes() == zh.tobytes()
     assert np.isfinite(zh).all()
+
+
+def test_many_shards_on_one_device():
+    """A handle over eight shards of one GPU (eight persistent host workers, eight streams and
+    schedule workspaces) gives the one-shard bytes at C3: the split changes nothing."""
+    n, T = 16384, 10
+    m, s = R.default_model(), R.default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=4, model=m, settings=s)
+    one = R.BatchRunner(n, m, s).solve(st, cm, ga, want_z=True)
+    br = R.BatchRunner(n, m, s, devices=[0] * 8)
+    assert br.workers() == 8
+    ranges = [br.shard_info(g)[1:] for g in range(8)]
+    from paper_2510_12717_b200.sharding import shard_range
+    assert [(b, b + c) for b, c in ranges] == [shard_range(g, 8, n) for g in range(8)]
+    for _ in range(2):
+        eight = br.solve(st, cm, ga, want_z=True)
+        assert eight[0].tobytes() == one[0].tobytes() and eight[1].tobytes() == one[1].tobytes()

@@ -275,6 +275,7 @@ inline CtaShapeShared cta_shape_shared(int NT, int cap = SHARED_AGENTS) {
 
 // ------------------------------------------------------------------------- squads
 // Lane-per-agent schedule-shared solve (rmpc_squad.cuh).
+constexpr int SQ_PACK_SLICES = 8;  // sq_pack_kernel CTAs per schedule
 constexpr int SQ_MAXT = 10;   // horizons served by squads (5 node slabs of 96 TMEM columns per thread)
 constexpr int SQ_SLAB = 98;   // TMEM columns per own node
 constexpr int SQ_X = 0;       // x (26)

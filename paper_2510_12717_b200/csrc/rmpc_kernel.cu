@@ -305,8 +305,8 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
     if (b * P.agents_per_cta >= ns) return;  // whole CTA idle
     sched = b * P.agents_per_cta + pair;
     agent = sched < ns ? P.rep_list[sched] : P.n_agents;
-  } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve)
-    const int nl = *P.n_list;
+  } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve):
+    const int nl = *P.n_list;              // a grid of at most one wave, looping over the list
     if (b * P.agents_per_cta >= nl) return;
     const int idx = b * P.agents_per_cta + pair;
     agent = idx < nl ? P.agent_list[idx] : P.n_agents;
@@ -330,8 +330,14 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
-    solve_agent<SPILL>(P, smem + pair * make_layout(P.NT, P.spill_nodes).total, tm, tmn, 1 + pair, agent, sched,
-                       lane, w & 1);
+    float* base = smem + pair * make_layout(P.NT, P.spill_nodes).total;
+    solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1);
+    if (P.mode == 0 && P.agent_list != nullptr) {  // the pair's further list entries
+      const int nl = *P.n_list;
+      for (int idx = (b + (int)gridDim.x) * P.agents_per_cta + pair; idx < nl;
+           idx += (int)gridDim.x * P.agents_per_cta)
+        solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, P.agent_list[idx], sched, lane, w & 1);
+    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -580,6 +586,20 @@ int rmpc_kernel_setup(int) {
 // gpu_launches is the difference over its timed region.
 static std::atomic<long long> g_launches{0};
 
+// SM count of the current device, cached (several host threads, one per shard, may launch at once)
+static int sm_count() {
+  static std::atomic<int> sms[64];
+  int dev = 0;
+  cudaGetDevice(&dev);
+  int nsm = dev < 64 ? sms[dev].load(std::memory_order_relaxed) : 0;
+  if (nsm == 0) {
+    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
+    if (nsm <= 0) nsm = 148;
+    if (dev < 64) sms[dev].store(nsm, std::memory_order_relaxed);
+  }
+  return nsm;
+}
+
 static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st) {
   if (grid <= 0) return 0;
   g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -602,16 +622,7 @@ int rmpc_launch_rti(const rmpc_dev::KParams& params, void* stream) {
   // Whole waves of full CTAs (one CTA per SM), then the remainder spread over the SMs at
   // ceil(R / SMs) agents per CTA: a partial wave of fewer agents per SM runs faster than a
   // partial wave of full CTAs on a subset of the SMs.
-  // SM count per device, cached; several host threads (one per shard) may launch at once
-  static std::atomic<int> sms[64];
-  int dev = 0;
-  cudaGetDevice(&dev);
-  int nsm = dev < 64 ? sms[dev].load(std::memory_order_relaxed) : 0;
-  if (nsm == 0) {
-    cudaDeviceGetAttribute(&nsm, cudaDevAttrMultiProcessorCount, dev);
-    if (nsm <= 0) nsm = 148;
-    if (dev < 64) sms[dev].store(nsm, std::memory_order_relaxed);
-  }
+  const int nsm = sm_count();
   const int wave = nsm * c.agents;
   const int full_waves = P.n_agents / wave;
   const int rem = P.n_agents - full_waves * wave;
@@ -667,18 +678,27 @@ __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
   }
   unsigned long long h = mix64(k0 ^ mix64(k1 + 0x9e3779b97f4a7c15ull));
   if (h == ~0ull) h = ~0ull - 1;
+  // one insert per distinct key of the warp (thousands of agents share a handful of schedules:
+  // a CAS per agent serialises on a few table slots), and a plain read before the CAS
+  const unsigned act = __activemask();
+  const unsigned peers = __match_any_sync(act, h);
+  const int leader = __ffs(peers) - 1;
   unsigned int slot = (unsigned int)h & (unsigned int)(b.slots - 1);
-  for (;;) {
-    const unsigned long long prev = atomicCAS(b.table + slot, ~0ull, h);
-    if (prev == ~0ull) {
-      const int id = atomicAdd(b.n_sched, 1);
-      b.slot_id[slot] = id < b.cap ? id : -1;
-      if (id < b.cap) b.rep_list[id] = a;
-      break;
+  if ((threadIdx.x & 31) == leader) {
+    for (;;) {
+      unsigned long long prev = *(volatile unsigned long long*)(b.table + slot);
+      if (prev == ~0ull) prev = atomicCAS(b.table + slot, ~0ull, h);
+      if (prev == ~0ull) {
+        const int id = atomicAdd(b.n_sched, 1);
+        b.slot_id[slot] = id < b.cap ? id : -1;
+        if (id < b.cap) b.rep_list[id] = a;
+        break;
+      }
+      if (prev == h) break;
+      slot = (slot + 1) & (unsigned int)(b.slots - 1);
     }
-    if (prev == h) break;
-    slot = (slot + 1) & (unsigned int)(b.slots - 1);
   }
+  slot = __shfl_sync(peers, slot, leader);
   b.slot_of[a] = (int)slot;
 }
 
@@ -689,8 +709,13 @@ __global__ void sched_count_kernel(const KParams P, RmpcSchedBuffers b) {
   if (a >= P.n_agents) return;
   const int sl = b.slot_of[a];
   const int id = sl >= 0 ? b.slot_id[sl] : -1;
-  if (id >= 0) {
-    b.pos[a] = atomicAdd(b.cnt + id, 1);
+  if (id >= 0) {  // warp-aggregated: one atomic per schedule id of the warp
+    const unsigned peers = __match_any_sync(__activemask(), id);
+    const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
+    int base = 0;
+    if (lane == leader) base = atomicAdd(b.cnt + id, __popc(peers));
+    base = __shfl_sync(peers, base, leader);
+    b.pos[a] = base + __popc(peers & ((1u << lane) - 1u));
   } else {
     b.pos[a] = -1;
     b.ulist[atomicAdd(b.n_unshared, 1)] = a;
@@ -820,7 +845,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   if (squads) {  // lane-per-agent squads, two per CTA (grid: an upper bound of sum ceil(count / 32) / 2)
     S.agents_per_cta = 32;
     S.sqpack = b.sqpack;
-    sq_pack_kernel<<<b.cap, 256, 0, st>>>(S);
+    sq_pack_kernel<<<dim3(b.cap, SQ_PACK_SLICES), 256, 0, st>>>(S);
     g_launches.fetch_add(1, std::memory_order_relaxed);
     const int nsq = (n + 31) / 32 + std::min(b.cap, n);
     S.pad2_ = solo;
@@ -854,7 +879,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   U.agents_per_cta = c.agents;
   U.spill_nodes = c.spill_nodes;
   U.tmem_cols = c.tmem_cols;
-  U.full_ctas = (n + c.agents - 1) / c.agents;
+  U.full_ctas = std::min((n + c.agents - 1) / c.agents, sm_count());  // one wave, looping over the list
   U.tail_agents = 0;
   if (co) {
     // the per-agent list writes the mapped host buffers too, after the first wave's copy-out: a

@@ -1139,18 +1139,21 @@ __global__ void sq_pack_kernel(const KParams P) {
   const StoreLayout SL = store_layout(NT);
   const float* entry = P.store + (size_t)g * P.store_stride;
   float* reg = P.sqpack + (size_t)g * L.priv;
-  for (int k = threadIdx.x; k < (NT + 1) * C_SIZE; k += blockDim.x) reg[L.coef + k] = entry[SL.coef + k];
-  for (int k = threadIdx.x; k < (NT + 1) * NSLOT; k += blockDim.x) {
+  // SQ_PACK_SLICES CTAs per schedule (blockIdx.y): a few independent loads per thread, not a
+  // serial loop of dependent L2 round trips
+  const int t0 = blockIdx.y * blockDim.x + threadIdx.x, ts = gridDim.y * blockDim.x;
+  for (int k = t0; k < (NT + 1) * C_SIZE; k += ts) reg[L.coef + k] = entry[SL.coef + k];
+  for (int k = t0; k < (NT + 1) * NSLOT; k += ts) {
     reg[L.lo + k] = entry[SL.rows + 2 * k];
     reg[L.hi + k] = entry[SL.rows + 2 * k + 1];
     reg[L.d + k] = entry[SL.d + k];
   }
-  for (int k = threadIdx.x; k < NT * NV; k += blockDim.x) {
+  for (int k = t0; k < NT * NV; k += ts) {
     reg[L.e + k] = entry[SL.e + k];
     reg[L.qh + k] = entry[SL.qh + k];
   }
-  for (int k = threadIdx.x; k <= NT; k += blockDim.x) reg[L.flags + k] = entry[SL.flags + k];
-  for (int k = threadIdx.x; k < NT * SQ_MF; k += blockDim.x) {
+  for (int k = t0; k <= NT; k += ts) reg[L.flags + k] = entry[SL.flags + k];
+  for (int k = t0; k < NT * SQ_MF; k += ts) {
     const int i = k / SQ_MF, r = (k % SQ_MF) / SQ_MROW, c = k % SQ_MROW;
     const float* blk = entry + SL.blocks + (size_t)i * 32 * TCOLS;
     float v = 0.f;

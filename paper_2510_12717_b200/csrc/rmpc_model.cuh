@@ -105,7 +105,10 @@ __device__ void inverse_dynamics(const KParams& P, const double* q, const double
 }
 
 __device__ __forceinline__ double wrap01(double x) {
-  const double w = fmod(x, 1.0);
+  // fmod(x, 1.0) (gait.cpp's std::fmod) without the division loop: for finite |x| < 2^53 the
+  // fraction x - trunc(x) is a multiple of ulp(x) below 1 in magnitude, so the subtraction is
+  // exact and equals fmod bit for bit (larger |x|: both give 0)
+  const double w = x - trunc(x);
   return w < 0.0 ? w + 1.0 : w;
 }
 

@@ -377,3 +377,26 @@ def test_auto_path_selection(n):
     br.set_schedule_sharing(0 if n <= 1776 else 3)
     forced = br.solve(st, cm, ga, want_z=True)
     assert auto[0].tobytes() == forced[0].tobytes() and auto[1].tobytes() == forced[1].tobytes()
+
+
+def test_schedule_store_over_capacity():
+    """More distinct schedules than the store holds (1 024 per shard): per-agent gait periods and
+    switch phases make almost every agent's schedule unique, so the ids past the capacity run the
+    per-agent list (rti_kernel over an agent list, a looping wave) next to the squads of the
+    stored ones -- every agent solved, within the parity gates of the per-agent factorization."""
+    n, T = 3000, 10
+    m, s = default_model(), default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, "random", seed=8, model=m, settings=s)
+    rng = np.random.default_rng(8)
+    ga = ga.copy()
+    ga[:, 1] = rng.uniform(0.35, 0.9, n)   # period
+    ga[:, 2] = rng.uniform(0.45, 0.7, n)   # phase_switch
+    br = R.BatchRunner(n, m, s)
+    br.set_schedule_sharing(3)
+    a, za = br.solve(st, cm, ga, want_z=True)
+    br.set_schedule_sharing(0)
+    b, zb = br.solve(st, cm, ga, want_z=True)
+    assert (a["status"] == 0).all()
+    c = compare(a, b, za, zb)
+    check(c, "over capacity: squads + list vs per-agent")
+    assert c["z"].max() <= 1e-3

@@ -341,6 +341,11 @@ struct RmpcSchedBuffers {
   float* store;               // cap x store_layout(T).total floats
   float* sqpack;              // cap x sq_layout(T).priv floats (squads), or NULL
   int32_t slots, cap, agents;
+  // the grouping pass (count, scan, scatter) runs on a side stream beside the store build:
+  // fork after the key kernel, join before the group solve (cudaStream_t / cudaEvent_t)
+  void* side;
+  void* ev_fork;
+  void* ev_join;
 };
 // The whole cold-start solve with schedule sharing for params.n_agents agents on `stream`:
 // hash every agent's stance schedule, build the store (one factorization per schedule), group

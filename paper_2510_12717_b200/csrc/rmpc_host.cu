@@ -289,6 +289,14 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
     sb.sqpack = nullptr;
     if (rmpc_dev::sq_supported(h.NT))
       CK(cudaMalloc(&sb.sqpack, (size_t)sb.cap * rmpc_dev::sq_layout(h.NT).priv * sizeof(float)));
+    cudaStream_t side = nullptr;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    CK(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking));
+    CK(cudaEventCreateWithFlags(&e0, cudaEventDisableTiming));
+    CK(cudaEventCreateWithFlags(&e1, cudaEventDisableTiming));
+    sb.side = side;
+    sb.ev_fork = e0;
+    sb.ev_join = e1;
   }
   const int rc = rmpc_kernel_setup(rmpc_dev::MAXT);
   if (rc != 0) {
@@ -309,6 +317,12 @@ void free_shard(Shard& sh) {
                     (void*)sb.ulist, (void*)sb.rep_list, (void*)sb.cnt, (void*)sb.grp_first, (void*)sb.grp_cta,
                     (void*)sb.n_sched, (void*)sb.n_unshared, (void*)sb.store, (void*)sb.sqpack})
       cudaFree(p);
+    if (sb.side) {
+      cudaStreamSynchronize((cudaStream_t)sb.side);
+      cudaStreamDestroy((cudaStream_t)sb.side);
+    }
+    if (sb.ev_fork) cudaEventDestroy((cudaEvent_t)sb.ev_fork);
+    if (sb.ev_join) cudaEventDestroy((cudaEvent_t)sb.ev_join);
   }
   for (auto& e : sh.ev) if (e) cudaEventDestroy(e);
   if (sh.stream) cudaStreamDestroy(sh.stream);

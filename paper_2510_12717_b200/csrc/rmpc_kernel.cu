@@ -774,13 +774,33 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   const cudaStream_t st = (cudaStream_t)stream;
   const int n = params.n_agents, NT = params.NT;
   const int blocks = (n + 255) / 256;
+  const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
+  static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
+    const char* e = getenv("RMPC_SQUAD_SOLO");
+    return e ? atoi(e) : 0;
+  }();
+  // host outputs: a split pays only where a second wave of squad CTAs follows the first; else
+  // the solve writes the mapped host buffers itself
+  if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > 2 * co->sms)) {
+    KParams Q = params;
+    Q.out = co->h_out;
+    Q.z_out = co->h_z;
+    return rmpc_launch_shared(Q, b, stream, variant, nullptr);
+  }
   int rc = (int)cudaMemsetAsync(b.table, 0xFF, (size_t)b.slots * sizeof(unsigned long long), st);
   if (rc == 0) rc = (int)cudaMemsetAsync(b.n_sched, 0, sizeof(int32_t), st);
   if (rc == 0) rc = (int)cudaMemsetAsync(b.n_unshared, 0, sizeof(int32_t), st);
   if (rc == 0) rc = (int)cudaMemsetAsync(b.cnt, 0, (size_t)b.cap * sizeof(int32_t), st);
   if (rc != 0) return rc;
   sched_key_kernel<<<blocks, 256, 0, st>>>(params, b);
-  sched_count_kernel<<<blocks, 256, 0, st>>>(params, b);
+  // fork: the grouping pass (count, scan, scatter) needs only the keys; it runs on the side
+  // stream while the store build (which needs only the representatives) runs here
+  const cudaStream_t side = b.side ? (cudaStream_t)b.side : st;
+  if (side != st) {
+    cudaEventRecord((cudaEvent_t)b.ev_fork, st);
+    cudaStreamWaitEvent(side, (cudaEvent_t)b.ev_fork, 0);
+  }
+  sched_count_kernel<<<blocks, 256, 0, side>>>(params, b);
   g_launches.fetch_add(2, std::memory_order_relaxed);
   // the store: setup + Ruiz + factorization of each schedule's representative (mode 1), one
   // warp pair per CTA (the few schedules' latency chains run alone on their SMs)
@@ -810,22 +830,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   F.tail_agents = 0;
   rc = launch_variant(F, c1, F.full_ctas, st);
   if (rc != 0) return rc;
-  const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
-  static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
-    const char* e = getenv("RMPC_SQUAD_SOLO");
-    return e ? atoi(e) : 0;
-  }();
-  // a split pays only where a second wave of squad CTAs follows the first
-  if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > 2 * co->sms)) {  // the solve writes the mapped host buffers
-    KParams Q = params;
-    Q.out = co->h_out;
-    Q.z_out = co->h_z;
-    return rmpc_launch_shared(Q, b, stream, variant, nullptr);
-  }
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
-  sched_scan_kernel<<<1, 1024, 0, st>>>(b, squads ? 32 : cs.agents);
-  sched_scatter_kernel<<<blocks, 256, 0, st>>>(params, b);
-  g_launches.fetch_add(3, std::memory_order_relaxed);  // + the group kernel below
   // the groups: one schedule per CTA (grid: an upper bound of sum ceil(count / A))
   KParams S = params;
   S.mode = 0;
@@ -845,8 +850,17 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   if (squads) {  // lane-per-agent squads, two per CTA (grid: an upper bound of sum ceil(count / 32) / 2)
     S.agents_per_cta = 32;
     S.sqpack = b.sqpack;
-    sq_pack_kernel<<<dim3(b.cap, SQ_PACK_SLICES), 256, 0, st>>>(S);
+    sq_pack_kernel<<<dim3(b.cap, SQ_PACK_SLICES), 256, 0, st>>>(S);  // (needs only the store)
     g_launches.fetch_add(1, std::memory_order_relaxed);
+  }
+  sched_scan_kernel<<<1, 1024, 0, side>>>(b, squads ? 32 : cs.agents);
+  sched_scatter_kernel<<<blocks, 256, 0, side>>>(params, b);
+  if (side != st) {  // join before the group solve
+    cudaEventRecord((cudaEvent_t)b.ev_join, side);
+    cudaStreamWaitEvent(st, (cudaEvent_t)b.ev_join, 0);
+  }
+  g_launches.fetch_add(3, std::memory_order_relaxed);  // + the group kernel below
+  if (squads) {
     const int nsq = (n + 31) / 32 + std::min(b.cap, n);
     S.pad2_ = solo;
     const int grid = solo ? nsq : (nsq + 1) / 2;

@@ -197,9 +197,43 @@ __device__ void dump_schedule(const KParams& P, const Sm& sm, float* st, int lan
 
 // One agent on one warp pair of the CTA: its shared-memory block at `base`, its TMEM node
 // blocks at `tm`, named barrier `bar`.  `sched` is the schedule id the pair builds in mode 1.
+__device__ __forceinline__ Sm make_sm(const KParams& P, float* base, uint32_t tm, int tmn, int bar, int warp,
+                                      bool spills) {
+  const int NT = P.NT;
+  const Layout L = make_layout(NT, P.spill_nodes);
+  Sm sm;
+  sm.scr = base + L.scr;
+  sm.coef = base + L.coef;
+  sm.vec = base + L.vec;
+  sm.row = reinterpret_cast<float4*>(base + L.row);
+  sm.tt = base + L.tt;
+  sm.dsc = base + L.dsc;
+  sm.bc = base + L.bc;
+  sm.flags = reinterpret_cast<uint32_t*>(base + L.flags);
+  sm.NT = NT;
+  sm.mid = mid_node(NT);
+  sm.tm = tm;
+  sm.tmn = tmn;
+  sm.spills = spills;
+  sm.spill = base + L.spill + warp * P.spill_nodes * SPILL_BLK;
+  sm.bar = bar;
+  return sm;
+}
+
+// Schedule store build (mode 1): warps 2.. of the CTA help the representative's warp pair with
+// the Ruiz passes -- the only stage of the build whose work splits by node without changing a
+// single operation (ruiz(): nodes are independent within a pass).  `go` is set by the pair.
+__device__ __forceinline__ void store_ruiz_helper(const KParams& P, float* base, int lane, int w, const int* go) {
+  const int nw = (int)(blockDim.x >> 5);
+  asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"((int)blockDim.x) : "memory");  // the pair's setup is done
+  if (*go == 0) return;
+  const Sm sm = make_sm(P, base, 0u, 0, 1, 0, false);
+  ruiz(P, sm, lane, w, nw, (int)blockDim.x);
+}
+
 template <bool SPILL>
 __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint32_t tm, int tmn, int bar,
-                                            int agent, int sched, int lane, int warp) {
+                                            int agent, int sched, int lane, int warp, int* go = nullptr) {
   const int NT = P.NT;
   const Layout L = make_layout(NT, P.spill_nodes);
   Sm sm;
@@ -259,6 +293,12 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
                   : setup_dynamics(P, sm, lane, st, cmd, gait, warm, pz)) && st_ok;
   ok = pair_and(sm, ok);
   prof_mark(P, tid, 2, t0);
+  const int nw_cta = (int)(blockDim.x >> 5);
+  const bool helped = P.mode == 1 && nw_cta > 2 && go != nullptr;
+  if (helped) {  // hand the setup to the helper warps for the Ruiz passes
+    if (tid == 0) *go = ok && P.ruiz_iters > 0;
+    asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"((int)blockDim.x) : "memory");
+  }
   if (P.mode == 1 && !ok) {  // cannot happen for a representative (finite inputs); unshared
     if (tid == 0) reinterpret_cast<int32_t*>(P.store + (size_t)sched * P.store_stride + store_layout(NT).flags)[NT] = -1;
     return;
@@ -266,7 +306,10 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   if (!ok) {
     out.status = RMPC_STATUS_NONFINITE_INPUT;
   } else {
-    if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp);
+    if (P.ruiz_iters > 0) {
+      if (helped) ruiz(P, sm, lane, warp, nw_cta, (int)blockDim.x);
+      else ruiz(P, sm, lane, warp);
+    }
     apply_scaling(P, sm, lane, warp);
     prof_mark(P, tid, 3, t0);
     const int good = factorize(P, sm, lane, warp);
@@ -296,15 +339,17 @@ template <bool SPILL, int MAXA>
 __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   extern __shared__ __align__(16) float smem[];
   __shared__ uint32_t tmem_base;
+  __shared__ int s_go;
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int pair = w >> 1;
   const int b = blockIdx.x;
   int agent, sched = -1;
-  if (P.mode == 1) {  // schedule store: pair -> schedule id -> its representative agent
+  if (P.mode == 1) {  // schedule store: one schedule per CTA, built by pair 0 (the other pairs
+                      // help with its Ruiz passes: store_ruiz_helper)
     const int ns = min(*P.n_sched, P.store_cap);
-    if (b * P.agents_per_cta >= ns) return;  // whole CTA idle
-    sched = b * P.agents_per_cta + pair;
-    agent = sched < ns ? P.rep_list[sched] : P.n_agents;
+    if (b >= ns) return;  // whole CTA idle
+    sched = b;
+    agent = pair == 0 ? P.rep_list[sched] : -1;
   } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve):
     const int nl = *P.n_list;              // a grid of at most one wave, looping over the list
     if (b * P.agents_per_cta >= nl) return;
@@ -327,11 +372,13 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
-  if (agent < P.n_agents) {
+  if (P.mode == 1 && pair > 0) {
+    store_ruiz_helper(P, smem, lane, w, &s_go);
+  } else if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
     float* base = smem + pair * make_layout(P.NT, P.spill_nodes).total;
-    solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1);
+    solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1, P.mode == 1 ? &s_go : nullptr);
     if (P.mode == 0 && P.agent_list != nullptr) {  // the pair's further list entries
       const int nl = *P.n_list;
       for (int idx = (b + (int)gridDim.x) * P.agents_per_cta + pair; idx < nl;
@@ -600,15 +647,17 @@ static int sm_count() {
   return nsm;
 }
 
-static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st) {
+static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st,
+                          int threads = 0) {
   if (grid <= 0) return 0;
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  const int nt = threads > 0 ? threads : 64 * c.agents;
   if (c.dense)
-    rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+    rmpc_dev::rti_kernel<false, rmpc_dev::DENSE_AGENTS><<<grid, nt, c.smem_bytes, st>>>(P);
   else if (c.spill_nodes > 0)
-    rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+    rmpc_dev::rti_kernel<true, rmpc_dev::MAX_AGENTS><<<grid, nt, c.smem_bytes, st>>>(P);
   else
-    rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS><<<grid, 64 * c.agents, c.smem_bytes, st>>>(P);
+    rmpc_dev::rti_kernel<false, rmpc_dev::MAX_AGENTS><<<grid, nt, c.smem_bytes, st>>>(P);
   return (int)cudaGetLastError();
 }
 
@@ -828,7 +877,8 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   F.tmem_cols = c1.tmem_cols;
   F.full_ctas = b.cap;
   F.tail_agents = 0;
-  rc = launch_variant(F, c1, F.full_ctas, st);
+  // one CTA per schedule: the representative's warp pair plus helper warps for its Ruiz passes
+  rc = launch_variant(F, c1, F.full_ctas, st, 64 * MAX_AGENTS);
   if (rc != 0) return rc;
   const CtaShapeShared cs = cta_shape_shared(NT, shared_agents_cap(NT));
   // the groups: one schedule per CTA (grid: an upper bound of sum ceil(count / A))

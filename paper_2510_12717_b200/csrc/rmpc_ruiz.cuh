@@ -16,7 +16,16 @@ namespace rmpc_dev {
 // [[P, A^T], [A, 0]]: each pass takes delta = 1/sqrt(inf-norm) of every row/column of the
 // current scaled matrix (1 for empty ones), then d *= delta (rows), e *= delta (columns).
 // Row deltas are parked in row.z, column deltas in V_S until the pass is applied.
-__device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
+// The pass loop runs on `nw` warps (wi = this warp's index among them): the agent's warp pair
+// (nw = 2, its pair barrier), or in the schedule store build the pair plus helper warps of its
+// CTA (nw > 2, CTA barrier RUIZ_BAR over `cnt` threads) -- nodes are independent within a
+// pass, so the split changes nothing but the latency.
+constexpr int RUIZ_BAR = 15;
+__device__ __forceinline__ void ruiz_sync(const Sm& sm, int nw, int cnt) {
+  if (nw <= 2) pair_sync(sm);
+  else asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"(cnt) : "memory");
+}
+__device__ void ruiz(const KParams& P, const Sm& sm, int lane, int wi, int nw = 2, int cnt = 64) {
   const int NT = P.NT;
   Terms T;
   build_terms(lane, T);
@@ -26,8 +35,8 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
   // the other, so one barrier per pass suffices.  The second d lives in the scratch region,
   // the second e in V_S.
   const int nd = (NT + 1) * NSLOT;
-  for (int r = lane + 32 * warp; r < nd; r += 64) sm.scr[r] = sm.dsc[r];
-  pair_sync(sm);
+  for (int r = lane + 32 * wi; r < nd; r += 32 * nw) sm.scr[r] = sm.dsc[r];
+  ruiz_sync(sm, nw, cnt);
   const float wl = lane < NV ? (float)wcost(P, lane) : 0.f;
   auto inv_sqrt1 = [](float nrm) { return nrm > 0.f ? rsqrtf(nrm) : 1.f; };  // MUFU.RSQ
 #pragma unroll 1
@@ -62,21 +71,21 @@ __device__ void ruiz(const KParams& P, const Sm& sm, int lane, int warp) {
       }
     };
     // nodes are independent within a pass: two per iteration, all loads ahead of the stores
-    int i = warp;
+    int i = wi;
 #pragma unroll 1
-    for (; i + 2 < NT; i += 4) {
-      const Norms a = norms(i), b = norms(i + 2);
+    for (; i + nw < NT; i += 2 * nw) {
+      const Norms a = norms(i), b = norms(i + nw);
       update(i, a);
-      update(i + 2, b);
+      update(i + nw, b);
     }
     if (i < NT) update(i, norms(i));
-    pair_sync(sm);  // every norm of the next pass uses the scales of this one
+    ruiz_sync(sm, nw, cnt);  // every norm of the next pass uses the scales of this one
   }
   if (P.ruiz_iters & 1) {  // the last pass wrote the second copies
-    for (int r = lane + 32 * warp; r < nd; r += 64) sm.dsc[r] = sm.scr[r];
-    for (int i = warp; i < NT; i += 2)
+    for (int r = lane + 32 * wi; r < nd; r += 32 * nw) sm.dsc[r] = sm.scr[r];
+    for (int i = wi; i < NT; i += nw)
       if (lane < NV) sm.V(i, V_E)[lane] = sm.V(i, V_S)[lane];
-    pair_sync(sm);
+    ruiz_sync(sm, nw, cnt);
   }
 }
 

@@ -834,21 +834,21 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
       const float a0 = cf[C_FORCE + 4 * c] * f0 + cf[C_FORCE + 4 * c + 1] * f1;
       const float a1 = cf[C_FORCE + 4 * c + 2] * f0 + cf[C_FORCE + 4 * c + 3] * f1;
       const int s0 = 12 + 4 * c;
-      prim = fmaxf(prim, fabsf(a0 - zo[4 * c]) / q.DS(i, s0));
-      prim = fmaxf(prim, fabsf(a1 - zo[4 * c + 1]) / q.DS(i, s0 + 1));
-      prim = fmaxf(prim, fabsf(pa - zo[4 * c + 2]) / q.DS(i, s0 + 2));
-      prim = fmaxf(prim, fabsf(pb - zo[4 * c + 3]) / q.DS(i, s0 + 3));
+      prim = fmaxf(prim, __fdividef(fabsf(a0 - zo[4 * c]), q.DS(i, s0)));
+      prim = fmaxf(prim, __fdividef(fabsf(a1 - zo[4 * c + 1]), q.DS(i, s0 + 1)));
+      prim = fmaxf(prim, __fdividef(fabsf(pa - zo[4 * c + 2]), q.DS(i, s0 + 2)));
+      prim = fmaxf(prim, __fdividef(fabsf(pb - zo[4 * c + 3]), q.DS(i, s0 + 3)));
     }
 #pragma unroll
     for (int mb = 0; mb < 12; ++mb) {
       const float ab = cf[C_BOX + mb] * x[mb < 6 ? 3 + mb : 6 + mb];
-      prim = fmaxf(prim, fabsf(ab - zo[16 + mb]) / q.DS(i, 28 + mb));
+      prim = fmaxf(prim, __fdividef(fabsf(ab - zo[16 + mb]), q.DS(i, 28 + mb)));
     }
     if (node0) {
 #pragma unroll
       for (int l = 0; l < NINIT; ++l) {
         const float zl = eqz ? q.pv(q.IL(l)) : 0.f;
-        prim = fmaxf(prim, fabsf(cf[C_INIT + l] * x[l] - zl) / q.DS(-1, INIT0 + l));
+        prim = fmaxf(prim, __fdividef(fabsf(cf[C_INIT + l] * x[l] - zl), q.DS(-1, INIT0 + l)));
       }
     }
     // interval i-1 rows: x_{i-1} (xprev) and x_i
@@ -856,7 +856,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
 #pragma unroll
       for (int k = 0; k < 9; ++k) {
         const float a = cp[C_A1 + k] * x[k] + cp[C_A2 + k] * xprev[k] + cp[C_A3 + k] * x[NQ + k];
-        prim = fmaxf(prim, fabsf(a - (eqz ? q.LO(i - 1, k) : 0.f)) / q.DS(i - 1, k));
+        prim = fmaxf(prim, __fdividef(fabsf(a - (eqz ? q.LO(i - 1, k) : 0.f)), q.DS(i - 1, k)));
       }
 #pragma unroll
       for (int bb = 0; bb < 3; ++bb) {
@@ -865,7 +865,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
         for (int k = 0; k < 9; ++k) a = fmaf(cp[C_DYNU + 12 * bb + k], x[NQ + k], a);
 #pragma unroll
         for (int jv = 0; jv < 17; ++jv) a = fmaf(cp[C_DYNV + 20 * bb + jv], xprev[9 + jv], a);
-        prim = fmaxf(prim, fabsf(a - (eqz ? q.LO(i - 1, 9 + bb) : 0.f)) / q.DS(i - 1, 9 + bb));
+        prim = fmaxf(prim, __fdividef(fabsf(a - (eqz ? q.LO(i - 1, 9 + bb) : 0.f)), q.DS(i - 1, 9 + bb)));
       }
     }
     // dual residual |P^ x + q^ + A^T y| / e, objective, z*
@@ -880,7 +880,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
     for (int j = 0; j < NV; ++j) {
       const float e = ei[j];
       const float ph = (float)(wcost(P, j) * P.dt[i]) * e * e;
-      dual = fmaxf(dual, fabsf(ph * x[j] + qh[j] + aty[j]) / e);
+      dual = fmaxf(dual, __fdividef(fabsf(ph * x[j] + qh[j] + aty[j]), e));
       double g, des;
       guess_and_target(P, i, j, false, nullptr, st, cmd, bits, g, des);
       const double w = wcost(P, j) * P.dt[i];

@@ -306,10 +306,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   if (!ok) {
     out.status = RMPC_STATUS_NONFINITE_INPUT;
   } else {
-    if (P.ruiz_iters > 0) {
-      if (helped) ruiz(P, sm, lane, warp, nw_cta, (int)blockDim.x);
-      else ruiz(P, sm, lane, warp);
-    }
+    if (P.ruiz_iters > 0) ruiz(P, sm, lane, warp, helped ? nw_cta : 2, helped ? (int)blockDim.x : 64);
     apply_scaling(P, sm, lane, warp);
     prof_mark(P, tid, 3, t0);
     const int good = factorize(P, sm, lane, warp);
@@ -350,8 +347,8 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
     if (b >= ns) return;  // whole CTA idle
     sched = b;
     agent = pair == 0 ? P.rep_list[sched] : -1;
-  } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve):
-    const int nl = *P.n_list;              // a grid of at most one wave, looping over the list
+  } else if (P.agent_list != nullptr) {  // an agent list (unshared agents of a shared solve)
+    const int nl = *P.n_list;
     if (b * P.agents_per_cta >= nl) return;
     const int idx = b * P.agents_per_cta + pair;
     agent = idx < nl ? P.agent_list[idx] : P.n_agents;
@@ -378,13 +375,9 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);
     float* base = smem + pair * make_layout(P.NT, P.spill_nodes).total;
+    // (one straight-line call: a loop around the inlined solve -- e.g. a looping wave over the
+    // agent list -- doubles the ADMM loop's spills, measured 2x slower)
     solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1, P.mode == 1 ? &s_go : nullptr);
-    if (P.mode == 0 && P.agent_list != nullptr) {  // the pair's further list entries
-      const int nl = *P.n_list;
-      for (int idx = (b + (int)gridDim.x) * P.agents_per_cta + pair; idx < nl;
-           idx += (int)gridDim.x * P.agents_per_cta)
-        solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, P.agent_list[idx], sched, lane, w & 1);
-    }
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
@@ -943,7 +936,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   U.agents_per_cta = c.agents;
   U.spill_nodes = c.spill_nodes;
   U.tmem_cols = c.tmem_cols;
-  U.full_ctas = std::min((n + c.agents - 1) / c.agents, sm_count());  // one wave, looping over the list
+  U.full_ctas = (n + c.agents - 1) / c.agents;  // (an upper bound: idle CTAs exit at once)
   U.tail_agents = 0;
   if (co) {
     // the per-agent list writes the mapped host buffers too, after the first wave's copy-out: a

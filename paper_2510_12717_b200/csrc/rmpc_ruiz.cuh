@@ -25,7 +25,7 @@ __device__ __forceinline__ void ruiz_sync(const Sm& sm, int nw, int cnt) {
   if (nw <= 2) pair_sync(sm);
   else asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"(cnt) : "memory");
 }
-__device__ void ruiz(const KParams& P, const Sm& sm, int lane, int wi, int nw = 2, int cnt = 64) {
+__device__ void ruiz(const KParams& P, const Sm& sm, int lane, int wi, int nw, int cnt) {
   const int NT = P.NT;
   Terms T;
   build_terms(lane, T);

@@ -311,7 +311,7 @@ __host__ __device__ inline SqLayout sq_layout(int NT) {
   L.flags = o; o += align4(NT + 1);     // stance bits per node, then the factorization status
   L.priv_warp = 32 * (nb * SQ_PRIV + NINIT + SQ_NXI);
   L.priv = o;  o += 2 * L.priv_warp;
-  L.cross = o; o += 32 * 56;
+  L.cross = o; o += 32 * 82;
   L.total = o;
   return L;
 }

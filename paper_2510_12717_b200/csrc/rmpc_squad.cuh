@@ -27,11 +27,12 @@ namespace rmpc_dev {
 // Layout constants and sq_layout: rmpc_device.cuh.
 
 // Cross-thread elements of an agent (shared by its two threads), [element][lane].
-constexpr int SQX_XM = 0;     // x~_m of the middle node (top -> bottom)
+constexpr int SQX_XM = 0;     // x~_m of the middle node (rows 0..15 from the top, 16..25 from the bottom)
 constexpr int SQX_TM = 26;    // t of interval m's rows (bottom writes, both read)
 constexpr int SQX_GB = 38;    // g'_{m+1}: gint (9), g (3) (bottom -> top)
 constexpr int SQX_BAD = 50;   // first non-finite iteration, top / bottom
 constexpr int SQX_SAME = 52;  // schedule check, top / bottom
+constexpr int SQX_UA = 56;    // the middle node's rhs with the top's coupling (top -> bottom), 26
 
 // ------------------------------------------------------------------------- TMEM (own lane)
 __device__ __forceinline__ void tq_ld1(uint32_t a, float* v) {
@@ -128,6 +129,9 @@ __device__ __forceinline__ void tq_fence(float* v) {
 }
 
 __device__ __forceinline__ void sq_bar(int id) { asm volatile("bar.sync %0, 64;" ::"r"(id) : "memory"); }
+// Producer / consumer halves of a pair barrier: the bottom warp arrives (no wait) once interval m's
+// rows are written, the top warp waits for that before reading them at the middle node.
+__device__ __forceinline__ void sq_arrive(int id) { asm volatile("bar.arrive %0, 64;" ::"r"(id) : "memory"); }
 
 // ------------------------------------------------------------------------- squad view
 struct Sq {
@@ -247,6 +251,42 @@ __device__ __forceinline__ void sq_matvec_tm(const float* M, const float u[NV], 
     for (int r = 0; r < 4; ++r) o[r] = a[r][0] + a[r][1];
     tq_st4(dst + 4 * c, o);
   }
+}
+
+// The middle node's x~_m = S_m^-1 u split over the pair: rows [4 c0, 4 (c0 + nch)) of the node
+// matrix times u, stored to the pair's cross elements XM (rows < 26); returns whether any is
+// non-finite.  Same chunk loop as sq_matvec_tm.
+__device__ __forceinline__ bool sq_matvec_mid(const Sq& q, const float* M, const float u[NV], int c0, int nch) {
+  bool bad = false;
+#pragma unroll 1
+  for (int c = c0; c < c0 + nch; ++c) {
+    const float4* R = reinterpret_cast<const float4*>(M + 4 * SQ_MROW * c);
+    float a[4][2];
+#pragma unroll
+    for (int r = 0; r < 4; ++r) a[r][0] = a[r][1] = 0.f;
+#pragma unroll
+    for (int qq = 0; qq < SQ_MROW / 4; ++qq) {
+#pragma unroll
+      for (int r = 0; r < 4; ++r) {
+        const float4 w = R[(SQ_MROW / 4) * r + qq];
+        a[r][0] = fmaf(w.x, u[4 * qq], a[r][0]);
+        a[r][1] = fmaf(w.y, u[4 * qq + 1], a[r][1]);
+        if (4 * qq + 2 < NV) {
+          a[r][0] = fmaf(w.z, u[4 * qq + 2], a[r][0]);
+          a[r][1] = fmaf(w.w, u[4 * qq + 3], a[r][1]);
+        }
+      }
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+      const float o = a[r][0] + a[r][1];
+      if (4 * c + r < NV) {
+        q.cx(SQX_XM + 4 * c + r) = o;
+        bad = bad || !isfinite(o);
+      }
+    }
+  }
+  return bad;
 }
 
 // acc[0..25] += sum_r xs[r] M[row(r)][:], row(r) = r < NQR ? r : 26 + r - NQR, for r < NR; the
@@ -419,7 +459,7 @@ __device__ __forceinline__ int sq_admm_top(const KParams& P, const Sq& q, const 
       float ti[12];
       if (mid) {
         tq_wait_st();
-        sq_bar(q.bar);  // the bottom half's forward sweep is done (g'_{m+1}, interval m rows)
+        sq_bar(q.bar + 2);  // interval m's rows are written (the bottom's first backward step)
 #pragma unroll
         for (int k = 0; k < 12; ++k) ti[k] = q.cx(SQX_TM + k);
       } else {
@@ -428,15 +468,21 @@ __device__ __forceinline__ int sq_admm_top(const KParams& P, const Sq& q, const 
       float u[NV];
       sq_rhs(P, q, i, i, ti, tp, u);
       sq_top_corr(q.C(i - 1), gint, g, rho, u);
-      if (mid && m + 1 < NT) {
+      if (mid) {  // the middle node, split over the pair: both halves finish u_m and each
+                  // multiplies half of S_m^-1's rows
+#pragma unroll
+        for (int j = 0; j < NV; ++j) q.cx(SQX_UA + j) = u[j];
+        sq_bar(q.bar);  // the bottom half's forward sweep is done (g'_{m+1})
         float gb[12];
 #pragma unroll
         for (int k = 0; k < 12; ++k) gb[k] = q.cx(SQX_GB + k);
         sq_bot_corr(q.C(m), gb, gb + 9, rho, u);
+        bad = sq_matvec_mid(q, q.MF(m), u, 0, 4) || bad;  // rows 0..15
+        break;
       }
-      sq_matvec_tm(q.MF(i), u, q.slab(i) + SQ_S, mid ? 7 : 8);
+      sq_matvec_tm(q.MF(i), u, q.slab(i) + SQ_S, 8);
       tq_wait_st();
-      if (!mid) {
+      {
         float s9[9], s3[3];
         tq_ld<9>(q.slab(i) + SQ_S, s9);
         tq_ld<3>(q.slab(i) + SQ_S + 26, s3);
@@ -451,18 +497,11 @@ __device__ __forceinline__ int sq_admm_top(const KParams& P, const Sq& q, const 
         g[2] = s3[2];
 #pragma unroll
         for (int k = 0; k < 12; ++k) tp[k] = ti[k];
-      } else {
-        tq_ld<NV>(q.slab(m) + SQ_S, xn);
-        tq_wait_ld();
-        tq_fence<NV>(xn);
-#pragma unroll
-        for (int j = 0; j < NV; ++j) {
-          bad = bad || !isfinite(xn[j]);
-          q.cx(SQX_XM + j) = xn[j];
-        }
       }
     }
-    sq_bar(q.bar);  // x~_m published
+    sq_bar(q.bar);  // x~_m published (both halves)
+#pragma unroll
+    for (int j = 0; j < NV; ++j) xn[j] = q.cx(SQX_XM + j);
     // ------------------------------------------------ backward i = m-1..0, then node 0's rows
 #pragma unroll 1
     for (int i = m - 1; i >= -1; --i) {
@@ -543,6 +582,7 @@ __device__ __forceinline__ int sq_admm_bot(const KParams& P, const Sq& q, const 
   const int NT = q.NT, m = q.m;
   const float rho = K.rho;
   int first_bad = 0x7fffffff;
+  if (P.n_qp > 0) sq_arrive(q.bar + 2);  // interval m's rows (zero) are ready for the first middle step
 #pragma unroll 1
   for (int it = 0; it < P.n_qp; ++it) {
     const bool first = it == 0;
@@ -590,7 +630,14 @@ __device__ __forceinline__ int sq_admm_bot(const KParams& P, const Sq& q, const 
     q.cx(SQX_GB + 9) = g[0];
     q.cx(SQX_GB + 10) = g[1];
     q.cx(SQX_GB + 11) = g[2];
-    sq_bar(q.bar);
+    sq_bar(q.bar);  // (the top half's u_m is published)
+    {  // the middle node's rows 16..25: u_m = the top's part - rho V_m g'_{m+1} (same operations as the top)
+      float u[NV];
+#pragma unroll
+      for (int j = 0; j < NV; ++j) u[j] = q.cx(SQX_UA + j);
+      sq_bot_corr(q.C(m), gint, g, rho, u);
+      bad = sq_matvec_mid(q, q.MF(m), u, 4, 3) || bad;
+    }
     sq_bar(q.bar);  // the middle node's x~_m is published
     // ---------------------------------------------------------------- backward i = m+1..T-1
     float xp[NV];
@@ -666,6 +713,7 @@ __device__ __forceinline__ int sq_admm_bot(const KParams& P, const Sq& q, const 
       } else {
 #pragma unroll
         for (int k = 0; k < 12; ++k) q.cx(SQX_TM + k) = tr[k];
+        if (it + 1 < P.n_qp) sq_arrive(q.bar + 2);  // for the top half's next middle step
       }
       bad = sq_finish_node(q, i, b, xt, first, K) || bad;
       tq_wait_st();

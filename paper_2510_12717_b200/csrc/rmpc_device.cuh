@@ -76,6 +76,11 @@ struct KParams {
   int32_t n_agents, profile;
   int32_t agents_per_cta, spill_nodes, tmem_cols;
   int32_t sq_cta_base;  // rti_squad_kernel: CTA index of this launch's first CTA (split launches)
+  // Schedule pass for squads: the store is built from the nominal state (the cold-start QP
+  // matrices, scales and factor depend on the schedule alone; the squads recompute every
+  // agent-dependent part), so the pass reads only the gaits and the states / commands may still
+  // be in flight: finiteness of the state and command is checked in the count kernel instead.
+  int32_t synth_rep;
   // launch shape: full_ctas CTAs of agents_per_cta agents, then CTAs of tail_agents (the
   // last, partial wave spread over every SM at fewer agents per CTA)
   int32_t full_ctas, tail_agents;
@@ -367,10 +372,13 @@ struct RmpcCopyOut {
   float* h_z;            // device address of the mapped host z* (NULL: no z*)
   int sms;
 };
+// ev_inputs (cudaEvent_t, optional): recorded when the states and commands have arrived on the
+// device -- the squad pass starts on the gaits alone and waits for it only where it reads them.
 int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant,
-                       const RmpcCopyOut* co = nullptr);
+                       const RmpcCopyOut* co = nullptr, void* ev_inputs = nullptr);
 int rmpc_kernel_setup(int NT);  // cudaFuncSetAttribute for the dynamic shared memory
 // SoA FP32 inputs (rmpc_solve_soa, RMPC_SOA_* rows of `ld` floats) -> the per-agent FP64
 // records the solve kernels read; one thread per agent, coalesced row loads.
+// part: 0 every row, 1 the gait rows only, 2 the state and command rows only.
 int rmpc_launch_soa_unpack(const float* soa, long long ld, int n, rmpc_state* states, rmpc_command* cmds,
-                           rmpc_gait* gaits, void* stream);
+                           rmpc_gait* gaits, void* stream, int part = 0);

@@ -356,7 +356,9 @@ struct SoaIn {
 // The shard's columns [begin, begin + count) of the SoA block: one 2D H2D copy (28 rows; a
 // pageable block is first gathered into the pinned staging buffer), then the unpack kernel into
 // the shard's FP64 records -- on `st`, in place of the three record copies.
-void stage_soa(Shard& sh, const SoaIn& in, cudaStream_t st) {
+// With `split` (squads: the schedule pass reads only the gaits), the gait rows go first on `st`
+// and the state / command rows follow on the second stream, unpacked there; sh.ev[6] marks them.
+void stage_soa(Shard& sh, const SoaIn& in, cudaStream_t st, bool split = false) {
   const size_t n = sh.count, b = sh.begin;
   const float* src = in.soa + b;
   size_t pitch = (size_t)in.ld * sizeof(float);
@@ -366,12 +368,30 @@ void stage_soa(Shard& sh, const SoaIn& in, cudaStream_t st) {
     src = stg;
     pitch = n * sizeof(float);
   }
-  if (pitch == n * sizeof(float))  // one contiguous block
-    CK(cudaMemcpyAsync(sh.d_soa, src, RMPC_SOA_FIELDS * n * sizeof(float), cudaMemcpyHostToDevice, st));
-  else
-    CK(cudaMemcpy2DAsync(sh.d_soa, n * sizeof(float), src, pitch, n * sizeof(float), RMPC_SOA_FIELDS,
-                         cudaMemcpyHostToDevice, st));
-  const int rc = rmpc_launch_soa_unpack(sh.d_soa, (long long)n, (int)n, sh.d_states, sh.d_cmds, sh.d_gaits, st);
+  auto copy_rows = [&](int r0, int nr, cudaStream_t s) {
+    if (pitch == n * sizeof(float))  // contiguous rows
+      CK(cudaMemcpyAsync(sh.d_soa + r0 * n, src + r0 * n, nr * n * sizeof(float), cudaMemcpyHostToDevice, s));
+    else
+      CK(cudaMemcpy2DAsync(sh.d_soa + r0 * n, n * sizeof(float), reinterpret_cast<const char*>(src) + r0 * pitch,
+                           pitch, n * sizeof(float), nr, cudaMemcpyHostToDevice, s));
+  };
+  int rc = 0;
+  if (!split) {
+    copy_rows(0, RMPC_SOA_FIELDS, st);
+    if (sh.err) return;
+    rc = rmpc_launch_soa_unpack(sh.d_soa, (long long)n, (int)n, sh.d_states, sh.d_cmds, sh.d_gaits, st, 0);
+  } else {
+    copy_rows(RMPC_SOA_PHASE, RMPC_SOA_FIELDS - RMPC_SOA_PHASE, st);
+    if (sh.err) return;
+    rc = rmpc_launch_soa_unpack(sh.d_soa, (long long)n, (int)n, sh.d_states, sh.d_cmds, sh.d_gaits, st, 1);
+    CK(cudaEventRecord(sh.ev[7], st));
+    CK(cudaStreamWaitEvent(sh.stream2, sh.ev[7], 0));
+    copy_rows(0, RMPC_SOA_PHASE, sh.stream2);
+    if (sh.err) return;
+    if (rc == 0)
+      rc = rmpc_launch_soa_unpack(sh.d_soa, (long long)n, (int)n, sh.d_states, sh.d_cmds, sh.d_gaits, sh.stream2, 2);
+    CK(cudaEventRecord(sh.ev[6], sh.stream2));
+  }
   if (rc != 0) {
     sh.err = RMPC_ERR_CUDA;
     sh.msg = std::string("soa_unpack_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);
@@ -415,12 +435,29 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   float* d_z = h_z ? mapped(h_z) : nullptr;
   CK(cudaEventRecord(sh.ev[0], st));
   if (h.profile) CK(cudaMemsetAsync(sh.d_prof, 0, 2 * RMPC_NUM_STAGES * sizeof(unsigned long long), st));
+  // squads: the schedule pass and the store build read only the gaits, so the states and
+  // commands (3/4 of the bytes) are copied on the second stream behind them and the solve waits
+  // for them only where it reads them (rmpc_launch_shared's ev_inputs)
+  const int path = solve_path(h, sh.sms);
+  const bool split_in = !soa && path == 2;
+  void* ev_inputs = nullptr;
   if (soa) {
-    stage_soa(sh, *soa, st);
+    stage_soa(sh, *soa, st, path == 2);
     if (sh.err) return;
+    if (path == 2) ev_inputs = sh.ev[6];
   }
-  for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, st));
-  CK(cudaEventRecord(sh.ev[1], st));
+  if (split_in) {
+    CK(cudaMemcpyAsync(ins[2].dst, ins[2].src, ins[2].bytes, cudaMemcpyHostToDevice, st));  // gaits
+    CK(cudaEventRecord(sh.ev[1], st));
+    CK(cudaStreamWaitEvent(sh.stream2, sh.ev[1], 0));  // behind the gaits, not beside them
+    for (int k = 0; k < 2; ++k)
+      CK(cudaMemcpyAsync(ins[k].dst, ins[k].src, ins[k].bytes, cudaMemcpyHostToDevice, sh.stream2));
+    CK(cudaEventRecord(sh.ev[6], sh.stream2));
+    ev_inputs = sh.ev[6];
+  } else {
+    for (const In& c : ins) CK(cudaMemcpyAsync(c.dst, c.src, c.bytes, cudaMemcpyHostToDevice, st));
+    CK(cudaEventRecord(sh.ev[1], st));
+  }
   rmpc_dev::KParams P = make_params(h);
   P.n_agents = (int)n;
   P.states = sh.d_states;
@@ -433,7 +470,7 @@ void run_shard_shared(rmpc_handle& h, Shard& sh, const rmpc_state* states, const
   const bool copyout = d_out != nullptr && d_z != nullptr;  // (records alone: written in the solve)
   P.out = copyout ? sh.d_out : (d_out ? d_out : sh.d_out);
   P.z_out = z_out ? (copyout ? sh.d_z : (d_z ? d_z : sh.d_z)) : nullptr;
-  const int rc = rmpc_launch_shared(P, sh.sched[0], st, solve_path(h, sh.sms), copyout ? &co : nullptr);
+  const int rc = rmpc_launch_shared(P, sh.sched[0], st, path, copyout ? &co : nullptr, ev_inputs);
   if (rc != 0) {
     sh.err = rc == (int)cudaErrorNoKernelImageForDevice ? RMPC_ERR_NO_KERNEL : RMPC_ERR_CUDA;
     sh.msg = std::string("rti_shared_kernel launch: ") + cudaGetErrorString((cudaError_t)rc);

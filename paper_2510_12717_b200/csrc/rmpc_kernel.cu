@@ -268,8 +268,19 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
     if (lane < NV) sm.V(i, V_E)[lane] = 1.f;
   sm.bc[tid] = 0.f;
 
-  const rmpc_state st = P.states[agent];
-  const rmpc_command cmd = P.cmds[agent];
+  rmpc_state st;
+  rmpc_command cmd;
+  if (P.mode == 1 && P.synth_rep) {  // the schedule alone matters: the nominal pose at rest
+#pragma unroll
+    for (int k = 0; k < RMPC_NQ; ++k) {
+      st.q[k] = P.nominal[k];
+      st.qd[k] = 0.0;
+    }
+    cmd.height = cmd.vx = cmd.wpitch = 0.0;
+  } else {
+    st = P.states[agent];
+    cmd = P.cmds[agent];
+  }
   const rmpc_gait gait = P.gaits[agent];
   const bool warm = P.warm_start && P.prev != nullptr && P.prev_z != nullptr &&
                     P.prev[agent].status == RMPC_STATUS_OK;
@@ -692,16 +703,19 @@ __device__ __forceinline__ unsigned long long mix64(unsigned long long x) {  // 
 // runs) as the hash key; the first agent to claim a key's slot becomes its representative and
 // draws the schedule id.  Agents with a non-finite input are left unshared (their own setup
 // reports the failure, as the reference's build_qp does).
+__device__ __forceinline__ bool state_cmd_finite(const rmpc_state& st, const rmpc_command& cmd) {
+  bool fin = isfinite(cmd.height) && isfinite(cmd.vx) && isfinite(cmd.wpitch);
+#pragma unroll
+  for (int k = 0; k < 9; ++k) fin = fin && isfinite(st.q[k]) && isfinite(st.qd[k]);
+  return fin;
+}
+
 __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= P.n_agents) return;
-  const rmpc_state st = P.states[a];
-  const rmpc_command cmd = P.cmds[a];
   const rmpc_gait g = P.gaits[a];
-  bool fin = isfinite(cmd.height) && isfinite(cmd.vx) && isfinite(cmd.wpitch) && isfinite(g.phase) &&
-             isfinite(g.period) && isfinite(g.phase_switch);
-#pragma unroll
-  for (int k = 0; k < 9; ++k) fin = fin && isfinite(st.q[k]) && isfinite(st.qd[k]);
+  bool fin = isfinite(g.phase) && isfinite(g.period) && isfinite(g.phase_switch);
+  if (!P.synth_rep) fin = fin && state_cmd_finite(P.states[a], P.cmds[a]);  // (else: the count kernel)
 #pragma unroll
   for (int c = 0; c < 4; ++c) fin = fin && isfinite(g.offsets[c]);
   if (!fin) {
@@ -750,7 +764,8 @@ __global__ void sched_count_kernel(const KParams P, RmpcSchedBuffers b) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= P.n_agents) return;
   const int sl = b.slot_of[a];
-  const int id = sl >= 0 ? b.slot_id[sl] : -1;
+  int id = sl >= 0 ? b.slot_id[sl] : -1;
+  if (id >= 0 && P.synth_rep && !state_cmd_finite(P.states[a], P.cmds[a])) id = -1;  // its own solve fails it
   if (id >= 0) {  // warp-aggregated: one atomic per schedule id of the warp
     const unsigned peers = __match_any_sync(__activemask(), id);
     const int leader = __ffs(peers) - 1, lane = threadIdx.x & 31;
@@ -808,15 +823,23 @@ __global__ void sched_scatter_kernel(const KParams P, RmpcSchedBuffers b) {
 
 }  // namespace rmpc_dev
 
-int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& b, void* stream, int variant,
-                       const RmpcCopyOut* co) {
+int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffers& b, void* stream, int variant,
+                       const RmpcCopyOut* co, void* ev_inputs) {
   using namespace rmpc_dev;
-  if (params.n_agents <= 0) return 0;
-  if (params.n_agents > b.agents) return (int)cudaErrorInvalidValue;
+  if (params_in.n_agents <= 0) return 0;
+  if (params_in.n_agents > b.agents) return (int)cudaErrorInvalidValue;
   const cudaStream_t st = (cudaStream_t)stream;
-  const int n = params.n_agents, NT = params.NT;
+  const int n = params_in.n_agents, NT = params_in.NT;
   const int blocks = (n + 255) / 256;
   const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
+  static const int synth_env = [] {  // RMPC_SYNTH_REP=0: build the store from the representative's own state
+    const char* e = getenv("RMPC_SYNTH_REP");
+    return e ? atoi(e) : 1;
+  }();
+  KParams params = params_in;
+  params.synth_rep = squads && synth_env != 0;
+  if (!params.synth_rep && ev_inputs)  // the whole pass reads the states: wait for them here
+    cudaStreamWaitEvent(st, (cudaEvent_t)ev_inputs, 0);
   static const int solo = [] {  // debugging: one squad per CTA (RMPC_SQUAD_SOLO=1: slot 0, 2: slot 1)
     const char* e = getenv("RMPC_SQUAD_SOLO");
     return e ? atoi(e) : 0;
@@ -824,10 +847,10 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
   // host outputs: a split pays only where a second wave of squad CTAs follows the first; else
   // the solve writes the mapped host buffers itself
   if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > 2 * co->sms)) {
-    KParams Q = params;
+    KParams Q = params_in;
     Q.out = co->h_out;
     Q.z_out = co->h_z;
-    return rmpc_launch_shared(Q, b, stream, variant, nullptr);
+    return rmpc_launch_shared(Q, b, stream, variant, nullptr, params.synth_rep ? ev_inputs : nullptr);
   }
   int rc = (int)cudaMemsetAsync(b.table, 0xFF, (size_t)b.slots * sizeof(unsigned long long), st);
   if (rc == 0) rc = (int)cudaMemsetAsync(b.n_sched, 0, sizeof(int32_t), st);
@@ -842,6 +865,8 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params, const RmpcSchedBuffers& 
     cudaEventRecord((cudaEvent_t)b.ev_fork, st);
     cudaStreamWaitEvent(side, (cudaEvent_t)b.ev_fork, 0);
   }
+  if (params.synth_rep && ev_inputs)  // the count kernel is the first to read the states
+    cudaStreamWaitEvent(side, (cudaEvent_t)ev_inputs, 0);
   sched_count_kernel<<<blocks, 256, 0, side>>>(params, b);
   g_launches.fetch_add(2, std::memory_order_relaxed);
   // the store: setup + Ruiz + factorization of each schedule's representative (mode 1), one
@@ -954,37 +979,43 @@ namespace rmpc_dev {
 // read is one coalesced 128-byte transaction) and writes agent a's FP64 records.  float -> double
 // is exact, so the solve sees exactly the values the caller's FP32 block holds.
 __global__ void __launch_bounds__(256) soa_unpack_kernel(const float* __restrict__ soa, long long ld, int n,
-                                                         rmpc_state* states, rmpc_command* cmds, rmpc_gait* gaits) {
+                                                         rmpc_state* states, rmpc_command* cmds, rmpc_gait* gaits,
+                                                         int part) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a >= n) return;
   const float* c = soa + a;
-  rmpc_state st;
+  if (part != 1) {  // the state and command rows
+    rmpc_state st;
 #pragma unroll
-  for (int k = 0; k < RMPC_NQ; ++k) {
-    st.q[k] = (double)__ldg(c + (RMPC_SOA_Q + k) * ld);
-    st.qd[k] = (double)__ldg(c + (RMPC_SOA_QD + k) * ld);
+    for (int k = 0; k < RMPC_NQ; ++k) {
+      st.q[k] = (double)__ldg(c + (RMPC_SOA_Q + k) * ld);
+      st.qd[k] = (double)__ldg(c + (RMPC_SOA_QD + k) * ld);
+    }
+    rmpc_command cm;
+    cm.height = (double)__ldg(c + RMPC_SOA_HEIGHT * ld);
+    cm.vx = (double)__ldg(c + RMPC_SOA_VX * ld);
+    cm.wpitch = (double)__ldg(c + RMPC_SOA_WPITCH * ld);
+    states[a] = st;
+    cmds[a] = cm;
   }
-  rmpc_command cm;
-  cm.height = (double)__ldg(c + RMPC_SOA_HEIGHT * ld);
-  cm.vx = (double)__ldg(c + RMPC_SOA_VX * ld);
-  cm.wpitch = (double)__ldg(c + RMPC_SOA_WPITCH * ld);
-  rmpc_gait g;
-  g.phase = (double)__ldg(c + RMPC_SOA_PHASE * ld);
-  g.period = (double)__ldg(c + RMPC_SOA_PERIOD * ld);
-  g.phase_switch = (double)__ldg(c + RMPC_SOA_PHASE_SWITCH * ld);
+  if (part != 2) {  // the gait rows
+    rmpc_gait g;
+    g.phase = (double)__ldg(c + RMPC_SOA_PHASE * ld);
+    g.period = (double)__ldg(c + RMPC_SOA_PERIOD * ld);
+    g.phase_switch = (double)__ldg(c + RMPC_SOA_PHASE_SWITCH * ld);
 #pragma unroll
-  for (int k = 0; k < RMPC_NC; ++k) g.offsets[k] = (double)__ldg(c + (RMPC_SOA_OFFSETS + k) * ld);
-  states[a] = st;
-  cmds[a] = cm;
-  gaits[a] = g;
+    for (int k = 0; k < RMPC_NC; ++k) g.offsets[k] = (double)__ldg(c + (RMPC_SOA_OFFSETS + k) * ld);
+    gaits[a] = g;
+  }
 }
 
 }  // namespace rmpc_dev
 
 int rmpc_launch_soa_unpack(const float* soa, long long ld, int n, rmpc_state* states, rmpc_command* cmds,
-                           rmpc_gait* gaits, void* stream) {
+                           rmpc_gait* gaits, void* stream, int part) {
   if (n <= 0) return 0;
-  rmpc_dev::soa_unpack_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(soa, ld, n, states, cmds, gaits);
+  rmpc_dev::soa_unpack_kernel<<<(n + 255) / 256, 256, 0, (cudaStream_t)stream>>>(soa, ld, n, states, cmds, gaits,
+                                                                                  part);
   g_launches.fetch_add(1, std::memory_order_relaxed);
   return (int)cudaGetLastError();
 }

@@ -85,3 +85,18 @@ def test_many_shards_on_one_device():
     for _ in range(2):
         eight = br.solve(st, cm, ga, want_z=True)
         assert eight[0].tobytes() == one[0].tobytes() and eight[1].tobytes() == one[1].tobytes()
+
+
+def test_store_build_independent_of_representative_state():
+    """The squad pass builds each schedule's store from the nominal state (the cold-start QP
+    matrices, Ruiz scales and factor depend on the schedule alone; rmpc_kernel.cu synth_rep), so
+    the host path can start it before the states and commands have arrived.  The results equal,
+    byte for byte, a store built from each schedule's first agent (RMPC_SYNTH_REP=0)."""
+    env = dict(os.environ)
+    script = SCRIPT % (ROOT, 10, 5000)
+    a = subprocess.run([sys.executable, "-c", script], env={**env, "RMPC_SYNTH_REP": "1"}, capture_output=True,
+                       timeout=600)
+    b = subprocess.run([sys.executable, "-c", script], env={**env, "RMPC_SYNTH_REP": "0"}, capture_output=True,
+                       timeout=600)
+    assert a.returncode == 0 and b.returncode == 0, (a.stderr.decode()[-1500:], b.stderr.decode()[-1500:])
+    assert len(a.stdout) > 0 and a.stdout == b.stdout

@@ -226,7 +226,8 @@ int32_t rmpc_solve_device_active_set(rmpc_handle* handle, const rmpc_state* d_st
  * first hashes every agent's schedule, factorizes each distinct schedule once, and lets every
  * agent of that schedule load the result.  Levels: 0 off (per-agent factorization, also every
  * warm-started solve); 1 one warp pair per agent on the shared factor (bit-identical to 0);
- * 3 squads -- 32 agents of a schedule per warp pair, lane = agent (horizon <= 10, else level 1);
+ * 3 squads -- 32 agents of a schedule per warp pair, lane = agent (horizon <= 10; horizons 11..20:
+ * long squads of four warps, the half-horizon chains handed between two warps each; beyond: 1);
  * 2 (default) squads where the shard is larger than two waves of the per-agent kernel, else 0
  * (a squad's latency exceeds a small batch's per-agent solve).  Calls on one handle share the
  * schedule workspace: issue device solves of one handle on one stream. */

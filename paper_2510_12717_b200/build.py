@@ -14,11 +14,9 @@ LIB_DIR = os.path.join(HERE, "lib")
 LIB_PATH = os.path.join(LIB_DIR, "librmpc_b200.so")
 SOURCES = [os.path.join(HERE, "csrc", f) for f in ("rmpc_kernel.cu", "rmpc_host.cu", "rmpc_env.cu", "rmpc_policy.cu",
                                                        "rmpc_ppo.cu")]
-HEADERS = [os.path.join(HERE, "csrc", h) for h in ("rmpc_device.cuh", "rmpc_kin.cuh", "rmpc_sm.cuh",
-                                                   "rmpc_views.cuh", "rmpc_model.cuh", "rmpc_setup.cuh",
-                                                   "rmpc_ruiz.cuh", "rmpc_factor.cuh", "rmpc_admm.cuh", "rmpc_squad.cuh",
-                                                   "rmpc_policy.cuh")] + \
-    [os.path.join(ROOT, "include", h) for h in ("rmpc_b200.h", "rmpc_b200_env.h")]
+# every header of csrc/ and include/ (a new header must rebuild the library too)
+HEADERS = sorted(os.path.join(HERE, "csrc", h) for h in os.listdir(os.path.join(HERE, "csrc")) if h.endswith(".cuh")) + \
+    sorted(os.path.join(ROOT, "include", h) for h in os.listdir(os.path.join(ROOT, "include")) if h.endswith((".h", ".hpp")))
 NVCC_FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
               "-Xcompiler", "-fPIC", "-Xptxas", "-v"]
 

@@ -323,6 +323,50 @@ __host__ __device__ inline SqLayout sq_layout(int NT) {
 inline int sq_smem_bytes(int NT) { return 2 * sq_layout(NT).total * 4; }
 inline bool sq_supported(int NT) { return NT >= 2 && NT <= SQ_MAXT && sq_smem_bytes(NT) <= 227 * 1024 - 256; }
 
+// ------------------------------------------------------------------------- long squads
+// Horizons 11..20: one squad of 32 agents per CTA on four warps (rmpc_squad4.cuh).
+// Cross-thread elements of a long squad ([element][lane]); the squad ones (rmpc_squad.cuh) first.
+constexpr int S4X_BAD = 56;   // first non-finite iteration of each warp (4)
+constexpr int S4X_SAME = 60;  // schedule check of each warp (4)
+constexpr int S4X_HTF = 64;   // top forward hand-over: g_int (9), g (3), interval nA-1 rows t (12)
+constexpr int S4X_HBF = 88;   // bottom forward hand-over: g'_int (9), g' (3)
+constexpr int S4X_HTB = 100;  // top backward hand-over: x~_nA (26)
+constexpr int S4X_HBB = 126;  // bottom backward hand-over: x~_{i0-1} (26)
+constexpr int S4X_BT = 152;   // t of interval i0-1's rows (12)
+constexpr int S4X_UA = 164;   // the middle node's u from top-B (26)
+constexpr int S4X_N = 190;
+// named barriers of a long squad (one squad per CTA; 0 is __syncthreads)
+constexpr int S4B_MID = 1, S4B_TM = 2, S4B_TF = 3, S4B_TB = 4, S4B_BF = 5, S4B_BB = 6, S4B_ALL = 7;
+
+struct Sq4Layout {
+  int img;  // the schedule image (sq_layout's region [0, priv))
+  int priv, priv_warp, cross, total;
+};
+__host__ __device__ inline Sq4Layout sq4_layout(int NT) {
+  const SqLayout L = sq_layout(NT);
+  Sq4Layout S;
+  S.img = 0;
+  S.priv_warp = 32 * (5 * SQ_PRIV + NINIT + SQ_NXI);
+  S.priv = L.priv;
+  S.cross = S.priv + 4 * S.priv_warp;
+  S.total = S.cross + 32 * S4X_N;
+  return S;
+}
+// node ranges: top-A [0, nA), top-B [nA, m], bottom-B [m+1, i0), bottom-A [i0, T)
+__host__ __device__ inline int sq4_na(int NT) { return (mid_node(NT) + 1) / 2; }
+__host__ __device__ inline int sq4_i0(int NT) { return NT - (NT - 1 - mid_node(NT)) / 2; }
+inline int sq4_smem_bytes(int NT) { return sq4_layout(NT).total * 4; }
+inline bool sq4_supported(int NT) {
+  if (NT <= SQ_MAXT || NT > 20) return false;
+  const int m = mid_node(NT), nA = sq4_na(NT), i0 = sq4_i0(NT);
+  const int w1 = nA > m + 1 - nA ? nA : m + 1 - nA, w2 = i0 - m - 1 > NT - i0 ? i0 - m - 1 : NT - i0;
+  const int w = w1 > w2 ? w1 : w2;
+  return w <= 5 && NT * SQ_MF >= 4 * 32 * 27 + 2 * 2 * NV * 32 + 4 * 5 * 32 + 32 &&
+         sq4_smem_bytes(NT) <= 227 * 1024 - 256;
+}
+
+
+
 }  // namespace rmpc_dev
 
 // Launch the fused kernel for params.n_agents agents on `stream` (implemented in

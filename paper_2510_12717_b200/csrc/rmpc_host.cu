@@ -287,7 +287,7 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
     CK(cudaMalloc(&sb.n_unshared, sizeof(int32_t)));
     CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
     sb.sqpack = nullptr;
-    if (rmpc_dev::sq_supported(h.NT))
+    if (rmpc_dev::sq_supported(h.NT) || rmpc_dev::sq4_supported(h.NT))
       CK(cudaMalloc(&sb.sqpack, (size_t)sb.cap * rmpc_dev::sq_layout(h.NT).priv * sizeof(float)));
     cudaStream_t side = nullptr;
     cudaEvent_t e0 = nullptr, e1 = nullptr;

@@ -43,6 +43,7 @@
 #include "rmpc_factor.cuh"
 #include "rmpc_admm.cuh"
 #include "rmpc_squad.cuh"
+#include "rmpc_squad4.cuh"
 
 namespace rmpc_dev {
 
@@ -630,6 +631,7 @@ int rmpc_kernel_setup(int) {
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::SHARED_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_shared_kernel<rmpc_dev::MAX_AGENTS>, a, bytes);
   if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_squad_kernel, a, bytes);
+  if (rc == 0) rc = (int)cudaFuncSetAttribute(rmpc_dev::rti_squad4_kernel, a, bytes);
   return rc;
 }
 
@@ -831,7 +833,11 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   const cudaStream_t st = (cudaStream_t)stream;
   const int n = params_in.n_agents, NT = params_in.NT;
   const int blocks = (n + 255) / 256;
-  const bool squads = variant == 2 && sq_supported(NT) && b.sqpack != nullptr;
+  // squads: two per CTA for T <= 10 (rmpc_squad.cuh), one long squad of four warps per CTA for
+  // T = 11..20 (rmpc_squad4.cuh)
+  const bool long_sq = variant == 2 && sq4_supported(NT) && b.sqpack != nullptr;
+  const bool squads = (variant == 2 && sq_supported(NT) && b.sqpack != nullptr) || long_sq;
+  const int spc = long_sq ? 1 : 2;  // squads per CTA
   static const int synth_env = [] {  // RMPC_SYNTH_REP=0: build the store from the representative's own state
     const char* e = getenv("RMPC_SYNTH_REP");
     return e ? atoi(e) : 1;
@@ -846,7 +852,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   }();
   // host outputs: a split pays only where a second wave of squad CTAs follows the first; else
   // the solve writes the mapped host buffers itself
-  if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > 2 * co->sms)) {
+  if (co && !(squads && !solo && (n + 31) / 32 + std::min(b.cap, n) > spc * co->sms)) {
     KParams Q = params_in;
     Q.out = co->h_out;
     Q.z_out = co->h_z;
@@ -931,21 +937,26 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   if (squads) {
     const int nsq = (n + 31) / 32 + std::min(b.cap, n);
     S.pad2_ = solo;
-    const int grid = solo ? nsq : (nsq + 1) / 2;
+    const int grid = (solo || long_sq) ? nsq : (nsq + 1) / 2;
+    const int smem = long_sq ? sq4_smem_bytes(NT) : sq_smem_bytes(NT);
+    auto launch_sq = [&](int g) {
+      if (long_sq) rti_squad4_kernel<<<g, 128, smem, st>>>(S);
+      else rti_squad_kernel<<<g, 128, smem, st>>>(S);
+    };
     if (co) {  // (grid > co->sms here)  // split: first wave, its copy-out beside the second launch
       S.sq_cta_base = 0;
-      rti_squad_kernel<<<co->sms, 128, sq_smem_bytes(NT), st>>>(S);
+      launch_sq(co->sms);
       cudaEventRecord((cudaEvent_t)co->ev_a, st);
       cudaStreamWaitEvent((cudaStream_t)co->stream2, (cudaEvent_t)co->ev_a, 0);
-      sq_copyout_kernel<<<64, 256, 0, (cudaStream_t)co->stream2>>>(S, 0, co->sms, 0, co->h_out, co->h_z);
+      sq_copyout_kernel<<<64, 256, 0, (cudaStream_t)co->stream2>>>(S, 0, co->sms, 0, co->h_out, co->h_z, spc);
       cudaEventRecord((cudaEvent_t)co->ev_b, (cudaStream_t)co->stream2);
       S.sq_cta_base = co->sms;  // the second launch writes the mapped host buffers itself: its
       S.out = co->h_out;        // CTAs are the last ones, nothing waits for their SMs
       S.z_out = co->h_z;
-      rti_squad_kernel<<<grid - co->sms, 128, sq_smem_bytes(NT), st>>>(S);
+      launch_sq(grid - co->sms);
       g_launches.fetch_add(2, std::memory_order_relaxed);
     } else {
-      rti_squad_kernel<<<grid, 128, sq_smem_bytes(NT), st>>>(S);
+      launch_sq(grid);
     }
   } else if (cs.agents > MAX_AGENTS)
     rti_shared_kernel<SHARED_AGENTS><<<grid_s, 64 * cs.agents, cs.smem_bytes, st>>>(S);

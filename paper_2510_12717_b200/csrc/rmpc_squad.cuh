@@ -1232,8 +1232,8 @@ __device__ __forceinline__ int sq_pos(const KParams& P, int sq) {
 // per agent, consecutive lanes on consecutive 8-byte words.  Runs beside the squad launch of the
 // next CTA range, so the PCIe transfer of one wave overlaps the solve of the next.
 __global__ void __launch_bounds__(256) sq_copyout_kernel(const KParams P, int cta_lo, int cta_hi, int list,
-                                                         rmpc_solution* h_out, float* h_z) {
-  const int p0 = sq_pos(P, 2 * cta_lo), p1 = cta_hi >= (1 << 29) ? sq_pos(P, 1 << 30) : sq_pos(P, 2 * cta_hi);
+                                                         rmpc_solution* h_out, float* h_z, int spc) {
+  const int p0 = sq_pos(P, spc * cta_lo), p1 = cta_hi >= (1 << 29) ? sq_pos(P, 1 << 30) : sq_pos(P, spc * cta_hi);
   const int nl = list ? *P.n_list : 0;
   const int lane = threadIdx.x & 31;
   const int wg = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, nw = (gridDim.x * blockDim.x) >> 5;

@@ -100,3 +100,31 @@ def test_store_build_independent_of_representative_state():
                        timeout=600)
     assert a.returncode == 0 and b.returncode == 0, (a.stderr.decode()[-1500:], b.stderr.decode()[-1500:])
     assert len(a.stdout) > 0 and a.stdout == b.stdout
+
+
+@pytest.mark.parametrize("T", [11, 16, 20])
+def test_long_squads_repeatable_and_path_independent(T):
+    """Long squads (T = 11..20: four warps per squad, the recurrences handed between warps
+    through producer / consumer barriers): repeated solves and the host / device paths give the
+    same bytes, and the result is within the parity gates of the per-agent factorization."""
+    import torch
+    from paper_2510_12717_b200.abi import SOLUTION_DTYPE
+    from parity import check, compare
+    n = 3000
+    m, s = R.default_model(), R.default_settings(T)
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=T, model=m, settings=s)
+    br = R.BatchRunner(n, m, s)
+    a = br.solve(st, cm, ga, want_z=True)
+    b = br.solve(st, cm, ga, want_z=True)
+    assert a[0].tobytes() == b[0].tobytes() and a[1].tobytes() == b[1].tobytes()
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    z = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
+    br.solve_device(*d, out, z_out=z)
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == a[0].tobytes() and z.cpu().numpy().tobytes() == a[1].tobytes()
+    br.set_schedule_sharing(0)
+    p = br.solve(st, cm, ga, want_z=True)
+    c = compare(a[0], p[0], a[1], p[1])
+    check(c, f"long squads vs per-agent T={T}")

@@ -60,7 +60,8 @@ def main():
         ok = int((out.cpu().numpy().view(SOLUTION_DTYPE)["status"] == 0).sum())
         rows.append({"horizon": T, "agents": n,
                      "path": "squads (32 agents per warp pair, 2 per SM)" if T <= 10 else
-                             "shared-schedule CTAs (warp pair per agent)",
+                             ("long squads (32 agents on four warps, 1 per SM)" if T <= 20 else
+                              "shared-schedule CTAs (warp pair per agent)"),
                      "ms_per_tick_p50": t, "solves_per_s": n / (t * 1e-3), "status_ok": ok,
                      "flop_alg_per_solve": fl, "achieved_tflops": ach,
                      "roofline_frac": (ach / peak) if ach else None})

@@ -335,8 +335,8 @@ def test_schedule_sharing(T, kind, n):
     """Cold start: the matrices, Ruiz scales and factor depend only on the stance schedule
     (mpc.cpp:266-276), so each distinct schedule is factorized once (rmpc_set_schedule_sharing).
     Level 1 (warp-pair CTAs of one schedule) gives exactly the per-agent bytes; level 3 (squads
-    forced: lane-per-agent squads for T <= 10, level 1 beyond) runs the same iterates with the
-    agent in the lane -- equal to the per-agent solve within the parity gates, identical statuses
+    forced: two-warp squads for T <= 10, four-warp long squads for T = 11..20, level 1 beyond)
+    runs the same iterates with the agent in the lane -- equal to the per-agent solve within the parity gates, identical statuses
     (a failing agent next to working ones included), and identical bytes on the host (chunked)
     and device paths."""
     import torch
@@ -382,7 +382,7 @@ def test_auto_path_selection(n):
 def test_schedule_store_over_capacity():
     """More distinct schedules than the store holds (1 024 per shard): per-agent gait periods and
     switch phases make almost every agent's schedule unique, so the ids past the capacity run the
-    per-agent list (rti_kernel over an agent list, a looping wave) next to the squads of the
+    per-agent list (rti_kernel over the agent list, an upper-bound grid) next to the squads of the
     stored ones -- every agent solved, within the parity gates of the per-agent factorization."""
     n, T = 3000, 10
     m, s = default_model(), default_settings(T)

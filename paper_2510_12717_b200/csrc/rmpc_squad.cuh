@@ -785,6 +785,45 @@ __device__ __forceinline__ bool sq_setup(const KParams& P, const Sq& q, bool top
   return same;
 }
 
+// z* out: this warp's nodes [i0, i0 + own) of an agent are one contiguous run of own x 26 floats.
+// The finish leaves each node's z* row in the node's dead x columns of the thread's TMEM lane; six
+// agents at a time go through the warp's transpose buffer `xp` (6 x 130 <= 32 x 27 floats) and out
+// as float2 words on consecutive lanes -- whole 128-byte lines instead of one 104-byte row per
+// store (mapped host memory over PCIe: 47 vs 38 GB/s, tools/micro/mapped_write.cu).
+__device__ __forceinline__ void sq_zstar_out(const KParams& P, const Sq& q, float* xp, int i0, int own, int agent,
+                                             bool write) {
+  constexpr int RUN = 5 * NV;  // xp floats per agent (own <= 5)
+  const int lane = q.lane, nw = own * NV / 2;
+  tq_wait_st();
+  const unsigned wm = __ballot_sync(FULL, write);
+#pragma unroll 1
+  for (int l0 = 0; l0 < 32; l0 += 6) {
+    if (((wm >> l0) & 0x3Fu) == 0u) continue;
+#pragma unroll 1
+    for (int b = 0; b < own; ++b) {
+      float v[NV];
+      tq_ld<NV>(q.slab(b) + SQ_X, v);
+      tq_wait_ld();
+      tq_fence<NV>(v);
+      if (lane >= l0 && lane < l0 + 6) {
+#pragma unroll
+        for (int j = 0; j < NV; ++j) xp[(lane - l0) * RUN + b * NV + j] = v[j];
+      }
+    }
+    __syncwarp();
+#pragma unroll 1
+    for (int k = 0; k < 6 && l0 + k < 32; ++k) {
+      const int al = __shfl_sync(FULL, agent, l0 + k);
+      if ((wm >> (l0 + k)) & 1u) {
+        float2* dst = reinterpret_cast<float2*>(P.z_out + ((size_t)al * q.NT + i0) * NV);
+        const float2* src = reinterpret_cast<const float2*>(xp + k * RUN);
+        for (int w = lane; w < nw; w += 32) dst[w] = src[w];
+      }
+    }
+    __syncwarp();
+  }
+}
+
 // Residuals and objective on the unscaled problem (qp.cpp:192-200), z* = guess + dz and the
 // inverse dynamics at node 0 (mpc.cpp:305-330), the active set (optional) and the record
 // (finish_agent), lane-parallel.  fin: the squad's finish scratch (the matrices are dead).
@@ -917,7 +956,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
       }
     }
     // dual residual |P^ x + q^ + A^T y| / e, objective, z*
-    float aty[NV];
+    float aty[NV], zr[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) aty[j] = 0.f;
     sq_colview(cf, cp, yi, yp, yo, yin, node0, aty);
@@ -936,19 +975,10 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
       obj += 0.5 * w * dz * dz + w * (g - des) * dz;
       dinf = fmaxf(dinf, fabsf(e * x[j]));
       const double zv = g + dz;  // z* = guess + dz (mpc.cpp:308-314)
-      xp[lane * 27 + j] = ok ? (float)zv : 0.f;  // (a failed agent's z* is zero)
+      zr[j] = ok ? (float)zv : 0.f;  // (a failed agent's z* is zero)
       if (i < 2) fz[(i * NV + j) * 32 + lane] = zv;
     }
-    if (P.z_out) {  // node i of the warp's agents: one contiguous 26-float row per agent
-      __syncwarp();
-      const unsigned wm = __ballot_sync(FULL, write);
-#pragma unroll 1
-      for (int l = 0; l < 32; ++l) {
-        const int al = __shfl_sync(FULL, agent, l);
-        if (((wm >> l) & 1u) && lane < NV) P.z_out[((size_t)al * NT + i) * NV + lane] = xp[l * 27 + lane];
-      }
-      __syncwarp();
-    }
+    if (P.z_out) tq_st<NV>(q.slab(b) + SQ_X, zr);  // (node i's x columns are dead: sq_zstar_out)
     if (P.act_out && write) {  // final active set (scaled space)
       uint8_t* ao = P.act_out + (size_t)agent * (NT + 1) * NSLOT + (size_t)(i + 1) * NSLOT;
       auto code = [](float lo, float hi, float z) -> uint8_t {
@@ -968,6 +998,7 @@ __device__ __forceinline__ void sq_finish(const KParams& P, const Sq& q, bool to
 #pragma unroll
     for (int k = 0; k < 12; ++k) tp[k] = ti[k];
   }
+  if (P.z_out) sq_zstar_out(P, q, xp, top ? 0 : m + 1, own, agent, write);
   if (!top) {
     fc[lane] = prim;
     fc[32 + lane] = dual;

@@ -578,7 +578,7 @@ __device__ __forceinline__ void sq4_finish(const KParams& P, const Sq& q, int ro
       }
     }
     // dual residual |P^ x + q^ + A^T y| / e, objective, z*
-    float aty[NV];
+    float aty[NV], zr[NV];
 #pragma unroll
     for (int j = 0; j < NV; ++j) aty[j] = 0.f;
     sq_colview(cf, cp, yi, yp, yo, yin, node0, aty);
@@ -597,19 +597,10 @@ __device__ __forceinline__ void sq4_finish(const KParams& P, const Sq& q, int ro
       obj += 0.5 * w * dz * dz + w * (g - des) * dz;
       dinf = fmaxf(dinf, fabsf(e * x[j]));
       const double zv = g + dz;  // z* = guess + dz (mpc.cpp:308-314)
-      xp[lane * 27 + j] = ok ? (float)zv : 0.f;  // (a failed agent's z* is zero)
+      zr[j] = ok ? (float)zv : 0.f;  // (a failed agent's z* is zero)
       if (i < 2) fz[(i * NV + j) * 32 + lane] = zv;
     }
-    if (P.z_out) {  // node i of the warp's agents: one contiguous 26-float row per agent
-      __syncwarp();
-      const unsigned wm = __ballot_sync(FULL, write);
-#pragma unroll 1
-      for (int l = 0; l < 32; ++l) {
-        const int al = __shfl_sync(FULL, agent, l);
-        if (((wm >> l) & 1u) && lane < NV) P.z_out[((size_t)al * NT + i) * NV + lane] = xp[l * 27 + lane];
-      }
-      __syncwarp();
-    }
+    if (P.z_out) tq_st<NV>(q.slab(b) + SQ_X, zr);  // (node i's x columns are dead: sq_zstar_out)
     if (P.act_out && write) {  // final active set (scaled space)
       uint8_t* ao = P.act_out + (size_t)agent * (NT + 1) * NSLOT + (size_t)(i + 1) * NSLOT;
       auto code = [](float lo, float hi, float z) -> uint8_t {
@@ -629,6 +620,7 @@ __device__ __forceinline__ void sq4_finish(const KParams& P, const Sq& q, int ro
 #pragma unroll
     for (int k = 0; k < 12; ++k) tp[k] = ti[k];
   }
+  if (P.z_out) sq_zstar_out(P, q, xp, lo, own, agent, write);
   {
     float* fw = fc + (threadIdx.x >> 5) * 5 * 32;
     fw[lane] = prim;

@@ -306,7 +306,7 @@ __device__ __forceinline__ void solve_agent(const KParams& P, float* base, uint3
   ok = pair_and(sm, ok);
   prof_mark(P, tid, 2, t0);
   const int nw_cta = (int)(blockDim.x >> 5);
-  const bool helped = P.mode == 1 && nw_cta > 2 && go != nullptr;
+  const bool helped = nw_cta > 2 && go != nullptr;
   if (helped) {  // hand the setup to the helper warps for the Ruiz passes
     if (tid == 0) *go = ok && P.ruiz_iters > 0;
     asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"((int)blockDim.x) : "memory");
@@ -381,7 +381,10 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
-  if (P.mode == 1 && pair > 0) {
+  // one agent per CTA (the schedule store; a per-agent batch of at most one agent per SM): the
+  // other pairs run the agent's Ruiz passes with it
+  const bool helpers = P.mode == 1 || (P.agent_list == nullptr && P.full_ctas == 0 && P.tail_agents == 1);
+  if (helpers && pair > 0) {
     store_ruiz_helper(P, smem, lane, w, &s_go);
   } else if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
@@ -389,7 +392,7 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
     float* base = smem + pair * make_layout(P.NT, P.spill_nodes).total;
     // (one straight-line call: a loop around the inlined solve -- e.g. a looping wave over the
     // agent list -- doubles the ADMM loop's spills, measured 2x slower)
-    solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1, P.mode == 1 ? &s_go : nullptr);
+    solve_agent<SPILL>(P, base, tm, tmn, 1 + pair, agent, sched, lane, w & 1, helpers ? &s_go : nullptr);
   }
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -221,10 +221,11 @@ __device__ __forceinline__ Sm make_sm(const KParams& P, float* base, uint32_t tm
   return sm;
 }
 
-// Schedule store build (mode 1): warps 2.. of the CTA help the representative's warp pair with
-// the Ruiz passes -- the only stage of the build whose work splits by node without changing a
-// single operation (ruiz(): nodes are independent within a pass).  `go` is set by the pair.
-__device__ __forceinline__ void store_ruiz_helper(const KParams& P, float* base, int lane, int w, const int* go) {
+// One agent per CTA (the schedule store's representative, or a per-agent batch of at most one
+// agent per SM): warps 2.. of the CTA help the agent's warp pair with the Ruiz passes -- the only
+// stage whose work splits by node without changing a single operation (ruiz(): nodes are
+// independent within a pass), so the results are bit-identical.  `go` is set by the pair.
+__device__ __forceinline__ void ruiz_helper(const KParams& P, float* base, int lane, int w, const int* go) {
   const int nw = (int)(blockDim.x >> 5);
   asm volatile("bar.sync %0, %1;" ::"r"(RUIZ_BAR), "r"((int)blockDim.x) : "memory");  // the pair's setup is done
   if (*go == 0) return;
@@ -354,7 +355,7 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   const int b = blockIdx.x;
   int agent, sched = -1;
   if (P.mode == 1) {  // schedule store: one schedule per CTA, built by pair 0 (the other pairs
-                      // help with its Ruiz passes: store_ruiz_helper)
+                      // help with its Ruiz passes: ruiz_helper)
     const int ns = min(*P.n_sched, P.store_cap);
     if (b >= ns) return;  // whole CTA idle
     sched = b;
@@ -385,7 +386,7 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_kernel(const KParams P) {
   // other pairs run the agent's Ruiz passes with it
   const bool helpers = P.mode == 1 || (P.agent_list == nullptr && P.full_ctas == 0 && P.tail_agents == 1);
   if (helpers && pair > 0) {
-    store_ruiz_helper(P, smem, lane, w, &s_go);
+    ruiz_helper(P, smem, lane, w, &s_go);
   } else if (agent < P.n_agents) {
     const int tmn = tm_nodes(P.NT, P.agents_per_cta, w & 3);
     const uint32_t tm = tb + ((uint32_t)(32 * (w & 3)) << 16) + (uint32_t)((w >> 2) * tmn * TCOLS);

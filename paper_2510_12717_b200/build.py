@@ -42,7 +42,10 @@ def build(force: bool = False, verbose: bool = False) -> str:
     tmp = LIB_PATH + ".tmp"
     # one nvcc per translation unit, in parallel (the solve kernel dominates), then one link
     objs = [os.path.join(LIB_DIR, os.path.basename(src).replace(".cu", ".o")) for src in SOURCES]
-    procs = [subprocess.Popen([nvcc(), *NVCC_FLAGS, "-c", "-o", o, src], stdout=subprocess.PIPE,
+    # (the solve TU is relocatable device code: its list dispatcher tail-launches the per-agent
+    # kernel from the device)
+    procs = [subprocess.Popen([nvcc(), *NVCC_FLAGS, *(["-rdc=true"] if src.endswith("rmpc_kernel.cu") else []),
+                               "-c", "-o", o, src], stdout=subprocess.PIPE,
                               stderr=subprocess.PIPE, text=True) for src, o in zip(SOURCES, objs)]
     logs = []
     for pr in procs:
@@ -51,8 +54,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
         if pr.returncode != 0:
             sys.stderr.write(out + err)
             raise RuntimeError("nvcc failed building librmpc_b200.so")
-    r = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp, *objs],
-                       capture_output=True, text=True)
+    r = subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-rdc=true", "-shared", "-o", tmp,
+                        *objs, "-lcudadevrt"], capture_output=True, text=True)
     if r.returncode != 0:
         sys.stderr.write(r.stdout + r.stderr)
         raise RuntimeError("nvcc failed linking librmpc_b200.so")

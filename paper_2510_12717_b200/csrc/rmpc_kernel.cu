@@ -657,6 +657,22 @@ static int sm_count() {
   return nsm;
 }
 
+namespace rmpc_dev {
+// The per-agent list of a shared solve (over-capacity schedules, non-finite inputs, schedule
+// hash collisions found by the squads) is known only on the device: this one-thread kernel reads
+// its length and tail-launches rti_kernel over exactly ceil(n_list / A) CTAs (none when the list
+// is empty -- an upper-bound grid of idle CTAs cost ~12 us per tick).  The tail launch runs after
+// this grid and before anything later in the stream.
+__global__ void list_dispatch_kernel(const KParams U, int variant, int threads, int smem) {
+  const int nl = *U.n_list;
+  if (nl <= 0) return;
+  const int grid = (nl + U.agents_per_cta - 1) / U.agents_per_cta;
+  if (variant == 0) rti_kernel<false, DENSE_AGENTS><<<grid, threads, smem, cudaStreamTailLaunch>>>(U);
+  else if (variant == 1) rti_kernel<true, MAX_AGENTS><<<grid, threads, smem, cudaStreamTailLaunch>>>(U);
+  else rti_kernel<false, MAX_AGENTS><<<grid, threads, smem, cudaStreamTailLaunch>>>(U);
+}
+}  // namespace rmpc_dev
+
 static int launch_variant(const rmpc_dev::KParams& P, const rmpc_dev::CtaShape& c, int grid, cudaStream_t st,
                           int threads = 0) {
   if (grid <= 0) return 0;
@@ -976,7 +992,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   U.agents_per_cta = c.agents;
   U.spill_nodes = c.spill_nodes;
   U.tmem_cols = c.tmem_cols;
-  U.full_ctas = (n + c.agents - 1) / c.agents;  // (an upper bound: idle CTAs exit at once)
+  U.full_ctas = (n + c.agents - 1) / c.agents;  // (the largest list)
   U.tail_agents = 0;
   if (co) {
     // the per-agent list writes the mapped host buffers too, after the first wave's copy-out: a
@@ -985,7 +1001,9 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
     U.out = co->h_out;
     U.z_out = co->h_z;
   }
-  return launch_variant(U, c, U.full_ctas, st);
+  list_dispatch_kernel<<<1, 1, 0, st>>>(U, c.dense ? 0 : (c.spill_nodes > 0 ? 1 : 2), 64 * c.agents, c.smem_bytes);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  return (int)cudaGetLastError();
 }
 
 namespace rmpc_dev {

@@ -382,7 +382,7 @@ def test_auto_path_selection(n):
 def test_schedule_store_over_capacity():
     """More distinct schedules than the store holds (1 024 per shard): per-agent gait periods and
     switch phases make almost every agent's schedule unique, so the ids past the capacity run the
-    per-agent list (rti_kernel over the agent list, an upper-bound grid) next to the squads of the
+    per-agent list (rti_kernel over the agent list, tail-launched from the device) next to the squads of the
     stored ones -- every agent solved, within the parity gates of the per-agent factorization."""
     n, T = 3000, 10
     m, s = default_model(), default_settings(T)

@@ -498,7 +498,7 @@ def main():
     # the same through the structure-of-arrays boundary (rmpc_solve_soa): one pinned FP32 block
     # of 28 component rows, 112 B per agent H2D instead of 224
     h_soa = pin(R.to_soa(st, cm, ga))
-    for _ in range(2):
+    for _ in range(5):
         br.solve_soa(h_soa, out=h_out, z_out=h_z)
     barrier()
     t0 = time.perf_counter()

@@ -22,7 +22,9 @@ FUNC = os.environ.get("RMPC_NCU_FUNC", "_ZN8rmpc_dev10rti_kernelILb0ELi6EEEvNS_7
 def line_table():
     with tempfile.TemporaryDirectory() as d:
         subprocess.run(["cuobjdump", "-xelf", "all", LIB], cwd=d, check=True, capture_output=True)
-        cub = [f for f in os.listdir(d) if f.startswith(os.environ.get("RMPC_NCU_CUBIN", "rmpc_kernel") + ".") and f.endswith(".cubin")][0]
+        # the solve TU's cubin: rmpc_kernel.*, or the device-linked librmpc_b200.* (-rdc=true)
+        pre = [os.environ["RMPC_NCU_CUBIN"]] if "RMPC_NCU_CUBIN" in os.environ else ["rmpc_kernel", "librmpc_b200"]
+        cub = [f for p in pre for f in sorted(os.listdir(d)) if f.startswith(p + ".") and f.endswith(".cubin")][0]
         txt = subprocess.run(["nvdisasm", "--print-line-info", os.path.join(d, cub)],
                              check=True, capture_output=True, text=True).stdout
     cur, out, inside = None, [], False

@@ -74,7 +74,12 @@ def main():
     h = rows[hi]
     cs, ci = h.index("Warp Stall Sampling (All Samples)"), h.index("Instructions Executed")
     cw, cx = h.index("L1 Wavefronts Shared"), h.index("L1 Wavefronts Shared Excessive")
-    ins = [r for r in rows[hi + 1:] if len(r) > ci]
+    ins = []
+    for r in rows[hi + 1:]:  # the kernel's own table (the page may list called functions after it)
+        if r and r[0] == "Address":
+            break
+        if len(r) > ci:
+            ins.append(r)
     lines = line_table()
     if len(lines) != len(ins):
         print(f"warning: {len(ins)} ncu instructions vs {len(lines)} disassembled", file=sys.stderr)

@@ -125,6 +125,7 @@ struct KParams {
   int32_t* n_list;           // its length (device); rti_shared_kernel appends fallbacks
   int32_t* list_out;         // = agent_list, writable (fallbacks of rti_shared_kernel)
   float* sqpack;             // per schedule id: the squad image (rti_squad_kernel, sq_pack_kernel)
+  const double* con_pz;      // contact heights of the nominal pose (sched_key_kernel), [4]
 };
 
 // One schedule's entry in the store (floats, 16-byte aligned regions): the Ruiz-scaled
@@ -389,6 +390,7 @@ struct RmpcSchedBuffers {
   int32_t* n_unshared;
   float* store;               // cap x store_layout(T).total floats
   float* sqpack;              // cap x sq_layout(T).priv floats (squads), or NULL
+  double* con;                // [4] contact heights of the nominal pose (the cold guess of every node)
   int32_t slots, cap, agents;
   // the grouping pass (count, scan, scatter) runs on a side stream beside the store build:
   // fork after the key kernel, join before the group solve (cudaStream_t / cudaEvent_t)

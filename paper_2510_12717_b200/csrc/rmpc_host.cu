@@ -286,6 +286,7 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
     CK(cudaMalloc(&sb.n_sched, sizeof(int32_t)));
     CK(cudaMalloc(&sb.n_unshared, sizeof(int32_t)));
     CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
+    CK(cudaMalloc(&sb.con, 4 * sizeof(double)));
     sb.sqpack = nullptr;
     if (rmpc_dev::sq_supported(h.NT) || rmpc_dev::sq4_supported(h.NT))
       CK(cudaMalloc(&sb.sqpack, (size_t)sb.cap * rmpc_dev::sq_layout(h.NT).priv * sizeof(float)));
@@ -315,7 +316,8 @@ void free_shard(Shard& sh) {
   for (RmpcSchedBuffers& sb : sh.sched) {
     for (void* p : {(void*)sb.table, (void*)sb.slot_id, (void*)sb.slot_of, (void*)sb.pos, (void*)sb.order,
                     (void*)sb.ulist, (void*)sb.rep_list, (void*)sb.cnt, (void*)sb.grp_first, (void*)sb.grp_cta,
-                    (void*)sb.n_sched, (void*)sb.n_unshared, (void*)sb.store, (void*)sb.sqpack})
+                    (void*)sb.n_sched, (void*)sb.n_unshared, (void*)sb.store, (void*)sb.sqpack,
+                    (void*)sb.con})
       cudaFree(p);
     if (sb.side) {
       cudaStreamSynchronize((cudaStream_t)sb.side);

@@ -576,18 +576,7 @@ __global__ void __launch_bounds__(64 * MAXA, 1) rti_shared_kernel(const KParams 
     const int32_t* fl = reinterpret_cast<const int32_t*>(entry + SL.flags);
     for (int k = tid; k < NT; k += blockDim.x) reinterpret_cast<int32_t*>(smem + L.flags)[k] = fl[k];
   }
-  if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)
-    double gq[9], gqd[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      gq[k] = P.nominal[k];
-      gqd[k] = 0.0;
-    }
-    Frames F;
-    fk_frames(P, gq, gqd, F);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) s_con[c] = F.con[c].pz;
-  }
+  if (tid < 4) s_con[tid] = P.con_pz[tid];  // contact heights of the nominal pose (sched_key_kernel)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
@@ -734,6 +723,19 @@ __device__ __forceinline__ bool state_cmd_finite(const rmpc_state& st, const rmp
 
 __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
+  if (a == 0) {  // contact heights of the nominal pose (the cold guess of every node), once for
+                 // every group CTA of the solve
+    double gq[9], gqd[9];
+#pragma unroll
+    for (int k = 0; k < 9; ++k) {
+      gq[k] = P.nominal[k];
+      gqd[k] = 0.0;
+    }
+    Frames F;
+    fk_frames(P, gq, gqd, F);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) b.con[c] = F.con[c].pz;
+  }
   if (a >= P.n_agents) return;
   const rmpc_gait g = P.gaits[a];
   bool fin = isfinite(g.phase) && isfinite(g.period) && isfinite(g.phase_switch);
@@ -936,6 +938,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   S.grp_cta = b.grp_cta;
   S.grp_first = b.grp_first;
   S.grp_count = b.cnt;
+  S.con_pz = b.con;
   S.n_list = b.n_unshared;
   S.list_out = b.ulist;
   S.agents_per_cta = cs.agents;

@@ -799,18 +799,7 @@ __global__ void __launch_bounds__(128, 1) rti_squad4_kernel(const KParams P) {
 #pragma unroll 4
     for (int k = tid; k < L.priv / 4; k += 128) dst[k] = src[k];
   }
-  if (tid == 0) {  // contact heights of the nominal pose (the cold guess of every node)
-    double gq[9], gqd[9];
-#pragma unroll
-    for (int k = 0; k < 9; ++k) {
-      gq[k] = P.nominal[k];
-      gqd[k] = 0.0;
-    }
-    Frames F;
-    fk_frames(P, gq, gqd, F);
-#pragma unroll
-    for (int c = 0; c < 4; ++c) s_con[c] = F.con[c].pz;
-  }
+  if (tid < 4) s_con[tid] = P.con_pz[tid];  // contact heights of the nominal pose (sched_key_kernel)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");

@@ -26,6 +26,37 @@ namespace rmpc_dev {
 
 // Layout constants and sq_layout: rmpc_device.cuh.
 
+// ------------------------------------------------------------------------- bulk image load
+// A squad's schedule image (sq_pack_kernel, contiguous in global and in shared memory) as bulk
+// asynchronous copies (`cp.async.bulk`, the TMA engine) completing on an mbarrier: one thread
+// issues them, the squad's threads wait on the barrier's phase 0 -- instead of 64 threads each
+// walking ~55 dependent L2 round trips of float4 loads.
+__device__ __forceinline__ void sq_mbar_init(uint64_t* mbar) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(mbar)) : "memory");
+}
+__device__ __forceinline__ void sq_mbar_fence_init() {
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+__device__ __forceinline__ void sq_bulk_image(float* dst, const float* src, uint32_t bytes, uint64_t* mbar) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(m), "r"(bytes) : "memory");
+  constexpr uint32_t CHUNK = 16384;
+  for (uint32_t o = 0; o < bytes; o += CHUNK) {
+    const uint32_t n = bytes - o < CHUNK ? bytes - o : CHUNK;
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(dst) + o),
+                 "l"(reinterpret_cast<const char*>(src) + o), "r"(n), "r"(m)
+                 : "memory");
+  }
+}
+__device__ __forceinline__ void sq_mbar_wait(uint64_t* mbar, uint32_t parity) {
+  const uint32_t m = (uint32_t)__cvta_generic_to_shared(mbar);
+  asm volatile(
+      "{\n .reg .pred p;\n SQ_WAIT_%=:\n mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n @!p bra SQ_WAIT_%=;\n}" ::"r"(m),
+      "r"(parity)
+      : "memory");
+}
+
 // Cross-thread elements of an agent (shared by its two threads), [element][lane].
 constexpr int SQX_XM = 0;     // x~_m of the middle node (rows 0..15 from the top, 16..25 from the bottom)
 constexpr int SQX_TM = 26;    // t of interval m's rows (bottom writes, both read)
@@ -1142,8 +1173,14 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
   __shared__ uint32_t tmem_base;
   __shared__ int s_g[2], s_first[2], s_cnt[2];
   __shared__ double s_con[4];
+  __shared__ uint64_t s_mbar[2];
   const int w = threadIdx.x >> 5, tid = threadIdx.x;
   const int NT = P.NT;
+  if (tid == 0) {
+    sq_mbar_init(&s_mbar[0]);
+    sq_mbar_init(&s_mbar[1]);
+    sq_mbar_fence_init();
+  }
   if (tid < 2) {
     const int ng = min(*P.n_sched, P.store_cap);
     const int cta = (int)blockIdx.x + P.sq_cta_base;
@@ -1176,18 +1213,14 @@ __global__ void __launch_bounds__(128, 1) rti_squad_kernel(const KParams P) {
   const StoreLayout SL = store_layout(NT);
   const int sqi = w >> 1;
   float* reg = smem + sqi * L.total;
-  if (s_cnt[sqi] > 0) {  // this squad's schedule image (sq_pack_kernel) into its region (64 threads)
-    const float4* src = reinterpret_cast<const float4*>(P.sqpack + (size_t)s_g[sqi] * L.priv);
-    float4* dst = reinterpret_cast<float4*>(reg);
-    const int t = tid & 63;
-#pragma unroll 4
-    for (int k = t; k < L.priv / 4; k += 64) dst[k] = src[k];
-  }
+  if (s_cnt[sqi] > 0 && (tid & 63) == 0)  // this squad's schedule image (sq_pack_kernel) into its region
+    sq_bulk_image(reg, P.sqpack + (size_t)s_g[sqi] * L.priv, (uint32_t)L.priv * 4u, &s_mbar[sqi]);
   if (tid < 4) s_con[tid] = P.con_pz[tid];  // contact heights of the nominal pose (sched_key_kernel)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
+  if (s_cnt[sqi] > 0) sq_mbar_wait(&s_mbar[sqi], 0);
   if (s_cnt[sqi] > 0)
     sq_solve(P, reg, tb + ((uint32_t)(32 * w) << 16), sqi, s_g[sqi], s_first[sqi], s_cnt[sqi], s_con);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");

@@ -763,9 +763,12 @@ __global__ void __launch_bounds__(128, 1) rti_squad4_kernel(const KParams P) {
   __shared__ uint32_t tmem_base;
   __shared__ int s_g, s_first, s_cnt;
   __shared__ double s_con[4];
+  __shared__ uint64_t s_mbar;
   const int w = threadIdx.x >> 5, tid = threadIdx.x;
   const int NT = P.NT;
   if (tid == 0) {
+    sq_mbar_init(&s_mbar);
+    sq_mbar_fence_init();
     const int ng = min(*P.n_sched, P.store_cap);
     const int sq = (int)blockIdx.x + P.sq_cta_base;
     int g = -1, first = 0, cnt = 0;
@@ -793,17 +796,14 @@ __global__ void __launch_bounds__(128, 1) rti_squad4_kernel(const KParams P) {
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;" ::: "memory");
   }
   const SqLayout L = sq_layout(NT);
-  {  // the schedule image (sq_pack_kernel) into shared memory
-    const float4* src = reinterpret_cast<const float4*>(P.sqpack + (size_t)s_g * L.priv);
-    float4* dst = reinterpret_cast<float4*>(smem);
-#pragma unroll 4
-    for (int k = tid; k < L.priv / 4; k += 128) dst[k] = src[k];
-  }
+  if (tid == 0)  // the schedule image (sq_pack_kernel) into shared memory
+    sq_bulk_image(smem, P.sqpack + (size_t)s_g * L.priv, (uint32_t)L.priv * 4u, &s_mbar);
   if (tid < 4) s_con[tid] = P.con_pz[tid];  // contact heights of the nominal pose (sched_key_kernel)
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tb = tmem_base;
+  sq_mbar_wait(&s_mbar, 0);
   sq4_solve(P, smem, tb + ((uint32_t)(32 * w) << 16), s_g, s_first, s_cnt, s_con);
   asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();

@@ -379,12 +379,16 @@ def test_auto_path_selection(n):
     assert auto[0].tobytes() == forced[0].tobytes() and auto[1].tobytes() == forced[1].tobytes()
 
 
-def test_schedule_store_over_capacity():
+@pytest.mark.parametrize("T", [10, 12])
+def test_schedule_store_over_capacity(T):
     """More distinct schedules than the store holds (1 024 per shard): per-agent gait periods and
     switch phases make almost every agent's schedule unique, so the ids past the capacity run the
-    per-agent list (rti_kernel over the agent list, tail-launched from the device) next to the squads of the
-    stored ones -- every agent solved, within the parity gates of the per-agent factorization."""
-    n, T = 3000, 10
+    per-agent list (rti_kernel over the agent list, tail-launched from the device) next to the
+    squads (T = 10) or long squads (T = 12) of the stored ones, with host outputs (the split
+    launch and its copy-out) -- every agent solved, within the parity gates of the per-agent
+    factorization, and the device path's bytes equal to the host path's."""
+    import torch
+    n = 3000
     m, s = default_model(), default_settings(T)
     st, cm, ga = R.synthetic_batch(n, "random", seed=8, model=m, settings=s)
     rng = np.random.default_rng(8)
@@ -398,5 +402,14 @@ def test_schedule_store_over_capacity():
     b, zb = br.solve(st, cm, ga, want_z=True)
     assert (a["status"] == 0).all()
     c = compare(a, b, za, zb)
-    check(c, "over capacity: squads + list vs per-agent")
+    check(c, f"over capacity T={T}: squads + list vs per-agent")
     assert c["z"].max() <= 1e-3
+    br.set_schedule_sharing(3)
+    dev = torch.device("cuda:0")
+    d = [torch.from_numpy(x).to(dev) for x in (st, cm, ga)]
+    out = torch.zeros(n * SOLUTION_DTYPE.itemsize, dtype=torch.uint8, device=dev)
+    zd = torch.zeros(n * T * 26, dtype=torch.float32, device=dev)
+    br.solve_device(*d, out, z_out=zd, stream=torch.cuda.current_stream())
+    torch.cuda.synchronize()
+    assert out.cpu().numpy().tobytes() == a.tobytes()
+    assert zd.cpu().numpy().tobytes() == za.tobytes()

@@ -721,6 +721,18 @@ __device__ __forceinline__ bool state_cmd_finite(const rmpc_state& st, const rmp
   return fin;
 }
 
+// The schedule pass's state for a new tick in one launch (instead of four memsets): the hash
+// table empty, the counters and group sizes zero.
+__global__ void __launch_bounds__(256) sched_init_kernel(RmpcSchedBuffers b) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x, nt = gridDim.x * blockDim.x;
+  for (int k = t; k < b.slots; k += nt) b.table[k] = ~0ull;
+  for (int k = t; k < b.cap; k += nt) b.cnt[k] = 0;
+  if (t == 0) {
+    *b.n_sched = 0;
+    *b.n_unshared = 0;
+  }
+}
+
 __global__ void sched_key_kernel(const KParams P, RmpcSchedBuffers b) {
   const int a = blockIdx.x * blockDim.x + threadIdx.x;
   if (a == 0) {  // contact heights of the nominal pose (the cold guess of every node), once for
@@ -880,12 +892,10 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
     Q.z_out = co->h_z;
     return rmpc_launch_shared(Q, b, stream, variant, nullptr, params.synth_rep ? ev_inputs : nullptr);
   }
-  int rc = (int)cudaMemsetAsync(b.table, 0xFF, (size_t)b.slots * sizeof(unsigned long long), st);
-  if (rc == 0) rc = (int)cudaMemsetAsync(b.n_sched, 0, sizeof(int32_t), st);
-  if (rc == 0) rc = (int)cudaMemsetAsync(b.n_unshared, 0, sizeof(int32_t), st);
-  if (rc == 0) rc = (int)cudaMemsetAsync(b.cnt, 0, (size_t)b.cap * sizeof(int32_t), st);
-  if (rc != 0) return rc;
+  sched_init_kernel<<<64, 256, 0, st>>>(b);
   sched_key_kernel<<<blocks, 256, 0, st>>>(params, b);
+  g_launches.fetch_add(1, std::memory_order_relaxed);
+  int rc = 0;
   // fork: the grouping pass (count, scan, scatter) needs only the keys; it runs on the side
   // stream while the store build (which needs only the representatives) runs here
   const cudaStream_t side = b.side ? (cudaStream_t)b.side : st;

@@ -609,9 +609,10 @@ def main():
             "stage_split": stage_split,
             "gpu_launches": launches,
             "gpu_launches_note": "solve-path kernels the library launched in the timed region "
-                                 "(rmpc_kernel_launches): per step the schedule pass (key, count, scan, "
-                                 "scatter), one factorization per schedule, the schedule images, the "
-                                 "squad solve and the per-agent list solve",
+                                 "(rmpc_kernel_launches): per step the schedule pass (init, key, count, "
+                                 "scan, scatter), one factorization per schedule, the schedule images, "
+                                 "the squad solve and the per-agent list's device dispatcher (which "
+                                 "tail-launches the list solve only when the list is non-empty)",
             "status_ok": ok, "clocks": clk, "cpu_baseline": cpu,
             "closed_loop": closed,
             "ppo_update": ppo,

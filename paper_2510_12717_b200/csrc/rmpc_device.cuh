@@ -401,7 +401,8 @@ struct RmpcSchedBuffers {
 // The whole cold-start solve with schedule sharing for params.n_agents agents on `stream`:
 // hash every agent's stance schedule, build the store (one factorization per schedule), group
 // the agents by schedule, solve the groups (rti_shared_kernel: one schedule per CTA) and the
-// rest (rti_kernel over an agent list).  Seven launches plus memsets, no host synchronisation.
+// rest (rti_kernel over an agent list, dispatched from the device).  Nine launches, no host
+// synchronisation.
 // variant 1: warp-pair-per-agent CTAs of one schedule (rti_shared_kernel, bit-identical to the
 // per-agent solve); 2: lane-per-agent squads (rti_squad_kernel) where the horizon fits them.
 // End-to-end outputs of a squad solve (host solve with outputs in pinned, mapped host memory):

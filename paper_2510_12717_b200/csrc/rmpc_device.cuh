@@ -391,6 +391,8 @@ struct RmpcSchedBuffers {
   float* store;               // cap x store_layout(T).total floats
   float* sqpack;              // cap x sq_layout(T).priv floats (squads), or NULL
   double* con;                // [4] contact heights of the nominal pose (the cold guess of every node)
+  int32_t* h_nsched;          // pinned host copy of n_sched (host outputs: one or two squad waves?)
+  void* ev_nsched;            // recorded after that copy (cudaEvent_t)
   int32_t slots, cap, agents;
   // the grouping pass (count, scan, scatter) runs on a side stream beside the store build:
   // fork after the key kernel, join before the group solve (cudaStream_t / cudaEvent_t)

@@ -287,6 +287,12 @@ void alloc_shard(rmpc_handle& h, Shard& sh) {
     CK(cudaMalloc(&sb.n_unshared, sizeof(int32_t)));
     CK(cudaMalloc(&sb.store, (size_t)sb.cap * rmpc_dev::store_layout(h.NT).total * sizeof(float)));
     CK(cudaMalloc(&sb.con, 4 * sizeof(double)));
+    CK(cudaHostAlloc(&sb.h_nsched, sizeof(int32_t), cudaHostAllocDefault));
+    {
+      cudaEvent_t en = nullptr;
+      CK(cudaEventCreateWithFlags(&en, cudaEventDisableTiming));
+      sb.ev_nsched = en;
+    }
     sb.sqpack = nullptr;
     if (rmpc_dev::sq_supported(h.NT) || rmpc_dev::sq4_supported(h.NT))
       CK(cudaMalloc(&sb.sqpack, (size_t)sb.cap * rmpc_dev::sq_layout(h.NT).priv * sizeof(float)));
@@ -319,6 +325,8 @@ void free_shard(Shard& sh) {
                     (void*)sb.n_sched, (void*)sb.n_unshared, (void*)sb.store, (void*)sb.sqpack,
                     (void*)sb.con})
       cudaFree(p);
+    if (sb.h_nsched) cudaFreeHost(sb.h_nsched);
+    if (sb.ev_nsched) cudaEventDestroy((cudaEvent_t)sb.ev_nsched);
     if (sb.side) {
       cudaStreamSynchronize((cudaStream_t)sb.side);
       cudaStreamDestroy((cudaStream_t)sb.side);

@@ -903,6 +903,13 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
     cudaEventRecord((cudaEvent_t)b.ev_fork, st);
     cudaStreamWaitEvent(side, (cudaEvent_t)b.ev_fork, 0);
   }
+  // host outputs: the schedule count to the host (side stream), so the squad launch below knows
+  // whether a second wave follows the first
+  const bool ask_nsched = co != nullptr && b.h_nsched != nullptr && b.ev_nsched != nullptr && side != st;
+  if (ask_nsched) {
+    cudaMemcpyAsync(b.h_nsched, b.n_sched, sizeof(int32_t), cudaMemcpyDeviceToHost, side);
+    cudaEventRecord((cudaEvent_t)b.ev_nsched, side);
+  }
   if (params.synth_rep && ev_inputs)  // the count kernel is the first to read the states
     cudaStreamWaitEvent(side, (cudaEvent_t)ev_inputs, 0);
   sched_count_kernel<<<blocks, 256, 0, side>>>(params, b);
@@ -954,6 +961,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   S.agents_per_cta = cs.agents;
   S.tmem_cols = cs.tmem_cols;
   const int grid_s = (n + cs.agents - 1) / cs.agents + std::min(b.cap, n);
+  bool single_wave = false;
   if (squads) {  // lane-per-agent squads, two per CTA (grid: an upper bound of sum ceil(count / 32) / 2)
     S.agents_per_cta = 32;
     S.sqpack = b.sqpack;
@@ -976,7 +984,16 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
       if (long_sq) rti_squad4_kernel<<<g, 128, smem, st>>>(S);
       else rti_squad_kernel<<<g, 128, smem, st>>>(S);
     };
-    if (co) {  // (grid > co->sms here)  // split: first wave, its copy-out beside the second launch
+    // host outputs with every squad in the first wave (known once the key kernel has counted the
+    // schedules; the host waits for that ~10 us copy while the store build runs): one launch into
+    // the device buffers, then copy-engine transfers of the whole contiguous outputs (56 vs 47
+    // GB/s of SM-issued mapped writes) after the per-agent list
+    if (co && ask_nsched && !solo) {
+      cudaEventSynchronize((cudaEvent_t)b.ev_nsched);
+      const int ns = std::min(std::max(*b.h_nsched, 0), b.cap);
+      single_wave = (n + 31) / 32 + ns <= spc * co->sms;
+    }
+    if (co && !single_wave) {  // split: first wave, its copy-out beside the second launch
       S.sq_cta_base = 0;
       launch_sq(co->sms);
       cudaEventRecord((cudaEvent_t)co->ev_a, st);
@@ -1007,7 +1024,7 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   U.tmem_cols = c.tmem_cols;
   U.full_ctas = (n + c.agents - 1) / c.agents;  // (the largest list)
   U.tail_agents = 0;
-  if (co) {
+  if (co && !single_wave) {
     // the per-agent list writes the mapped host buffers too, after the first wave's copy-out: a
     // fallback agent of the first wave is in both, and its list record must land last
     cudaStreamWaitEvent(st, (cudaEvent_t)co->ev_b, 0);
@@ -1016,6 +1033,11 @@ int rmpc_launch_shared(const rmpc_dev::KParams& params_in, const RmpcSchedBuffer
   }
   list_dispatch_kernel<<<1, 1, 0, st>>>(U, c.dense ? 0 : (c.spill_nodes > 0 ? 1 : 2), 64 * c.agents, c.smem_bytes);
   g_launches.fetch_add(1, std::memory_order_relaxed);
+  if (single_wave) {  // every record and z* row is in the device buffers: two contiguous copies
+    cudaMemcpyAsync(co->h_out, params.out, (size_t)n * sizeof(rmpc_solution), cudaMemcpyDefault, st);
+    if (co->h_z && params.z_out)
+      cudaMemcpyAsync(co->h_z, params.z_out, (size_t)n * NT * NV * sizeof(float), cudaMemcpyDefault, st);
+  }
   return (int)cudaGetLastError();
 }
 

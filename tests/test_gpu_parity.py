@@ -413,3 +413,32 @@ def test_schedule_store_over_capacity(T):
     torch.cuda.synchronize()
     assert out.cpu().numpy().tobytes() == a.tobytes()
     assert zd.cpu().numpy().tobytes() == za.tobytes()
+
+
+@pytest.mark.parametrize("T,n_qp", [(10, 1), (10, 7), (10, 60), (12, 3), (12, 40), (5, 40)])
+def test_iteration_count_setting(oracle, T, n_qp):
+    """MpcSettings::n_qp other than the default 25 (qp.cpp:156-190 runs exactly n_qp iterations
+    from x = y = z = 0): the squads / long squads (level 3) and the per-agent kernel (level 0)
+    against the oracle, identical statuses."""
+    n = 160
+    m, s = default_model(), default_settings(T)
+    s.n_qp = n_qp
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=11 + n_qp, model=m, settings=s)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=16)
+    br = R.BatchRunner(n, m, s)
+    for level in (3, 0):
+        br.set_schedule_sharing(level)
+        sol, z = br.solve(st, cm, ga, want_z=True)
+        assert (sol["status"] == ref["status"]).all()
+        c = compare(sol, ref, z, zr)
+        print(f"T={T} n_qp={n_qp} level={level}:", summary(c))
+        check(c, f"n_qp={n_qp} T={T} level={level}")
+        assert c["z"].max() <= 1e-3
+
+
+def test_zero_iterations_rejected():
+    """n_qp < 1 is the reference's constructor error (AdmmSolver: n_iters must be >= 1)."""
+    m, s = default_model(), default_settings(10)
+    s.n_qp = 0
+    with pytest.raises(R.RmpcError, match="n_iters"):
+        R.BatchRunner(4, m, s)

@@ -68,7 +68,8 @@ typedef struct rmpc_settings {
   int32_t n_qp;                          /* fixed ADMM iteration count, no early exit */
   double mu, sigma, rho, over_relax;
   int32_t warm_start;                    /* 0: cold nominal guess (default) */
-  int32_t ruiz_iters;                    /* 10 (AdmmSettings default); 0 disables */
+  int32_t ruiz_iters;                    /* 10 (AdmmSettings default, the reference MPC's fixed
+                                            value); >= 1 (RMPC_ERR_STRUCTURAL otherwise) */
 } rmpc_settings;
 
 /* RobotState (robot.hpp:52-55). */

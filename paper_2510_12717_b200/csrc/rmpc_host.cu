@@ -787,6 +787,13 @@ int32_t rmpc_create(const rmpc_model* model, const rmpc_settings* settings, int3
   if (settings->horizon < 2) { g_create_error = "MpcController: horizon must be >= 2"; return RMPC_ERR_STRUCTURAL; }
   if (settings->horizon > RMPC_MAX_HORIZON) { g_create_error = "MpcController: horizon > RMPC_MAX_HORIZON"; return RMPC_ERR_STRUCTURAL; }
   if (settings->n_qp < 1) { g_create_error = "AdmmSolver: n_iters must be >= 1"; return RMPC_ERR_STRUCTURAL; }
+  // The reference's MPC always equilibrates (MpcSettings::admm() leaves AdmmSettings::ruiz_iters at
+  // 10, mpc.hpp:49-56); the FP32 reduced system H = P^ + sigma I + rho A^T A squares the row
+  // scales of an unequilibrated A and loses the 1e-4 bar without at least one Ruiz pass.
+  if (settings->ruiz_iters < 1) {
+    g_create_error = "rmpc_create: ruiz_iters must be >= 1 (the FP32 reduced ADMM system needs equilibration)";
+    return RMPC_ERR_STRUCTURAL;
+  }
   for (int i = 0; i < settings->horizon; ++i)
     if (!(settings->dt_schedule[i] > 0.0)) { g_create_error = "MpcController: dt_schedule entries must be > 0"; return RMPC_ERR_STRUCTURAL; }
   int ndev = 0;

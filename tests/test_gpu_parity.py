@@ -437,8 +437,45 @@ def test_iteration_count_setting(oracle, T, n_qp):
 
 
 def test_zero_iterations_rejected():
-    """n_qp < 1 is the reference's constructor error (AdmmSolver: n_iters must be >= 1)."""
+    """n_qp < 1 is the reference's constructor error (AdmmSolver: n_iters must be >= 1), and
+    ruiz_iters < 1 is refused: the reference's MPC always runs 10 Ruiz passes
+    (MpcSettings::admm(), mpc.hpp:49-56) and the FP32 reduced system needs at least one."""
     m, s = default_model(), default_settings(10)
     s.n_qp = 0
     with pytest.raises(R.RmpcError, match="n_iters"):
         R.BatchRunner(4, m, s)
+    s = default_settings(10)
+    s.ruiz_iters = 0
+    with pytest.raises(R.RmpcError, match="ruiz_iters"):
+        R.BatchRunner(4, m, s)
+
+
+@pytest.mark.parametrize("T,variant", [(10, "admm"), (10, "model"), (12, "admm"), (5, "model"), (10, "ruiz5")])
+def test_non_default_settings(oracle, T, variant):
+    """MpcSettings away from the defaults -- ADMM constants (rho, sigma, over-relaxation), a
+    non-uniform dt schedule, cost weights, friction, swing height, fewer Ruiz passes (5; with 1-2
+    the FP32 reduced system's error grows past 1e-4 on some agents, as the reference algorithm's
+    own FP32 instantiation does) -- through the squads / long squads (level 3) and the per-agent
+    kernel (level 0), against the oracle with the same settings."""
+    n = 160
+    m, s = default_model(), default_settings(T)
+    if variant == "admm":
+        s.rho, s.sigma, s.over_relax = 0.25, 1e-5, 1.4
+    elif variant == "model":
+        for i in range(T):
+            s.dt_schedule[i] = 0.03 + 0.005 * i
+        s.w_q[0], s.w_qd[2], s.w_f[1] = 3.0 * s.w_q[0], 0.5 * s.w_qd[2], 2.0 * s.w_f[1]
+        s.mu, s.z_swing = 0.9, 0.12
+    else:
+        s.ruiz_iters = 5
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=21 + T, model=m, settings=s)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=16)
+    br = R.BatchRunner(n, m, s)
+    for level in (3, 0):
+        br.set_schedule_sharing(level)
+        sol, z = br.solve(st, cm, ga, want_z=True)
+        assert (sol["status"] == ref["status"]).all()
+        c = compare(sol, ref, z, zr)
+        print(f"T={T} {variant} level={level}:", summary(c))
+        check(c, f"{variant} T={T} level={level}")
+        assert c["z"].max() <= 1e-3

@@ -479,3 +479,30 @@ def test_non_default_settings(oracle, T, variant):
         print(f"T={T} {variant} level={level}:", summary(c))
         check(c, f"{variant} T={T} level={level}")
         assert c["z"].max() <= 1e-3
+
+
+@pytest.mark.parametrize("T", [10, 12])
+def test_randomized_model(oracle, T):
+    """ModelParams away from the defaults (the trainer's randomize_model draws, ppo.cpp /
+    robot.hpp:24-50: heavier torso, longer shanks, stiffer joint limits, another nominal stance):
+    the nominal pose, the contact heights and every linearization follow the model -- squads /
+    long squads (level 3) and the per-agent kernel (level 0) against the oracle."""
+    n = 160
+    m, s = default_model(), default_settings(T)
+    m.torso_mass *= 1.15
+    m.shank_len *= 1.06
+    m.thigh_mass *= 0.9
+    m.nominal_stagger *= 1.2
+    for j in range(6):
+        m.qd_limit[j] *= 0.8
+    st, cm, ga = R.synthetic_batch(n, "mixed", seed=31 + T, model=m, settings=s)
+    ref, zr, _, _ = oracle.solve_batch(m, s, st, cm, ga, workers=16)
+    br = R.BatchRunner(n, m, s)
+    for level in (3, 0):
+        br.set_schedule_sharing(level)
+        sol, z = br.solve(st, cm, ga, want_z=True)
+        assert (sol["status"] == ref["status"]).all()
+        c = compare(sol, ref, z, zr)
+        print(f"T={T} randomized model level={level}:", summary(c))
+        check(c, f"model T={T} level={level}")
+        assert c["z"].max() <= 1e-3
